@@ -1,0 +1,351 @@
+"""Benchmark: ResNet-50 K-FAC update ms/iter on B200 (BASELINE.json `metric`).
+
+A "step" is one full K-FAC update of the hot path (Alg. 1 steps 1-3 + Eq. 18) over one
+synthetic mini-batch per GPU (32 images of 224x224, ResNet-50 layer shapes, configs[2]):
+  factors (all 54 layers, im2col SYRK + running average)  -> factor allreduce (W > 1)
+  -> LPT assignment -> eigendecomposition of the owned factors -> eigenbasis all-gather
+  -> preconditioning (Eqs. 13-15) -> KL-clip (Eq. 18).
+Weak scaling: every rank has its own batch of 32; value = max-over-ranks ms per step.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config r50] [--impl ours|reference]
+
+--impl reference times the FP64 CPU oracle (the deliberately slow reference arm) on a bounded
+sample of the same workload and extrapolates per stage (stated in `cpu_baseline.sample`).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from workloads import shapes  # noqa: E402
+
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--config", default="r50", choices=["mlp", "r32", "r50", "r101"])
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--variant", default="eigen", choices=["eigen", "factored", "inverse"])
+    p.add_argument("--exchange", default="bcast-eig", choices=["bcast-eig", "allgather-grad"])
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--seed", type=int, default=0)
+    return p.parse_args()
+
+
+# ------------------------------------------------------------------ work model --
+def work_model(layers):
+    """Algorithmic work per GPU per full update."""
+    fac_flops = sum(l.rows * l.d_a * (l.d_a + 1) + l.rows * l.d_g * (l.d_g + 1) for l in layers)
+    pc_flops = sum(4 * l.d_g * l.d_a * (l.d_g + l.d_a) for l in layers)
+    eig_flops = sum(9 * (l.d_a ** 3 + l.d_g ** 3) for l in layers)
+    act_bytes = sum(4 * int(np.prod(l.act_shape)) for l in layers)
+    gout_bytes = sum(4 * l.rows * l.d_g for l in layers)
+    ema_bytes = sum(8 * (l.d_a ** 2 + l.d_g ** 2) for l in layers)
+    params = sum(l.d_g * l.d_a for l in layers)
+    return dict(fac_flops=fac_flops, pc_flops=pc_flops, eig_flops=eig_flops,
+                fac_bytes=act_bytes + gout_bytes + ema_bytes, params=params,
+                kl_bytes=16 * params)
+
+
+def peaks():
+    try:
+        pk = json.load(open(PEAKS_PATH))
+        return dict(hbm=pk["hbm_gbs"], bf16=pk["bf16_tflops"], bf16_sus=pk.get("bf16_tflops_sustained"),
+                    src="measured")
+    except Exception:
+        return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, src="fallback")
+
+
+# ---------------------------------------------------------------- clocks ------
+class ClockSampler:
+    def __init__(self, idx):
+        self.idx, self.samples, self.proc = idx, [], None
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            for n, v in zip(names, s[5:9]):
+                if v.strip().lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------- oracle timing --
+def oracle_sample(layers, hp, seed, sample_idx):
+    """Run the FP64 oracle stages on a subset of the layers; return per-stage seconds and the
+    work fraction of the sample so the time can be scaled to the whole workload."""
+    import oracle
+    from workloads.gen import layer_inputs
+    sub = [layers[i] for i in sample_idx]
+    acts, gouts, grads = layer_inputs(sub, seed=seed)
+    t0 = time.perf_counter()
+    A, G = oracle.update_factors(sub, acts, gouts, decay=hp["decay"], first=True)
+    t1 = time.perf_counter()
+    Qs, vs = oracle.symeig_batch(A + G)
+    t2 = time.perf_counter()
+    n = len(sub)
+    P = oracle.precondition_batch(grads, Qs[n:], vs[n:], Qs[:n], vs[:n], hp["damping"])
+    oracle.kl_clip(P, grads, hp["lr"], hp["kappa"])
+    t3 = time.perf_counter()
+    w_all, w_sub = work_model(layers), work_model(sub)
+    est = ((t1 - t0) * w_all["fac_flops"] / w_sub["fac_flops"]
+           + (t2 - t1) * w_all["eig_flops"] / w_sub["eig_flops"]
+           + (t3 - t2) * w_all["pc_flops"] / w_sub["pc_flops"])
+    return est, dict(factors_s=t1 - t0, eigen_s=t2 - t1, precond_s=t3 - t2,
+                     names=[l.name for l in sub])
+
+
+SAMPLE = {"r50": [0, 1, 5, 12], "r101": [0, 1, 5, 12], "r32": [0, 1, 12, 31], "mlp": [0, 1]}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    layers = shapes.layers_for(args.config)
+    hp = shapes.HPARAMS[args.config]
+    import oracle
+    oracle.build()
+    times, det = [], None
+    for i in range(args.warmup + args.steps):
+        est, det = oracle_sample(layers, hp, args.seed + i, SAMPLE[args.config])
+        if i >= args.warmup:
+            times.append(est * 1e3)
+    ms = float(np.mean(times))
+    cores = len(os.sched_getaffinity(0))
+    sample = (f"oracle stages on layers {det['names']} of {args.config} (batch {layers[0].batch}), "
+              f"each stage scaled by algorithmic work (factors n*d(d+1), eigen 9d^3, precond "
+              f"4 dG dA (dG+dA)) to all {len(layers)} layers")
+    line = {"metric": metric_name(args.config), "value": ms, "unit": "ms/iter", "impl": "reference",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": config_block(args, layers),
+            "cpu_baseline": {"value": ms, "unit": "ms/iter", "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": ms, "unit": "ms/iter", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def metric_name(cfg):
+    name = {"r50": "ResNet-50", "r101": "ResNet-101", "r32": "ResNet-32", "mlp": "MLP-784-64-10"}[cfg]
+    return f"{name} K-FAC update ms/iter"
+
+
+def config_block(args, layers):
+    return {"workload": f"{args.config} full K-FAC update (factors+allreduce+eigen+exchange+precondition+KL-clip)",
+            "layers": len(layers), "batch_per_gpu": layers[0].batch, "variant": args.variant,
+            "exchange": args.exchange, "assignment": "lpt-d3" if args.exchange == "bcast-eig" else "layerwise-lpt",
+            "l2": "inputs larger than L2 (activations+gradients stream >2.7 GB per step)"
+            if args.config in ("r50", "r101") else "no flush (small config)"}
+
+
+# ----------------------------------------------------------------- our arm ----
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2007_00784_b200 import _lib
+    from paper_2007_00784_b200.preconditioner import KFACPreconditioner
+    from workloads.gen import layer_inputs
+
+    layers = shapes.layers_for(args.config)
+    hp = shapes.HPARAMS[args.config]
+    lr = hp["lr"] * world
+    acts_h, gouts_h, grads_h = layer_inputs(layers, seed=args.seed, rank=rank, device="cuda")
+    acts = [torch.from_numpy(a).cuda() for a in acts_h]
+    gouts = [torch.from_numpy(g).cuda() for g in gouts_h]
+    pc = KFACPreconditioner(layers, damping=hp["damping"], decay=hp["decay"], kappa=hp["kappa"], lr=lr,
+                            variant=args.variant, exchange=args.exchange)
+    grads, grad_flat = KFACPreconditioner.grad_buffer(layers, "cuda", return_flat=True)
+    for t, w in zip(grads, grads_h):
+        t.copy_(torch.from_numpy(w))
+    if world > 1:   # the gradient allreduce (Alg. 1) is the caller's DP step, done once here
+        dist.all_reduce(grad_flat, op=dist.ReduceOp.SUM)
+        grad_flat.mul_(1.0 / world)
+    stream = torch.cuda.current_stream()
+    ev = lambda: torch.cuda.Event(enable_timing=True)
+    stage_ms = {"factors": [], "eigen": [], "precond": []}
+
+    def one_step(first, timed=False):
+        e0, e1, e2, e3 = ev(), ev(), ev(), ev()
+        e0.record(stream)
+        pc.update_factors(acts, gouts, first)
+        e1.record(stream)
+        pc.compute_eigen()
+        e2.record(stream)
+        pc.precondition(grads)
+        e3.record(stream)
+        if timed:
+            stage_ms["_ev"] = stage_ms.get("_ev", []) + [(e0, e1, e2, e3)]
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for i in range(args.warmup):
+        one_step(first=(i == 0))
+    barrier()
+    n0 = _lib.kfac_launch_count()
+    with ClockSampler(local) as clk:
+        t0, t1 = ev(), ev()
+        barrier()
+        t0.record(stream)
+        for i in range(args.steps):
+            one_step(first=False, timed=True)
+        t1.record(stream)
+        barrier()
+    launches = _lib.kfac_launch_count() - n0
+    ms = t0.elapsed_time(t1) / args.steps
+    for e0, e1, e2, e3 in stage_ms.pop("_ev"):
+        stage_ms["factors"].append(e0.elapsed_time(e1))
+        stage_ms["eigen"].append(e1.elapsed_time(e2))
+        stage_ms["precond"].append(e2.elapsed_time(e3))
+    stages = {k: float(np.mean(v)) for k, v in stage_ms.items()}
+    info = pc.info.cpu().tolist()
+
+    # end-to-end through the public API with host buffers (pinned H2D inputs, D2H of nu/s)
+    e2e = None
+    if not args.no_e2e:
+        acts_p = [torch.from_numpy(a).pin_memory() for a in acts_h]
+        gouts_p = [torch.from_numpy(g).pin_memory() for g in gouts_h]
+        grads_p = [torch.from_numpy(np.ascontiguousarray(t.cpu().numpy())).pin_memory() for t in grads]
+        nu_h = torch.empty(1, pin_memory=True)
+        h2d = sum(t.numel() * 4 for t in acts_p + gouts_p + grads_p)
+
+        def e2e_step():
+            for d, h in zip(acts, acts_p):
+                d.copy_(h, non_blocking=True)
+            for d, h in zip(gouts, gouts_p):
+                d.copy_(h, non_blocking=True)
+            for d, h in zip(grads, grads_p):
+                d.copy_(h, non_blocking=True)
+            pc.update_factors(acts, gouts, False)
+            pc.compute_eigen()
+            pc.precondition(grads)
+            nu_h.copy_(pc.nu, non_blocking=True)
+
+        e2e_step()
+        barrier()
+        a0, a1 = ev(), ev()
+        a0.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        a1.record(stream)
+        barrier()
+        e2e = {"value": a0.elapsed_time(a1) / args.steps, "unit": "ms/iter", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": 4}
+
+    # max over ranks
+    vals = torch.tensor([ms] + [stages[k] for k in ("factors", "eigen", "precond")] +
+                        [e2e["value"] if e2e else 0.0], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+    vals = vals.tolist()
+    ms, stages = vals[0], dict(zip(("factors", "eigen", "precond"), vals[1:4]))
+    if e2e:
+        e2e["value"] = vals[4]
+
+    if rank == 0:
+        wm = work_model(layers)
+        pk = peaks()
+        tf32_peak = pk["bf16"] * (1.1 / 2.25)                  # guide's nominal tf32/bf16 ratio
+        simt_peak = 148 * 128 * 2 * 1.965e9 / 1e12             # fp32 FMA lanes x clock
+        dom = max(stages, key=stages.get)
+        if dom == "factors":
+            ach = wm["fac_flops"] / (stages["factors"] * 1e-3) / 1e12
+            roof = {"bound": "alu", "achieved": ach, "peak": simt_peak, "unit": "TFLOP/s",
+                    "kernel": "syrk_partial+syrk_reduce (factor stage)"}
+        elif dom == "precond":
+            ach = wm["pc_flops"] / (stages["precond"] * 1e-3) / 1e12
+            roof = {"bound": "alu", "achieved": ach, "peak": simt_peak, "unit": "TFLOP/s",
+                    "kernel": "gemm chain (precondition stage)"}
+        else:
+            ach = wm["eig_flops"] / (stages["eigen"] * 1e-3) / 1e12
+            roof = {"bound": "alu", "achieved": ach, "peak": simt_peak, "unit": "TFLOP/s",
+                    "kernel": "eig_round (eigen stage, conventional 9d^3 flops)"}
+        roof["frac"] = roof["achieved"] / roof["peak"]
+        roof["traffic"] = None
+        roof["peak_source"] = f"fp32 SIMT lanes x 1965 MHz (MEASURED_PEAKS {pk['src']} for hbm/tensor)"
+        line = {"metric": metric_name(args.config), "value": ms, "unit": "ms/iter", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": dict(config_block(args, layers), parallelism=f"dp{world}"),
+                "stages_ms": stages,
+                "factor_precond_tflops": (wm["fac_flops"] + wm["pc_flops"]) / ((stages["factors"] + stages["precond"]) * 1e-3) / 1e12,
+                "eigen_info": info[:8],
+                "roofline": roof, "gpu_launches": int(launches),
+                "clocks": clk.summary(), "e2e": e2e}
+        if not args.no_cpu_baseline and world == 1:
+            import oracle
+            oracle.build()
+            est, det = oracle_sample(layers, hp, args.seed, SAMPLE[args.config])
+            line["cpu_baseline"] = {"value": est * 1e3, "unit": "ms/iter", "cores": len(os.sched_getaffinity(0)),
+                                    "kind": "oracle",
+                                    "sample": f"oracle on layers {det['names']}, per-stage times scaled by "
+                                              f"algorithmic work to all {len(layers)} layers; measured "
+                                              f"{det['factors_s']:.1f}/{det['eigen_s']:.1f}/{det['precond_s']:.1f} s"}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)

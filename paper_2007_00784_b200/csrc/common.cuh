@@ -1,0 +1,74 @@
+// common.cuh -- shared host/device helpers of libkfac (CUDA path only).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include <atomic>
+#include <string>
+
+#include "kfac.h"
+
+namespace kfac {
+
+// ---------------------------------------------------------------- errors --
+void set_error(const std::string &msg);
+std::atomic<uint64_t> &launch_counter();
+
+struct Status {
+    kfac_status_t code;
+};
+
+#define KFAC_CHECK_ARG(cond, code, ...)                                   \
+    do {                                                                  \
+        if (!(cond)) {                                                    \
+            char _buf[512];                                               \
+            snprintf(_buf, sizeof(_buf), __VA_ARGS__);                    \
+            ::kfac::set_error(_buf);                                      \
+            return code;                                                  \
+        }                                                                 \
+    } while (0)
+
+#define KFAC_CUDA_TRY(expr)                                                        \
+    do {                                                                           \
+        cudaError_t _e = (expr);                                                   \
+        if (_e != cudaSuccess) {                                                   \
+            ::kfac::set_error(std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+            return KFAC_ERR_CUDA;                                                  \
+        }                                                                          \
+    } while (0)
+
+// Count and check one launch (call right after <<<>>>).
+#define KFAC_LAUNCHED()                                                            \
+    do {                                                                           \
+        ::kfac::launch_counter().fetch_add(1, std::memory_order_relaxed);          \
+        cudaError_t _e = cudaGetLastError();                                       \
+        if (_e != cudaSuccess) {                                                   \
+            ::kfac::set_error(std::string("kernel launch: ") + cudaGetErrorString(_e)); \
+            return KFAC_ERR_CUDA;                                                  \
+        }                                                                          \
+    } while (0)
+
+inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+inline size_t round_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+// Bump allocator over the caller's workspace (256-byte aligned slices).
+struct WsArena {
+    char *base;
+    size_t cap, off = 0;
+    WsArena(void *p, size_t n) : base(static_cast<char *>(p)), cap(n) {}
+    template <class T>
+    T *take(size_t count) {
+        off = round_up(off, 256);
+        T *p = reinterpret_cast<T *>(base ? base + off : nullptr);
+        off += count * sizeof(T);
+        return p;
+    }
+    bool ok() const { return off <= cap; }
+};
+
+int num_sms();   // cached multiprocessor count of the current device
+
+}  // namespace kfac

@@ -1,0 +1,307 @@
+// factors.cu -- Stage 1 of Alg. 1: Kronecker factors and their running average.
+//
+//   A_batch = X^T X / n, X = [im2col(a_{i-1}) | 1]   (Eq. 5; im2col fused into the loads)
+//   G_batch = g^T g / n                                (Eq. 5)
+//   F = first ? F_batch : decay F + (1 - decay) F_batch;  F *= out_scale   (Eqs. 16-17, R5)
+//
+// Two launches per group of factors:
+//   syrk_partial : one CTA per (upper-triangle 128x128 tile, row chunk); im2col patches are
+//                  gathered straight from the NHWC activations (never materialised) and the
+//                  symmetric rank-k update is accumulated for the chunk;
+//   syrk_reduce  : sums the chunk partials in a fixed order (deterministic, no atomics),
+//                  applies 1/n, the running average and out_scale, and writes both triangles.
+// The SIMT tile is the numerics baseline; the tcgen05 3xTF32 SYRK replaces the partial kernel
+// for large factors.
+#include "internal.cuh"
+
+#include <vector>
+
+namespace kfac {
+namespace {
+
+constexpr int T = 128, BK = 16, NT = 256;
+constexpr int kChunkRows = 4096;
+constexpr int kMaxJobs = 64;
+
+struct FactorJob {
+    const float *src;       // act (NHWC) for A, gout for G
+    float *F;
+    float *partial;         // [splits][tiles][T*T]
+    long long n;            // rows
+    int ldF, d, is_a;
+    int splits, chunk, t1d, tiles, item_begin, tile_begin;
+    // im2col geometry (A factor); for G: c_in = d (row length of gout)
+    int c_in, h_in, w_in, h_out, w_out, k_w, stride_h, stride_w, pad_h, pad_w;
+    int patch_cols, bias_col;
+};
+
+struct FactorBatch {
+    int count;
+    float decay, out_scale;
+    int first;
+    FactorJob j[kMaxJobs];
+};
+
+__device__ __forceinline__ int find_job(const FactorBatch &b, int item, bool by_tile) {
+    int lo = 0, hi = b.count - 1;
+    while (lo < hi) {
+        int mid = (lo + hi + 1) >> 1;
+        int beg = by_tile ? b.j[mid].tile_begin : b.j[mid].item_begin;
+        if (beg <= item) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ void upper_tile(int tau, int t1d, int &ti, int &tj) {
+    int i = 0;
+    while (tau >= t1d - i) { tau -= t1d - i; ++i; }
+    ti = i;
+    tj = i + tau;
+}
+
+// Per-column gather descriptor: offset inside the receptive field and (kh, kw) for bounds.
+struct ColInfo {
+    int off, kh, kw, kind;   // kind: 0 regular, 1 bias (constant 1), 2 outside d (0)
+};
+
+__device__ __forceinline__ ColInfo col_info(const FactorJob &J, int c) {
+    ColInfo ci;
+    if (c >= J.d) { ci.kind = 2; ci.off = ci.kh = ci.kw = 0; return ci; }
+    if (!J.is_a) { ci.kind = 0; ci.off = c; ci.kh = ci.kw = 0; return ci; }
+    if (c >= J.patch_cols) { ci.kind = 1; ci.off = ci.kh = ci.kw = 0; return ci; }
+    const int kwc = J.k_w * J.c_in;
+    ci.kh = c / kwc;
+    const int rem = c - ci.kh * kwc;
+    ci.kw = rem / J.c_in;
+    const int ch = rem - ci.kw * J.c_in;
+    ci.off = (ci.kh * J.w_in + ci.kw) * J.c_in + ch;
+    ci.kind = 0;
+    return ci;
+}
+
+__global__ void __launch_bounds__(NT) syrk_partial_kernel(const __grid_constant__ FactorBatch batch) {
+    __shared__ float As[2][BK][T + 4];
+    __shared__ float Bs[2][BK][T + 4];
+    const int item = blockIdx.x;
+    const FactorJob &J = batch.j[find_job(batch, item, false)];
+    const int local = item - J.item_begin;
+    const int tau = local / J.splits, split = local % J.splits;
+    int ti, tj;
+    upper_tile(tau, J.t1d, ti, tj);
+    const int t = threadIdx.x;
+    const int lr = t / 16, lc = (t % 16) * 8;        // loader: row lr of the slab, 8 columns
+    ColInfo ca[8], cb[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        ca[i] = col_info(J, ti * T + lc + i);
+        cb[i] = col_info(J, tj * T + lc + i);
+    }
+    const long long r_begin = (long long)split * J.chunk;
+    const long long r_end = min(J.n, r_begin + J.chunk);
+    const int hw = J.h_out * J.w_out;
+
+    float ra[8], rb[8];
+    auto load = [&](long long r0) {
+        const long long r = r0 + lr;
+        const bool rv = r < r_end;
+        if (!J.is_a) {
+            const float *row = J.src + r * J.c_in;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                ra[i] = (rv && ca[i].kind == 0) ? __ldg(row + ca[i].off) : 0.f;
+                rb[i] = (rv && cb[i].kind == 0) ? __ldg(row + cb[i].off) : 0.f;
+            }
+            return;
+        }
+        int img = 0, oh = 0, ow = 0;
+        if (rv) {
+            img = (int)(r / hw);
+            const int p = (int)(r - (long long)img * hw);
+            oh = p / J.w_out;
+            ow = p - oh * J.w_out;
+        }
+        const int ih0 = oh * J.stride_h - J.pad_h, iw0 = ow * J.stride_w - J.pad_w;
+        const float *base = J.src + (((long long)img * J.h_in + ih0) * J.w_in + iw0) * J.c_in;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            float va = 0.f, vb = 0.f;
+            if (rv) {
+                if (ca[i].kind == 1) va = 1.f;
+                else if (ca[i].kind == 0) {
+                    const int ih = ih0 + ca[i].kh, iw = iw0 + ca[i].kw;
+                    if (ih >= 0 && ih < J.h_in && iw >= 0 && iw < J.w_in) va = __ldg(base + ca[i].off);
+                }
+                if (cb[i].kind == 1) vb = 1.f;
+                else if (cb[i].kind == 0) {
+                    const int ih = ih0 + cb[i].kh, iw = iw0 + cb[i].kw;
+                    if (ih >= 0 && ih < J.h_in && iw >= 0 && iw < J.w_in) vb = __ldg(base + cb[i].off);
+                }
+            }
+            ra[i] = va;
+            rb[i] = vb;
+        }
+    };
+    auto store = [&](int buf) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            As[buf][lr][lc + i] = ra[i];
+            Bs[buf][lr][lc + i] = rb[i];
+        }
+    };
+
+    float acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+    const int ty = t / 16, tx = t % 16;
+    const int nk = (int)((r_end - r_begin + BK - 1) / BK);
+    load(r_begin);
+    store(0);
+    __syncthreads();
+    for (int kt = 0; kt < nk; ++kt) {
+        const int buf = kt & 1;
+        if (kt + 1 < nk) load(r_begin + (long long)(kt + 1) * BK);
+#pragma unroll
+        for (int k = 0; k < BK; ++k) {
+            float a[8], b[8];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                a[i] = As[buf][k][ty * 4 + i];
+                a[4 + i] = As[buf][k][64 + ty * 4 + i];
+                b[i] = Bs[buf][k][tx * 4 + i];
+                b[4 + i] = Bs[buf][k][64 + tx * 4 + i];
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+        }
+        if (kt + 1 < nk) {
+            store(buf ^ 1);
+            __syncthreads();
+        }
+    }
+    float *out = J.partial + ((size_t)split * J.tiles + tau) * (T * T);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int m = i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4);
+        float4 *dst = reinterpret_cast<float4 *>(out + m * T);
+        dst[tx] = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+        dst[16 + tx] = make_float4(acc[i][4], acc[i][5], acc[i][6], acc[i][7]);
+    }
+}
+
+// One CTA (32x8 threads) per 32x32 sub-tile of an upper 128x128 tile.
+__global__ void __launch_bounds__(256) syrk_reduce_kernel(const __grid_constant__ FactorBatch batch) {
+    __shared__ float tr[32][33];
+    const int blk = blockIdx.x;                  // tile_begin counts sub-tiles (16 per tile)
+    const FactorJob &J = batch.j[find_job(batch, blk, true)];
+    const int local = blk - J.tile_begin;
+    const int tau = local / 16, sub = local % 16;
+    int ti, tj;
+    upper_tile(tau, J.t1d, ti, tj);
+    const int si = sub / 4, sj = sub % 4;
+    if (ti == tj && si > sj) return;             // the (sj, si) sub-tile writes both copies
+    const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;
+    const float inv_n = 1.0f / (float)J.n;
+    const int gj = tj * T + sj * 32 + tx;
+    for (int rr = ty; rr < 32; rr += 8) {
+        const int li = si * 32 + rr, lj = sj * 32 + tx;
+        const int gi = ti * T + li;
+        float s = 0.f;
+        for (int sp = 0; sp < J.splits; ++sp)
+            s += J.partial[((size_t)sp * J.tiles + tau) * (T * T) + li * T + lj];
+        float v = s * inv_n;
+        if (gi < J.d && gj < J.d) {
+            float *dst = J.F + (size_t)gi * J.ldF + gj;
+            if (!batch.first) v = batch.decay * (*dst) + (1.f - batch.decay) * v;
+            v *= batch.out_scale;
+            *dst = v;
+        }
+        tr[rr][tx] = v;
+    }
+    if (ti == tj && si == sj) return;            // diagonal sub-tile already holds both triangles
+    __syncthreads();
+    const int gcol = ti * T + si * 32 + tx;      // mirrored write: F[gj][gi]
+    for (int rr = ty; rr < 32; rr += 8) {
+        const int grow = tj * T + sj * 32 + rr;
+        if (grow < J.d && gcol < J.d) J.F[(size_t)grow * J.ldF + gcol] = tr[tx][rr];
+    }
+}
+
+struct Plan {
+    std::vector<FactorJob> jobs;
+    size_t partial_floats = 0;
+};
+
+Plan make_plan(const kfac_layer_t *layers, int nl, float *const *A, const int32_t *ldA,
+               float *const *G, const int32_t *ldG, const float *const *act,
+               const float *const *gout) {
+    Plan p;
+    for (int l = 0; l < nl; ++l) {
+        const kfac_layer_t &L = layers[l];
+        for (int f = 0; f < 2; ++f) {
+            FactorJob j{};
+            j.is_a = f == 0;
+            j.n = (long long)L.batch * L.h_out * L.w_out;
+            j.d = j.is_a ? L.c_in * L.k_h * L.k_w + L.bias_col : L.c_out;
+            j.src = act ? (j.is_a ? act[l] : gout[l]) : nullptr;
+            j.F = A ? (j.is_a ? A[l] : G[l]) : nullptr;
+            j.ldF = ldA ? (j.is_a ? ldA[l] : ldG[l]) : 0;
+            j.c_in = j.is_a ? L.c_in : L.c_out;
+            j.h_in = L.h_in; j.w_in = L.w_in; j.h_out = L.h_out; j.w_out = L.w_out;
+            j.k_w = L.k_w; j.stride_h = L.stride_h; j.stride_w = L.stride_w;
+            j.pad_h = L.pad_h; j.pad_w = L.pad_w;
+            j.patch_cols = L.c_in * L.k_h * L.k_w;
+            j.bias_col = L.bias_col;
+            j.chunk = kChunkRows;
+            j.splits = (int)((j.n + kChunkRows - 1) / kChunkRows);
+            j.t1d = cdiv(j.d, T);
+            j.tiles = j.t1d * (j.t1d + 1) / 2;
+            j.partial = reinterpret_cast<float *>(p.partial_floats);   // offset, rebased later
+            p.partial_floats += (size_t)j.splits * j.tiles * T * T;
+            p.jobs.push_back(j);
+        }
+    }
+    return p;
+}
+
+}  // namespace
+
+size_t factors_workspace_bytes(const kfac_layer_t *layers, int nl) {
+    Plan p = make_plan(layers, nl, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
+    return p.partial_floats * sizeof(float) + 256;
+}
+
+kfac_status_t factors_run(const kfac_layer_t *layers, int nl, const float *const *act,
+                          const float *const *gout, float *const *A, const int32_t *ldA,
+                          float *const *G, const int32_t *ldG, float decay, int first,
+                          float out_scale, void *ws, cudaStream_t s) {
+    Plan p = make_plan(layers, nl, A, ldA, G, ldG, act, gout);
+    float *base = reinterpret_cast<float *>(round_up(reinterpret_cast<uintptr_t>(ws), 256));
+    for (auto &j : p.jobs) j.partial = base + reinterpret_cast<uintptr_t>(j.partial);
+    for (size_t b0 = 0; b0 < p.jobs.size(); b0 += kMaxJobs) {
+        FactorBatch fb;
+        fb.count = 0;
+        fb.decay = decay;
+        fb.out_scale = out_scale;
+        fb.first = first;
+        int items = 0, subtiles = 0;
+        for (size_t i = b0; i < p.jobs.size() && fb.count < kMaxJobs; ++i) {
+            FactorJob j = p.jobs[i];
+            j.item_begin = items;
+            j.tile_begin = subtiles;
+            items += j.tiles * j.splits;
+            subtiles += j.tiles * 16;
+            fb.j[fb.count++] = j;
+        }
+        syrk_partial_kernel<<<items, NT, 0, s>>>(fb);
+        KFAC_LAUNCHED();
+        syrk_reduce_kernel<<<subtiles, 256, 0, s>>>(fb);
+        KFAC_LAUNCHED();
+    }
+    return KFAC_OK;
+}
+
+}  // namespace kfac

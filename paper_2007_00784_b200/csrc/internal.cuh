@@ -1,0 +1,51 @@
+// internal.cuh -- launchers shared between the libkfac translation units.
+#pragma once
+
+#include "common.cuh"
+
+namespace kfac {
+
+// ----------------------------------------------------------- grouped GEMM --
+// C = op(A) op(B) (+ epilogue), fp32 in/out.  op(A) is M x K, op(B) is K x N.
+//   trans_a = 0: A[m*lda + k]   trans_a = 1: A[k*lda + m]
+//   trans_b = 0: B[k*ldb + n]   trans_b = 1: B[n*ldb + k]
+enum GemmEpi : int {
+    EPI_STORE = 0,
+    EPI_DIV_EIGEN = 1,      // C /= max(vr[m]*vc[n] + damping, 1e-12)        (Eq. 14)
+    EPI_DIV_FACTORED = 2,   // C /= max((vr[m]+damping)*(vc[n]+damping), 1e-12)
+};
+
+struct GemmDesc {
+    const float *A;
+    const float *B;
+    float *C;
+    const float *vr;
+    const float *vc;
+    int M, N, K;
+    int lda, ldb, ldc;
+    int trans_a, trans_b, epi;
+    int tile_begin;          // filled by the launcher
+};
+
+constexpr int kGemmMaxDescs = 64;
+
+struct GemmBatch {
+    int count;
+    int tiles_total;
+    float damping;
+    GemmDesc d[kGemmMaxDescs];
+};
+
+// SIMT fp32 grouped GEMM (any shape/transposition); used for small/ragged
+// problems and as the numerics baseline of the tensor-core path.
+kfac_status_t gemm_simt_grouped(const GemmDesc *descs, int count, float damping, cudaStream_t s);
+
+// Tensor-core (tcgen05, kind::tf32, 3xTF32) grouped GEMM.  Returns
+// KFAC_ERR_UNSUPPORTED if a descriptor does not meet its layout rules.
+kfac_status_t gemm_tc_grouped(const GemmDesc *descs, int count, float damping, cudaStream_t s);
+bool gemm_tc_supported(const GemmDesc &d);
+
+// Dispatch each descriptor to the tensor-core or SIMT engine.
+kfac_status_t gemm_grouped(const GemmDesc *descs, int count, float damping, cudaStream_t s);
+
+}  // namespace kfac

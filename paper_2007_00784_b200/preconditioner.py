@@ -1,0 +1,204 @@
+"""KFACPreconditioner: device buffers + Alg. 1 orchestration over the C-ABI calls.
+
+One process per GPU.  Every arithmetic step runs in libkfac's CUDA kernels
+(`_lib`); this module owns the buffers (torch CUDA tensors), decides which
+calls to make, and issues the collectives through torch.distributed:
+
+  step 1  kfac_update_factors (all layers, local mini-batch), then ONE allreduce
+          of the flat factor buffer (out_scale = 1/W fused into the kernel,
+          SUM on the wire) -- Alg. 1
+  step 2  kfac_assign (host, identical on all ranks) -> kfac_compute_eigen on the
+          owned factors -> exchange:
+            K-FAC-opt ("bcast-eig"): all-gather of the eigenbases, laid out
+              owner-major so each rank's slice is contiguous (no packing);
+            K-FAC-lw ("allgather-grad"): layer owners keep their
+              eigenbases and the preconditioned gradients are all-gathered.
+  step 3  kfac_precondition (Eqs. 13-15) and kfac_kl_clip (Eq. 18).
+
+Buffers are allocated once, in the layout the collectives need, so no copy
+kernel is issued on the path.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import List, Optional
+
+import torch
+import torch.distributed as dist
+
+from . import _lib
+
+
+def _ld(d: int) -> int:
+    return (d + 3) // 4 * 4
+
+
+def _aligned(n: int) -> int:          # keep every matrix 256-byte aligned inside flat buffers
+    return (n + 63) // 64 * 64
+
+
+@dataclass
+class Segment:
+    offset: int
+    rows: int
+    cols: int
+    ld: int
+
+    @property
+    def numel(self):
+        return _aligned(self.rows * self.ld)
+
+
+def _views(flat: torch.Tensor, segs: List[Segment]) -> List[torch.Tensor]:
+    return [flat[s.offset:s.offset + s.rows * s.ld].view(s.rows, s.ld)[:, :s.cols] for s in segs]
+
+
+class KFACPreconditioner:
+    def __init__(self, layers, device=None, damping: float = 1e-3, decay: float = 0.95,
+                 kappa: float = 1e-3, lr: float = 0.1, variant: str = "eigen",
+                 exchange: str = "bcast-eig", assign_policy: int = _lib.LPT_D3,
+                 process_group=None):
+        self.layers = list(layers)
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.damping, self.decay, self.kappa, self.lr = damping, decay, kappa, lr
+        assert variant in ("eigen", "factored", "inverse")
+        assert exchange in ("bcast-eig", "allgather-grad")
+        self.variant, self.exchange = variant, exchange
+        self.pg = process_group
+        self.world = dist.get_world_size(process_group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(process_group) if dist.is_initialized() else 0
+        L = len(self.layers)
+        self.d_a = [l.d_a for l in self.layers]
+        self.d_g = [l.d_g for l in self.layers]
+        self.dims = [d for l in self.layers for d in (l.d_a, l.d_g)]       # [A0, G0, A1, G1, ...]
+        self.layer_of = [i for i in range(L) for _ in range(2)]
+        policy = _lib.LAYERWISE_LPT if exchange == "allgather-grad" else assign_policy
+        self.owner = _lib.kfac_assign(self.dims, self.layer_of, L, self.world, policy)
+        self.layer_owner = [self.owner[2 * i] for i in range(L)]
+
+        f32 = dict(dtype=torch.float32, device=self.device)
+        # factors: flat, factor order, all-reduced as one message
+        off, self.fseg = 0, []
+        for d in self.dims:
+            s = Segment(off, d, d, _ld(d))
+            self.fseg.append(s)
+            off += s.numel
+        self.factor_flat = torch.zeros(off, **f32)
+        self.F = _views(self.factor_flat, self.fseg)
+        self.A = self.F[0::2]
+        self.G = self.F[1::2]
+        # eigenbases / inverses: owner-major, one equal-size slice per rank (all-gather in place)
+        per_rank = [[f for f in range(len(self.dims)) if self.owner[f] == r] for r in range(self.world)]
+        q_sizes = [sum(_aligned(self.dims[f] * _ld(self.dims[f])) for f in fs) for fs in per_rank]
+        v_sizes = [sum(_aligned(self.dims[f]) for f in fs) for fs in per_rank]
+        self.q_slice, self.v_slice = max(q_sizes + [64]), max(v_sizes + [64])
+        self.q_flat = torch.zeros(self.q_slice * self.world, **f32)
+        self.v_flat = torch.zeros(self.v_slice * self.world, **f32)
+        self.qseg, self.vseg = [None] * len(self.dims), [None] * len(self.dims)
+        for r, fs in enumerate(per_rank):
+            qo, vo = r * self.q_slice, r * self.v_slice
+            for f in fs:
+                d = self.dims[f]
+                self.qseg[f] = Segment(qo, d, d, _ld(d))
+                qo += self.qseg[f].numel
+                self.vseg[f] = Segment(vo, 1, d, _aligned(d))
+                vo += _aligned(d)
+        self.Q = _views(self.q_flat, self.qseg)
+        self.v = [self.v_flat[s.offset:s.offset + s.cols] for s in self.vseg]
+        self.owned = per_rank[self.rank]
+        self.info = torch.zeros(max(1, len(self.owned)), dtype=torch.int32, device=self.device)
+        # preconditioned gradients: owner-major by layer (K-FAC-lw all-gathers them in place)
+        per_rank_l = [[i for i in range(L) if self.layer_owner[i] == r] for r in range(self.world)]
+        p_sizes = [sum(_aligned(self.d_g[i] * _ld(self.d_a[i])) for i in ls) for ls in per_rank_l]
+        self.p_slice = max(p_sizes + [64])
+        self.p_flat = torch.zeros(self.p_slice * self.world, **f32)
+        self.pseg = [None] * L
+        for r, ls in enumerate(per_rank_l):
+            o = r * self.p_slice
+            for i in ls:
+                self.pseg[i] = Segment(o, self.d_g[i], self.d_a[i], _ld(self.d_a[i]))
+                o += self.pseg[i].numel
+        self.P = _views(self.p_flat, self.pseg)
+        self.owned_layers = per_rank_l[self.rank]
+        self.nu = torch.ones(1, **f32)
+        self.s = torch.zeros(1, dtype=torch.float64, device=self.device)
+        self.ws = {k: _lib.Workspace(self.device) for k in ("factors", "eigen", "precond", "klclip")}
+        self.have_eigen = False
+
+    # ------------------------------------------------------------ helpers --
+    @staticmethod
+    def grad_buffer(layers, device=None, return_flat=False):
+        """Padded (d_G x ld) gradient views of one flat buffer, in the layout kfac_precondition
+        expects (the flat buffer is what a data-parallel gradient allreduce would reduce)."""
+        segs, off = [], 0
+        for l in layers:
+            s = Segment(off, l.d_g, l.d_a, _ld(l.d_a))
+            segs.append(s)
+            off += s.numel
+        flat = torch.zeros(off, dtype=torch.float32, device=device)
+        views = _views(flat, segs)
+        return (views, flat) if return_flat else views
+
+    # -------------------------------------------------------------- steps --
+    def update_factors(self, acts, gouts, first: bool):
+        """Alg. 1 step 1: local factors + running average, then the factor allreduce."""
+        _lib.kfac_update_factors(self.layers, acts, gouts, self.A, self.G, self.decay, first,
+                                 1.0 / self.world, ws=self.ws["factors"])
+        if self.world > 1:
+            dist.all_reduce(self.factor_flat, op=dist.ReduceOp.SUM, group=self.pg)
+
+    def compute_eigen(self, warm: bool = False):
+        """Alg. 1 step 2 on the owned factors, then the exchange of the results."""
+        if self.owned:
+            F = [self.F[f] for f in self.owned]
+            Q = [self.Q[f] for f in self.owned]
+            if self.variant == "inverse":
+                _lib.kfac_compute_inverse(F, self.damping, Q, self.info, ws=self.ws["eigen"])
+            else:
+                flags = _lib.EIG_WARM_START if (warm and self.have_eigen) else 0
+                _lib.kfac_compute_eigen(F, Q, [self.v[f] for f in self.owned], self.info, flags,
+                                        ws=self.ws["eigen"])
+        self.have_eigen = True
+        if self.world > 1 and self.exchange == "bcast-eig":
+            all_gather_inplace(self.q_flat, self.q_slice, self.pg)
+            if self.variant != "inverse":
+                all_gather_inplace(self.v_flat, self.v_slice, self.pg)
+
+    def precondition(self, grads: List[torch.Tensor]) -> List[torch.Tensor]:
+        """Alg. 1 step 3 (Eqs. 13-15 / Eq. 12) followed by the KL-clip (Eq. 18)."""
+        mode = {"eigen": _lib.EIGEN, "factored": _lib.EIGEN_FACTORED, "inverse": _lib.INVERSE}[self.variant]
+        layers = range(len(self.layers)) if (self.world == 1 or self.exchange == "bcast-eig") \
+            else self.owned_layers
+        layers = list(layers)
+        if layers:
+            g = [grads[i] for i in layers]
+            QG = [self.Q[2 * i + 1] for i in layers]
+            QA = [self.Q[2 * i] for i in layers]
+            vG = vA = None
+            if mode != _lib.INVERSE:
+                vG = [self.v[2 * i + 1] for i in layers]
+                vA = [self.v[2 * i] for i in layers]
+            _lib.kfac_precondition(g, QG, vG, QA, vA, self.damping, mode, [self.P[i] for i in layers],
+                                   ws=self.ws["precond"])
+        if self.world > 1 and self.exchange == "allgather-grad":
+            all_gather_inplace(self.p_flat, self.p_slice, self.pg)
+        _lib.kfac_kl_clip(self.P, grads, self.lr, self.kappa, self.nu, self.s, ws=self.ws["klclip"])
+        return self.P
+
+    def step(self, acts, gouts, grads, update_factors=True, update_eigen=True, first=False, warm=False):
+        if update_factors:
+            self.update_factors(acts, gouts, first)
+        if update_eigen or not self.have_eigen:
+            self.compute_eigen(warm=warm)
+        return self.precondition(grads)
+
+
+def all_gather_inplace(flat: torch.Tensor, slice_numel: int, group=None):
+    """Every rank contributes flat[rank*slice:(rank+1)*slice]; afterwards all ranks hold all slices."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    mine = flat[rank * slice_numel:(rank + 1) * slice_numel]
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(flat, mine, group=group)
+    else:
+        dist.all_gather(list(flat.split(slice_numel)), mine.clone(), group=group)
