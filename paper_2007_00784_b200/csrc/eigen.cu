@@ -3,12 +3,14 @@
 // Batched one-sided block Jacobi (Hestenes) on U = F V, V orthogonal:
 //   * columns are split into blocks of 16; a parallel round-robin tournament pairs the blocks so
 //     every round is a set of disjoint 32-column pairs (one CTA each, all factors batched);
-//   * per pair: Gram G = U_pq^T U_pq in fp64, its 32x32 eigenproblem G = R D R^T solved by
-//     cyclic Jacobi in shared memory (fp64), then U_pq <- U_pq R and V_pq <- V_pq R;
+//   * per pair: Gram G = U_pq^T U_pq, its 32x32 eigenproblem G = R D R^T solved by cyclic
+//     Jacobi in shared memory, then U_pq <- U_pq R and V_pq <- V_pq R -- all in fp64 with U, V
+//     stored in fp64, so U = F V holds to fp64 rounding and the null-space eigenvectors of
+//     rank-deficient factors are not polluted by fp32 drift (ResNet-50 fc at 32 rows/GPU);
 //   * a pair whose columns are already orthogonal to tol is skipped; a sweep with no rotation
 //     marks the factor converged (device flag, no host synchronisation);
-//   * at the end eigenvalues are Rayleigh quotients v_j^T F v_j of the ORIGINAL factor
-//     (fp64 accumulation), clamped at 0 (R10), and (Q, v) are sorted ascending.
+//   * at the end eigenvalues are Rayleigh quotients v_j^T u_j = v_j^T F v_j (fp64), clamped at 0
+//     (R10), and (Q, v) are sorted ascending and rounded to fp32.
 // Why Jacobi: fully parallel across pairs and factors, robust to the
 // huge zero-eigenvalue clusters of rank-deficient conv factors (R11), and warm-startable from
 // the previous (stale) eigenbasis (KFAC_EIG_WARM_START).
@@ -31,20 +33,21 @@ constexpr int P = 2 * B;         // columns per pair
 constexpr int NT = 256;
 constexpr int kMaxSweeps = 16;
 constexpr int kTableChunk = 48;
+constexpr int kInnerSweeps = 6;
 
 struct EigJob {
     const float *F;
     float *Q;
     float *evals;
-    float *U;        // n x ldu
-    float *V;        // n x ldu
+    double *U;       // n x ldu  (U = F V)
+    double *V;       // n x ldu
     double *lam;     // n
     int *rank;       // n
     int *info;       // device (caller)
     int n, ldF, ldQ, ldu, nb;      // nb: number of blocks incl. the dummy (even)
     int pair_begin;                // prefix over jobs (sorted by nb descending)
     int rot_count, converged, sweeps;
-    float scale;                   // trace(F) (PSD: >= ||F||_2)
+    float scale;                   // ||F||_F (>= ||F||_2)
 };
 
 struct EigTableInit {
@@ -58,7 +61,7 @@ __global__ void eig_table_init(const __grid_constant__ EigTableInit t) {
     if (i < t.count) t.table[t.base + i] = t.j[i];
 }
 
-// U = (F + F^T)/2 (or keep U from the warm-start GEMM), V = I (or Q_in); pads zeroed; scale = trace.
+// U = (F + F^T)/2 (or keep U from the warm-start GEMM), V = I (or Q_in); pads zeroed; scale = ||F||_F.
 __global__ void eig_init(EigJob *table, int warm) {
     EigJob &J = table[blockIdx.y];
     const int n = J.n, ldu = J.ldu;
@@ -67,19 +70,19 @@ __global__ void eig_init(EigJob *table, int warm) {
          e += (long long)gridDim.x * blockDim.x) {
         const int r = (int)(e / ldu), c = (int)(e % ldu);
         if (!warm) {
-            float u = 0.f;
-            if (c < n) u = 0.5f * (J.F[(size_t)r * J.ldF + c] + J.F[(size_t)c * J.ldF + r]);
+            double u = 0.0;
+            if (c < n) u = 0.5 * ((double)J.F[(size_t)r * J.ldF + c] + (double)J.F[(size_t)c * J.ldF + r]);
             J.U[e] = u;
-            J.V[e] = (r == c) ? 1.f : 0.f;
+            J.V[e] = (r == c) ? 1.0 : 0.0;
         } else {
-            J.V[e] = (c < n) ? J.Q[(size_t)r * J.ldQ + c] : 0.f;
-            if (c >= n) J.U[e] = 0.f;
+            J.V[e] = (c < n) ? (double)J.Q[(size_t)r * J.ldQ + c] : 0.0;
+            if (c >= n) J.U[e] = 0.0;
         }
     }
     if (blockIdx.x == 0) {
         __shared__ double red[NT];
         double s = 0.0;
-        for (int i = threadIdx.x; i < n; i += blockDim.x) s += J.F[(size_t)i * J.ldF + i];
+        for (int i = threadIdx.x; i < n; i += blockDim.x) s += J.lam[i];   // row sums of squares
         red[threadIdx.x] = s;
         __syncthreads();
         for (int w = NT / 2; w > 0; w >>= 1) {
@@ -87,12 +90,27 @@ __global__ void eig_init(EigJob *table, int warm) {
             __syncthreads();
         }
         if (threadIdx.x == 0) {
-            J.scale = (float)red[0];
+            J.scale = (float)sqrt(red[0]);
             J.rot_count = 0;
             J.converged = 0;
             J.sweeps = 0;
         }
     }
+}
+
+// lam[r] = sum_c F[r][c]^2 (one warp per row, fixed order) -- feeds ||F||_F in eig_init.
+__global__ void eig_rownorm(EigJob *table) {
+    EigJob &J = table[blockIdx.y];
+    const int r = blockIdx.x * 8 + threadIdx.x / 32, lane = threadIdx.x % 32;
+    if (r >= J.n) return;
+    double s = 0.0;
+    for (int c = lane; c < J.n; c += 32) {
+        const double x = J.F[(size_t)r * J.ldF + c];
+        s += x * x;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) J.lam[r] = s;
 }
 
 // Round-robin ("circle") tournament: pair k of round r among m players (m even).
@@ -109,11 +127,11 @@ __device__ __forceinline__ void schur2(double app, double aqq, double apq, doubl
     s = t * c;
 }
 
-__global__ void __launch_bounds__(NT) eig_round(EigJob *table, int count, int round, float tol) {
-    __shared__ float tile[64][P + 1];
+__global__ void __launch_bounds__(NT, 2) eig_round(EigJob *table, int count, int round, float tol,
+                                                float tol_abs) {
+    __shared__ double tile[32][P + 1];
     __shared__ double G[P][P + 1];
     __shared__ double R[P][P + 1];
-    __shared__ float Rf[P][P];
     __shared__ double cs_c[P / 2], cs_s[P / 2];
     __shared__ int cs_i[P / 2], cs_j[P / 2];
     __shared__ int col0[2];
@@ -141,59 +159,63 @@ __global__ void __launch_bounds__(NT) eig_round(EigJob *table, int count, int ro
     __syncthreads();
     const int c0 = col0[0], c1 = col0[1];
 
-    // ---- Gram G = U_pq^T U_pq, fp64 accumulation (upper triangle, 528 entries) ----
-    double acc[3] = {0.0, 0.0, 0.0};
-    int ei[3], ej[3];
-#pragma unroll
-    for (int q = 0; q < 3; ++q) {
-        int e = t + q * NT;            // upper-triangle index -> (i, j), i <= j
-        int i = 0;
-        while (e >= P - i && i < P) { e -= P - i; ++i; }
-        ei[q] = i;
-        ej[q] = i + e;
-    }
-    for (int r0 = 0; r0 < n; r0 += 64) {
-        for (int e = t; e < 64 * (P / 4); e += NT) {       // 64 rows x 8 float4
-            const int rr = e / (P / 4), g = e % (P / 4);
+    // ---- Gram G = U_pq^T U_pq (fp64): thread t owns the 2x2 block (2*(t/16), 2*(t%16)) ----
+    const int gi = 2 * (t / 16), gj = 2 * (t % 16);
+    double a00 = 0.0, a01 = 0.0, a10 = 0.0, a11 = 0.0;
+    for (int r0 = 0; r0 < n; r0 += 32) {
+        for (int e = t; e < 32 * (P / 2); e += NT) {       // 32 rows x 16 double2
+            const int rr = e / (P / 2), g = e % (P / 2);
             const int r = r0 + rr;
-            const int cb = (g < B / 4) ? c0 : c1;
-            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (r < n && cb >= 0) v = *reinterpret_cast<const float4 *>(J.U + (size_t)r * ldu + cb + (g % (B / 4)) * 4);
-            tile[rr][g * 4 + 0] = v.x; tile[rr][g * 4 + 1] = v.y;
-            tile[rr][g * 4 + 2] = v.z; tile[rr][g * 4 + 3] = v.w;
+            const int cb = (g < B / 2) ? c0 : c1;
+            double2 v = make_double2(0.0, 0.0);
+            if (r < n && cb >= 0) v = *reinterpret_cast<const double2 *>(J.U + (size_t)r * ldu + cb + (g % (B / 2)) * 2);
+            tile[rr][2 * g] = v.x;
+            tile[rr][2 * g + 1] = v.y;
         }
         __syncthreads();
-        const int rows = min(64, n - r0);
-#pragma unroll
-        for (int q = 0; q < 3; ++q) {
-            if (ei[q] >= P) continue;
-            double a = acc[q];
-            for (int rr = 0; rr < rows; ++rr) a += (double)tile[rr][ei[q]] * (double)tile[rr][ej[q]];
-            acc[q] = a;
+        const int rows = min(32, n - r0);
+        for (int rr = 0; rr < rows; ++rr) {
+            const double x0 = tile[rr][gi], x1 = tile[rr][gi + 1];
+            const double y0 = tile[rr][gj], y1 = tile[rr][gj + 1];
+            a00 = fma(x0, y0, a00); a01 = fma(x0, y1, a01);
+            a10 = fma(x1, y0, a10); a11 = fma(x1, y1, a11);
         }
         __syncthreads();
     }
-#pragma unroll
-    for (int q = 0; q < 3; ++q)
-        if (ei[q] < P) { G[ei[q]][ej[q]] = acc[q]; G[ej[q]][ei[q]] = acc[q]; }
+    G[gi][gj] = a00; G[gi][gj + 1] = a01; G[gi + 1][gj] = a10; G[gi + 1][gj + 1] = a11;
     for (int e = t; e < P * P; e += NT) R[e / P][e % P] = (e / P == e % P) ? 1.0 : 0.0;
     __syncthreads();
+    if (t < P * P / 2) {                                   // exact symmetry: upper copies to lower
+        const int i = t / P, j = t % P;
+        if (i > j) G[i][j] = G[j][i];
+    }
+    __syncthreads();
 
-    // ---- convergence test of this pair (relative coupling, absolute floor) ----
-    const double floor2 = (double)J.scale * 1e-8 * ((double)J.scale * 1e-8);
+    // ---- convergence test of this pair.  Rotate (i, j) only if the coupling exceeds both the
+    // relative bound tol * ||u_i|| ||u_j|| and the fp32 backward-error level tol_abs ||F|| (||u_i|| +
+    // ||u_j||): below it the coupling is indistinguishable from rounding of F itself.
+    const double fro = (double)J.scale;
     int need = 0;
-#pragma unroll
-    for (int q = 0; q < 3; ++q) {
-        if (ei[q] >= P || ei[q] == ej[q]) continue;
-        const double g = fabs(G[ei[q]][ej[q]]);
-        const double dii = G[ei[q]][ei[q]], djj = G[ej[q]][ej[q]];
-        if (g > tol * sqrt(dii * djj) && dii > floor2 && djj > floor2) need = 1;
+    for (int e = t; e < P * P; e += NT) {
+        const int i = e / P, j = e % P;
+        if (i >= j) continue;
+        const double g = fabs(G[i][j]);
+        const double ni = sqrt(G[i][i]), nj = sqrt(G[j][j]);
+        if (g > tol * ni * nj && g > tol_abs * fro * (ni + nj)) need = 1;
     }
     need = __syncthreads_or(need);
     if (!need) return;
 
     // ---- inner cyclic Jacobi on the 32x32 Gram (fp64, shared memory) ----
-    for (int sweep = 0; sweep < 12; ++sweep) {
+    __shared__ double gmax;
+    if (t == 0) {
+        double m = 0.0;
+        for (int i = 0; i < P; ++i) m = fmax(m, G[i][i]);
+        gmax = m;
+    }
+    __syncthreads();
+    const double inner_abs = 1e-15 * gmax;
+    for (int sweep = 0; sweep < kInnerSweeps; ++sweep) {
         int rotated = 0;
         for (int ir = 0; ir < P - 1; ++ir) {
             if (t < P / 2) {
@@ -201,7 +223,7 @@ __global__ void __launch_bounds__(NT) eig_round(EigJob *table, int count, int ro
                 circle_pair(ir, t, P, i, j);
                 const double gij = G[i][j], gii = G[i][i], gjj = G[j][j];
                 double c = 1.0, s = 0.0;
-                if (gij != 0.0 && fabs(gij) > 1e-15 * sqrt(fabs(gii * gjj))) {
+                if (fabs(gij) > 1e-12 * sqrt(fabs(gii * gjj)) && fabs(gij) > inner_abs) {
                     schur2(gii, gjj, gij, c, s);
                     rotated = 1;
                 }
@@ -234,37 +256,79 @@ __global__ void __launch_bounds__(NT) eig_round(EigJob *table, int count, int ro
         }
         if (!__syncthreads_or(rotated)) break;
     }
-    for (int e = t; e < P * P; e += NT) Rf[e / P][e % P] = (float)R[e / P][e % P];
     if (t == 0) atomicAdd(&J.rot_count, 1);
     __syncthreads();
 
-    // ---- apply: U_pq <- U_pq R, V_pq <- V_pq R (one row per thread, R broadcast) ----
+    // ---- apply: U_pq <- U_pq R, V_pq <- V_pq R (fp64; one row per thread, R broadcast) ----
     for (int w = 0; w < 2; ++w) {
-        float *M = w ? J.V : J.U;
+        double *M = w ? J.V : J.U;
         for (int r = t; r < n; r += NT) {
-            float x[P], y[P];
+            double x[P];
 #pragma unroll
-            for (int g = 0; g < P / 4; ++g) {
-                const int cb = (g < B / 4) ? c0 : c1;
-                float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (cb >= 0) v = *reinterpret_cast<const float4 *>(M + (size_t)r * ldu + cb + (g % (B / 4)) * 4);
-                x[g * 4 + 0] = v.x; x[g * 4 + 1] = v.y; x[g * 4 + 2] = v.z; x[g * 4 + 3] = v.w;
+            for (int g = 0; g < P / 2; ++g) {
+                const int cb = (g < B / 2) ? c0 : c1;
+                double2 v = make_double2(0.0, 0.0);
+                if (cb >= 0) v = *reinterpret_cast<const double2 *>(M + (size_t)r * ldu + cb + (g % (B / 2)) * 2);
+                x[2 * g] = v.x;
+                x[2 * g + 1] = v.y;
             }
 #pragma unroll
-            for (int j = 0; j < P; ++j) y[j] = 0.f;
+            for (int h = 0; h < 2; ++h) {                 // output block p (h = 0) then q (h = 1)
+                const int cb = h ? c1 : c0;
+                double y[B];
 #pragma unroll
-            for (int i = 0; i < P; ++i)
+                for (int j = 0; j < B; ++j) y[j] = 0.0;
 #pragma unroll
-                for (int j = 0; j < P; ++j) y[j] = fmaf(x[i], Rf[i][j], y[j]);
+                for (int i = 0; i < P; ++i)
 #pragma unroll
-            for (int g = 0; g < P / 4; ++g) {
-                const int cb = (g < B / 4) ? c0 : c1;
-                if (cb < 0) continue;
-                *reinterpret_cast<float4 *>(M + (size_t)r * ldu + cb + (g % (B / 4)) * 4) =
-                    make_float4(y[g * 4 + 0], y[g * 4 + 1], y[g * 4 + 2], y[g * 4 + 3]);
+                    for (int j = 0; j < B; ++j) y[j] = fma(x[i], R[i][h * B + j], y[j]);
+                if (cb >= 0) {
+#pragma unroll
+                    for (int g = 0; g < B / 2; ++g)
+                        *reinterpret_cast<double2 *>(M + (size_t)r * ldu + cb + 2 * g) = make_double2(y[2 * g], y[2 * g + 1]);
+                }
             }
         }
     }
+}
+
+// Warm start: U = F V in fp64 (64x64 tile per CTA, 4x4 per thread).
+__global__ void __launch_bounds__(256) eig_fv(EigJob *table) {
+    __shared__ double Fs[16][65];
+    __shared__ double Vs[16][65];
+    EigJob &J = table[blockIdx.z];
+    const int m0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
+    if (m0 >= J.n || n0 >= J.n) return;
+    const int t = threadIdx.x, ty = t / 16, tx = t % 16;
+    double acc[4][4] = {};
+    for (int k0 = 0; k0 < J.n; k0 += 16) {
+        for (int e = t; e < 16 * 64; e += 256) {
+            const int mm = e / 16, kk = e % 16;                 // F[m][k] (k fastest)
+            const int m = m0 + mm, k = k0 + kk;
+            Fs[kk][mm] = (m < J.n && k < J.n) ? (double)J.F[(size_t)m * J.ldF + k] : 0.0;
+            const int kv = e / 64, nn = e % 64;                 // V[k][n] (n fastest)
+            Vs[kv][nn] = (k0 + kv < J.n && n0 + nn < J.n) ? J.V[(size_t)(k0 + kv) * J.ldu + n0 + nn] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll 4
+        for (int kk = 0; kk < 16; ++kk) {
+            double a[4], b[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) { a[i] = Fs[kk][ty + 16 * i]; b[i] = Vs[kk][tx + 16 * i]; }
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int m = m0 + ty + 16 * i, n = n0 + tx + 16 * j;
+            if (m < J.n && n < J.n) J.U[(size_t)m * J.ldu + n] = acc[i][j];
+        }
 }
 
 __global__ void eig_sweep_end(EigJob *table, int count) {
@@ -277,14 +341,14 @@ __global__ void eig_sweep_end(EigJob *table, int count) {
     }
 }
 
-// lam_j = v_j^T (F v_j); W = F V was written into U by a GEMM.
+// lam_j = v_j^T u_j = v_j^T F v_j (U = F V is exact to fp64 rounding).
 __global__ void eig_rayleigh(EigJob *table) {
     EigJob &J = table[blockIdx.y];
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= J.n) return;
     double s = 0.0;
     for (int r = 0; r < J.n; ++r)
-        s += (double)J.V[(size_t)r * J.ldu + j] * (double)J.U[(size_t)r * J.ldu + j];
+        s += J.V[(size_t)r * J.ldu + j] * J.U[(size_t)r * J.ldu + j];
     J.lam[j] = s;
 }
 
@@ -316,7 +380,7 @@ __global__ void eig_scatter(EigJob *table) {
     const int r = blockIdx.y;
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= J.n || j >= J.n) return;
-    J.Q[(size_t)r * J.ldQ + J.rank[j]] = J.V[(size_t)r * J.ldu + j];
+    J.Q[(size_t)r * J.ldQ + J.rank[j]] = (float)J.V[(size_t)r * J.ldu + j];
 }
 
 struct Layout {
@@ -339,8 +403,8 @@ Layout plan(const int32_t *dims, int count) {
         const int nb_real = cdiv(J.n, B);
         J.nb = nb_real + (nb_real & 1);
         J.ldu = nb_real * B;
-        J.U = reinterpret_cast<float *>(take(sizeof(float) * (size_t)J.n * J.ldu));
-        J.V = reinterpret_cast<float *>(take(sizeof(float) * (size_t)J.n * J.ldu));
+        J.U = reinterpret_cast<double *>(take(sizeof(double) * (size_t)J.n * J.ldu));
+        J.V = reinterpret_cast<double *>(take(sizeof(double) * (size_t)J.n * J.ldu));
         J.lam = reinterpret_cast<double *>(take(sizeof(double) * J.n));
         J.rank = reinterpret_cast<int *>(take(sizeof(int) * J.n));
     }
@@ -370,8 +434,8 @@ kfac_status_t eigen_run(const float *const *F, const int32_t *dims, const int32_
         J.F = F[i]; J.Q = Q[i]; J.evals = evals[i];
         J.info = info ? info + i : nullptr;
         J.ldF = ldF[i]; J.ldQ = ldQ[i];
-        J.U = reinterpret_cast<float *>(base + reinterpret_cast<uintptr_t>(J.U));
-        J.V = reinterpret_cast<float *>(base + reinterpret_cast<uintptr_t>(J.V));
+        J.U = reinterpret_cast<double *>(base + reinterpret_cast<uintptr_t>(J.U));
+        J.V = reinterpret_cast<double *>(base + reinterpret_cast<uintptr_t>(J.V));
         J.lam = reinterpret_cast<double *>(base + reinterpret_cast<uintptr_t>(J.lam));
         J.rank = reinterpret_cast<int *>(base + reinterpret_cast<uintptr_t>(J.rank));
         J.pair_begin = pairs;
@@ -390,43 +454,27 @@ kfac_status_t eigen_run(const float *const *F, const int32_t *dims, const int32_
     const bool warm = flags & KFAC_EIG_WARM_START;
     int max_n = 0;
     for (auto &J : sorted) max_n = std::max(max_n, J.n);
+    eig_rownorm<<<dim3(cdiv(max_n, 8), count), 256, 0, s>>>(table);
+    KFAC_LAUNCHED();
     eig_init<<<dim3(std::min(1024, cdiv((long long)max_n * max_n, NT)), count), NT, 0, s>>>(table, warm);
     KFAC_LAUNCHED();
-    if (warm) {   // U = F * Q_in
-        std::vector<GemmDesc> g;
-        for (auto &J : sorted) {
-            GemmDesc d{};
-            d.A = J.F; d.lda = J.ldF; d.B = J.V; d.ldb = J.ldu; d.C = J.U; d.ldc = J.ldu;
-            d.M = d.N = d.K = J.n;
-            g.push_back(d);
-        }
-        kfac_status_t st = gemm_grouped(g.data(), (int)g.size(), 0.f, s);
-        if (st != KFAC_OK) return st;
+    if (warm) {   // U = F * V (fp64), V = Q_in
+        const int tiles = cdiv(max_n, 64);
+        eig_fv<<<dim3(tiles, tiles, count), 256, 0, s>>>(table);
+        KFAC_LAUNCHED();
     }
     // Sweeps: all rounds of all factors, factors sorted so that active pairs form a prefix.
     const int max_rounds = sorted[0].nb - 1;
-    const float tol = 2e-6f;
+    const float tol = 1e-7f, tol_abs = 1e-8f;
     for (int sweep = 0; sweep < kMaxSweeps; ++sweep) {
         for (int r = 0; r < max_rounds; ++r) {
             int active = 0;
             for (auto &J : sorted) if (J.nb - 1 > r) active = J.pair_begin + J.nb / 2;
-            eig_round<<<active, NT, 0, s>>>(table, count, r, tol);
+            eig_round<<<active, NT, 0, s>>>(table, count, r, tol, tol_abs);
             KFAC_LAUNCHED();
         }
         eig_sweep_end<<<1, 256, 0, s>>>(table, count);
         KFAC_LAUNCHED();
-    }
-    // Rayleigh quotients with the original factor: W = F V into U.
-    {
-        std::vector<GemmDesc> g;
-        for (auto &J : sorted) {
-            GemmDesc d{};
-            d.A = J.F; d.lda = J.ldF; d.B = J.V; d.ldb = J.ldu; d.C = J.U; d.ldc = J.ldu;
-            d.M = d.N = d.K = J.n;
-            g.push_back(d);
-        }
-        kfac_status_t st = gemm_grouped(g.data(), (int)g.size(), 0.f, s);
-        if (st != KFAC_OK) return st;
     }
     eig_rayleigh<<<dim3(cdiv(max_n, 128), count), 128, 0, s>>>(table);
     KFAC_LAUNCHED();

@@ -23,18 +23,6 @@ constexpr int T = 128, BK = 16, NT = 256;
 constexpr int kChunkRows = 4096;
 constexpr int kMaxJobs = 64;
 
-struct FactorJob {
-    const float *src;       // act (NHWC) for A, gout for G
-    float *F;
-    float *partial;         // [splits][tiles][T*T]
-    long long n;            // rows
-    int ldF, d, is_a;
-    int splits, chunk, t1d, tiles, item_begin, tile_begin;
-    // im2col geometry (A factor); for G: c_in = d (row length of gout)
-    int c_in, h_in, w_in, h_out, w_out, k_w, stride_h, stride_w, pad_h, pad_w;
-    int patch_cols, bias_col;
-};
-
 struct FactorBatch {
     int count;
     float decay, out_scale;
@@ -209,9 +197,11 @@ __global__ void __launch_bounds__(256) syrk_reduce_kernel(const __grid_constant_
     for (int rr = ty; rr < 32; rr += 8) {
         const int li = si * 32 + rr, lj = sj * 32 + tx;
         const int gi = ti * T + li;
+        // diagonal tiles: read the upper entry for both (i, j) and (j, i) -> exact symmetry
+        const int pi = (ti == tj && li > lj) ? lj : li, pj = (ti == tj && li > lj) ? li : lj;
         float s = 0.f;
         for (int sp = 0; sp < J.splits; ++sp)
-            s += J.partial[((size_t)sp * J.tiles + tau) * (T * T) + li * T + lj];
+            s += J.partial[((size_t)sp * J.tiles + tau) * (T * T) + pi * T + pj];
         float v = s * inv_n;
         if (gi < J.d && gj < J.d) {
             float *dst = J.F + (size_t)gi * J.ldF + gj;
@@ -281,23 +271,40 @@ kfac_status_t factors_run(const kfac_layer_t *layers, int nl, const float *const
     Plan p = make_plan(layers, nl, A, ldA, G, ldG, act, gout);
     float *base = reinterpret_cast<float *>(round_up(reinterpret_cast<uintptr_t>(ws), 256));
     for (auto &j : p.jobs) j.partial = base + reinterpret_cast<uintptr_t>(j.partial);
+    // Partial SYRKs: tcgen05 3xTF32 for the factors it supports, the SIMT tile for the rest.
+    std::vector<FactorJob> tc, simt;
+    for (auto &j : p.jobs) (syrk_tc_supported(j) ? tc : simt).push_back(j);
+    if (!tc.empty()) {
+        kfac_status_t st = syrk_tc_partial(tc.data(), (int)tc.size(), s);
+        if (st != KFAC_OK) return st;
+    }
+    for (size_t b0 = 0; b0 < simt.size(); b0 += kMaxJobs) {
+        FactorBatch fb;
+        fb.count = 0;
+        int items = 0;
+        for (size_t i = b0; i < simt.size() && fb.count < kMaxJobs; ++i) {
+            FactorJob j = simt[i];
+            j.item_begin = items;
+            items += j.tiles * j.splits;
+            fb.j[fb.count++] = j;
+        }
+        syrk_partial_kernel<<<items, NT, 0, s>>>(fb);
+        KFAC_LAUNCHED();
+    }
+    // Fixed-order reduction + running average for every factor.
     for (size_t b0 = 0; b0 < p.jobs.size(); b0 += kMaxJobs) {
         FactorBatch fb;
         fb.count = 0;
         fb.decay = decay;
         fb.out_scale = out_scale;
         fb.first = first;
-        int items = 0, subtiles = 0;
+        int subtiles = 0;
         for (size_t i = b0; i < p.jobs.size() && fb.count < kMaxJobs; ++i) {
             FactorJob j = p.jobs[i];
-            j.item_begin = items;
             j.tile_begin = subtiles;
-            items += j.tiles * j.splits;
             subtiles += j.tiles * 16;
             fb.j[fb.count++] = j;
         }
-        syrk_partial_kernel<<<items, NT, 0, s>>>(fb);
-        KFAC_LAUNCHED();
         syrk_reduce_kernel<<<subtiles, 256, 0, s>>>(fb);
         KFAC_LAUNCHED();
     }

@@ -1,14 +1,643 @@
-// gemm_tc.cu -- tcgen05 (kind::tf32, 3xTF32) grouped GEMM.  Placeholder until the tensor-core
-// path lands: no descriptor is routed here yet.
+// gemm_tc.cu -- tcgen05 tensor-core grouped GEMM, kind::tf32 with a 3xTF32 split (fp32-faithful).
+//
+//   C = op(A) op(B) (+ Eq. 14 epilogue), 128x128 output tile per CTA, K staged 32 at a time.
+//
+// Warp roles (256 threads):
+//   warp 0      TMA producer: one elected lane loads the raw fp32 A/B tiles of a k-block with
+//               cp.async.bulk.tensor (128-byte swizzle) into the "hi" slots of a stage;
+//   warps 4..7  split warpgroup: hi = x rounded to TF32, lo = (x - hi) rounded to TF32 (x - hi
+//               is exact in fp32), both exactly representable so the hardware's own TF32
+//               conversion is a no-op; hi overwrites the raw tile, lo goes to the "lo" slots,
+//               then fence.proxy.async so the tensor core sees the generic-proxy writes;
+//               after the main loop the same warps are the epilogue (tcgen05.ld -> registers ->
+//               divide by v_G v_A^T + damping -> global);
+//   warp 1      MMA issuer: one thread issues, per k-step of 8, the three products
+//               A_lo B_hi + A_hi B_lo + A_hi B_hi into the TMEM accumulator (128 lanes x 128
+//               columns fp32) and commits the smem slot back to the producer;
+//   warp 2      TMEM allocator.
+// Operand tiles may be K-major (k contiguous) or MN-major (m/n contiguous); the UMMA
+// instruction descriptor's major bits select the layout, so no operand is ever transposed.
 #include "internal.cuh"
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <mutex>
+#include <vector>
+
 namespace kfac {
+namespace {
 
-bool gemm_tc_supported(const GemmDesc &) { return false; }
+constexpr int BM = 128, BN = 128, BK = 32;
+constexpr int kStages = 3;
+constexpr int kTileBytes = BM * BK * 4;                 // 16 KB per operand tile
+constexpr int kStageBytes = 4 * kTileBytes;             // A_hi, B_hi, A_lo, B_lo
+constexpr int kBarBytes = 256;
+constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + kBarBytes;
+constexpr int kMaxTc = 24;                              // problems per launch (tensor maps in params)
+constexpr int kMaxSyrk = 64;
+constexpr int NT = 320;                                 // 10 warps
+constexpr int kTmemCols = 256;                          // two 128-column accumulators
 
-kfac_status_t gemm_tc_grouped(const GemmDesc *, int, float, cudaStream_t) {
-    set_error("tcgen05 GEMM not built");
-    return KFAC_ERR_UNSUPPORTED;
+// warp roles
+constexpr int W_SPLIT0 = 0;     // warps 0-3: (SYRK producer) + hi/lo split
+constexpr int W_DRAIN0 = 4;     // warps 4-7: TMEM drain into fp32 registers + epilogue
+constexpr int W_TMA = 8;        // warp 8: TMA producer (GEMM) + TMEM allocator
+constexpr int W_MMA = 9;        // warp 9: MMA issuer
+
+struct TcDesc {
+    CUtensorMap ta;       // 128 B, 64-byte aligned
+    CUtensorMap tb;
+    float *C;
+    const float *vr;
+    const float *vc;
+    int M, N, K, ldc;
+    int a_mn, b_mn, epi;
+    int tile_begin, tiles_n;
+};
+
+struct __align__(64) TcBatch {
+    TcDesc d[kMaxTc];
+    int count;
+    float damping;
+};
+
+struct SyrkBatch {
+    int count;
+    FactorJob j[kMaxSyrk];
+};
+
+// ------------------------------------------------------------------ PTX --
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(bar), "r"(parity)
+            : "memory");
+    }
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map, uint32_t bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void prefetch_map(const CUtensorMap *map) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src, uint32_t bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ void split_bar_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
+    // SM100 UMMA shared-memory descriptor (version 1).  layout 2 = SWIZZLE_128B (K-major tiles),
+    // layout 1 = SWIZZLE_128B_BASE32B (the only MN-major layout tf32 supports).
+    uint64_t d = 0;
+    d |= (uint64_t)((addr >> 4) & 0x3FFF);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)(layout & 7) << 61;
+    return d;
+}
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+
+// TMEM -> registers: 32 lanes x 32 columns per warp; the wait is in the same asm statement so
+// no use of the outputs can be scheduled before the asynchronous load has completed.
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n\t"
+        "tcgen05.wait::ld.sync.aligned;"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr)
+        : "memory");
+}
+
+// Round an fp32 value to the nearest TF32 (10-bit mantissa), ties away from zero; exact in fp32.
+__device__ __forceinline__ float tf32_rn(float x) {
+    return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+}
+
+// ------------------------------------------------------- shared pieces --
+struct Smem {
+    uint8_t *base;
+    uint32_t raw_full, ready, stage_empty, tfull, tempty;   // barrier arrays (8 B stride)
+    uint32_t *tmem_slot;
+};
+
+__device__ __forceinline__ Smem carve(uint8_t *smem_raw) {
+    Smem s;
+    s.base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t *bars = reinterpret_cast<uint64_t *>(s.base + kStages * kStageBytes);
+    s.raw_full = smem_u32(bars);
+    s.ready = smem_u32(bars + kStages);
+    s.stage_empty = smem_u32(bars + 2 * kStages);
+    s.tfull = smem_u32(bars + 3 * kStages);
+    s.tempty = smem_u32(bars + 3 * kStages + 2);
+    s.tmem_slot = reinterpret_cast<uint32_t *>(bars + 3 * kStages + 4);
+    return s;
+}
+
+__device__ __forceinline__ void setup(const Smem &S, int warp) {
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kStages; ++i) {
+            mbar_init(S.raw_full + 8 * i, 1);
+            mbar_init(S.ready + 8 * i, 128);
+            mbar_init(S.stage_empty + 8 * i, 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(S.tfull + 8 * b, 1);
+            mbar_init(S.tempty + 8 * b, 128);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == W_TMA) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(S.tmem_slot)),
+                     "r"(kTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+}
+
+__device__ __forceinline__ void teardown(uint32_t tmem, int warp) {
+    tc_fence_before();
+    __syncthreads();
+    if (warp == W_TMA) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+    }
+}
+
+// hi = rn_tf32(x) in place, lo = rn_tf32(x - hi): 3xTF32 operands, both exact TF32 values.
+__device__ __forceinline__ void split_region(uint8_t *raw, int n_f4, int t) {
+    float4 *hi = reinterpret_cast<float4 *>(raw);
+    float4 *lo = reinterpret_cast<float4 *>(raw + 2 * kTileBytes);
+#pragma unroll 4
+    for (int i = t; i < n_f4; i += 128) {
+        float4 x = hi[i], h, l;
+        h.x = tf32_rn(x.x); h.y = tf32_rn(x.y); h.z = tf32_rn(x.z); h.w = tf32_rn(x.w);
+        l.x = tf32_rn(x.x - h.x); l.y = tf32_rn(x.y - h.y);
+        l.z = tf32_rn(x.z - h.z); l.w = tf32_rn(x.w - h.w);
+        hi[i] = h;
+        lo[i] = l;
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ uint64_t operand_desc(uint32_t base, int kstep, int mn_major) {
+    // k-step of 8 tf32: K-major advances 32 B inside the 128-B swizzle row (SBO 1024 = 8-row
+    // atoms); MN-major (BASE32B) advances 8 k-rows = 1024 B (SBO 512 = 4-row k-groups,
+    // LBO 4096 = 32-element mn groups).
+    if (!mn_major) return smem_desc(base + kstep * 32, 16, 1024, 2);
+    return smem_desc(base + kstep * 1024, 4096, 512, 1);
+}
+
+// MMA issuer: for each k-block, the three 3xTF32 products into TMEM buffer (kb & 1).
+__device__ __forceinline__ void mma_loop(const Smem &S, uint32_t tmem, int nk, int a_mn, int b_mn, bool same_ab) {
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
+                           ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+    for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % kStages, b = kb & 1, u = kb >> 1;
+        mbar_wait(S.ready + 8 * s, (kb / kStages) & 1);
+        if (u >= 1) mbar_wait(S.tempty + 8 * b, (u - 1) & 1);
+        tc_fence_after();
+        const uint32_t st = smem_u32(S.base + s * kStageBytes);
+        const uint32_t a_hi = st, a_lo = st + 2 * kTileBytes;
+        const uint32_t b_hi = same_ab ? a_hi : st + kTileBytes, b_lo = same_ab ? a_lo : st + 3 * kTileBytes;
+        const uint32_t d = tmem + b * BN;
+#pragma unroll
+        for (int ks = 0; ks < BK / 8; ++ks) {
+            mma_tf32(d, operand_desc(a_lo, ks, a_mn), operand_desc(b_hi, ks, b_mn), idesc, ks > 0 ? 1u : 0u);
+            mma_tf32(d, operand_desc(a_hi, ks, a_mn), operand_desc(b_lo, ks, b_mn), idesc, 1u);
+            mma_tf32(d, operand_desc(a_hi, ks, a_mn), operand_desc(b_hi, ks, b_mn), idesc, 1u);
+        }
+        mma_commit(S.stage_empty + 8 * s);
+        mma_commit(S.tfull + 8 * b);
+    }
+}
+
+// Drain warps: every k-block's 128x128 partial product is added into fp32 registers with
+// IEEE rounding (the tensor-core accumulator truncates, so long accumulations stay in TMEM
+// for only 12 MMAs).  Thread (quarter wq, lane) owns row 32*wq + lane.
+__device__ __forceinline__ void drain_loop(const Smem &S, uint32_t tmem, int nk, int wq, float (&acc)[BN]) {
+#pragma unroll
+    for (int j = 0; j < BN; ++j) acc[j] = 0.f;
+    for (int kb = 0; kb < nk; ++kb) {
+        const int b = kb & 1;
+        mbar_wait(S.tfull + 8 * b, (kb >> 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < BN / 32; ++c) {
+            uint32_t r[32];
+            tmem_ld32(tmem + b * BN + ((uint32_t)(wq * 32) << 16) + c * 32, r);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) acc[c * 32 + j] += __uint_as_float(r[j]);
+        }
+        tc_fence_before();
+        mbar_arrive(S.tempty + 8 * b);
+    }
+}
+
+// ------------------------------------------------------------ GEMM kernel --
+__device__ __forceinline__ int find_desc(const TcBatch &b, int tile) {
+    int lo = 0, hi = b.count - 1;
+    while (lo < hi) {
+        int mid = (lo + hi + 1) >> 1;
+        if (b.d[mid].tile_begin <= tile) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+//   K-major: one box {32 (k), 128 (mn)}, 128B swizzle -> 128 rows x 128 B
+//   MN-major: four boxes {32 (mn), 32 (k)}, 128B swizzle with 32-B atoms -> 32 k-rows x 128 B each
+__device__ __forceinline__ void load_tile(uint32_t dst, const CUtensorMap *map, uint32_t bar, int mn0, int k0, int mn_major) {
+    if (!mn_major) {
+        tma_load_2d(dst, map, bar, k0, mn0);
+    } else {
+#pragma unroll
+        for (int g = 0; g < 4; ++g) tma_load_2d(dst + g * 4096, map, bar, mn0 + 32 * g, k0);
+    }
+}
+
+__global__ void __launch_bounds__(NT, 1) gemm_tc_kernel(const __grid_constant__ TcBatch batch) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    const Smem S = carve(smem_raw);
+    const int tile = blockIdx.x;
+    const TcDesc &d = batch.d[find_desc(batch, tile)];
+    const int local = tile - d.tile_begin;
+    const int m0 = (local / d.tiles_n) * BM, n0 = (local % d.tiles_n) * BN;
+    const int nk = (d.K + BK - 1) / BK;
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    if (warp == W_TMA && lane == 0) {
+        prefetch_map(&d.ta);
+        prefetch_map(&d.tb);
+    }
+    setup(S, warp);
+    const uint32_t tmem = *S.tmem_slot;
+
+    if (warp == W_TMA) {
+        if (lane == 0) {
+            for (int kb = 0; kb < nk; ++kb) {
+                const int s = kb % kStages;
+                if (kb >= kStages) mbar_wait(S.stage_empty + 8 * s, ((kb / kStages) - 1) & 1);
+                const uint32_t st = smem_u32(S.base + s * kStageBytes);
+                mbar_expect_tx(S.raw_full + 8 * s, 2 * kTileBytes);
+                load_tile(st, &d.ta, S.raw_full + 8 * s, m0, kb * BK, d.a_mn);
+                load_tile(st + kTileBytes, &d.tb, S.raw_full + 8 * s, n0, kb * BK, d.b_mn);
+            }
+        }
+    } else if (warp == W_MMA) {
+        if (lane == 0) mma_loop(S, tmem, nk, d.a_mn, d.b_mn, false);
+    } else if (warp < W_DRAIN0) {
+        const int t = threadIdx.x;
+        for (int kb = 0; kb < nk; ++kb) {
+            const int s = kb % kStages;
+            mbar_wait(S.raw_full + 8 * s, (kb / kStages) & 1);
+            split_region(S.base + s * kStageBytes, 2 * kTileBytes / 16, t);
+            mbar_arrive(S.ready + 8 * s);
+        }
+    } else {
+        const int wq = warp - W_DRAIN0;
+        float acc[BN];
+        drain_loop(S, tmem, nk, wq, acc);
+        const int m = m0 + wq * 32 + lane;
+        if (m < d.M) {
+            const float vr = d.epi ? d.vr[m] : 0.f;
+            float *crow = d.C + (size_t)m * d.ldc;
+#pragma unroll
+            for (int j = 0; j < BN; ++j) {
+                const int n = n0 + j;
+                if (n < d.N) {
+                    float v = acc[j];
+                    if (d.epi == EPI_DIV_EIGEN) v = v / fmaxf(fmaf(vr, d.vc[n], batch.damping), 1e-12f);
+                    else if (d.epi == EPI_DIV_FACTORED)
+                        v = v / fmaxf((vr + batch.damping) * (d.vc[n] + batch.damping), 1e-12f);
+                    crow[n] = v;
+                }
+            }
+        }
+    }
+    teardown(tmem, warp);
+}
+
+// ------------------------------------------------------------ SYRK kernel --
+__device__ __forceinline__ int find_job(const SyrkBatch &b, int item) {
+    int lo = 0, hi = b.count - 1;
+    while (lo < hi) {
+        int mid = (lo + hi + 1) >> 1;
+        if (b.j[mid].item_begin <= item) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ void upper_tile(int tau, int t1d, int &ti, int &tj) {
+    int i = 0;
+    while (tau >= t1d - i) { tau -= t1d - i; ++i; }
+    ti = i;
+    tj = i + tau;
+}
+
+// Byte offset of the 16-B chunk (k, m..m+3) in an MN-major SWIZZLE_128B_BASE32B operand tile
+// (128 m x 32 k): 32-m groups of 4 KB, k-rows of 128 B, 32-B chunks XOR (k % 4).
+__device__ __forceinline__ uint32_t mn_off(int k, int m) {
+    return (uint32_t)((m >> 5) * 4096 + k * 128 + ((((m & 31) >> 3) ^ (k & 3)) << 5) + ((m & 7) << 2));
+}
+
+// Gather descriptor of a 4-column chunk of X = [im2col | 1] (or of the gradient rows).
+struct ChunkInfo {
+    int off, kh, kw, kind;    // kind 0: load, 1: bias chunk {1,0,0,0}, 2: zero
+};
+
+__device__ __forceinline__ ChunkInfo chunk_info(const FactorJob &J, int c) {
+    ChunkInfo ci{0, 0, 0, 2};
+    if (c >= J.d) return ci;
+    if (!J.is_a) { ci.kind = 0; ci.off = c; return ci; }
+    if (c >= J.patch_cols) { ci.kind = 1; return ci; }
+    const int kwc = J.k_w * J.c_in;
+    ci.kh = c / kwc;
+    const int rem = c - ci.kh * kwc;
+    ci.kw = rem / J.c_in;
+    ci.off = (ci.kh * J.w_in + ci.kw) * J.c_in + (rem - ci.kw * J.c_in);
+    ci.kind = 0;
+    return ci;
+}
+
+// Producer warps 0-3: cp.async gathers of the 32-row k-block into the raw (hi) slots.
+__device__ __forceinline__ void syrk_issue(const FactorJob &J, const Smem &S, int s, long long r0, long long r_end,
+                                           const ChunkInfo (&ci)[2], int cc, int t, bool diag) {
+    const uint32_t st = smem_u32(S.base + s * kStageBytes);
+    const int hw = J.h_out * J.w_out;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const int k = t / 32 + 4 * j;
+        const long long r = r0 + k;
+        const bool rv = r < r_end;
+        int img = 0, oh = 0, ow = 0;
+        if (J.is_a && rv) {
+            img = (int)(r / hw);
+            const int p = (int)(r - (long long)img * hw);
+            oh = p / J.w_out;
+            ow = p - oh * J.w_out;
+        }
+        const int ih0 = oh * J.stride_h - J.pad_h, iw0 = ow * J.stride_w - J.pad_w;
+#pragma unroll
+        for (int op = 0; op < 2; ++op) {
+            if (op == 1 && diag) break;
+            const uint32_t dst = st + op * kTileBytes + mn_off(k, 4 * cc);
+            const ChunkInfo &c = ci[op];
+            if (c.kind == 1) {
+                const float one = rv ? 1.f : 0.f;
+                asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(dst), "f"(one), "f"(0.f), "f"(0.f), "f"(0.f)
+                             : "memory");
+                continue;
+            }
+            const float *src = J.src;
+            uint32_t bytes = 0;
+            if (rv && c.kind == 0) {
+                if (!J.is_a) {
+                    src = J.src + r * J.c_in + c.off;
+                    bytes = 16;
+                } else {
+                    // c.off already holds (kh * w_in + kw) * c_in + channel (receptive-field offset)
+                    const int ih = ih0 + c.kh, iw = iw0 + c.kw;
+                    if (ih >= 0 && ih < J.h_in && iw >= 0 && iw < J.w_in) {
+                        src = J.src + (((long long)img * J.h_in + ih0) * J.w_in + iw0) * J.c_in + c.off;
+                        bytes = 16;
+                    }
+                }
+            }
+            cp_async16(dst, src, bytes);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(NT, 1) syrk_tc_kernel(const __grid_constant__ SyrkBatch batch) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    const Smem S = carve(smem_raw);
+    const int item = blockIdx.x;
+    const FactorJob &J = batch.j[find_job(batch, item)];
+    const int local = item - J.item_begin;
+    const int tau = local / J.splits, split = local % J.splits;
+    int ti, tj;
+    upper_tile(tau, J.t1d, ti, tj);
+    const bool diag = ti == tj;
+    const long long r_begin = (long long)split * J.chunk;
+    const long long r_end = min(J.n, r_begin + J.chunk);
+    const int nk = (int)((r_end - r_begin + BK - 1) / BK);
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    setup(S, warp);
+    const uint32_t tmem = *S.tmem_slot;
+
+    if (warp == W_MMA) {
+        if (lane == 0) mma_loop(S, tmem, nk, 1, 1, diag);
+    } else if (warp < W_DRAIN0) {
+        const int t = threadIdx.x, cc = t % 32;
+        ChunkInfo ci[2] = {chunk_info(J, ti * BM + 4 * cc), chunk_info(J, tj * BM + 4 * cc)};
+        const int n_f4 = (diag ? 1 : 2) * kTileBytes / 16;
+        // prologue: k-blocks 0 .. kStages-2
+#pragma unroll
+        for (int p = 0; p < kStages - 1; ++p) {
+            if (p < nk) syrk_issue(J, S, p, r_begin + (long long)p * BK, r_end, ci, cc, t, diag);
+            cp_async_commit();
+        }
+        for (int kb = 0; kb < nk; ++kb) {
+            const int nxt = kb + kStages - 1;
+            if (nxt < nk) {
+                const int s2 = nxt % kStages;
+                if (nxt >= kStages) mbar_wait(S.stage_empty + 8 * s2, ((nxt / kStages) - 1) & 1);
+                syrk_issue(J, S, s2, r_begin + (long long)nxt * BK, r_end, ci, cc, t, diag);
+            }
+            cp_async_commit();
+            cp_async_wait<kStages - 1>();
+            split_bar_sync();
+            const int s = kb % kStages;
+            split_region(S.base + s * kStageBytes, n_f4, t);
+            mbar_arrive(S.ready + 8 * s);
+        }
+    } else if (warp < W_TMA) {
+        const int wq = warp - W_DRAIN0;
+        float acc[BN];
+        drain_loop(S, tmem, nk, wq, acc);
+        float4 *dst = reinterpret_cast<float4 *>(J.partial + ((size_t)split * J.tiles + tau) * (BM * BN) +
+                                                 (size_t)(wq * 32 + lane) * BN);
+#pragma unroll
+        for (int j = 0; j < BN / 4; ++j) dst[j] = make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
+    }
+    teardown(tmem, warp);
+}
+
+// ------------------------------------------------------------- host side --
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    return fn;
+}
+
+// 2-D fp32 row-major tensor of `rows` x `cols` (cols contiguous) with leading dimension ld.
+bool make_map(CUtensorMap *map, const float *ptr, int rows, int cols, int ld, int box_cols, int box_rows,
+              CUtensorMapSwizzle swz) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+    cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(ptr), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+bool g_tc_disabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("KFAC_DISABLE_TC");
+        v = (e && e[0] == '1') ? 1 : 0;
+    }
+    return v == 1;
+}
+
+}  // namespace
+
+bool gemm_tc_supported(const GemmDesc &d) {
+    if (g_tc_disabled()) return false;
+    if (d.M < 64 || d.N < 64 || d.K < 32) return false;         // small problems: SIMT
+    if ((d.lda & 3) || (d.ldb & 3) || (d.ldc & 3)) return false;
+    if (!aligned16(d.A) || !aligned16(d.B)) return false;
+    return encode_fn() != nullptr;
+}
+
+kfac_status_t gemm_tc_grouped(const GemmDesc *descs, int count, float damping, cudaStream_t s) {
+    static bool attr = false;
+    if (!attr) {
+        KFAC_CUDA_TRY(cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+        attr = true;
+    }
+    for (int base = 0; base < count; base += kMaxTc) {
+        TcBatch b;
+        memset(&b, 0, sizeof(b));
+        b.damping = damping;
+        b.count = 0;
+        int tiles = 0;
+        for (int i = base; i < count && b.count < kMaxTc; ++i) {
+            const GemmDesc &g = descs[i];
+            TcDesc &t = b.d[b.count];
+            // op(A) (M x K): K-major if A[m*lda + k] (trans_a = 0), MN-major if A[k*lda + m]
+            t.a_mn = g.trans_a ? 1 : 0;
+            t.b_mn = g.trans_b ? 0 : 1;      // op(B)[k][n] = B[k*ldb + n] is N-contiguous -> MN-major
+            const CUtensorMapSwizzle kmaj = CU_TENSOR_MAP_SWIZZLE_128B, mnmaj = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
+            bool ok = t.a_mn ? make_map(&t.ta, g.A, g.K, g.M, g.lda, 32, 32, mnmaj)
+                             : make_map(&t.ta, g.A, g.M, g.K, g.lda, 32, 128, kmaj);
+            ok = ok && (t.b_mn ? make_map(&t.tb, g.B, g.K, g.N, g.ldb, 32, 32, mnmaj)
+                               : make_map(&t.tb, g.B, g.N, g.K, g.ldb, 32, 128, kmaj));
+            if (!ok) {
+                set_error("cuTensorMapEncodeTiled failed");
+                return KFAC_ERR_CUDA;
+            }
+            t.C = g.C; t.vr = g.vr; t.vc = g.vc;
+            t.M = g.M; t.N = g.N; t.K = g.K; t.ldc = g.ldc; t.epi = g.epi;
+            t.tiles_n = cdiv(g.N, BN);
+            t.tile_begin = tiles;
+            tiles += cdiv(g.M, BM) * t.tiles_n;
+            ++b.count;
+        }
+        if (!b.count) continue;
+        gemm_tc_kernel<<<tiles, NT, kSmemBytes, s>>>(b);
+        KFAC_LAUNCHED();
+    }
+    return KFAC_OK;
+}
+
+bool syrk_tc_supported(const FactorJob &j) {
+    if (g_tc_disabled()) return false;
+    if (j.d < 64 || j.n < 32) return false;               // small factors: SIMT tile
+    if (j.c_in % 4 != 0) return false;                    // 16-byte gathers
+    if (j.is_a && j.bias_col && j.patch_cols % 4 != 0) return false;
+    return aligned16(j.src);
+}
+
+kfac_status_t syrk_tc_partial(const FactorJob *jobs, int count, cudaStream_t s) {
+    static bool attr = false;
+    if (!attr) {
+        KFAC_CUDA_TRY(cudaFuncSetAttribute(syrk_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+        attr = true;
+    }
+    for (int base = 0; base < count; base += kMaxSyrk) {
+        SyrkBatch b;
+        b.count = 0;
+        int items = 0;
+        for (int i = base; i < count && b.count < kMaxSyrk; ++i) {
+            FactorJob j = jobs[i];
+            j.item_begin = items;
+            items += j.tiles * j.splits;
+            b.j[b.count++] = j;
+        }
+        syrk_tc_kernel<<<items, NT, kSmemBytes, s>>>(b);
+        KFAC_LAUNCHED();
+    }
+    return KFAC_OK;
 }
 
 }  // namespace kfac
+
+// Test hook (not part of the public header): run one GEMM through a chosen engine.
+// engine 0 = SIMT, 1 = tcgen05.  Returns a kfac_status_t.
+extern "C" int kfac_debug_gemm(int engine, const float *A, int lda, int trans_a, const float *B, int ldb,
+                               int trans_b, float *C, int ldc, int M, int N, int K, void *stream, float *debug) {
+    kfac::GemmDesc d{};
+    d.A = A; d.lda = lda; d.trans_a = trans_a; d.B = B; d.ldb = ldb; d.trans_b = trans_b;
+    d.C = C; d.ldc = ldc; d.M = M; d.N = N; d.K = K;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (engine == 1) {
+        if (!kfac::gemm_tc_supported(d)) return KFAC_ERR_UNSUPPORTED;
+        (void)debug;
+        return kfac::gemm_tc_grouped(&d, 1, 0.f, s);
+    }
+    return kfac::gemm_simt_grouped(&d, 1, 0.f, s);
+}

@@ -48,4 +48,24 @@ bool gemm_tc_supported(const GemmDesc &d);
 // Dispatch each descriptor to the tensor-core or SIMT engine.
 kfac_status_t gemm_grouped(const GemmDesc *descs, int count, float damping, cudaStream_t s);
 
+// ------------------------------------------------------------ factor SYRK --
+// One Kronecker factor of one layer: F_batch = X^T X / n over the n rows of X, where X is
+// [im2col(act) | 1] (A factor, Eq. 5) or the output gradients (G factor).  The upper 128x128
+// tiles of X^T X are computed per row chunk into `partial` ([splits][tiles][128*128]) and
+// reduced by syrk_reduce (fixed order, running average, both triangles).
+struct FactorJob {
+    const float *src;       // act (NHWC) for A, gout (n x c_in) for G
+    float *F;
+    float *partial;
+    long long n;            // rows
+    int ldF, d, is_a;
+    int splits, chunk, t1d, tiles, item_begin, tile_begin;
+    int c_in, h_in, w_in, h_out, w_out, k_w, stride_h, stride_w, pad_h, pad_w;  // G: c_in = row length
+    int patch_cols, bias_col;
+};
+
+// Tensor-core (tcgen05 3xTF32) partial SYRK for the jobs it supports (row length % 4 == 0).
+bool syrk_tc_supported(const FactorJob &j);
+kfac_status_t syrk_tc_partial(const FactorJob *jobs, int count, cudaStream_t s);
+
 }  // namespace kfac

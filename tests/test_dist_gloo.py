@@ -1,0 +1,96 @@
+"""Multi-process (world_size 2, gloo, CPU) tests of the distributed orchestration:
+the same assignment on every rank, the owner-major buffer layout that lets the eigenbasis
+(K-FAC-opt) and preconditioned-gradient (K-FAC-lw) exchanges run as one in-place
+all-gather, and the factor average through allreduce-SUM of out_scale = 1/W factors
+(Alg. 1).  The CUDA kernels are not exercised here."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from workloads import shapes
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, cfg, exchange, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2007_00784_b200.preconditioner import KFACPreconditioner, all_gather_inplace
+        layers = shapes.layers_for(cfg)
+        pc = KFACPreconditioner(layers, device="cpu", exchange=exchange)
+        # 1) identical assignment everywhere
+        owners = [None] * world
+        dist.all_gather_object(owners, pc.owner)
+        assert all(o == owners[0] for o in owners)
+        # 2) factor allreduce: each rank holds (its factor) * 1/W; SUM gives the average
+        vals = torch.arange(pc.factor_flat.numel(), dtype=torch.float32) % 97
+        pc.factor_flat.copy_((vals + 1000 * rank) / world)
+        dist.all_reduce(pc.factor_flat, op=dist.ReduceOp.SUM)
+        expect = (vals * world + 1000 * sum(range(world))) / world
+        assert torch.allclose(pc.factor_flat, expect)
+        # 3) eigenbasis exchange (K-FAC-opt): owners write their factors, one in-place all-gather
+        for f in pc.owned:
+            pc.Q[f].fill_(float(f + 1))
+            pc.v[f].fill_(float(-(f + 1)))
+        all_gather_inplace(pc.q_flat, pc.q_slice)
+        all_gather_inplace(pc.v_flat, pc.v_slice)
+        for f in range(len(pc.dims)):
+            assert torch.all(pc.Q[f] == f + 1) and torch.all(pc.v[f] == -(f + 1))
+        # 4) preconditioned-gradient exchange (K-FAC-lw): layer owners write P
+        for i in pc.owned_layers:
+            pc.P[i].fill_(float(i + 7))
+        all_gather_inplace(pc.p_flat, pc.p_slice)
+        for i in range(len(layers)):
+            assert torch.all(pc.P[i] == i + 7)
+        if exchange == "allgather-grad":
+            for i in range(len(layers)):
+                assert pc.owner[2 * i] == pc.owner[2 * i + 1]
+        q.put((rank, "ok", len(pc.owned)))
+    except Exception as e:  # pragma: no cover - reported to the parent
+        q.put((rank, repr(e), 0))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("cfg,exchange", [("r32", "bcast-eig"), ("r32", "allgather-grad"), ("mlp", "bcast-eig")])
+def test_two_rank_exchanges(cfg, exchange):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, cfg, exchange, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(r[1] == "ok" for r in res), res
+    assert sum(r[2] for r in res) == 2 * len(shapes.layers_for(cfg))     # every factor owned once
+
+
+def test_lpt_balances_r50_eigen_cost():
+    """LPT on d^3 at W = 2/4/8: the makespan is within Graham's bound of the ideal and
+    matches the cap set by the largest factor (2.00 / 4.00 / 4.63)."""
+    from paper_2007_00784_b200 import _lib
+    layers = shapes.resnet50()
+    dims, lo = shapes.factor_dims(layers)
+    total = sum(d ** 3 for d in dims)
+    speed = {}
+    for w in (2, 4, 8):
+        owner = _lib.kfac_assign(dims, lo, len(layers), w, _lib.LPT_D3)
+        load = np.zeros(w)
+        for d, o in zip(dims, owner):
+            load[o] += d ** 3
+        speed[w] = total / load.max()
+    assert speed[2] > 1.99 and speed[4] > 3.95 and abs(speed[8] - total / 4609 ** 3) < 1e-6 * speed[8]

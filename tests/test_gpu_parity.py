@@ -128,6 +128,8 @@ FACTOR_LAYERS = [
     shapes.conv("c1s2", 2, 130, 300, 1, 2, 8),           # d_A 131, d_G 300 (3 tiles)
     shapes.linear("fc", 37, 785, 64),
     shapes.linear("fc2", 5000, 20, 10),                  # 2 row chunks
+    shapes.conv("c3big", 2, 64, 128, 3, 2, 30),          # tcgen05 path, im2col stride 2 + padding, d_A 577
+    shapes.conv("c1big", 4, 256, 64, 1, 1, 36),          # tcgen05 path, 5184 rows = 2 row chunks
 ]
 
 
@@ -232,9 +234,30 @@ def test_full_step_mlp(L, orc, seed):
     assert abs(pc.nu.item() - ref["nu"]) <= 1e-4 * ref["nu"]
 
 
+def _noise_floor(orc, layers, A, G, grads, hp, mode):
+    """Per-layer floor: the oracle on fp32-rounded factors vs on fp64 factors.
+    The GPU stores factors in fp32, so its P cannot be closer to the oracle than this."""
+    r32 = lambda xs: [np.asarray(x, np.float32).astype(np.float64) for x in xs]
+    outs = []
+    for fa, fg in ((A, G), (r32(A), r32(G))):
+        if mode == 2:
+            QA = [orc.damped_inverse(a, hp["damping"]) for a in fa]
+            QG = [orc.damped_inverse(g, hp["damping"]) for g in fg]
+            vA = vG = None
+        else:
+            QA, vA = orc.symeig_batch(fa)
+            QG, vG = orc.symeig_batch(fg)
+        outs.append(orc.precondition_batch(grads, QG, vG, QA, vA, hp["damping"], mode))
+    return [relF(b, a) for a, b in zip(*outs)]
+
+
 @pytest.mark.parametrize("variant", ["eigen", "factored", "inverse"])
 def test_full_step_r32_small_batch(L, orc, variant):
-    """ResNet-32 layer shapes (all 32 layers) at batch 4 so the oracle finishes in seconds."""
+    """ResNet-32 layer shapes (all 32 layers) at batch 4 so the oracle finishes in seconds.
+    The eigen path is graded at relF <= 1e-3.  The factored / explicit-inverse variants divide
+    by (v_G + g)(v_A + g) ~ g^2 on the null spaces of the rank-deficient stage-3 factors
+    (256 rows, d_A = 577), where fp32 factor storage alone moves P; there they are graded
+    against max(1e-3, 3 x the per-layer fp32-storage noise floor) (SURVEY 8(c) consequence 4)."""
     layers = shapes.resnet32(batch=4)
     hp = shapes.HPARAMS["r32"]
     acts, gouts, grads = layer_inputs(layers, seed=11)
@@ -243,14 +266,20 @@ def test_full_step_r32_small_batch(L, orc, variant):
     ref = orc.full_step(layers, acts, gouts, grads, hp["damping"], hp["lr"], hp["kappa"], mode=mode)
     for x, r in zip(pc.A + pc.G, ref["A"] + ref["G"]):
         assert relF(host(x), r) <= 1e-4
+    nu = ref["nu"]
     errs = [relF(p, r) for p, r in zip(P, ref["P"])]
-    assert max(errs) <= 1e-3, errs
+    if variant == "eigen":
+        assert max(errs) <= 1e-3, errs
+    else:
+        floors = _noise_floor(orc, layers, ref["A"], ref["G"], [g for g in grads], hp, mode)
+        bound = [max(1e-3, 3 * f) for f in floors]
+        assert all(e <= b for e, b in zip(errs, bound)), list(zip(errs, floors))
 
 
 def test_full_size_r50_sampled_layers(L, orc):
-    """Full ResNet-50 shapes (batch 32/GPU) for conv1 (401,408 rows, C_in = 3), a 1x1 conv and
-    the fc layer, in the launch configuration the bench uses (all 54 layers in one call);
-    the oracle checks the sampled layers one by one."""
+    """Full ResNet-50 shapes (batch 32/GPU) for conv1 (401,408 rows, C_in = 3, SIMT SYRK), a
+    1x1 conv (tcgen05 SYRK) and the fc layer (2049 x 1000 from 32 rows: both factors rank-
+    deficient, the worst-conditioned layer of the network), checked one by one."""
     layers = shapes.resnet50()
     hp = shapes.HPARAMS["r50"]
     pick = [0, 1, 53]
@@ -261,4 +290,6 @@ def test_full_size_r50_sampled_layers(L, orc):
     for x, r in zip(pc.A + pc.G, ref["A"] + ref["G"]):
         assert relF(host(x), r) <= 1e-4
     errs = [relF(p, r) for p, r in zip(P, ref["P"])]
-    assert max(errs) <= 1e-3, errs
+    floors = _noise_floor(orc, sub, ref["A"], ref["G"], grads, dict(hp, kappa=1e12), 0)
+    print("R50 sampled relF(P):", errs, "fp32-storage floors:", floors)
+    assert max(errs) <= 1e-3, (errs, floors)
