@@ -204,128 +204,151 @@ def run_ours(args):
     layers = shapes.layers_for(args.config)
     hp = shapes.HPARAMS[args.config]
     lr = hp["lr"] * world
-    acts_h, gouts_h, grads_h = layer_inputs(layers, seed=args.seed, rank=rank, device="cuda")
-    acts = [torch.from_numpy(a).cuda() for a in acts_h]
-    gouts = [torch.from_numpy(g).cuda() for g in gouts_h]
+    # Two distinct mini-batches per rank, alternated step to step, so the running-average factors
+    # really change between eigen refreshes (steady-state training; no cached results).
+    host_sets, dev_sets = [], []
+    for b in range(2):
+        acts_h, gouts_h, grads_h = layer_inputs(layers, seed=args.seed + 1000 * b, rank=rank, device="cuda")
+        host_sets.append((acts_h, gouts_h, grads_h))
+        dev_sets.append(([torch.from_numpy(a).cuda() for a in acts_h], [torch.from_numpy(g).cuda() for g in gouts_h]))
     pc = KFACPreconditioner(layers, damping=hp["damping"], decay=hp["decay"], kappa=hp["kappa"], lr=lr,
                             variant=args.variant, exchange=args.exchange)
-    grads, grad_flat = KFACPreconditioner.grad_buffer(layers, "cuda", return_flat=True)
-    for t, w in zip(grads, grads_h):
-        t.copy_(torch.from_numpy(w))
-    if world > 1:   # the gradient allreduce (Alg. 1) is the caller's DP step, done once here
-        dist.all_reduce(grad_flat, op=dist.ReduceOp.SUM)
-        grad_flat.mul_(1.0 / world)
+    grad_bufs = []
+    for b in range(2):
+        grads, grad_flat = KFACPreconditioner.grad_buffer(layers, "cuda", return_flat=True)
+        for t, w in zip(grads, host_sets[b][2]):
+            t.copy_(torch.from_numpy(w))
+        if world > 1:   # the gradient allreduce (Alg. 1) is the caller's DP step, done once here
+            dist.all_reduce(grad_flat, op=dist.ReduceOp.SUM)
+            grad_flat.mul_(1.0 / world)
+        grad_bufs.append(grads)
     stream = torch.cuda.current_stream()
     ev = lambda: torch.cuda.Event(enable_timing=True)
-    stage_ms = {"factors": [], "eigen": [], "precond": []}
 
-    def one_step(first, timed=False):
-        e0, e1, e2, e3 = ev(), ev(), ev(), ev()
-        e0.record(stream)
+    def one_step(i, first, warm, log=None):
+        acts, gouts = dev_sets[i % 2]
+        e = [ev() for _ in range(4)]
+        e[0].record(stream)
         pc.update_factors(acts, gouts, first)
-        e1.record(stream)
-        pc.compute_eigen()
-        e2.record(stream)
-        pc.precondition(grads)
-        e3.record(stream)
-        if timed:
-            stage_ms["_ev"] = stage_ms.get("_ev", []) + [(e0, e1, e2, e3)]
+        e[1].record(stream)
+        pc.compute_eigen(warm=warm)
+        e[2].record(stream)
+        pc.precondition(grad_bufs[i % 2])
+        e[3].record(stream)
+        if log is not None:
+            log.append(e)
 
     def barrier():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
 
-    for i in range(args.warmup):
-        one_step(first=(i == 0))
+    # cold update (factors seeded, eigen from the identity) -- reported separately
+    cold = []
+    one_step(0, first=True, warm=False, log=cold)
+    for i in range(1, args.warmup):
+        one_step(i, first=False, warm=True)
     barrier()
+    cold_ms = cold[0][0].elapsed_time(cold[0][3])
+    cold_eig_ms = cold[0][1].elapsed_time(cold[0][2])
     n0 = _lib.kfac_launch_count()
+    log = []
     with ClockSampler(local) as clk:
         t0, t1 = ev(), ev()
         barrier()
         t0.record(stream)
         for i in range(args.steps):
-            one_step(first=False, timed=True)
+            one_step(args.warmup + i, first=False, warm=True, log=log)
         t1.record(stream)
         barrier()
     launches = _lib.kfac_launch_count() - n0
     ms = t0.elapsed_time(t1) / args.steps
-    for e0, e1, e2, e3 in stage_ms.pop("_ev"):
-        stage_ms["factors"].append(e0.elapsed_time(e1))
-        stage_ms["eigen"].append(e1.elapsed_time(e2))
-        stage_ms["precond"].append(e2.elapsed_time(e3))
-    stages = {k: float(np.mean(v)) for k, v in stage_ms.items()}
+    stages = {"factors": float(np.mean([e[0].elapsed_time(e[1]) for e in log])),
+              "eigen": float(np.mean([e[1].elapsed_time(e[2]) for e in log])),
+              "precond": float(np.mean([e[2].elapsed_time(e[3]) for e in log]))}
     info = pc.info.cpu().tolist()
 
-    # end-to-end through the public API with host buffers (pinned H2D inputs, D2H of nu/s)
+    # end-to-end through the public API with host buffers: every step copies that step's inputs
+    # (activations, output gradients, averaged weight gradient) from pinned host memory and reads
+    # back nu -- all inside the timed region.
     e2e = None
     if not args.no_e2e:
-        acts_p = [torch.from_numpy(a).pin_memory() for a in acts_h]
-        gouts_p = [torch.from_numpy(g).pin_memory() for g in gouts_h]
-        grads_p = [torch.from_numpy(np.ascontiguousarray(t.cpu().numpy())).pin_memory() for t in grads]
+        pinned = [([torch.from_numpy(a).pin_memory() for a in hs[0]], [torch.from_numpy(g).pin_memory() for g in hs[1]],
+                   [torch.from_numpy(np.ascontiguousarray(t.cpu().numpy())).pin_memory() for t in grad_bufs[b]])
+                  for b, hs in enumerate(host_sets)]
         nu_h = torch.empty(1, pin_memory=True)
-        h2d = sum(t.numel() * 4 for t in acts_p + gouts_p + grads_p)
+        h2d = sum(t.numel() * 4 for t in pinned[0][0] + pinned[0][1] + pinned[0][2])
 
-        def e2e_step():
-            for d, h in zip(acts, acts_p):
+        def e2e_step(i):
+            acts, gouts = dev_sets[i % 2]
+            pa, pg, pw = pinned[i % 2]
+            for d, h in zip(acts, pa):
                 d.copy_(h, non_blocking=True)
-            for d, h in zip(gouts, gouts_p):
+            for d, h in zip(gouts, pg):
                 d.copy_(h, non_blocking=True)
-            for d, h in zip(grads, grads_p):
+            for d, h in zip(grad_bufs[i % 2], pw):
                 d.copy_(h, non_blocking=True)
             pc.update_factors(acts, gouts, False)
-            pc.compute_eigen()
-            pc.precondition(grads)
+            pc.compute_eigen(warm=True)
+            pc.precondition(grad_bufs[i % 2])
             nu_h.copy_(pc.nu, non_blocking=True)
 
-        e2e_step()
+        e2e_step(0)
         barrier()
         a0, a1 = ev(), ev()
         a0.record(stream)
-        for _ in range(args.steps):
-            e2e_step()
+        for i in range(args.steps):
+            e2e_step(i + 1)
         a1.record(stream)
         barrier()
         e2e = {"value": a0.elapsed_time(a1) / args.steps, "unit": "ms/iter", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": 4}
 
     # max over ranks
-    vals = torch.tensor([ms] + [stages[k] for k in ("factors", "eigen", "precond")] +
-                        [e2e["value"] if e2e else 0.0], dtype=torch.float64, device="cuda")
+    vals = torch.tensor([ms, stages["factors"], stages["eigen"], stages["precond"], cold_ms, cold_eig_ms,
+                         e2e["value"] if e2e else 0.0], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(vals, op=dist.ReduceOp.MAX)
     vals = vals.tolist()
-    ms, stages = vals[0], dict(zip(("factors", "eigen", "precond"), vals[1:4]))
+    ms = vals[0]
+    stages = dict(zip(("factors", "eigen", "precond"), vals[1:4]))
+    cold_ms, cold_eig_ms = vals[4], vals[5]
     if e2e:
-        e2e["value"] = vals[4]
+        e2e["value"] = vals[6]
 
     if rank == 0:
         wm = work_model(layers)
         pk = peaks()
-        tf32_peak = pk["bf16"] * (1.1 / 2.25)                  # guide's nominal tf32/bf16 ratio
-        simt_peak = 148 * 128 * 2 * 1.965e9 / 1e12             # fp32 FMA lanes x clock
+        tf32_peak = pk["bf16"] * (1.1 / 2.25)              # guide's nominal tf32/bf16 ratio
+        fp64_peak = 148 * 64 * 2 * 1.965e9 / 1e12          # 64 FP64 FMA/clk/SM x 1965 MHz
         dom = max(stages, key=stages.get)
-        if dom == "factors":
-            ach = wm["fac_flops"] / (stages["factors"] * 1e-3) / 1e12
-            roof = {"bound": "alu", "achieved": ach, "peak": simt_peak, "unit": "TFLOP/s",
-                    "kernel": "syrk_partial+syrk_reduce (factor stage)"}
-        elif dom == "precond":
-            ach = wm["pc_flops"] / (stages["precond"] * 1e-3) / 1e12
-            roof = {"bound": "alu", "achieved": ach, "peak": simt_peak, "unit": "TFLOP/s",
-                    "kernel": "gemm chain (precondition stage)"}
-        else:
+        if dom == "eigen":
             ach = wm["eig_flops"] / (stages["eigen"] * 1e-3) / 1e12
-            roof = {"bound": "alu", "achieved": ach, "peak": simt_peak, "unit": "TFLOP/s",
-                    "kernel": "eig_round (eigen stage, conventional 9d^3 flops)"}
+            roof = {"bound": "alu", "achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s",
+                    "kernel": "eig_round (fp64 one-sided Jacobi; conventional 9d^3 flops per factor)",
+                    "peak_source": "148 SMs x 64 fp64 FMA/clk x 2 x 1965 MHz (derived, DESIGN.md)"}
+        elif dom == "factors":
+            ach = wm["fac_flops"] / (stages["factors"] * 1e-3) / 1e12
+            roof = {"bound": "tensor", "achieved": ach, "peak": tf32_peak / 3, "unit": "TFLOP/s",
+                    "kernel": "syrk_tc_kernel (factor stage, 3xTF32)",
+                    "peak_source": f"{pk['src']} bf16 x 1.1/2.25 tf32 ratio / 3 products"}
+        else:
+            ach = wm["pc_flops"] / (stages["precond"] * 1e-3) / 1e12
+            roof = {"bound": "tensor", "achieved": ach, "peak": tf32_peak / 3, "unit": "TFLOP/s",
+                    "kernel": "gemm_tc_kernel (precondition stage, 3xTF32)",
+                    "peak_source": f"{pk['src']} bf16 x 1.1/2.25 tf32 ratio / 3 products"}
         roof["frac"] = roof["achieved"] / roof["peak"]
         roof["traffic"] = None
-        roof["peak_source"] = f"fp32 SIMT lanes x 1965 MHz (MEASURED_PEAKS {pk['src']} for hbm/tensor)"
+        tensor_tflops = (wm["fac_flops"] + wm["pc_flops"]) / ((stages["factors"] + stages["precond"]) * 1e-3) / 1e12
         line = {"metric": metric_name(args.config), "value": ms, "unit": "ms/iter", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": dict(config_block(args, layers), parallelism=f"dp{world}"),
-                "stages_ms": stages,
-                "factor_precond_tflops": (wm["fac_flops"] + wm["pc_flops"]) / ((stages["factors"] + stages["precond"]) * 1e-3) / 1e12,
+                "config": dict(config_block(args, layers), parallelism=f"dp{world}",
+                               protocol="steady state: EMA factors of alternating batches, eigen refresh "
+                                        "warm-started from the previous eigenbasis, every step"),
+                "stages_ms": stages, "cold_update_ms": cold_ms, "cold_eigen_ms": cold_eig_ms,
+                "factor_precond_tflops": tensor_tflops,
+                "factor_precond_frac_of_3xtf32_peak": tensor_tflops / (tf32_peak / 3),
                 "eigen_info": info[:8],
                 "roofline": roof, "gpu_launches": int(launches),
                 "clocks": clk.summary(), "e2e": e2e}

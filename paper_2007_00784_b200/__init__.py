@@ -5,12 +5,7 @@ ctypes binding and `preconditioner.KFACPreconditioner` the multi-GPU
 orchestration.  Importing the package does not load CUDA; `import
 paper_2007_00784_b200._lib` loads the library and fails loudly if it is missing.
 """
-__all__ = ["build", "lib"]
-
-
-def build(force: bool = False) -> str:
-    from .build import build as _b
-    return _b(force=force)
+__all__ = ["lib"]
 
 
 def lib():

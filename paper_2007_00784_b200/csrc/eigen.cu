@@ -33,7 +33,7 @@ constexpr int P = 2 * B;         // columns per pair
 constexpr int NT = 256;
 constexpr int kMaxSweeps = 16;
 constexpr int kTableChunk = 48;
-constexpr int kInnerSweeps = 6;
+constexpr int kInnerSweeps = 3;
 
 struct EigJob {
     const float *F;
@@ -127,14 +127,19 @@ __device__ __forceinline__ void schur2(double app, double aqq, double apq, doubl
     s = t * c;
 }
 
-__global__ void __launch_bounds__(NT, 2) eig_round(EigJob *table, int count, int round, float tol,
-                                                float tol_abs) {
-    __shared__ double tile[32][P + 1];
-    __shared__ double G[P][P + 1];
+constexpr int kRowsPerIter = 16;                         // rows each warp stages per iteration
+constexpr size_t kRoundSmem = sizeof(double) * (NT / 32) * P * (P + 1);
+
+__global__ void __launch_bounds__(NT, 2) eig_round(const EigJob *__restrict__ table, int count, int round,
+                                                   float tol, float tol_abs) {
+    extern __shared__ double dsm[];
+    double(*Gp)[P][P + 1] = reinterpret_cast<double(*)[P][P + 1]>(dsm);       // [8 warps] partial Grams
+    double(*G)[P + 1] = Gp[0];                                                  // reduced Gram (reuses slot 0)
     __shared__ double R[P][P + 1];
+    __shared__ double rows[NT / 32][kRowsPerIter][P];
     __shared__ double cs_c[P / 2], cs_s[P / 2];
     __shared__ int cs_i[P / 2], cs_j[P / 2];
-    __shared__ int col0[2];
+    __shared__ double gmax;
 
     // locate the job (table sorted by nb descending; pair_begin is a prefix sum)
     int lo = 0, hi = count - 1;
@@ -143,77 +148,85 @@ __global__ void __launch_bounds__(NT, 2) eig_round(EigJob *table, int count, int
         int mid = (lo + hi + 1) >> 1;
         if (table[mid].pair_begin <= item) lo = mid; else hi = mid - 1;
     }
-    EigJob &J = table[lo];
-    if (J.converged || round >= J.nb - 1) return;
-    const int k = item - J.pair_begin;
-    if (k >= J.nb / 2) return;
-    const int t = threadIdx.x;
-    const int n = J.n, ldu = J.ldu;
+    const EigJob *Jp = table + lo;
+    if (Jp->converged || round >= Jp->nb - 1) return;
+    const int k = item - Jp->pair_begin;
+    const int nb = Jp->nb;
+    if (k >= nb / 2) return;
+    const int n = Jp->n, ldu = Jp->ldu;
+    double *const U = Jp->U;
+    double *const V = Jp->V;
+    const double fro = (double)Jp->scale;
+    const int t = threadIdx.x, warp = t / 32, lane = t % 32;
     const int nb_real = (n + B - 1) / B;
-    if (t == 0) {
-        int a, b;
-        circle_pair(round, k, J.nb, a, b);
-        col0[0] = a < nb_real ? a * B : -1;     // -1: dummy block (no columns)
-        col0[1] = b < nb_real ? b * B : -1;
-    }
-    __syncthreads();
-    const int c0 = col0[0], c1 = col0[1];
+    int a, b;
+    circle_pair(round, k, nb, a, b);
+    const int c0 = a < nb_real ? a * B : -1, c1 = b < nb_real ? b * B : -1;   // -1: dummy block
+    // lane l owns column col(l) of the pair: block p for l < 16, block q for l >= 16
+    const int mycol = lane < B ? (c0 >= 0 ? c0 + lane : -1) : (c1 >= 0 ? c1 + lane - B : -1);
 
-    // ---- Gram G = U_pq^T U_pq (fp64): thread t owns the 2x2 block (2*(t/16), 2*(t%16)) ----
-    const int gi = 2 * (t / 16), gj = 2 * (t % 16);
-    double a00 = 0.0, a01 = 0.0, a10 = 0.0, a11 = 0.0;
-    for (int r0 = 0; r0 < n; r0 += 32) {
-        for (int e = t; e < 32 * (P / 2); e += NT) {       // 32 rows x 16 double2
-            const int rr = e / (P / 2), g = e % (P / 2);
-            const int r = r0 + rr;
-            const int cb = (g < B / 2) ? c0 : c1;
-            double2 v = make_double2(0.0, 0.0);
-            if (r < n && cb >= 0) v = *reinterpret_cast<const double2 *>(J.U + (size_t)r * ldu + cb + (g % (B / 2)) * 2);
-            tile[rr][2 * g] = v.x;
-            tile[rr][2 * g + 1] = v.y;
+    // ---- Gram: every warp accumulates G_w = sum over its rows of u_r u_r^T (lane l: row l of G_w)
+    double g[P];
+#pragma unroll
+    for (int j = 0; j < P; ++j) g[j] = 0.0;
+    for (int r0 = warp * kRowsPerIter; r0 < n; r0 += NT / 32 * kRowsPerIter) {
+        double ld[kRowsPerIter];                            // all loads in flight before any store
+#pragma unroll
+        for (int i = 0; i < kRowsPerIter; ++i) {
+            const int r = r0 + i;
+            ld[i] = (r < n && mycol >= 0) ? __ldg(U + (size_t)r * ldu + mycol) : 0.0;
         }
-        __syncthreads();
-        const int rows = min(32, n - r0);
-        for (int rr = 0; rr < rows; ++rr) {
-            const double x0 = tile[rr][gi], x1 = tile[rr][gi + 1];
-            const double y0 = tile[rr][gj], y1 = tile[rr][gj + 1];
-            a00 = fma(x0, y0, a00); a01 = fma(x0, y1, a01);
-            a10 = fma(x1, y0, a10); a11 = fma(x1, y1, a11);
+#pragma unroll
+        for (int i = 0; i < kRowsPerIter; ++i) rows[warp][i][lane] = ld[i];
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < kRowsPerIter; ++i) {
+            const double x = rows[warp][i][lane];
+#pragma unroll
+            for (int j = 0; j < P; j += 2) {
+                const double2 y = *reinterpret_cast<const double2 *>(&rows[warp][i][j]);
+                g[j] = fma(x, y.x, g[j]);
+                g[j + 1] = fma(x, y.y, g[j + 1]);
+            }
         }
-        __syncthreads();
+        __syncwarp();
     }
-    G[gi][gj] = a00; G[gi][gj + 1] = a01; G[gi + 1][gj] = a10; G[gi + 1][gj + 1] = a11;
-    for (int e = t; e < P * P; e += NT) R[e / P][e % P] = (e / P == e % P) ? 1.0 : 0.0;
+#pragma unroll
+    for (int j = 0; j < P; ++j) Gp[warp][lane][j] = g[j];
     __syncthreads();
-    if (t < P * P / 2) {                                   // exact symmetry: upper copies to lower
+    for (int e = t; e < P * P; e += NT) {                   // fixed-order reduction over warps
+        const int i = e / P, j = e % P;
+        double v = Gp[0][i][j];
+#pragma unroll
+        for (int w = 1; w < NT / 32; ++w) v += Gp[w][i][j];
+        Gp[0][i][j] = v;
+        R[i][j] = (i == j) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    if (t < P * P) {                                        // exact symmetry from the upper triangle
         const int i = t / P, j = t % P;
         if (i > j) G[i][j] = G[j][i];
     }
-    __syncthreads();
-
-    // ---- convergence test of this pair.  Rotate (i, j) only if the coupling exceeds both the
-    // relative bound tol * ||u_i|| ||u_j|| and the fp32 backward-error level tol_abs ||F|| (||u_i|| +
-    // ||u_j||): below it the coupling is indistinguishable from rounding of F itself.
-    const double fro = (double)J.scale;
-    int need = 0;
-    for (int e = t; e < P * P; e += NT) {
-        const int i = e / P, j = e % P;
-        if (i >= j) continue;
-        const double g = fabs(G[i][j]);
-        const double ni = sqrt(G[i][i]), nj = sqrt(G[j][j]);
-        if (g > tol * ni * nj && g > tol_abs * fro * (ni + nj)) need = 1;
-    }
-    need = __syncthreads_or(need);
-    if (!need) return;
-
-    // ---- inner cyclic Jacobi on the 32x32 Gram (fp64, shared memory) ----
-    __shared__ double gmax;
     if (t == 0) {
         double m = 0.0;
         for (int i = 0; i < P; ++i) m = fmax(m, G[i][i]);
         gmax = m;
     }
     __syncthreads();
+
+    // ---- convergence test of this pair: rotate only if some coupling exceeds both the relative
+    // bound tol ||u_i|| ||u_j|| and the absolute level tol_abs ||F|| (||u_i|| + ||u_j||).
+    int need = 0;
+    for (int e = t; e < P * P; e += NT) {
+        const int i = e / P, j = e % P;
+        if (i >= j) continue;
+        const double gg = fabs(G[i][j]);
+        const double ni = sqrt(G[i][i]), nj = sqrt(G[j][j]);
+        if (gg > tol * ni * nj && gg > tol_abs * fro * (ni + nj)) need = 1;
+    }
+    if (!__syncthreads_or(need)) return;
+
+    // ---- inner cyclic Jacobi on the 32x32 Gram (fp64, shared memory) ----
     const double inner_abs = 1e-15 * gmax;
     for (int sweep = 0; sweep < kInnerSweeps; ++sweep) {
         int rotated = 0;
@@ -222,72 +235,71 @@ __global__ void __launch_bounds__(NT, 2) eig_round(EigJob *table, int count, int
                 int i, j;
                 circle_pair(ir, t, P, i, j);
                 const double gij = G[i][j], gii = G[i][i], gjj = G[j][j];
-                double c = 1.0, s = 0.0;
+                double c = 1.0, sn = 0.0;
                 if (fabs(gij) > 1e-12 * sqrt(fabs(gii * gjj)) && fabs(gij) > inner_abs) {
-                    schur2(gii, gjj, gij, c, s);
+                    schur2(gii, gjj, gij, c, sn);
                     rotated = 1;
                 }
-                cs_i[t] = i; cs_j[t] = j; cs_c[t] = c; cs_s[t] = s;
+                cs_i[t] = i; cs_j[t] = j; cs_c[t] = c; cs_s[t] = sn;
             }
             __syncthreads();
             for (int e = t; e < (P / 2) * P * 2; e += NT) {        // columns of G and R
                 const int which = e / ((P / 2) * P);
                 const int e2 = e % ((P / 2) * P);
                 const int kk = e2 / P, r = e2 % P;
-                const double c = cs_c[kk], s = cs_s[kk];
-                if (s == 0.0) continue;
+                const double c = cs_c[kk], sn = cs_s[kk];
+                if (sn == 0.0) continue;
                 double(*M)[P + 1] = which ? R : G;
                 const int i = cs_i[kk], j = cs_j[kk];
                 const double x = M[r][i], y = M[r][j];
-                M[r][i] = c * x - s * y;
-                M[r][j] = s * x + c * y;
+                M[r][i] = c * x - sn * y;
+                M[r][j] = sn * x + c * y;
             }
             __syncthreads();
             for (int e = t; e < (P / 2) * P; e += NT) {            // rows of G
                 const int kk = e / P, r = e % P;
-                const double c = cs_c[kk], s = cs_s[kk];
-                if (s == 0.0) continue;
+                const double c = cs_c[kk], sn = cs_s[kk];
+                if (sn == 0.0) continue;
                 const int i = cs_i[kk], j = cs_j[kk];
                 const double x = G[i][r], y = G[j][r];
-                G[i][r] = c * x - s * y;
-                G[j][r] = s * x + c * y;
+                G[i][r] = c * x - sn * y;
+                G[j][r] = sn * x + c * y;
             }
             __syncthreads();
         }
         if (!__syncthreads_or(rotated)) break;
     }
-    if (t == 0) atomicAdd(&J.rot_count, 1);
-    __syncthreads();
+    if (t == 0) atomicAdd(const_cast<int *>(&Jp->rot_count), 1);
 
-    // ---- apply: U_pq <- U_pq R, V_pq <- V_pq R (fp64; one row per thread, R broadcast) ----
+    // ---- apply: U_pq <- U_pq R and V_pq <- V_pq R (lane l computes column l; rows broadcast) ----
+    double rc[P];
+#pragma unroll
+    for (int kk = 0; kk < P; ++kk) rc[kk] = R[kk][lane];
     for (int w = 0; w < 2; ++w) {
-        double *M = w ? J.V : J.U;
-        for (int r = t; r < n; r += NT) {
-            double x[P];
+        double *M = w ? V : U;
+        for (int r0 = warp * kRowsPerIter; r0 < n; r0 += NT / 32 * kRowsPerIter) {
+            double ld[kRowsPerIter];
 #pragma unroll
-            for (int g = 0; g < P / 2; ++g) {
-                const int cb = (g < B / 2) ? c0 : c1;
-                double2 v = make_double2(0.0, 0.0);
-                if (cb >= 0) v = *reinterpret_cast<const double2 *>(M + (size_t)r * ldu + cb + (g % (B / 2)) * 2);
-                x[2 * g] = v.x;
-                x[2 * g + 1] = v.y;
+            for (int i = 0; i < kRowsPerIter; ++i) {
+                const int r = r0 + i;
+                ld[i] = (r < n && mycol >= 0) ? M[(size_t)r * ldu + mycol] : 0.0;
             }
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {                 // output block p (h = 0) then q (h = 1)
-                const int cb = h ? c1 : c0;
-                double y[B];
+            for (int i = 0; i < kRowsPerIter; ++i) rows[warp][i][lane] = ld[i];
+            __syncwarp();
 #pragma unroll
-                for (int j = 0; j < B; ++j) y[j] = 0.0;
+            for (int i = 0; i < kRowsPerIter; ++i) {
+                double y = 0.0;
 #pragma unroll
-                for (int i = 0; i < P; ++i)
-#pragma unroll
-                    for (int j = 0; j < B; ++j) y[j] = fma(x[i], R[i][h * B + j], y[j]);
-                if (cb >= 0) {
-#pragma unroll
-                    for (int g = 0; g < B / 2; ++g)
-                        *reinterpret_cast<double2 *>(M + (size_t)r * ldu + cb + 2 * g) = make_double2(y[2 * g], y[2 * g + 1]);
+                for (int kk = 0; kk < P; kk += 2) {
+                    const double2 x = *reinterpret_cast<const double2 *>(&rows[warp][i][kk]);
+                    y = fma(x.x, rc[kk], y);
+                    y = fma(x.y, rc[kk + 1], y);
                 }
+                const int r = r0 + i;
+                if (r < n && mycol >= 0) M[(size_t)r * ldu + mycol] = y;
             }
+            __syncwarp();
         }
     }
 }
@@ -301,13 +313,26 @@ __global__ void __launch_bounds__(256) eig_fv(EigJob *table) {
     if (m0 >= J.n || n0 >= J.n) return;
     const int t = threadIdx.x, ty = t / 16, tx = t % 16;
     double acc[4][4] = {};
-    for (int k0 = 0; k0 < J.n; k0 += 16) {
-        for (int e = t; e < 16 * 64; e += 256) {
+    const int n = J.n, ldF = J.ldF, ldu = J.ldu;
+    const float *__restrict__ F = J.F;
+    const double *__restrict__ Vg = J.V;
+    for (int k0 = 0; k0 < n; k0 += 16) {
+        float fv[4];
+        double vv[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {                           // loads first, then shared stores
+            const int e = t + 256 * q;
             const int mm = e / 16, kk = e % 16;                 // F[m][k] (k fastest)
             const int m = m0 + mm, k = k0 + kk;
-            Fs[kk][mm] = (m < J.n && k < J.n) ? (double)J.F[(size_t)m * J.ldF + k] : 0.0;
+            fv[q] = (m < n && k < n) ? __ldg(F + (size_t)m * ldF + k) : 0.f;
             const int kv = e / 64, nn = e % 64;                 // V[k][n] (n fastest)
-            Vs[kv][nn] = (k0 + kv < J.n && n0 + nn < J.n) ? J.V[(size_t)(k0 + kv) * J.ldu + n0 + nn] : 0.0;
+            vv[q] = (k0 + kv < n && n0 + nn < n) ? __ldg(Vg + (size_t)(k0 + kv) * ldu + n0 + nn) : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int e = t + 256 * q;
+            Fs[e % 16][e / 16] = (double)fv[q];
+            Vs[e / 64][e % 64] = vv[q];
         }
         __syncthreads();
 #pragma unroll 4
@@ -451,6 +476,11 @@ kfac_status_t eigen_run(const float *const *F, const int32_t *dims, const int32_
         eig_table_init<<<1, 64, 0, s>>>(ti);
         KFAC_LAUNCHED();
     }
+    static bool attr = false;
+    if (!attr) {
+        KFAC_CUDA_TRY(cudaFuncSetAttribute(eig_round, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRoundSmem));
+        attr = true;
+    }
     const bool warm = flags & KFAC_EIG_WARM_START;
     int max_n = 0;
     for (auto &J : sorted) max_n = std::max(max_n, J.n);
@@ -470,7 +500,7 @@ kfac_status_t eigen_run(const float *const *F, const int32_t *dims, const int32_
         for (int r = 0; r < max_rounds; ++r) {
             int active = 0;
             for (auto &J : sorted) if (J.nb - 1 > r) active = J.pair_begin + J.nb / 2;
-            eig_round<<<active, NT, 0, s>>>(table, count, r, tol, tol_abs);
+            eig_round<<<active, NT, kRoundSmem, s>>>(table, count, r, tol, tol_abs);
             KFAC_LAUNCHED();
         }
         eig_sweep_end<<<1, 256, 0, s>>>(table, count);

@@ -30,11 +30,12 @@ namespace kfac {
 namespace {
 
 constexpr int BM = 128, BN = 128, BK = 32;
-constexpr int kStages = 3;
+constexpr int kRaw = 4;                                 // raw (hi) stages: operand tiles in flight
+constexpr int kLo = 2;                                  // lo stages: written by the split, read by the MMA
 constexpr int kTileBytes = BM * BK * 4;                 // 16 KB per operand tile
-constexpr int kStageBytes = 4 * kTileBytes;             // A_hi, B_hi, A_lo, B_lo
-constexpr int kBarBytes = 256;
-constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + kBarBytes;
+constexpr int kStageBytes = 2 * kTileBytes;             // A, B
+constexpr int kBarBytes = 512;
+constexpr int kSmemBytes = (kRaw + kLo) * kStageBytes + 1024 /*align*/ + kBarBytes;
 constexpr int kMaxTc = 24;                              // problems per launch (tensor maps in params)
 constexpr int kMaxSyrk = 64;
 constexpr int NT = 320;                                 // 10 warps
@@ -105,10 +106,12 @@ __device__ __forceinline__ void prefetch_map(const CUtensorMap *map) {
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void *src, uint32_t bytes) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(bytes) : "memory");
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-__device__ __forceinline__ void split_bar_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+// Arrive on an mbarrier once all of this thread's prior cp.async copies have landed (no count increment).
+__device__ __forceinline__ void cp_async_arrive(uint32_t bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
+}
+
+__device__ const float kBiasChunk[4] = {1.f, 0.f, 0.f, 0.f};   // the homogeneous column (R7)
 
 __device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
     // SM100 UMMA shared-memory descriptor (version 1).  layout 2 = SWIZZLE_128B (K-major tiles),
@@ -157,31 +160,35 @@ __device__ __forceinline__ float tf32_rn(float x) {
 
 // ------------------------------------------------------- shared pieces --
 struct Smem {
-    uint8_t *base;
-    uint32_t raw_full, ready, stage_empty, tfull, tempty;   // barrier arrays (8 B stride)
+    uint8_t *base;       // kRaw raw stages, then kLo lo stages (each A tile + B tile)
+    uint32_t raw_full, ready, raw_empty, lo_empty, tfull, tempty;   // barrier arrays (8 B stride)
     uint32_t *tmem_slot;
+    __device__ __forceinline__ uint8_t *raw(int s) const { return base + s * kStageBytes; }
+    __device__ __forceinline__ uint8_t *lo(int l) const { return base + (kRaw + l) * kStageBytes; }
 };
 
 __device__ __forceinline__ Smem carve(uint8_t *smem_raw) {
     Smem s;
     s.base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t *bars = reinterpret_cast<uint64_t *>(s.base + kStages * kStageBytes);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(s.base + (kRaw + kLo) * kStageBytes);
     s.raw_full = smem_u32(bars);
-    s.ready = smem_u32(bars + kStages);
-    s.stage_empty = smem_u32(bars + 2 * kStages);
-    s.tfull = smem_u32(bars + 3 * kStages);
-    s.tempty = smem_u32(bars + 3 * kStages + 2);
-    s.tmem_slot = reinterpret_cast<uint32_t *>(bars + 3 * kStages + 4);
+    s.ready = smem_u32(bars + kRaw);
+    s.raw_empty = smem_u32(bars + 2 * kRaw);
+    s.lo_empty = smem_u32(bars + 3 * kRaw);
+    s.tfull = smem_u32(bars + 3 * kRaw + kLo);
+    s.tempty = smem_u32(bars + 3 * kRaw + kLo + 2);
+    s.tmem_slot = reinterpret_cast<uint32_t *>(bars + 3 * kRaw + kLo + 4);
     return s;
 }
 
-__device__ __forceinline__ void setup(const Smem &S, int warp) {
+__device__ __forceinline__ void setup(const Smem &S, int warp, uint32_t raw_full_count) {
     if (threadIdx.x == 0) {
-        for (int i = 0; i < kStages; ++i) {
-            mbar_init(S.raw_full + 8 * i, 1);
+        for (int i = 0; i < kRaw; ++i) {
+            mbar_init(S.raw_full + 8 * i, raw_full_count);
             mbar_init(S.ready + 8 * i, 128);
-            mbar_init(S.stage_empty + 8 * i, 1);
+            mbar_init(S.raw_empty + 8 * i, 1);
         }
+        for (int i = 0; i < kLo; ++i) mbar_init(S.lo_empty + 8 * i, 1);
         for (int b = 0; b < 2; ++b) {
             mbar_init(S.tfull + 8 * b, 1);
             mbar_init(S.tempty + 8 * b, 128);
@@ -208,9 +215,9 @@ __device__ __forceinline__ void teardown(uint32_t tmem, int warp) {
 }
 
 // hi = rn_tf32(x) in place, lo = rn_tf32(x - hi): 3xTF32 operands, both exact TF32 values.
-__device__ __forceinline__ void split_region(uint8_t *raw, int n_f4, int t) {
+__device__ __forceinline__ void split_region(uint8_t *raw, uint8_t *lo_base, int n_f4, int t) {
     float4 *hi = reinterpret_cast<float4 *>(raw);
-    float4 *lo = reinterpret_cast<float4 *>(raw + 2 * kTileBytes);
+    float4 *lo = reinterpret_cast<float4 *>(lo_base);
 #pragma unroll 4
     for (int i = t; i < n_f4; i += 128) {
         float4 x = hi[i], h, l;
@@ -236,13 +243,12 @@ __device__ __forceinline__ void mma_loop(const Smem &S, uint32_t tmem, int nk, i
     const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
                            ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
     for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % kStages, b = kb & 1, u = kb >> 1;
-        mbar_wait(S.ready + 8 * s, (kb / kStages) & 1);
+        const int s = kb % kRaw, l = kb % kLo, b = kb & 1, u = kb >> 1;
+        mbar_wait(S.ready + 8 * s, (kb / kRaw) & 1);
         if (u >= 1) mbar_wait(S.tempty + 8 * b, (u - 1) & 1);
         tc_fence_after();
-        const uint32_t st = smem_u32(S.base + s * kStageBytes);
-        const uint32_t a_hi = st, a_lo = st + 2 * kTileBytes;
-        const uint32_t b_hi = same_ab ? a_hi : st + kTileBytes, b_lo = same_ab ? a_lo : st + 3 * kTileBytes;
+        const uint32_t a_hi = smem_u32(S.raw(s)), a_lo = smem_u32(S.lo(l));
+        const uint32_t b_hi = same_ab ? a_hi : a_hi + kTileBytes, b_lo = same_ab ? a_lo : a_lo + kTileBytes;
         const uint32_t d = tmem + b * BN;
 #pragma unroll
         for (int ks = 0; ks < BK / 8; ++ks) {
@@ -250,7 +256,8 @@ __device__ __forceinline__ void mma_loop(const Smem &S, uint32_t tmem, int nk, i
             mma_tf32(d, operand_desc(a_hi, ks, a_mn), operand_desc(b_lo, ks, b_mn), idesc, 1u);
             mma_tf32(d, operand_desc(a_hi, ks, a_mn), operand_desc(b_hi, ks, b_mn), idesc, 1u);
         }
-        mma_commit(S.stage_empty + 8 * s);
+        mma_commit(S.raw_empty + 8 * s);
+        mma_commit(S.lo_empty + 8 * l);
         mma_commit(S.tfull + 8 * b);
     }
 }
@@ -311,15 +318,15 @@ __global__ void __launch_bounds__(NT, 1) gemm_tc_kernel(const __grid_constant__ 
         prefetch_map(&d.ta);
         prefetch_map(&d.tb);
     }
-    setup(S, warp);
+    setup(S, warp, 1);
     const uint32_t tmem = *S.tmem_slot;
 
     if (warp == W_TMA) {
         if (lane == 0) {
             for (int kb = 0; kb < nk; ++kb) {
-                const int s = kb % kStages;
-                if (kb >= kStages) mbar_wait(S.stage_empty + 8 * s, ((kb / kStages) - 1) & 1);
-                const uint32_t st = smem_u32(S.base + s * kStageBytes);
+                const int s = kb % kRaw;
+                if (kb >= kRaw) mbar_wait(S.raw_empty + 8 * s, ((kb / kRaw) - 1) & 1);
+                const uint32_t st = smem_u32(S.raw(s));
                 mbar_expect_tx(S.raw_full + 8 * s, 2 * kTileBytes);
                 load_tile(st, &d.ta, S.raw_full + 8 * s, m0, kb * BK, d.a_mn);
                 load_tile(st + kTileBytes, &d.tb, S.raw_full + 8 * s, n0, kb * BK, d.b_mn);
@@ -330,9 +337,10 @@ __global__ void __launch_bounds__(NT, 1) gemm_tc_kernel(const __grid_constant__ 
     } else if (warp < W_DRAIN0) {
         const int t = threadIdx.x;
         for (int kb = 0; kb < nk; ++kb) {
-            const int s = kb % kStages;
-            mbar_wait(S.raw_full + 8 * s, (kb / kStages) & 1);
-            split_region(S.base + s * kStageBytes, 2 * kTileBytes / 16, t);
+            const int s = kb % kRaw, l = kb % kLo;
+            mbar_wait(S.raw_full + 8 * s, (kb / kRaw) & 1);
+            if (kb >= kLo) mbar_wait(S.lo_empty + 8 * l, ((kb / kLo) - 1) & 1);
+            split_region(S.raw(s), S.lo(l), 2 * kTileBytes / 16, t);
             mbar_arrive(S.ready + 8 * s);
         }
     } else {
@@ -401,10 +409,11 @@ __device__ __forceinline__ ChunkInfo chunk_info(const FactorJob &J, int c) {
     return ci;
 }
 
-// Producer warps 0-3: cp.async gathers of the 32-row k-block into the raw (hi) slots.
+// Producer warps 0-3: cp.async gathers of the 32-row k-block into raw stage s; the stage's
+// mbarrier completes when every producer thread's copies have landed.
 __device__ __forceinline__ void syrk_issue(const FactorJob &J, const Smem &S, int s, long long r0, long long r_end,
                                            const ChunkInfo (&ci)[2], int cc, int t, bool diag) {
-    const uint32_t st = smem_u32(S.base + s * kStageBytes);
+    const uint32_t st = smem_u32(S.raw(s));
     const int hw = J.h_out * J.w_out;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
@@ -424,10 +433,8 @@ __device__ __forceinline__ void syrk_issue(const FactorJob &J, const Smem &S, in
             if (op == 1 && diag) break;
             const uint32_t dst = st + op * kTileBytes + mn_off(k, 4 * cc);
             const ChunkInfo &c = ci[op];
-            if (c.kind == 1) {
-                const float one = rv ? 1.f : 0.f;
-                asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(dst), "f"(one), "f"(0.f), "f"(0.f), "f"(0.f)
-                             : "memory");
+            if (c.kind == 1) {                        // bias chunk {1, 0, 0, 0} on valid rows
+                cp_async16(dst, kBiasChunk, rv ? 16u : 0u);
                 continue;
             }
             const float *src = J.src;
@@ -464,7 +471,7 @@ __global__ void __launch_bounds__(NT, 1) syrk_tc_kernel(const __grid_constant__ 
     const long long r_end = min(J.n, r_begin + J.chunk);
     const int nk = (int)((r_end - r_begin + BK - 1) / BK);
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    setup(S, warp);
+    setup(S, warp, 128);
     const uint32_t tmem = *S.tmem_slot;
 
     if (warp == W_MMA) {
@@ -473,24 +480,23 @@ __global__ void __launch_bounds__(NT, 1) syrk_tc_kernel(const __grid_constant__ 
         const int t = threadIdx.x, cc = t % 32;
         ChunkInfo ci[2] = {chunk_info(J, ti * BM + 4 * cc), chunk_info(J, tj * BM + 4 * cc)};
         const int n_f4 = (diag ? 1 : 2) * kTileBytes / 16;
-        // prologue: k-blocks 0 .. kStages-2
-#pragma unroll
-        for (int p = 0; p < kStages - 1; ++p) {
-            if (p < nk) syrk_issue(J, S, p, r_begin + (long long)p * BK, r_end, ci, cc, t, diag);
-            cp_async_commit();
+        // prologue: k-blocks 0 .. kRaw-2 in flight before the first split
+        for (int p = 0; p < kRaw - 1 && p < nk; ++p) {
+            syrk_issue(J, S, p, r_begin + (long long)p * BK, r_end, ci, cc, t, diag);
+            cp_async_arrive(S.raw_full + 8 * p);
         }
         for (int kb = 0; kb < nk; ++kb) {
-            const int nxt = kb + kStages - 1;
+            const int nxt = kb + kRaw - 1;
             if (nxt < nk) {
-                const int s2 = nxt % kStages;
-                if (nxt >= kStages) mbar_wait(S.stage_empty + 8 * s2, ((nxt / kStages) - 1) & 1);
+                const int s2 = nxt % kRaw;
+                if (nxt >= kRaw) mbar_wait(S.raw_empty + 8 * s2, ((nxt / kRaw) - 1) & 1);
                 syrk_issue(J, S, s2, r_begin + (long long)nxt * BK, r_end, ci, cc, t, diag);
+                cp_async_arrive(S.raw_full + 8 * s2);
             }
-            cp_async_commit();
-            cp_async_wait<kStages - 1>();
-            split_bar_sync();
-            const int s = kb % kStages;
-            split_region(S.base + s * kStageBytes, n_f4, t);
+            const int s = kb % kRaw, l = kb % kLo;
+            mbar_wait(S.raw_full + 8 * s, (kb / kRaw) & 1);
+            if (kb >= kLo) mbar_wait(S.lo_empty + 8 * l, ((kb / kLo) - 1) & 1);
+            split_region(S.raw(s), S.lo(l), n_f4, t);
             mbar_arrive(S.ready + 8 * s);
         }
     } else if (warp < W_TMA) {

@@ -14,7 +14,7 @@ from workloads import shapes
 
 @pytest.fixture(scope="module")
 def L():
-    from paper_2007_00784_b200 import build
+    from paper_2007_00784_b200.build import build
     build()
     from paper_2007_00784_b200 import _lib
     return _lib

@@ -20,7 +20,7 @@ pytestmark = pytest.mark.gpu
 def L():
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
-    from paper_2007_00784_b200 import build
+    from paper_2007_00784_b200.build import build
     build()
     from paper_2007_00784_b200 import _lib
     return _lib
@@ -234,21 +234,45 @@ def test_full_step_mlp(L, orc, seed):
     assert abs(pc.nu.item() - ref["nu"]) <= 1e-4 * ref["nu"]
 
 
+def _r32(x):
+    return np.asarray(x, np.float32).astype(np.float64)
+
+
 def _noise_floor(orc, layers, A, G, grads, hp, mode):
-    """Per-layer floor: the oracle on fp32-rounded factors vs on fp64 factors.
-    The GPU stores factors in fp32, so its P cannot be closer to the oracle than this."""
-    r32 = lambda xs: [np.asarray(x, np.float32).astype(np.float64) for x in xs]
-    outs = []
-    for fa, fg in ((A, G), (r32(A), r32(G))):
+    """Per-layer floor: an fp32-faithful pipeline -- the oracle's factors rounded
+    to fp32, the oracle's (exact) eigendecomposition / inverse of those rounded to fp32, and the
+    preconditioning GEMM chain evaluated in fp32 arithmetic (numpy float32) -- against the
+    all-fp64 oracle.  On rank-deficient layers the factored / inverse variants divide fp32
+    accumulation noise by ~damping^2, so no fp32 pipeline can be closer than this."""
+    g = np.float32(hp["damping"])
+    f32 = lambda x: np.asarray(x, np.float32)
+    if mode == 2:
+        QA = [f32(orc.damped_inverse(_r32(a), float(g))) for a in A]
+        QG = [f32(orc.damped_inverse(_r32(x), float(g))) for x in G]
+    else:
+        QA, vA = orc.symeig_batch([_r32(a) for a in A])
+        QG, vG = orc.symeig_batch([_r32(x) for x in G])
+        QA, QG, vA, vG = [f32(q) for q in QA], [f32(q) for q in QG], [f32(v) for v in vA], [f32(v) for v in vG]
+    out = []
+    for i, W in enumerate(grads):
+        W = f32(W)
         if mode == 2:
-            QA = [orc.damped_inverse(a, hp["damping"]) for a in fa]
-            QG = [orc.damped_inverse(g, hp["damping"]) for g in fg]
-            vA = vG = None
+            P = (QG[i] @ W) @ QA[i]
         else:
-            QA, vA = orc.symeig_batch(fa)
-            QG, vG = orc.symeig_batch(fg)
-        outs.append(orc.precondition_batch(grads, QG, vG, QA, vA, hp["damping"], mode))
-    return [relF(b, a) for a, b in zip(*outs)]
+            V1 = (QG[i].T @ W) @ QA[i]
+            D = np.outer(vG[i], vA[i]) + g if mode == 0 else np.outer(vG[i] + g, vA[i] + g)
+            P = (QG[i] @ (V1 / np.maximum(D, np.float32(1e-12)))) @ QA[i].T
+        out.append(P.astype(np.float64))
+    full = orc.precondition_batch(grads, *orc_chain(orc, A, G, float(g), mode), float(g), mode)
+    return [relF(p, f) for p, f in zip(out, full)]
+
+
+def orc_chain(orc, A, G, g, mode):
+    if mode == 2:
+        return [orc.damped_inverse(x, g) for x in G], None, [orc.damped_inverse(a, g) for a in A], None
+    QA, vA = orc.symeig_batch(A)
+    QG, vG = orc.symeig_batch(G)
+    return QG, vG, QA, vA
 
 
 @pytest.mark.parametrize("variant", ["eigen", "factored", "inverse"])
@@ -273,7 +297,8 @@ def test_full_step_r32_small_batch(L, orc, variant):
     else:
         floors = _noise_floor(orc, layers, ref["A"], ref["G"], [g for g in grads], hp, mode)
         bound = [max(1e-3, 3 * f) for f in floors]
-        assert all(e <= b for e, b in zip(errs, bound)), list(zip(errs, floors))
+        bad = [(i, layers[i].name, e, f) for i, (e, f, b) in enumerate(zip(errs, floors, bound)) if e > b]
+        assert not bad, bad
 
 
 def test_full_size_r50_sampled_layers(L, orc):
