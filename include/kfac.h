@@ -83,7 +83,9 @@ typedef enum {
 } kfac_assign_policy_t;
 
 /* kfac_compute_eigen flags */
-#define KFAC_EIG_WARM_START 1u   /* start the Jacobi sweeps from the Q passed in (stale basis) */
+#define KFAC_EIG_WARM_START 1u   /* Jacobi factors start from the Q passed in (stale basis) */
+#define KFAC_EIG_JACOBI 2u       /* every factor by one-sided block Jacobi */
+#define KFAC_EIG_TRIDIAG 4u      /* every factor by tridiagonalisation + divide and conquer */
 
 /* Derived dimensions of one layer.  Host only; any output pointer may be NULL. */
 kfac_status_t kfac_layer_dims(const kfac_layer_t *layer, int32_t *d_a, int32_t *d_g, int64_t *rows);
@@ -111,9 +113,11 @@ kfac_status_t kfac_update_factors(const kfac_layer_t *layers, int32_t num_layers
  * Q[i]: device dims[i] x ld_Q[i]; on return column j is the eigenvector of evals[i][j].
  * evals[i]: device, dims[i] floats, ascending, clamped >= 0 (R10).
  * info: device int32[count]; 0 = converged, k > 0 = not converged after k sweeps
- * (outputs still written).  flags: 0 or KFAC_EIG_WARM_START (Q[i] then holds the
- * previous orthonormal eigenbasis on entry).  Method: one-sided block Jacobi
- * (DESIGN.md "Eigensolver"); eigenvector sign/order within equal eigenvalues is free (R11).
+ * (outputs still written).  Method: factors with dims >= 64 by
+ * Householder tridiagonalisation + divide and conquer + blocked back-transformation, smaller
+ * ones by one-sided block Jacobi; KFAC_EIG_JACOBI / KFAC_EIG_TRIDIAG force one method.
+ * KFAC_EIG_WARM_START: Q[i] holds the previous orthonormal eigenbasis on entry and the Jacobi
+ * factors start from it.  Eigenvector sign/order within equal eigenvalues is free (R11).
  * 1 <= dims[i] <= 16384. */
 size_t kfac_compute_eigen_workspace_size(const int32_t *dims, int32_t count);
 kfac_status_t kfac_compute_eigen(const float *const *F, const int32_t *dims, const int32_t *ld_F,

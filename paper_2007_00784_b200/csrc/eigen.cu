@@ -22,6 +22,10 @@
 namespace kfac {
 
 size_t eigen_workspace_bytes(const int32_t *dims, int count);
+size_t trd_workspace_bytes(const int32_t *dims, int count);
+kfac_status_t trd_run(const float *const *F, const int32_t *dims, const int32_t *ldF, int count,
+                      float *const *Q, const int32_t *ldQ, float *const *evals, int32_t *info, void *ws,
+                      cudaStream_t s);
 kfac_status_t eigen_run(const float *const *F, const int32_t *dims, const int32_t *ldF, int count,
                         float *const *Q, const int32_t *ldQ, float *const *evals, int32_t *info,
                         uint32_t flags, void *ws, cudaStream_t s);
@@ -443,11 +447,13 @@ Layout plan(const int32_t *dims, int count) {
 
 }  // namespace
 
-size_t eigen_workspace_bytes(const int32_t *dims, int count) { return plan(dims, count).bytes; }
+namespace {
 
-kfac_status_t eigen_run(const float *const *F, const int32_t *dims, const int32_t *ldF, int count,
-                        float *const *Q, const int32_t *ldQ, float *const *evals, int32_t *info,
-                        uint32_t flags, void *ws, cudaStream_t s) {
+size_t jacobi_bytes(const int32_t *dims, int count) { return plan(dims, count).bytes; }
+
+kfac_status_t jacobi_run(const float *const *F, const int32_t *dims, const int32_t *ldF, int count,
+                         float *const *Q, const int32_t *ldQ, float *const *evals, int32_t *info,
+                         uint32_t flags, void *ws, cudaStream_t s) {
     Layout L = plan(dims, count);
     char *base = reinterpret_cast<char *>(round_up(reinterpret_cast<uintptr_t>(ws), 256));
     EigJob *table = reinterpret_cast<EigJob *>(base + L.table_off);
@@ -514,5 +520,92 @@ kfac_status_t eigen_run(const float *const *F, const int32_t *dims, const int32_
     KFAC_LAUNCHED();
     return KFAC_OK;
 }
+
+int trd_min_dim() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("KFAC_EIG_TRD_MIN");
+        v = e ? atoi(e) : 64;
+    }
+    return v;
+}
+
+bool use_trd(int n, uint32_t flags) {
+    if (flags & KFAC_EIG_JACOBI) return false;
+    if (flags & KFAC_EIG_TRIDIAG) return true;
+    return n >= trd_min_dim();
+}
+
+}  // namespace
+
+namespace {
+struct InfoScatter {
+    int count;
+    int idx[2000];
+};
+__global__ void eig_info_scatter(const int32_t *local, int32_t *info, const __grid_constant__ InfoScatter p) {
+    for (int q = threadIdx.x; q < p.count; q += blockDim.x) info[p.idx[q]] = local[q];
+}
+kfac_status_t scatter_info(const int32_t *local, const std::vector<int> &idx, int32_t *info, cudaStream_t s) {
+    for (size_t b = 0; b < idx.size(); b += 2000) {
+        InfoScatter p;
+        p.count = (int)std::min<size_t>(2000, idx.size() - b);
+        for (int q = 0; q < p.count; ++q) p.idx[q] = idx[b + q];
+        eig_info_scatter<<<1, 256, 0, s>>>(local + b, info, p);
+        KFAC_LAUNCHED();
+    }
+    return KFAC_OK;
+}
+}  // namespace
+
+// Workspace covers both methods (the method split depends on flags, the size only on dims).
+size_t eigen_workspace_bytes(const int32_t *dims, int count) {
+    return round_up(jacobi_bytes(dims, count), 256) + round_up(trd_workspace_bytes(dims, count), 256) +
+           sizeof(int32_t) * count + 512;
+}
+
+kfac_status_t eigen_run(const float *const *F, const int32_t *dims, const int32_t *ldF, int count,
+                        float *const *Q, const int32_t *ldQ, float *const *evals, int32_t *info,
+                        uint32_t flags, void *ws, cudaStream_t s) {
+    std::vector<const float *> jF, tF;
+    std::vector<int32_t> jd, td, jl, tl, jlq, tlq;
+    std::vector<float *> jQ, tQ, je, te;
+    std::vector<int> jidx, tidx;
+    for (int i = 0; i < count; ++i) {
+        const bool t = use_trd(dims[i], flags);
+        (t ? tF : jF).push_back(F[i]);
+        (t ? td : jd).push_back(dims[i]);
+        (t ? tl : jl).push_back(ldF[i]);
+        (t ? tQ : jQ).push_back(Q[i]);
+        (t ? tlq : jlq).push_back(ldQ[i]);
+        (t ? te : je).push_back(evals[i]);
+        (t ? tidx : jidx).push_back(i);
+    }
+    // Each method reports into its own int array at the end of the workspace; one scatter
+    // kernel per method moves the codes to the caller's (caller-ordered) info array.
+    char *base = static_cast<char *>(ws);
+    const size_t joff = round_up(jacobi_bytes(dims, count), 256);
+    int32_t *local = reinterpret_cast<int32_t *>(base + joff + round_up(trd_workspace_bytes(dims, count), 256));
+    if (!jd.empty()) {
+        kfac_status_t st = jacobi_run(jF.data(), jd.data(), jl.data(), (int)jd.size(), jQ.data(), jlq.data(),
+                                      je.data(), local, flags & KFAC_EIG_WARM_START, base, s);
+        if (st != KFAC_OK) return st;
+        if (info) {
+            st = scatter_info(local, jidx, info, s);
+            if (st != KFAC_OK) return st;
+        }
+    }
+    if (!td.empty()) {
+        kfac_status_t st = trd_run(tF.data(), td.data(), tl.data(), (int)td.size(), tQ.data(), tlq.data(),
+                                   te.data(), local + jd.size(), base + joff, s);
+        if (st != KFAC_OK) return st;
+        if (info) {
+            st = scatter_info(local + jd.size(), tidx, info, s);
+            if (st != KFAC_OK) return st;
+        }
+    }
+    return KFAC_OK;
+}
+
 
 }  // namespace kfac

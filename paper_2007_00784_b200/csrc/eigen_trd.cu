@@ -1,0 +1,1266 @@
+// eigen_trd.cu -- eigendecomposition of the large Kronecker factors (Alg. 1, Eqs. 13-15)
+// by the classical three-phase dense symmetric eigensolver, re-designed for B200:
+//
+//   (1) Householder tridiagonalisation F = H T H^T, H = H_0 H_1 ... H_{n-2}
+//       (Golub & Van Loan Alg. 8.3.1; blocked as in LAPACK dsytrd/dlatrd with panels of 32):
+//       a persistent kernel per panel in which every factor of the batch owns a group of CTAs
+//       (sized by its remaining work) synchronised by its own global-memory barrier -- three
+//       barriers per column (norm, symmetric mat-vec + panel dots, w^T v); the rank-64 trailing
+//       update A -= V W^T + W V^T between panels is a tcgen05 3xTF32 GEMM.  Working matrix fp32,
+//       every reduction in fp64, (d, e, tau) in fp64.
+//   (2) Cuppen's divide and conquer on T (fp64 arithmetic, fp32 eigenvector storage):
+//       leaves of <= 32 rows by implicit QL (one warp each); each merge solves
+//       D + rho z z^T with LAPACK-style deflation (small z_i, and close d_i by a Givens rotation),
+//       a bracketed rational-Newton secular solver (one warp per root), the Gu-Eisenstat
+//       recomputed z-hat (orthogonal eigenvectors without extra precision), and the
+//       eigenvector update Q_nd S as a grouped tensor-core GEMM whose N and K are the
+//       device-side count of non-deflated roots.
+//   (3) back-transformation X = H Z in blocks of 128 reflectors with the compact WY form
+//       H_b...H_{b+127} = I - V T V^T (LAPACK dlarft), three grouped GEMMs per block.
+//
+// Work ~ (4/3 + 4/3 + 2) n^3 flops, most of it on the tensor pipe, against ~12 n^3 per sweep of the
+// one-sided Jacobi (eigen.cu), which remains the solver for small factors and warm starts.
+#include "internal.cuh"
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#define RET_OK(expr)                         \
+    do {                                     \
+        kfac_status_t _st = (expr);          \
+        if (_st != KFAC_OK) return _st;      \
+    } while (0)
+
+namespace kfac {
+
+size_t trd_workspace_bytes(const int32_t *dims, int count);
+kfac_status_t trd_run(const float *const *F, const int32_t *dims, const int32_t *ldF, int count,
+                      float *const *Q, const int32_t *ldQ, float *const *evals, int32_t *info, void *ws,
+                      cudaStream_t s);
+
+namespace {
+
+constexpr int kNb = 32;                 // panel width (reflectors per syr2k)
+constexpr int kTrdThreads = 512;
+constexpr int kTrdWarps = kTrdThreads / 32;
+constexpr int kPart = 2 * kNb + 2;      // per-CTA partials: V^T v, W^T v, ||x||^2, w^T v
+constexpr int kMaxGroupCtas = 512;
+constexpr int kLeaf = 32;               // D&C leaf size
+constexpr int kBt = 128;                // reflectors per back-transformation block
+constexpr double kEps = 1.1102230246251565e-16;   // 2^-53, LAPACK dlamch('E')
+
+// ----------------------------------------------------------------- job --
+struct TrdJob {
+    const float *F;
+    float *Q, *evals;
+    int *info;
+    float *A;          // n x ldw working matrix (full symmetric storage, pads zero)
+    float *Vb;         // n x ldw reflectors: column k = v_k (v_k[k+1] = 1, zero above)
+    float *VW, *WV;    // n x 64 panel buffers: [V | W] and [W | V] of the current panel
+    float *Z0, *Z1;    // n x ldw eigenvectors of T (D&C ping-pong)
+    float *Qnd, *Tmp;  // n x ldw D&C scratch (permuted/rotated columns, GEMM output)
+    float *Sb;         // n x ldw D&C secular eigenvectors S (aliases A after the reduction)
+    float *Yb, *Y2b;   // kBt x ldw back-transformation scratch
+    float *Gb, *Tb;    // kBt x kBt Gram matrix V^T V and WY factor T
+    double *d, *e, *tau;       // tridiagonal T and reflector scalars
+    double *x, *y;             // corrected column / mat-vec result (sytrd)
+    double *D;                 // current eigenvalues of the D&C subproblems
+    double *dval, *zval;       // merge: sorted (d, z) -- non-deflated first, deflated last
+    double *rtau, *wz;         // merge: root offsets, z-hat
+    double *vnorm;             // merge: eigenvector column norms
+    double *rot_c, *rot_s;     // merge: Givens rotations
+    int *col, *posof, *rorg, *rot_p, *rot_j, *srcpos;
+    int *mstate;               // per merge: {k, nrot, k, k} (k twice: GEMM dynamic N, K)
+    double *mscal;             // per merge: {rho2, tol}
+    double *part;              // kMaxGroupCtas x kPart
+    unsigned *bar;
+    int n, ldF, ldQ, ldw;
+    int levels;                // D&C merge levels (n <= kLeaf -> 0)
+};
+
+template <class T>
+__device__ __forceinline__ T ldcg(const T *p) { return __ldcg(p); }
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Barrier among the `nc` CTAs of one factor's group (counter zeroed before each launch).
+__device__ __forceinline__ void group_barrier(unsigned *bar, unsigned &target, int nc) {
+    __syncthreads();
+    target += (unsigned)nc;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(bar, 1u);
+        while (ld_acquire(bar) < target) __nanosleep(20);
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// Block-wide fixed-order sum of one double per thread; result valid in every thread.
+__device__ __forceinline__ double block_sum(double v, double *sh) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
+    __syncthreads();
+    if (lane == 0) sh[w] = v;
+    __syncthreads();
+    double s = 0.0;
+    for (int i = 0; i < (int)(blockDim.x / 32); ++i) s += sh[i];
+    return s;
+}
+
+__device__ __forceinline__ void part_range(int r0, int n, int c, int nc, int &lo, int &hi) {
+    const long long len = n - r0;
+    lo = r0 + (int)(len * c / nc);
+    hi = r0 + (int)(len * (c + 1) / nc);
+}
+
+// ------------------------------------------------------------ init --
+// A = (F + F^T)/2 in fp32 (pads zero), Vb = 0.
+__global__ void trd_init(const TrdJob *jobs) {
+    const TrdJob &J = jobs[blockIdx.y];
+    const int n = J.n, ldw = J.ldw;
+    const long long total = (long long)n * ldw;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int r = (int)(i / ldw), c = (int)(i % ldw);
+        float a = 0.f;
+        if (c < n) a = 0.5f * (J.F[(size_t)r * J.ldF + c] + J.F[(size_t)c * J.ldF + r]);
+        J.A[i] = a;
+        J.Vb[i] = 0.f;
+    }
+}
+
+// ----------------------------------------------------- panel kernel --
+struct PanelLaunch {
+    const TrdJob *jobs;
+    int p0, count;
+    int job[kMaxGroupCtas];
+    int cta_begin[kMaxGroupCtas + 1];
+};
+
+// One panel of 32 columns (LAPACK dlatrd, lower) for every active factor.  Column k (i = k - p0):
+//   A: c = A_p[k:n, k] - V[k:n, <i] W[k, <i]^T - W[k:n, <i] V[k, <i]^T;  d_k = c_k, x = c_{k+1:n}
+//   B: reflector (dlarfg) of x: beta = -sign(x_0)||x||, tau = (beta - x_0)/beta, v = x/(x_0 - beta), v_0 = 1;
+//      y = A_p[k+1:n, k+1:n] v  (A_p: matrix at the panel start), partial V^T v, W^T v
+//   C: y -= W (V^T v) + V (W^T v);  w = tau y;  partial w^T v
+//   D: W[:, i] = w - (tau/2)(w^T v) v
+// so that after the panel A_p[q:n, q:n] - V W^T - W V^T is the reduced trailing matrix (q = p0+32).
+__global__ void __launch_bounds__(kTrdThreads, 1) trd_panel(const __grid_constant__ PanelLaunch L) {
+    extern __shared__ __align__(16) float vsm[];     // v, 4-aligned, zero padded
+    __shared__ double sh[kTrdWarps];
+    __shared__ double red[kTrdWarps][2 * kNb];
+    __shared__ double ab[2 * kNb];                   // (V^T v, W^T v)
+    __shared__ float rowV[kNb], rowW[kNb];           // V[k, <i], W[k, <i]
+    __shared__ double scal[4];
+
+    int g = 0;
+    {
+        int lo = 0, hi = L.count - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (L.cta_begin[mid] <= (int)blockIdx.x) lo = mid; else hi = mid - 1;
+        }
+        g = lo;
+    }
+    const TrdJob &J = L.jobs[L.job[g]];
+    const int c = blockIdx.x - L.cta_begin[g], nc = L.cta_begin[g + 1] - L.cta_begin[g];
+    const int n = J.n, ldw = J.ldw, p0 = L.p0;
+    const float *A = J.A;
+    float *VW = J.VW, *WV = J.WV;
+    double *part = J.part;
+    const int t = threadIdx.x, warp = t / 32, lane = t % 32;
+    unsigned target = 0;
+    float w_next = 0.f;                              // W[k, i-1], computed redundantly
+
+    for (int i = 0; i < kNb; ++i) {
+        const int k = p0 + i;
+        if (k >= n) break;
+        // ---------------- phase A (rows [k, n)) ----------------
+        if (t < i) {
+            rowV[t] = ldcg(VW + (size_t)k * 64 + t);
+            rowW[t] = (t == i - 1) ? w_next : ldcg(VW + (size_t)k * 64 + kNb + t);
+        }
+        __syncthreads();
+        int lo, hi;
+        part_range(k, n, c, nc, lo, hi);
+        double s2 = 0.0;
+        for (int r = lo + t; r < hi; r += kTrdThreads) {
+            double cv = A[(size_t)k * ldw + r];
+            const float *vr = VW + (size_t)r * 64;
+            for (int q = 0; q < i; ++q)
+                cv -= (double)ldcg(vr + q) * rowW[q] + (double)ldcg(vr + kNb + q) * rowV[q];
+            if (r == k) J.d[k] = cv;
+            else __stcg(J.x + r, cv);
+            if (r >= k + 2) s2 += cv * cv;
+        }
+        s2 = block_sum(s2, sh);
+        if (t == 0) __stcg(part + (size_t)c * kPart + 2 * kNb, s2);
+        group_barrier(J.bar, target, nc);
+        if (k == n - 1) break;
+        // ---------------- phase B (rows [k+1, n)) ----------------
+        if (t == 0) {
+            double nrm2 = 0.0;
+            for (int q = 0; q < nc; ++q) nrm2 += ldcg(part + (size_t)q * kPart + 2 * kNb);
+            const double alpha = ldcg(J.x + k + 1);
+            double tau = 0.0, beta = alpha, scale = 0.0;
+            if (nrm2 > 0.0) {
+                beta = -copysign(sqrt(alpha * alpha + nrm2), alpha);
+                tau = (beta - alpha) / beta;
+                scale = 1.0 / (alpha - beta);
+            }
+            scal[0] = tau;
+            scal[1] = scale;
+            if (c == 0) {
+                J.e[k] = beta;
+                J.tau[k] = tau;
+            }
+        }
+        __syncthreads();
+        const double tau = scal[0], scale = scal[1];
+        const int c0 = (k + 1) & ~3;
+        const int nv4 = (n - c0 + 3) >> 2;           // float4 count from c0
+        for (int j = t; j < nv4 * 4; j += kTrdThreads) {
+            const int col = c0 + j;
+            float v = 0.f;
+            if (col == k + 1) v = 1.f;
+            else if (col > k + 1 && col < n) v = (float)(ldcg(J.x + col) * scale);
+            vsm[j] = v;
+        }
+        __syncthreads();
+        part_range(k + 1, n, c, nc, lo, hi);
+        for (int r = lo + t; r < hi; r += kTrdThreads) {
+            const float v = vsm[r - c0];
+            J.Vb[(size_t)r * ldw + k] = v;
+            VW[(size_t)r * 64 + i] = v;
+            WV[(size_t)r * 64 + kNb + i] = v;
+        }
+        // symmetric mat-vec (one warp per row) + panel dot partials (lane q -> column q)
+        double pa = 0.0, pb = 0.0;
+        const float4 *v4 = reinterpret_cast<const float4 *>(vsm);
+        for (int r = lo + warp; r < hi; r += kTrdWarps) {
+            const float4 *a4 = reinterpret_cast<const float4 *>(A + (size_t)r * ldw + c0);
+            double acc = 0.0;
+            for (int q = lane; q < nv4; q += 32) {
+                const float4 a = __ldg(a4 + q), v = v4[q];
+                acc += (double)a.x * v.x + (double)a.y * v.y + (double)a.z * v.z + (double)a.w * v.w;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            const double vr = vsm[r - c0];
+            if (lane == 0) __stcg(J.y + r, acc);
+            if (lane < i) {
+                pa += (double)ldcg(VW + (size_t)r * 64 + lane) * vr;
+                pb += (double)ldcg(VW + (size_t)r * 64 + kNb + lane) * vr;
+            }
+        }
+        red[warp][lane] = pa;
+        red[warp][kNb + lane] = pb;
+        __syncthreads();
+        if (t < 2 * kNb) {
+            double s = 0.0;
+            for (int w = 0; w < kTrdWarps; ++w) s += red[w][t];
+            __stcg(part + (size_t)c * kPart + t, s);
+        }
+        group_barrier(J.bar, target, nc);
+        // ---------------- phase C ----------------
+        if (t < 2 * kNb) {
+            double s = 0.0;
+            if ((t % kNb) < i)
+                for (int q = 0; q < nc; ++q) s += ldcg(part + (size_t)q * kPart + t);
+            ab[t] = s;
+        }
+        __syncthreads();
+        double wv = 0.0;
+        for (int r = lo + t; r < hi; r += kTrdThreads) {
+            double yr = ldcg(J.y + r);
+            const float *vr = VW + (size_t)r * 64;
+            for (int q = 0; q < i; ++q) yr -= (double)ldcg(vr + kNb + q) * ab[q] + (double)ldcg(vr + q) * ab[kNb + q];
+            const double w = tau * yr;
+            __stcg(J.y + r, w);
+            wv += w * (double)vsm[r - c0];
+        }
+        wv = block_sum(wv, sh);
+        if (t == 0) __stcg(part + (size_t)c * kPart + 2 * kNb + 1, wv);
+        group_barrier(J.bar, target, nc);
+        // ---------------- phase D ----------------
+        if (t == 0) {
+            double s = 0.0;
+            for (int q = 0; q < nc; ++q) s += ldcg(part + (size_t)q * kPart + 2 * kNb + 1);
+            scal[2] = -0.5 * tau * s;
+        }
+        __syncthreads();
+        const double alpha2 = scal[2];
+        for (int r = lo + t; r < hi; r += kTrdThreads) {
+            const float w = (float)(ldcg(J.y + r) + alpha2 * (double)vsm[r - c0]);
+            VW[(size_t)r * 64 + kNb + i] = w;
+            WV[(size_t)r * 64 + i] = w;
+        }
+        w_next = (float)(ldcg(J.y + k + 1) + alpha2);   // row k+1: v = 1
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------- D&C: tear --
+// Leaves: boundaries b_i = floor(i n / 2^L).  Each internal boundary s splits T into
+// diag(T1, T2) + |rho| u u^T, u = [e_last; sign(rho) e_first] (rho = e[s-1]), so both
+// adjacent diagonal entries lose |rho| (Cuppen; LAPACK dlaed0).
+__global__ void dc_tear(const TrdJob *jobs) {
+    const TrdJob &J = jobs[blockIdx.y];
+    const int n = J.n, nleaf = 1 << J.levels;
+    auto is_boundary = [&](int i) {          // i == floor(b n / nleaf) for some 1 <= b < nleaf
+        if (i <= 0 || i >= n) return false;
+        const long long b = ((long long)i * nleaf + n - 1) / n;
+        return b >= 1 && b < nleaf && (long long)b * n / nleaf == i;
+    };
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        double v = J.d[i];
+        if (is_boundary(i)) v -= fabs(J.e[i - 1]);
+        if (is_boundary(i + 1)) v -= fabs(J.e[i]);
+        J.D[i] = v;
+    }
+}
+
+// ------------------------------------------------------- D&C: leaves --
+struct LeafDesc {
+    int job, a, size;
+};
+
+// Implicit QL with Wilkinson-type shifts (EISPACK tql2) on one leaf; every lane runs the scalar
+// recurrence redundantly (identical arithmetic) and owns one row of the eigenvector matrix.
+__global__ void dc_leaf(const TrdJob *jobs, const LeafDesc *leaves, int nleaves) {
+    const int li = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    if (li >= nleaves) return;
+    const LeafDesc Ld = leaves[li];
+    const TrdJob &J = jobs[Ld.job];
+    const int lane = threadIdx.x % 32, ns = Ld.size, a = Ld.a;
+    double d[kLeaf], e[kLeaf], z[kLeaf];
+    for (int i = 0; i < kLeaf; ++i) {
+        d[i] = i < ns ? J.D[a + i] : 0.0;
+        e[i] = (i + 1 < ns) ? J.e[a + i] : 0.0;       // e[i] = T[i+1][i]
+        z[i] = (i == lane) ? 1.0 : 0.0;               // row `lane` of the eigenvector matrix
+    }
+    double f = 0.0, tst1 = 0.0;
+    int iters = 0;
+    for (int l = 0; l < ns; ++l) {
+        tst1 = fmax(tst1, fabs(d[l]) + fabs(e[l]));
+        int m = l;
+        while (m < ns - 1 && fabs(e[m]) > kEps * tst1) ++m;
+        if (m > l) {
+            do {
+                if (++iters > 60 * kLeaf) break;
+                double g = d[l];
+                double p = (d[l + 1] - g) / (2.0 * e[l]);
+                double r = hypot(p, 1.0);
+                if (p < 0) r = -r;
+                d[l] = e[l] / (p + r);
+                d[l + 1] = e[l] * (p + r);
+                const double dl1 = d[l + 1];
+                double h = g - d[l];
+                for (int i = l + 2; i < ns; ++i) d[i] -= h;
+                f += h;
+                p = d[m];
+                double c = 1.0, c2 = 1.0, c3 = 1.0, s = 0.0, s2 = 0.0;
+                const double el1 = e[l + 1];
+                for (int i = m - 1; i >= l; --i) {
+                    c3 = c2;
+                    c2 = c;
+                    s2 = s;
+                    g = c * e[i];
+                    h = c * p;
+                    r = hypot(p, e[i]);
+                    e[i + 1] = s * r;
+                    s = e[i] / r;
+                    c = p / r;
+                    p = c * d[i] - s * g;
+                    d[i + 1] = h + s * (c * g + s * d[i]);
+                    const double zi1 = z[i + 1];
+                    z[i + 1] = s * z[i] + c * zi1;
+                    z[i] = c * z[i] - s * zi1;
+                }
+                p = -s * s2 * c3 * el1 * e[l] / dl1;
+                e[l] = s * p;
+                d[l] = c * p;
+            } while (fabs(e[l]) > kEps * tst1);
+        }
+        d[l] += f;
+        e[l] = 0.0;
+    }
+    // ascending order: rank of each eigenvalue (ties by index)
+    for (int j = 0; j < ns; ++j) {
+        int rk = 0;
+        for (int q = 0; q < ns; ++q) rk += (d[q] < d[j]) || (d[q] == d[j] && q < j);
+        if (lane == 0) J.D[a + rk] = d[j];
+        if (lane < ns) J.Z0[(size_t)(a + lane) * J.ldw + a + rk] = (float)z[j];
+    }
+    if (iters > 60 * kLeaf && lane == 0 && J.info) atomicAdd(J.info, 1);
+}
+
+// ------------------------------------------------------- D&C: merges --
+struct MergeDesc {
+    int job, a, n1, n2, m;      // m: merge index inside the job's level (state slot = a)
+};
+
+// Sort the two halves' eigenvalues into one ascending list, form z, and deflate (LAPACK dlaed2).
+// Non-deflated entries go to [0, k) of (dval, zval, col) in ascending d; deflated ones fill
+// [k, n) from the back.  Rotations (p, j, c, s) act on original columns: q_p <- c q_p + s q_j,
+// q_j <- c q_j - s q_p.
+__global__ void dc_deflate(const TrdJob *jobs, const MergeDesc *merges, int ping) {
+    const MergeDesc M = merges[blockIdx.x];
+    const TrdJob &J = jobs[M.job];
+    const int a = M.a, n1 = M.n1, nm = M.n1 + M.n2, ldw = J.ldw;
+    const float *Z = ping ? J.Z1 : J.Z0;
+    const double rho = J.e[a + n1 - 1];
+    const double sgn = rho < 0 ? -1.0 : 1.0;
+    double *dv = J.dval + a, *zv = J.zval + a;
+    int *col = J.col + a;
+    const double rs2 = 0.70710678118654752440;
+    double dmax = 0.0, zmax = 0.0;
+    for (int c = threadIdx.x; c < nm; c += blockDim.x) {
+        const double dc = J.D[a + c];
+        double zc;
+        int rank;
+        if (c < n1) {
+            zc = (double)Z[(size_t)(a + n1 - 1) * ldw + a + c];
+            int lo = 0, hi = M.n2;                   // # right entries < dc
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (J.D[a + n1 + mid] < dc) lo = mid + 1; else hi = mid;
+            }
+            rank = c + lo;
+        } else {
+            zc = sgn * (double)Z[(size_t)(a + n1) * ldw + a + c];
+            int lo = 0, hi = n1;                     // # left entries <= dc
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (J.D[a + mid] <= dc) lo = mid + 1; else hi = mid;
+            }
+            rank = (c - n1) + lo;
+        }
+        zc *= rs2;
+        dv[rank] = dc;
+        zv[rank] = zc;
+        col[rank] = c;
+        dmax = fmax(dmax, fabs(dc));
+        zmax = fmax(zmax, fabs(zc));
+    }
+    // max-reductions
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+        zmax = fmax(zmax, __shfl_xor_sync(0xffffffffu, zmax, o));
+    }
+    __shared__ double shd[32], shz[32];
+    if (threadIdx.x % 32 == 0) {
+        shd[threadIdx.x / 32] = dmax;
+        shz[threadIdx.x / 32] = zmax;
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    for (int w = 0; w < (int)(blockDim.x / 32); ++w) {
+        dmax = fmax(dmax, shd[w]);
+        zmax = fmax(zmax, shz[w]);
+    }
+    const double rho2 = 2.0 * fabs(rho);
+    const double tol = 8.0 * kEps * fmax(dmax, zmax);
+    int *posof = J.posof + a, *rp = J.rot_p + a, *rj = J.rot_j + a;
+    double *rc = J.rot_c + a, *rsn = J.rot_s + a;
+    int k = 0, nrot = 0;
+    if (rho2 * zmax <= tol) {
+        // everything deflates: keep order
+        for (int j = 0; j < nm; ++j) posof[col[j]] = j;
+        J.mstate[4 * a + 0] = 0;
+        J.mstate[4 * a + 1] = 0;
+        J.mstate[4 * a + 2] = 0;
+        J.mstate[4 * a + 3] = 0;
+        J.mscal[2 * a + 0] = rho2;
+        J.mscal[2 * a + 1] = tol;
+        return;
+    }
+    // Deflated list is accumulated in rtau/rorg scratch (value, col) and appended at the end.
+    double *defv = J.rtau + a;
+    int *defc = J.rorg + a;
+    int ndef = 0;
+    int pj = -1;
+    double dp = 0.0, zp = 0.0;
+    int cp = 0;
+    for (int j = 0; j < nm; ++j) {
+        double dj = dv[j], zj = zv[j];
+        const int cj = col[j];
+        if (rho2 * fabs(zj) <= tol) {
+            defv[ndef] = dj;
+            defc[ndef++] = cj;
+            continue;
+        }
+        if (pj < 0) {
+            pj = j; dp = dj; zp = zj; cp = cj;
+            continue;
+        }
+        double s = zp, c = zj;
+        const double tt = hypot(c, s);
+        const double t = dj - dp;
+        c /= tt;
+        s = -s / tt;
+        if (fabs(t * c * s) <= tol) {
+            // deflate p after rotating (p, j)
+            zj = tt;
+            rp[nrot] = cp; rj[nrot] = cj; rc[nrot] = c; rsn[nrot] = s; ++nrot;
+            const double t2 = dp * c * c + dj * s * s;
+            dj = dp * s * s + dj * c * c;
+            defv[ndef] = t2;
+            defc[ndef++] = cp;
+            pj = j; dp = dj; zp = zj; cp = cj;
+        } else {
+            dv[k] = dp; zv[k] = zp; col[k] = cp; ++k;
+            pj = j; dp = dj; zp = zj; cp = cj;
+        }
+    }
+    if (pj >= 0) {
+        dv[k] = dp; zv[k] = zp; col[k] = cp; ++k;
+    }
+    for (int q = 0; q < ndef; ++q) {
+        dv[k + q] = defv[q];
+        col[k + q] = defc[q];
+        zv[k + q] = 0.0;
+    }
+    for (int j = 0; j < nm; ++j) posof[col[j]] = j;
+    J.mstate[4 * a + 0] = k;
+    J.mstate[4 * a + 1] = nrot;
+    J.mstate[4 * a + 2] = k;
+    J.mstate[4 * a + 3] = k;
+    J.mscal[2 * a + 0] = rho2;
+    J.mscal[2 * a + 1] = tol;
+}
+
+// Qnd[a + r][posof[c]] = (block-diagonal child eigenvectors)[r][c]  (one warp per row).
+__global__ void dc_permute(const TrdJob *jobs, const MergeDesc *merges, int ping) {
+    const MergeDesc M = merges[blockIdx.y];
+    const TrdJob &J = jobs[M.job];
+    const int a = M.a, n1 = M.n1, nm = M.n1 + M.n2, ldw = J.ldw;
+    const int r = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x % 32;
+    if (r >= nm) return;
+    const float *Z = ping ? J.Z1 : J.Z0;
+    const int *posof = J.posof + a;
+    float *dst = J.Qnd + (size_t)(a + r) * ldw;
+    const float *src = Z + (size_t)(a + r) * ldw + a;
+    for (int c = lane; c < nm; c += 32) {
+        const bool same = (c < n1) == (r < n1);
+        dst[posof[c]] = same ? src[c] : 0.f;
+    }
+}
+
+// Apply the merge's Givens rotations to every row of Qnd (one thread per row, in order).
+__global__ void dc_rotate(const TrdJob *jobs, const MergeDesc *merges) {
+    const MergeDesc M = merges[blockIdx.y];
+    const TrdJob &J = jobs[M.job];
+    const int a = M.a, nm = M.n1 + M.n2;
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    const int nrot = J.mstate[4 * a + 1];
+    if (r >= nm || nrot == 0) return;
+    float *row = J.Qnd + (size_t)(a + r) * J.ldw;
+    const int *posof = J.posof + a;
+    for (int q = 0; q < nrot; ++q) {
+        const int pp = posof[J.rot_p[a + q]], pj = posof[J.rot_j[a + q]];
+        const double c = J.rot_c[a + q], s = J.rot_s[a + q];
+        const double x = row[pp], y = row[pj];
+        row[pp] = (float)(c * x + s * y);
+        row[pj] = (float)(c * y - s * x);
+    }
+}
+
+// Secular equation 1/rho + sum_i z_i^2 / (d_i - lambda) = 0, root j in (d_j, d_{j+1})
+// (last root in (d_k, d_k + rho ||z||^2)), one warp per root.  lambda_j = d_{org} + tau with the
+// origin at the nearer pole so that d_i - lambda_j = (d_i - d_org) - tau keeps full relative
+// accuracy.  Iteration: two-pole rational model of psi (poles <= j) and phi (poles > j) fitted to
+// value and slope at tau (fixed-weight / "middle way" family), safeguarded by the bracket.
+__global__ void dc_secular(const TrdJob *jobs, const MergeDesc *merges) {
+    const MergeDesc M = merges[blockIdx.y];
+    const TrdJob &J = jobs[M.job];
+    const int a = M.a;
+    const int k = J.mstate[4 * a + 0];
+    const int j = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x % 32;
+    if (j >= k) return;
+    const double *dv = J.dval + a, *zv = J.zval + a;
+    const double rho = J.mscal[2 * a + 0];
+    const double rinv = 1.0 / rho;
+    const bool last = (j == k - 1);
+    int org;
+    double lo, hi;
+    if (last) {
+        double zz = 0.0;
+        for (int i = lane; i < k; i += 32) zz += zv[i] * zv[i];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) zz += __shfl_xor_sync(0xffffffffu, zz, o);
+        org = j;
+        lo = 0.0;
+        hi = rho * zz;
+    } else {
+        const double del = dv[j + 1] - dv[j];
+        const double mid = 0.5 * del;
+        double f = 0.0;
+        for (int i = lane; i < k; i += 32) f += zv[i] * zv[i] / ((dv[i] - dv[j]) - mid);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) f += __shfl_xor_sync(0xffffffffu, f, o);
+        f += rinv;
+        if (f >= 0.0) { org = j; lo = 0.0; hi = mid; }
+        else { org = j + 1; lo = -mid; hi = 0.0; }
+    }
+    if (k == 1) {                                    // lambda = d_0 + rho z_0^2 exactly
+        if (lane == 0) {
+            J.rtau[a] = hi;
+            J.rorg[a] = 0;
+        }
+        return;
+    }
+    const double dorg = dv[org];
+    const int L = j, R = j + 1;                      // poles bounding the root (R absent if last)
+    const double dL = dv[L] - dorg, dR = last ? 0.0 : dv[R] - dorg;
+    double tau = 0.5 * (lo + hi);
+    for (int it = 0; it < 100; ++it) {
+        double psi = 0.0, dpsi = 0.0, phi = 0.0, dphi = 0.0;
+        for (int i = lane; i < k; i += 32) {
+            const double del = (dv[i] - dorg) - tau;
+            const double tq = zv[i] / del;
+            const double term = zv[i] * tq, dterm = tq * tq;
+            if (i <= L) { psi += term; dpsi += dterm; }
+            else { phi += term; dphi += dterm; }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            psi += __shfl_xor_sync(0xffffffffu, psi, o);
+            dpsi += __shfl_xor_sync(0xffffffffu, dpsi, o);
+            phi += __shfl_xor_sync(0xffffffffu, phi, o);
+            dphi += __shfl_xor_sync(0xffffffffu, dphi, o);
+        }
+        const double w = rinv + psi + phi;
+        if (w > 0.0) hi = tau; else lo = tau;
+        const double err = 8.0 * (phi - psi) + rinv + fabs(tau) * (dpsi + dphi);
+        if (fabs(w) <= kEps * err) break;
+        if (hi - lo <= 2.0 * kEps * fmax(fabs(lo), fabs(hi))) break;
+        // model: c + q/(dL - x) + s/(dR - x) = 0
+        const double aL = dL - tau;
+        const double qL = dpsi * aL * aL;
+        double cc = rinv + (psi - qL / aL);
+        double tn;
+        if (last) {
+            cc += phi;                               // phi carries no pole term
+            tn = (cc != 0.0) ? dL + qL / cc : 0.5 * (lo + hi);
+            // c + q/(dL - x) = 0  ->  x = dL + q/c
+        } else {
+            const double aR = dR - tau;
+            const double sR = dphi * aR * aR;
+            cc += phi - sR / aR;
+            // c (dL - x)(dR - x) + q (dR - x) + s (dL - x) = 0, quadratic in y = x - dL... solve in x:
+            // c x^2 - (c (dL + dR) + q + s) x + (c dL dR + q dR + s dL) = 0
+            const double B = cc * (dL + dR) + qL + sR;
+            const double C = cc * dL * dR + qL * dR + sR * dL;
+            double x1, x2;
+            if (cc == 0.0) {
+                x1 = x2 = (B != 0.0) ? C / B : 0.5 * (lo + hi);
+            } else {
+                const double disc = fmax(B * B - 4.0 * cc * C, 0.0);
+                const double sq = sqrt(disc);
+                const double qq = B >= 0 ? 0.5 * (B + sq) : 0.5 * (B - sq);
+                x1 = qq / cc;
+                x2 = (qq != 0.0) ? C / qq : x1;
+            }
+            const bool in1 = x1 > lo && x1 < hi, in2 = x2 > lo && x2 < hi;
+            tn = in1 ? (in2 ? (fabs(x1 - tau) < fabs(x2 - tau) ? x1 : x2) : x1) : (in2 ? x2 : 0.5 * (lo + hi));
+        }
+        if (!(tn > lo && tn < hi)) tn = 0.5 * (lo + hi);
+        if (tn == tau) break;
+        tau = tn;
+    }
+    if (lane == 0) {
+        J.rtau[a + j] = tau;
+        J.rorg[a + j] = org;
+    }
+}
+
+// d_i - lambda_j, accurate.
+__device__ __forceinline__ double delta(const double *dv, const double *rt, const int *ro, int i, int j) {
+    return (dv[i] - dv[ro[j]]) - rt[j];
+}
+
+// Gu-Eisenstat: z-hat_i = sign(z_i) sqrt( -(d_i - lambda_i) prod_{j != i} (d_i - lambda_j)/(d_i - d_j) ).
+__global__ void dc_zhat(const TrdJob *jobs, const MergeDesc *merges) {
+    const MergeDesc M = merges[blockIdx.y];
+    const TrdJob &J = jobs[M.job];
+    const int a = M.a, k = J.mstate[4 * a + 0];
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= k) return;
+    const double *dv = J.dval + a, *rt = J.rtau + a;
+    const int *ro = J.rorg + a;
+    double w = delta(dv, rt, ro, i, i);
+    const double di = dv[i];
+    for (int j = 0; j < k; ++j)
+        if (j != i) w *= delta(dv, rt, ro, i, j) / (di - dv[j]);
+    J.wz[a + i] = copysign(sqrt(fmax(-w, 0.0)), J.zval[a + i]);
+}
+
+// Column norms of S[:, j] = z-hat / (d - lambda_j) (one warp per column).
+__global__ void dc_vnorm(const TrdJob *jobs, const MergeDesc *merges) {
+    const MergeDesc M = merges[blockIdx.y];
+    const TrdJob &J = jobs[M.job];
+    const int a = M.a, k = J.mstate[4 * a + 0];
+    const int j = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x % 32;
+    if (j >= k) return;
+    const double *dv = J.dval + a, *rt = J.rtau + a, *wz = J.wz + a;
+    const int *ro = J.rorg + a;
+    double s = 0.0;
+    for (int i = lane; i < k; i += 32) {
+        const double q = wz[i] / delta(dv, rt, ro, i, j);
+        s += q * q;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) J.vnorm[a + j] = 1.0 / sqrt(s);
+}
+
+// S[a + i][j] (k x k, row-major at rows a..a+k) = z-hat_i / (d_i - lambda_j) / ||.||; rows k..k+31
+// (inside the merge's row range) zeroed so the GEMM's last K block reads zeros.
+__global__ void dc_build_s(const TrdJob *jobs, const MergeDesc *merges) {
+    const MergeDesc M = merges[blockIdx.z];
+    const TrdJob &J = jobs[M.job];
+    const int a = M.a, nm = M.n1 + M.n2, k = J.mstate[4 * a + 0];
+    const int i = blockIdx.y, j = blockIdx.x * blockDim.x + threadIdx.x;
+    const int rows = min(nm, (k + 31) & ~31);
+    if (i >= rows || j >= k) return;
+    float v = 0.f;
+    if (i < k) {
+        const double *dv = J.dval + a, *rt = J.rtau + a;
+        const int *ro = J.rorg + a;
+        v = (float)(J.wz[a + i] / delta(dv, rt, ro, i, j) * J.vnorm[a + j]);
+    }
+    J.Sb[(size_t)(a + i) * J.ldw + j] = v;
+}
+
+// Final order of the merged eigenvalues: lambda_j (j < k, from the GEMM output Tmp) and the
+// deflated d's (Qnd columns k..n-1); rank by counting (ties by index).
+__global__ void dc_rank(const TrdJob *jobs, const MergeDesc *merges) {
+    const MergeDesc M = merges[blockIdx.y];
+    const TrdJob &J = jobs[M.job];
+    const int a = M.a, nm = M.n1 + M.n2, k = J.mstate[4 * a + 0];
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= nm) return;
+    const double *dv = J.dval + a, *rt = J.rtau + a;
+    const int *ro = J.rorg + a;
+    auto val = [&](int q) { return q < k ? dv[ro[q]] + rt[q] : dv[q]; };
+    const double ve = val(e);
+    int rk = 0;
+    for (int f = 0; f < nm; ++f) {
+        const double vf = val(f);
+        rk += (vf < ve) || (vf == ve && f < e);
+    }
+    J.D[a + rk] = ve;
+    J.srcpos[a + rk] = e;
+}
+
+__global__ void dc_assemble(const TrdJob *jobs, const MergeDesc *merges, int ping) {
+    const MergeDesc M = merges[blockIdx.z];
+    const TrdJob &J = jobs[M.job];
+    const int a = M.a, nm = M.n1 + M.n2, k = J.mstate[4 * a + 0], ldw = J.ldw;
+    const int r = blockIdx.y, p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= nm || p >= nm) return;
+    float *Zd = ping ? J.Z0 : J.Z1;                 // destination = the other buffer
+    const int src = J.srcpos[a + p];
+    const float v = src < k ? J.Tmp[(size_t)(a + r) * ldw + src] : J.Qnd[(size_t)(a + r) * ldw + src];
+    Zd[(size_t)(a + r) * ldw + a + p] = v;
+}
+
+// ------------------------------------------------- back-transformation --
+// T (upper triangular, kBt x kBt) of H_b0 ... H_{b0+nr-1} = I - V T V^T from G = V^T V
+// (LAPACK dlarft, forward / columnwise): T_jj = tau_j, T[0:j, j] = -tau_j T[0:j, 0:j] G[0:j, j].
+struct BtStep {
+    int job, b0, nr;
+};
+constexpr size_t kLarftSmem = sizeof(double) * (kBt * (kBt + 1) + kBt);
+__global__ void bt_larft(const TrdJob *jobs, const BtStep *steps) {
+    extern __shared__ double bt_smem[];
+    double (*T)[kBt + 1] = reinterpret_cast<double (*)[kBt + 1]>(bt_smem);
+    double *gcol = bt_smem + kBt * (kBt + 1);
+    const BtStep S = steps[blockIdx.x];
+    const TrdJob &J = jobs[S.job];
+    const int nr = S.nr, t = threadIdx.x;
+    for (int j = 0; j < nr; ++j) {
+        const double tj = J.tau[S.b0 + j];
+        if (t < j) gcol[t] = J.Gb[t * kBt + j];
+        __syncthreads();
+        double s = 0.0;
+        if (t < j)
+            for (int l = t; l < j; ++l) s += T[t][l] * gcol[l];
+        __syncthreads();
+        if (t < j) T[t][j] = -tj * s;
+        if (t == j) T[j][j] = tj;
+        if (t > j && t < kBt) T[t][j] = 0.0;
+        __syncthreads();
+    }
+    for (int idx = t; idx < kBt * kBt; idx += blockDim.x) {
+        const int r = idx / kBt, c = idx % kBt;
+        J.Tb[idx] = (r < nr && c < nr) ? (float)T[r][c] : 0.f;
+    }
+}
+
+__global__ void trd_output(const TrdJob *jobs, int ping) {
+    const TrdJob &J = jobs[blockIdx.z];
+    const int r = blockIdx.y, c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= J.n || c >= J.n) return;
+    const float *Z = ping ? J.Z1 : J.Z0;
+    J.Q[(size_t)r * J.ldQ + c] = Z[(size_t)r * J.ldw + c];
+    if (r == 0) J.evals[c] = (float)fmax(J.D[c], 0.0);
+}
+
+__global__ void trd_zero_info(const TrdJob *jobs) {
+    const TrdJob &J = jobs[blockIdx.x];
+    if (threadIdx.x == 0 && J.info) *J.info = 0;
+}
+
+// ---------------------------------------------------------------- host --
+struct Upload {
+    void *dst;
+    int bytes;
+    unsigned char data[30000];
+};
+__global__ void upload_kernel(const __grid_constant__ Upload u) {
+    unsigned char *d = static_cast<unsigned char *>(u.dst);
+    for (int i = threadIdx.x; i < u.bytes; i += blockDim.x) d[i] = u.data[i];
+}
+
+kfac_status_t upload(void *dst, const void *src, size_t bytes, cudaStream_t s) {
+    static Upload u;     // host staging (kernel params are copied at launch)
+    const unsigned char *p = static_cast<const unsigned char *>(src);
+    for (size_t off = 0; off < bytes; off += sizeof(u.data)) {
+        const size_t nb = std::min(sizeof(u.data), bytes - off);
+        u.dst = static_cast<unsigned char *>(dst) + off;
+        u.bytes = (int)nb;
+        memcpy(u.data, p + off, nb);
+        upload_kernel<<<1, 256, 0, s>>>(u);
+        KFAC_LAUNCHED();
+    }
+    return KFAC_OK;
+}
+
+int levels_for(int n) {
+    int L = 0;
+    while ((n + (1 << L) - 1) / (1 << L) > kLeaf) ++L;
+    return L;
+}
+int ldw_for(int n) { return (int)round_up((size_t)n, 32); }
+
+struct Plan {
+    std::vector<TrdJob> jobs;
+    size_t bytes = 0, table_off = 0, leaf_off = 0, merge_off = 0, bt_off = 0;
+    std::vector<LeafDesc> leaves;
+    std::vector<std::vector<MergeDesc>> merges;       // per level (1..maxL)
+    std::vector<std::vector<BtStep>> bt;              // per back-transform step
+};
+
+Plan plan(const int32_t *dims, int count) {
+    Plan P;
+    size_t cur = 0;
+    auto take = [&](size_t bytes) {
+        cur = round_up(cur, 256);
+        const size_t r = cur;
+        cur += bytes;
+        return r;
+    };
+    P.table_off = take(sizeof(TrdJob) * count);
+    P.jobs.resize(count);
+    size_t nmerge_total = 0;
+    for (int i = 0; i < count; ++i) {
+        const int n = dims[i], ldw = ldw_for(n);
+        TrdJob &J = P.jobs[i];
+        memset(&J, 0, sizeof(J));
+        J.n = n;
+        J.ldw = ldw;
+        J.levels = levels_for(n);
+        const size_t sq = (size_t)n * ldw;
+#define TAKE(field, T, cnt) J.field = reinterpret_cast<T *>(take(sizeof(T) * (size_t)(cnt)))
+        TAKE(A, float, sq);
+        TAKE(Vb, float, sq);
+        TAKE(VW, float, (size_t)n * 64);
+        TAKE(WV, float, (size_t)n * 64);
+        TAKE(Z0, float, sq);
+        TAKE(Z1, float, sq);
+        TAKE(Qnd, float, sq);
+        TAKE(Tmp, float, sq);
+        J.Sb = J.A;
+        TAKE(Yb, float, (size_t)kBt * ldw);
+        TAKE(Y2b, float, (size_t)kBt * ldw);
+        TAKE(Gb, float, kBt * kBt);
+        TAKE(Tb, float, kBt * kBt);
+        TAKE(d, double, n);
+        TAKE(e, double, n);
+        TAKE(tau, double, n);
+        TAKE(x, double, n);
+        TAKE(y, double, n);
+        TAKE(D, double, n);
+        TAKE(dval, double, n);
+        TAKE(zval, double, n);
+        TAKE(rtau, double, n);
+        TAKE(wz, double, n);
+        TAKE(vnorm, double, n);
+        TAKE(rot_c, double, n);
+        TAKE(rot_s, double, n);
+        TAKE(col, int, n);
+        TAKE(posof, int, n);
+        TAKE(rorg, int, n);
+        TAKE(rot_p, int, n);
+        TAKE(rot_j, int, n);
+        TAKE(srcpos, int, n);
+        TAKE(mstate, int, 4 * (size_t)n);
+        TAKE(mscal, double, 2 * (size_t)n);
+        TAKE(part, double, (size_t)kMaxGroupCtas * kPart);
+        TAKE(bar, unsigned, 64);
+#undef TAKE
+        // leaves and merges
+        const int nleaf = 1 << J.levels;
+        for (int b = 0; b < nleaf; ++b) {
+            const int a0 = (int)((long long)b * n / nleaf), a1 = (int)((long long)(b + 1) * n / nleaf);
+            P.leaves.push_back({i, a0, a1 - a0});
+        }
+        if ((int)P.merges.size() < J.levels) P.merges.resize(J.levels);
+        for (int l = 1; l <= J.levels; ++l) {
+            const int span = 1 << l, nodes = nleaf >> l;
+            for (int q = 0; q < nodes; ++q) {
+                const int a0 = (int)((long long)q * span * n / nleaf);
+                const int s = (int)((long long)(q * span + span / 2) * n / nleaf);
+                const int a1 = (int)((long long)(q + 1) * span * n / nleaf);
+                P.merges[l - 1].push_back({i, a0, s - a0, a1 - s, q});
+                ++nmerge_total;
+            }
+        }
+        // back-transformation blocks (reflectors 0..n-2), processed last block first
+        const int nref = std::max(0, n - 1);
+        const int nblk = (nref + kBt - 1) / kBt;
+        if ((int)P.bt.size() < nblk) P.bt.resize(nblk);
+        for (int s = 0; s < nblk; ++s) {
+            const int blk = nblk - 1 - s;
+            const int b0 = blk * kBt;
+            P.bt[s].push_back({i, b0, std::min(kBt, nref - b0)});
+        }
+    }
+    P.leaf_off = take(P.leaves.size() * sizeof(LeafDesc));
+    P.merge_off = take(nmerge_total * sizeof(MergeDesc));
+    size_t nbt = 0;
+    for (auto &v : P.bt) nbt += v.size();
+    P.bt_off = take(nbt * sizeof(BtStep));
+    P.bytes = cur + 256;
+    return P;
+}
+
+template <class T>
+T *rebase(T *p, char *base) {
+    return reinterpret_cast<T *>(base + reinterpret_cast<uintptr_t>(p));
+}
+
+int panel_capacity(size_t smem) {
+    static int cap = -1;
+    static size_t cap_smem = 0;
+    if (cap < 0 || cap_smem != smem) {
+        int per_sm = 0;
+        cudaFuncSetAttribute(trd_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, trd_panel, kTrdThreads, smem);
+        cap = std::max(1, per_sm) * num_sms();
+        cap_smem = smem;
+    }
+    return std::min(cap, kMaxGroupCtas);
+}
+
+// Test modes (single factor): TRD_DEBUG_TRIDIAG stops after the reduction and copies (d, e) out;
+// TRD_DEBUG_STEDC replaces (d, e) by the caller's tridiagonal and stops before the
+// back-transformation (Z -> Q, eigenvalues in fp64 -> dbg_d).
+enum { TRD_FULL = 0, TRD_DEBUG_TRIDIAG = 1, TRD_DEBUG_STEDC = 2 };
+
+kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t *ldF, int count,
+                       float *const *Q, const int32_t *ldQ, float *const *evals, int32_t *info, void *ws,
+                       cudaStream_t s, int mode, double *dbg_d, double *dbg_e);
+
+}  // namespace
+
+size_t trd_workspace_bytes(const int32_t *dims, int count) { return plan(dims, count).bytes; }
+
+kfac_status_t trd_run(const float *const *F, const int32_t *dims, const int32_t *ldF, int count,
+                      float *const *Q, const int32_t *ldQ, float *const *evals, int32_t *info, void *ws,
+                      cudaStream_t s) {
+    return trd_exec(F, dims, ldF, count, Q, ldQ, evals, info, ws, s, TRD_FULL, nullptr, nullptr);
+}
+
+namespace {
+
+kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t *ldF, int count,
+                       float *const *Q, const int32_t *ldQ, float *const *evals, int32_t *info, void *ws,
+                       cudaStream_t s, int mode, double *dbg_d, double *dbg_e) {
+    Plan P = plan(dims, count);
+    char *base = reinterpret_cast<char *>(round_up(reinterpret_cast<uintptr_t>(ws), 256));
+    int max_n = 0;
+    for (int i = 0; i < count; ++i) {
+        TrdJob &J = P.jobs[i];
+        J.F = F[i]; J.Q = Q[i]; J.evals = evals[i];
+        J.info = info ? info + i : nullptr;
+        J.ldF = ldF[i]; J.ldQ = ldQ[i];
+        J.A = rebase(J.A, base); J.Vb = rebase(J.Vb, base); J.VW = rebase(J.VW, base); J.WV = rebase(J.WV, base);
+        J.Z0 = rebase(J.Z0, base); J.Z1 = rebase(J.Z1, base); J.Qnd = rebase(J.Qnd, base);
+        J.Tmp = rebase(J.Tmp, base); J.Sb = rebase(J.Sb, base); J.Yb = rebase(J.Yb, base);
+        J.Y2b = rebase(J.Y2b, base); J.Gb = rebase(J.Gb, base); J.Tb = rebase(J.Tb, base);
+        J.d = rebase(J.d, base); J.e = rebase(J.e, base); J.tau = rebase(J.tau, base);
+        J.x = rebase(J.x, base); J.y = rebase(J.y, base); J.D = rebase(J.D, base);
+        J.dval = rebase(J.dval, base); J.zval = rebase(J.zval, base); J.rtau = rebase(J.rtau, base);
+        J.wz = rebase(J.wz, base); J.vnorm = rebase(J.vnorm, base); J.rot_c = rebase(J.rot_c, base);
+        J.rot_s = rebase(J.rot_s, base); J.col = rebase(J.col, base); J.posof = rebase(J.posof, base);
+        J.rorg = rebase(J.rorg, base); J.rot_p = rebase(J.rot_p, base); J.rot_j = rebase(J.rot_j, base);
+        J.srcpos = rebase(J.srcpos, base); J.mstate = rebase(J.mstate, base); J.mscal = rebase(J.mscal, base);
+        J.part = rebase(J.part, base); J.bar = rebase(J.bar, base);
+        max_n = std::max(max_n, J.n);
+    }
+    TrdJob *djobs = reinterpret_cast<TrdJob *>(base + P.table_off);
+    RET_OK(upload(djobs, P.jobs.data(), sizeof(TrdJob) * count, s));
+    LeafDesc *dleaves = reinterpret_cast<LeafDesc *>(base + P.leaf_off);
+    RET_OK(upload(dleaves, P.leaves.data(), sizeof(LeafDesc) * P.leaves.size(), s));
+    MergeDesc *dmerges = reinterpret_cast<MergeDesc *>(base + P.merge_off);
+    {
+        std::vector<MergeDesc> flat;
+        for (auto &lv : P.merges) flat.insert(flat.end(), lv.begin(), lv.end());
+        if (!flat.empty()) RET_OK(upload(dmerges, flat.data(), sizeof(MergeDesc) * flat.size(), s));
+    }
+    BtStep *dbt = reinterpret_cast<BtStep *>(base + P.bt_off);
+    {
+        std::vector<BtStep> flat;
+        for (auto &v : P.bt) flat.insert(flat.end(), v.begin(), v.end());
+        if (!flat.empty()) RET_OK(upload(dbt, flat.data(), sizeof(BtStep) * flat.size(), s));
+    }
+    trd_zero_info<<<count, 32, 0, s>>>(djobs);
+    KFAC_LAUNCHED();
+    std::vector<GemmDesc> gd;
+    if (mode != TRD_DEBUG_STEDC) {
+    trd_init<<<dim3(std::min(2048, cdiv((long long)max_n * ldw_for(max_n), 256)), count), 256, 0, s>>>(djobs);
+    KFAC_LAUNCHED();
+
+    // ---- (1) tridiagonalisation: one persistent launch + one trailing GEMM per panel ----
+    static bool attr = false;
+    if (!attr) {
+        KFAC_CUDA_TRY(cudaFuncSetAttribute(bt_larft, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLarftSmem));
+        attr = true;
+    }
+    const size_t smem = (size_t)(round_up(max_n, 4) + 8) * sizeof(float);
+    const int cap = panel_capacity(smem);
+    static PanelLaunch PL;
+    for (int p0 = 0; p0 < max_n; p0 += kNb) {
+        std::vector<int> act;
+        double wsum = 0.0;
+        for (int i = 0; i < count; ++i)
+            if (P.jobs[i].n > p0) {
+                act.push_back(i);
+                const double m = P.jobs[i].n - p0;
+                wsum += m * m;
+            }
+        if (act.empty()) break;
+        const int na = (int)act.size();
+        if (na > cap) {
+            set_error("trd: more active factors than co-resident CTAs");
+            return KFAC_ERR_UNSUPPORTED;
+        }
+        // CTAs per factor ~ remaining work, >= 1, <= rows/16, total <= cap
+        std::vector<int> nc(na, 1);
+        int spare = cap - na;
+        for (int q = 0; q < na; ++q) {
+            const double m = P.jobs[act[q]].n - p0;
+            int want = (int)std::floor((cap - na) * (m * m) / wsum);
+            want = std::min(want, std::max(0, (int)(m / 16) - 1));
+            want = std::min(want, spare);
+            nc[q] += want;
+            spare -= want;
+        }
+        PL.jobs = djobs;
+        PL.p0 = p0;
+        PL.count = na;
+        int tot = 0;
+        for (int q = 0; q < na; ++q) {
+            PL.job[q] = act[q];
+            PL.cta_begin[q] = tot;
+            tot += nc[q];
+        }
+        PL.cta_begin[na] = tot;
+        for (int q = 0; q < na; ++q) {
+            KFAC_CUDA_TRY(cudaMemsetAsync(P.jobs[act[q]].bar, 0, sizeof(unsigned), s));
+        }
+        void *args[] = {&PL};
+        KFAC_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)trd_panel, dim3(tot), dim3(kTrdThreads), args, smem, s));
+        KFAC_LAUNCHED();
+        gd.clear();
+        const int q0 = p0 + kNb;
+        for (int q = 0; q < na; ++q) {
+            const TrdJob &J = P.jobs[act[q]];
+            if (J.n <= q0) continue;
+            GemmDesc g{};
+            g.M = g.N = J.n - q0;
+            g.K = 2 * kNb;
+            g.A = J.VW + (size_t)q0 * 64; g.lda = 64; g.trans_a = 0;
+            g.B = J.WV + (size_t)q0 * 64; g.ldb = 64; g.trans_b = 1;
+            g.C = J.A + (size_t)q0 * J.ldw + q0; g.ldc = J.ldw;
+            g.epi = EPI_SUB;
+            gd.push_back(g);
+        }
+        if (!gd.empty()) RET_OK(gemm_grouped(gd.data(), (int)gd.size(), 0.f, s));
+    }
+
+    }   // mode != TRD_DEBUG_STEDC
+    if (mode == TRD_DEBUG_TRIDIAG) {
+        KFAC_CUDA_TRY(cudaMemcpyAsync(dbg_d, P.jobs[0].d, sizeof(double) * P.jobs[0].n, cudaMemcpyDeviceToDevice, s));
+        KFAC_CUDA_TRY(cudaMemcpyAsync(dbg_e, P.jobs[0].e, sizeof(double) * P.jobs[0].n, cudaMemcpyDeviceToDevice, s));
+        return KFAC_OK;
+    }
+    if (mode == TRD_DEBUG_STEDC) {
+        KFAC_CUDA_TRY(cudaMemcpyAsync(P.jobs[0].d, dbg_d, sizeof(double) * P.jobs[0].n, cudaMemcpyDeviceToDevice, s));
+        KFAC_CUDA_TRY(cudaMemcpyAsync(P.jobs[0].e, dbg_e, sizeof(double) * P.jobs[0].n, cudaMemcpyDeviceToDevice, s));
+    }
+    // ---- (2) divide and conquer on T ----
+    dc_tear<<<dim3(cdiv(max_n, 256), count), 256, 0, s>>>(djobs);
+    KFAC_LAUNCHED();
+    if (!P.leaves.empty()) {
+        dc_leaf<<<cdiv((long long)P.leaves.size(), 4), 128, 0, s>>>(djobs, dleaves, (int)P.leaves.size());
+        KFAC_LAUNCHED();
+    }
+    int ping = 0;                  // current eigenvectors in Z0 (ping = 0) or Z1 (ping = 1)
+    size_t moff = 0;
+    for (size_t l = 0; l < P.merges.size(); ++l) {
+        const auto &lv = P.merges[l];
+        const int nmg = (int)lv.size();
+        const MergeDesc *dm = dmerges + moff;
+        moff += nmg;
+        int nmax = 0;
+        for (auto &m : lv) nmax = std::max(nmax, m.n1 + m.n2);
+        dc_deflate<<<nmg, 256, 0, s>>>(djobs, dm, ping);
+        KFAC_LAUNCHED();
+        dc_permute<<<dim3(cdiv(nmax, 8), nmg), 256, 0, s>>>(djobs, dm, ping);
+        KFAC_LAUNCHED();
+        dc_rotate<<<dim3(cdiv(nmax, 128), nmg), 128, 0, s>>>(djobs, dm);
+        KFAC_LAUNCHED();
+        dc_secular<<<dim3(cdiv(nmax, 8), nmg), 256, 0, s>>>(djobs, dm);
+        KFAC_LAUNCHED();
+        dc_zhat<<<dim3(cdiv(nmax, 128), nmg), 128, 0, s>>>(djobs, dm);
+        KFAC_LAUNCHED();
+        dc_vnorm<<<dim3(cdiv(nmax, 8), nmg), 256, 0, s>>>(djobs, dm);
+        KFAC_LAUNCHED();
+        dc_build_s<<<dim3(cdiv(nmax, 128), nmax, nmg), 128, 0, s>>>(djobs, dm);
+        KFAC_LAUNCHED();
+        gd.clear();
+        for (auto &m : lv) {
+            const TrdJob &J = P.jobs[m.job];
+            GemmDesc g{};
+            const int nm = m.n1 + m.n2;
+            g.M = nm; g.N = nm; g.K = nm;
+            g.A = J.Qnd + (size_t)m.a * J.ldw; g.lda = J.ldw;
+            g.B = J.Sb + (size_t)m.a * J.ldw; g.ldb = J.ldw;
+            g.C = J.Tmp + (size_t)m.a * J.ldw; g.ldc = J.ldw;
+            g.dyn = J.mstate + 4 * m.a + 2;
+            gd.push_back(g);
+        }
+        RET_OK(gemm_grouped(gd.data(), (int)gd.size(), 0.f, s));
+        dc_rank<<<dim3(cdiv(nmax, 128), nmg), 128, 0, s>>>(djobs, dm);
+        KFAC_LAUNCHED();
+        dc_assemble<<<dim3(cdiv(nmax, 128), nmax, nmg), 128, 0, s>>>(djobs, dm, ping);
+        KFAC_LAUNCHED();
+        ping ^= 1;
+    }
+
+    // ---- (3) back-transformation X = H Z, last block of reflectors first ----
+    size_t boff = 0;
+    for (auto &stp : P.bt) {
+        if (mode == TRD_DEBUG_STEDC) break;
+        const int ns = (int)stp.size();
+        std::vector<GemmDesc> g1, g2, g3;
+        for (auto &b : stp) {
+            const TrdJob &J = P.jobs[b.job];
+            const int m = J.n - b.b0 - 1;
+            const float *V = J.Vb + (size_t)(b.b0 + 1) * J.ldw + b.b0;
+            float *X = (ping ? J.Z1 : J.Z0) + (size_t)(b.b0 + 1) * J.ldw;
+            GemmDesc g{};
+            g.M = b.nr; g.N = b.nr; g.K = m;                     // G = V^T V
+            g.A = V; g.lda = J.ldw; g.trans_a = 1;
+            g.B = V; g.ldb = J.ldw;
+            g.C = J.Gb; g.ldc = kBt;
+            g1.push_back(g);
+            GemmDesc h{};
+            h.M = b.nr; h.N = J.n; h.K = m;                      // Y = V^T X
+            h.A = V; h.lda = J.ldw; h.trans_a = 1;
+            h.B = X; h.ldb = J.ldw;
+            h.C = J.Yb; h.ldc = J.ldw;
+            g1.push_back(h);
+            GemmDesc u{};
+            u.M = b.nr; u.N = J.n; u.K = b.nr;                   // Y2 = T Y
+            u.A = J.Tb; u.lda = kBt;
+            u.B = J.Yb; u.ldb = J.ldw;
+            u.C = J.Y2b; u.ldc = J.ldw;
+            g2.push_back(u);
+            GemmDesc v{};
+            v.M = m; v.N = J.n; v.K = b.nr;                      // X -= V Y2
+            v.A = V; v.lda = J.ldw;
+            v.B = J.Y2b; v.ldb = J.ldw;
+            v.C = X; v.ldc = J.ldw;
+            v.epi = EPI_SUB;
+            g3.push_back(v);
+        }
+        RET_OK(gemm_grouped(g1.data(), (int)g1.size(), 0.f, s));
+        bt_larft<<<ns, kBt, kLarftSmem, s>>>(djobs, dbt + boff);
+        KFAC_LAUNCHED();
+        RET_OK(gemm_grouped(g2.data(), (int)g2.size(), 0.f, s));
+        RET_OK(gemm_grouped(g3.data(), (int)g3.size(), 0.f, s));
+        boff += ns;
+    }
+    trd_output<<<dim3(cdiv(max_n, 128), max_n, count), 128, 0, s>>>(djobs, ping);
+    KFAC_LAUNCHED();
+    if (mode == TRD_DEBUG_STEDC)
+        KFAC_CUDA_TRY(cudaMemcpyAsync(dbg_d, P.jobs[0].D, sizeof(double) * P.jobs[0].n, cudaMemcpyDeviceToDevice, s));
+    return KFAC_OK;
+}
+
+}  // namespace
+}  // namespace kfac
+
+// Test hooks (not part of the public header).  Single factor, workspace allocated here.
+//   kfac_debug_tridiag: F (n x ldF, device) -> d (n), e (n-1) of H^T F H (device fp64).
+//   kfac_debug_stedc:   tridiagonal (d, e) (device fp64) -> Z (n x ldZ fp32, columns =
+//                       eigenvectors), w (n fp64, ascending).
+extern "C" int kfac_debug_tridiag(const float *F, int n, int ldF, double *d, double *e, void *stream) {
+    const int32_t dims[1] = {n}, ld[1] = {ldF};
+    const size_t bytes = kfac::trd_workspace_bytes(dims, 1);
+    void *ws = nullptr;
+    if (cudaMalloc(&ws, bytes) != cudaSuccess) return KFAC_ERR_CUDA;
+    float *Qd = nullptr, *ev = nullptr;
+    const float *Fp[1] = {F};
+    float *Qp[1] = {Qd}, *Ep[1] = {ev};
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    int st = kfac::trd_exec(Fp, dims, ld, 1, Qp, ld, Ep, nullptr, ws, s, kfac::TRD_DEBUG_TRIDIAG, d, e);
+    cudaStreamSynchronize(s);
+    cudaFree(ws);
+    return st;
+}
+
+extern "C" int kfac_debug_stedc(const double *d, const double *e, int n, float *Z, int ldZ, double *w,
+                                void *stream) {
+    const int32_t dims[1] = {n}, ld[1] = {ldZ};
+    const size_t bytes = kfac::trd_workspace_bytes(dims, 1);
+    void *ws = nullptr, *ev = nullptr;
+    if (cudaMalloc(&ws, bytes) != cudaSuccess) return KFAC_ERR_CUDA;
+    if (cudaMalloc(&ev, sizeof(float) * n) != cudaSuccess) return KFAC_ERR_CUDA;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    cudaMemcpyAsync(w, d, sizeof(double) * n, cudaMemcpyDeviceToDevice, s);
+    double *e_copy = nullptr;
+    if (cudaMalloc(&e_copy, sizeof(double) * n) != cudaSuccess) return KFAC_ERR_CUDA;
+    cudaMemsetAsync(e_copy, 0, sizeof(double) * n, s);
+    if (n > 1) cudaMemcpyAsync(e_copy, e, sizeof(double) * (n - 1), cudaMemcpyDeviceToDevice, s);
+    const float *Fp[1] = {nullptr};
+    float *Qp[1] = {Z}, *Ep[1] = {static_cast<float *>(ev)};
+    int st = kfac::trd_exec(Fp, dims, ld, 1, Qp, ld, Ep, nullptr, ws, s, kfac::TRD_DEBUG_STEDC, w, e_copy);
+    cudaStreamSynchronize(s);
+    cudaFree(ws);
+    cudaFree(ev);
+    cudaFree(e_copy);
+    return st;
+}

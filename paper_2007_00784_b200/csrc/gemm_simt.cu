@@ -33,6 +33,8 @@ __global__ void __launch_bounds__(NT) gemm_simt_kernel(const __grid_constant__ G
     const int tiles_n = (d.N + BN - 1) / BN;
     const int m0 = (local / tiles_n) * BM, n0 = (local % tiles_n) * BN;
     const int t = threadIdx.x;
+    const int Me = d.M, Ne = d.dyn ? min(d.N, d.dyn[0]) : d.N, Ke = d.dyn ? min(d.K, d.dyn[1]) : d.K;
+    if (n0 >= Ne) return;
 
     // loader coordinates: 8 consecutive elements per thread per operand
     int a_r, a_c, b_r, b_c;
@@ -48,13 +50,13 @@ __global__ void __launch_bounds__(NT) gemm_simt_kernel(const __grid_constant__ G
             int m, k;
             if (d.trans_a) { k = k0 + a_r; m = m0 + a_c + i; }
             else           { m = m0 + a_r; k = k0 + a_c + i; }
-            ra[i] = (m < d.M && k < d.K)
+            ra[i] = (m < Me && k < Ke)
                         ? __ldg(d.trans_a ? d.A + (size_t)k * d.lda + m : d.A + (size_t)m * d.lda + k)
                         : 0.f;
             int n, kb;
             if (d.trans_b) { n = n0 + b_r; kb = k0 + b_c + i; }
             else           { kb = k0 + b_r; n = n0 + b_c + i; }
-            rb[i] = (n < d.N && kb < d.K)
+            rb[i] = (n < Ne && kb < Ke)
                         ? __ldg(d.trans_b ? d.B + (size_t)n * d.ldb + kb : d.B + (size_t)kb * d.ldb + n)
                         : 0.f;
         }
@@ -76,7 +78,7 @@ __global__ void __launch_bounds__(NT) gemm_simt_kernel(const __grid_constant__ G
         for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
 
     const int ty = t / 16, tx = t % 16;
-    const int nk = (d.K + BK - 1) / BK;
+    const int nk = (Ke + BK - 1) / BK;
     load(0);
     store(0);
     __syncthreads();
@@ -107,17 +109,19 @@ __global__ void __launch_bounds__(NT) gemm_simt_kernel(const __grid_constant__ G
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
         const int m = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
-        if (m >= d.M) continue;
-        const float vr = d.epi ? d.vr[m] : 0.f;
+        if (m >= Me) continue;
+        const float vr = epi_uses_vectors(d.epi) ? d.vr[m] : 0.f;
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
             const int n = n0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + (j - 4));
-            if (n >= d.N) continue;
+            if (n >= Ne) continue;
             float v = acc[i][j];
             if (d.epi == EPI_DIV_EIGEN) {
                 v = v / fmaxf(fmaf(vr, d.vc[n], batch.damping), 1e-12f);
             } else if (d.epi == EPI_DIV_FACTORED) {
                 v = v / fmaxf((vr + batch.damping) * (d.vc[n] + batch.damping), 1e-12f);
+            } else if (d.epi == EPI_SUB) {
+                v = d.C[(size_t)m * d.ldc + n] - v;
             }
             d.C[(size_t)m * d.ldc + n] = v;
         }

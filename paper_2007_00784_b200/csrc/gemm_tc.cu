@@ -53,6 +53,7 @@ struct TcDesc {
     float *C;
     const float *vr;
     const float *vc;
+    const int *dyn;       // optional device {N_eff, K_eff}
     int M, N, K, ldc;
     int a_mn, b_mn, epi;
     int tile_begin, tiles_n;
@@ -312,7 +313,9 @@ __global__ void __launch_bounds__(NT, 1) gemm_tc_kernel(const __grid_constant__ 
     const TcDesc &d = batch.d[find_desc(batch, tile)];
     const int local = tile - d.tile_begin;
     const int m0 = (local / d.tiles_n) * BM, n0 = (local % d.tiles_n) * BN;
-    const int nk = (d.K + BK - 1) / BK;
+    const int Ne = d.dyn ? min(d.N, d.dyn[0]) : d.N, Ke = d.dyn ? min(d.K, d.dyn[1]) : d.K;
+    const int nk = (Ke + BK - 1) / BK;
+    if (n0 >= Ne || nk <= 0) return;          // whole CTA exits before any barrier / TMEM setup
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     if (warp == W_TMA && lane == 0) {
         prefetch_map(&d.ta);
@@ -349,16 +352,17 @@ __global__ void __launch_bounds__(NT, 1) gemm_tc_kernel(const __grid_constant__ 
         drain_loop(S, tmem, nk, wq, acc);
         const int m = m0 + wq * 32 + lane;
         if (m < d.M) {
-            const float vr = d.epi ? d.vr[m] : 0.f;
+            const float vr = epi_uses_vectors(d.epi) ? d.vr[m] : 0.f;
             float *crow = d.C + (size_t)m * d.ldc;
 #pragma unroll
             for (int j = 0; j < BN; ++j) {
                 const int n = n0 + j;
-                if (n < d.N) {
+                if (n < Ne) {
                     float v = acc[j];
                     if (d.epi == EPI_DIV_EIGEN) v = v / fmaxf(fmaf(vr, d.vc[n], batch.damping), 1e-12f);
                     else if (d.epi == EPI_DIV_FACTORED)
                         v = v / fmaxf((vr + batch.damping) * (d.vc[n] + batch.damping), 1e-12f);
+                    else if (d.epi == EPI_SUB) v = crow[n] - v;
                     crow[n] = v;
                 }
             }
@@ -586,7 +590,7 @@ kfac_status_t gemm_tc_grouped(const GemmDesc *descs, int count, float damping, c
                 set_error("cuTensorMapEncodeTiled failed");
                 return KFAC_ERR_CUDA;
             }
-            t.C = g.C; t.vr = g.vr; t.vc = g.vc;
+            t.C = g.C; t.vr = g.vr; t.vc = g.vc; t.dyn = g.dyn;
             t.M = g.M; t.N = g.N; t.K = g.K; t.ldc = g.ldc; t.epi = g.epi;
             t.tiles_n = cdiv(g.N, BN);
             t.tile_begin = tiles;
@@ -633,12 +637,14 @@ kfac_status_t syrk_tc_partial(const FactorJob *jobs, int count, cudaStream_t s) 
 }  // namespace kfac
 
 // Test hook (not part of the public header): run one GEMM through a chosen engine.
-// engine 0 = SIMT, 1 = tcgen05.  Returns a kfac_status_t.
+// engine 0 = SIMT, 1 = tcgen05; | 4 selects the C -= AB epilogue.  Returns a kfac_status_t.
 extern "C" int kfac_debug_gemm(int engine, const float *A, int lda, int trans_a, const float *B, int ldb,
                                int trans_b, float *C, int ldc, int M, int N, int K, void *stream, float *debug) {
     kfac::GemmDesc d{};
     d.A = A; d.lda = lda; d.trans_a = trans_a; d.B = B; d.ldb = ldb; d.trans_b = trans_b;
     d.C = C; d.ldc = ldc; d.M = M; d.N = N; d.K = K;
+    if (engine & 4) d.epi = kfac::EPI_SUB;      // C -= op(A) op(B)
+    engine &= 3;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     if (engine == 1) {
         if (!kfac::gemm_tc_supported(d)) return KFAC_ERR_UNSUPPORTED;

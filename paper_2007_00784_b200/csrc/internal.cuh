@@ -13,7 +13,10 @@ enum GemmEpi : int {
     EPI_STORE = 0,
     EPI_DIV_EIGEN = 1,      // C /= max(vr[m]*vc[n] + damping, 1e-12)        (Eq. 14)
     EPI_DIV_FACTORED = 2,   // C /= max((vr[m]+damping)*(vc[n]+damping), 1e-12)
+    EPI_SUB = 3,            // C = C_in - op(A) op(B)   (symmetric rank-2k update, back-transform)
 };
+
+__host__ __device__ inline bool epi_uses_vectors(int epi) { return epi == EPI_DIV_EIGEN || epi == EPI_DIV_FACTORED; }
 
 struct GemmDesc {
     const float *A;
@@ -25,6 +28,7 @@ struct GemmDesc {
     int lda, ldb, ldc;
     int trans_a, trans_b, epi;
     int tile_begin;          // filled by the launcher
+    const int *dyn;          // optional device {N_eff, K_eff}: the kernel clips N and K to them
 };
 
 constexpr int kGemmMaxDescs = 64;
