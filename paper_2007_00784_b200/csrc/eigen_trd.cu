@@ -58,11 +58,11 @@ struct TrdJob {
     float *A;          // n x ldw working matrix (full symmetric storage, pads zero)
     float *Vb;         // n x ldw reflectors: column k = v_k (v_k[k+1] = 1, zero above)
     float *VW, *WV;    // n x 64 panel buffers: [V | W] and [W | V] of the current panel
-    float *Z0, *Z1;    // n x ldw eigenvectors of T (D&C ping-pong)
-    float *Qnd, *Tmp;  // n x ldw D&C scratch (permuted/rotated columns, GEMM output)
-    float *Sb;         // n x ldw D&C secular eigenvectors S (aliases A after the reduction)
-    float *Yb, *Y2b;   // kBt x ldw back-transformation scratch
-    float *Gb, *Tb;    // kBt x kBt Gram matrix V^T V and WY factor T
+    double *Z0, *Z1;   // n x ldw eigenvectors of T (D&C ping-pong), fp64
+    double *Qnd, *Tmp; // n x ldw D&C scratch (permuted/rotated columns, GEMM output)
+    double *Sb;        // n x ldw D&C secular eigenvectors S
+    double *Yb, *Y2b;  // kBt x ldw back-transformation scratch
+    double *Gb, *Tb;   // kBt x kBt Gram matrix V^T V and WY factor T
     double *d, *e, *tau;       // tridiagonal T and reflector scalars
     double *x, *y;             // corrected column / mat-vec result (sytrd)
     double *D;                 // current eigenvalues of the D&C subproblems
@@ -139,8 +139,9 @@ __global__ void trd_init(const TrdJob *jobs) {
 // ----------------------------------------------------- panel kernel --
 struct PanelLaunch {
     const TrdJob *jobs;
-    int p0, count;
+    int count;
     int job[kMaxGroupCtas];
+    int p0[kMaxGroupCtas];                 // panel start of each group's factor (staggered)
     int cta_begin[kMaxGroupCtas + 1];
 };
 
@@ -170,7 +171,7 @@ __global__ void __launch_bounds__(kTrdThreads, 1) trd_panel(const __grid_constan
     }
     const TrdJob &J = L.jobs[L.job[g]];
     const int c = blockIdx.x - L.cta_begin[g], nc = L.cta_begin[g + 1] - L.cta_begin[g];
-    const int n = J.n, ldw = J.ldw, p0 = L.p0;
+    const int n = J.n, ldw = J.ldw, p0 = L.p0[g];
     const float *A = J.A;
     float *VW = J.VW, *WV = J.WV;
     double *part = J.part;
@@ -240,23 +241,53 @@ __global__ void __launch_bounds__(kTrdThreads, 1) trd_panel(const __grid_constan
             VW[(size_t)r * 64 + i] = v;
             WV[(size_t)r * 64 + kNb + i] = v;
         }
-        // symmetric mat-vec (one warp per row) + panel dot partials (lane q -> column q)
+        // symmetric mat-vec (one warp per pair of rows, 8 float4 loads in flight per lane) + panel
+        // dot partials (lane q -> panel column q)
         double pa = 0.0, pb = 0.0;
         const float4 *v4 = reinterpret_cast<const float4 *>(vsm);
-        for (int r = lo + warp; r < hi; r += kTrdWarps) {
-            const float4 *a4 = reinterpret_cast<const float4 *>(A + (size_t)r * ldw + c0);
-            double acc = 0.0;
-            for (int q = lane; q < nv4; q += 32) {
-                const float4 a = __ldg(a4 + q), v = v4[q];
-                acc += (double)a.x * v.x + (double)a.y * v.y + (double)a.z * v.z + (double)a.w * v.w;
+        for (int r = lo + 2 * warp; r < hi; r += 2 * kTrdWarps) {
+            const bool two = r + 1 < hi;
+            const float4 *a0 = reinterpret_cast<const float4 *>(A + (size_t)r * ldw + c0);
+            const float4 *a1 = two ? a0 + ldw / 4 : a0;
+            double s0 = 0.0, s1 = 0.0;
+            int q = lane;
+            for (; q + 96 < nv4; q += 128) {
+                float4 x[4], z[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    x[u] = __ldg(a0 + q + 32 * u);
+                    z[u] = __ldg(a1 + q + 32 * u);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const float4 v = v4[q + 32 * u];
+                    s0 += (double)x[u].x * v.x + (double)x[u].y * v.y + (double)x[u].z * v.z + (double)x[u].w * v.w;
+                    s1 += (double)z[u].x * v.x + (double)z[u].y * v.y + (double)z[u].z * v.z + (double)z[u].w * v.w;
+                }
+            }
+            for (; q < nv4; q += 32) {
+                const float4 x = __ldg(a0 + q), z = __ldg(a1 + q), v = v4[q];
+                s0 += (double)x.x * v.x + (double)x.y * v.y + (double)x.z * v.z + (double)x.w * v.w;
+                s1 += (double)z.x * v.x + (double)z.y * v.y + (double)z.z * v.z + (double)z.w * v.w;
             }
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-            const double vr = vsm[r - c0];
-            if (lane == 0) __stcg(J.y + r, acc);
+            for (int o = 16; o > 0; o >>= 1) {
+                s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+                s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+            }
+            if (lane == 0) {
+                __stcg(J.y + r, s0);
+                if (two) __stcg(J.y + r + 1, s1);
+            }
             if (lane < i) {
-                pa += (double)ldcg(VW + (size_t)r * 64 + lane) * vr;
-                pb += (double)ldcg(VW + (size_t)r * 64 + kNb + lane) * vr;
+                const double v0 = vsm[r - c0];
+                pa += (double)ldcg(VW + (size_t)r * 64 + lane) * v0;
+                pb += (double)ldcg(VW + (size_t)r * 64 + kNb + lane) * v0;
+                if (two) {
+                    const double v1 = vsm[r + 1 - c0];
+                    pa += (double)ldcg(VW + (size_t)(r + 1) * 64 + lane) * v1;
+                    pb += (double)ldcg(VW + (size_t)(r + 1) * 64 + kNb + lane) * v1;
+                }
             }
         }
         red[warp][lane] = pa;
@@ -396,7 +427,7 @@ __global__ void dc_leaf(const TrdJob *jobs, const LeafDesc *leaves, int nleaves)
         int rk = 0;
         for (int q = 0; q < ns; ++q) rk += (d[q] < d[j]) || (d[q] == d[j] && q < j);
         if (lane == 0) J.D[a + rk] = d[j];
-        if (lane < ns) J.Z0[(size_t)(a + lane) * J.ldw + a + rk] = (float)z[j];
+        if (lane < ns) J.Z0[(size_t)(a + lane) * J.ldw + a + rk] = z[j];
     }
     if (iters > 60 * kLeaf && lane == 0 && J.info) atomicAdd(J.info, 1);
 }
@@ -414,7 +445,7 @@ __global__ void dc_deflate(const TrdJob *jobs, const MergeDesc *merges, int ping
     const MergeDesc M = merges[blockIdx.x];
     const TrdJob &J = jobs[M.job];
     const int a = M.a, n1 = M.n1, nm = M.n1 + M.n2, ldw = J.ldw;
-    const float *Z = ping ? J.Z1 : J.Z0;
+    const double *Z = ping ? J.Z1 : J.Z0;
     const double rho = J.e[a + n1 - 1];
     const double sgn = rho < 0 ? -1.0 : 1.0;
     double *dv = J.dval + a, *zv = J.zval + a;
@@ -426,7 +457,7 @@ __global__ void dc_deflate(const TrdJob *jobs, const MergeDesc *merges, int ping
         double zc;
         int rank;
         if (c < n1) {
-            zc = (double)Z[(size_t)(a + n1 - 1) * ldw + a + c];
+            zc = Z[(size_t)(a + n1 - 1) * ldw + a + c];
             int lo = 0, hi = M.n2;                   // # right entries < dc
             while (lo < hi) {
                 const int mid = (lo + hi) >> 1;
@@ -434,7 +465,7 @@ __global__ void dc_deflate(const TrdJob *jobs, const MergeDesc *merges, int ping
             }
             rank = c + lo;
         } else {
-            zc = sgn * (double)Z[(size_t)(a + n1) * ldw + a + c];
+            zc = sgn * Z[(size_t)(a + n1) * ldw + a + c];
             int lo = 0, hi = n1;                     // # left entries <= dc
             while (lo < hi) {
                 const int mid = (lo + hi) >> 1;
@@ -544,13 +575,13 @@ __global__ void dc_permute(const TrdJob *jobs, const MergeDesc *merges, int ping
     const int a = M.a, n1 = M.n1, nm = M.n1 + M.n2, ldw = J.ldw;
     const int r = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x % 32;
     if (r >= nm) return;
-    const float *Z = ping ? J.Z1 : J.Z0;
+    const double *Z = ping ? J.Z1 : J.Z0;
     const int *posof = J.posof + a;
-    float *dst = J.Qnd + (size_t)(a + r) * ldw;
-    const float *src = Z + (size_t)(a + r) * ldw + a;
+    double *dst = J.Qnd + (size_t)(a + r) * ldw;
+    const double *src = Z + (size_t)(a + r) * ldw + a;
     for (int c = lane; c < nm; c += 32) {
         const bool same = (c < n1) == (r < n1);
-        dst[posof[c]] = same ? src[c] : 0.f;
+        dst[posof[c]] = same ? src[c] : 0.0;
     }
 }
 
@@ -562,14 +593,14 @@ __global__ void dc_rotate(const TrdJob *jobs, const MergeDesc *merges) {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     const int nrot = J.mstate[4 * a + 1];
     if (r >= nm || nrot == 0) return;
-    float *row = J.Qnd + (size_t)(a + r) * J.ldw;
+    double *row = J.Qnd + (size_t)(a + r) * J.ldw;
     const int *posof = J.posof + a;
     for (int q = 0; q < nrot; ++q) {
         const int pp = posof[J.rot_p[a + q]], pj = posof[J.rot_j[a + q]];
         const double c = J.rot_c[a + q], s = J.rot_s[a + q];
         const double x = row[pp], y = row[pj];
-        row[pp] = (float)(c * x + s * y);
-        row[pj] = (float)(c * y - s * x);
+        row[pp] = c * x + s * y;
+        row[pj] = c * y - s * x;
     }
 }
 
@@ -731,11 +762,11 @@ __global__ void dc_build_s(const TrdJob *jobs, const MergeDesc *merges) {
     const int i = blockIdx.y, j = blockIdx.x * blockDim.x + threadIdx.x;
     const int rows = min(nm, (k + 31) & ~31);
     if (i >= rows || j >= k) return;
-    float v = 0.f;
+    double v = 0.0;
     if (i < k) {
         const double *dv = J.dval + a, *rt = J.rtau + a;
         const int *ro = J.rorg + a;
-        v = (float)(J.wz[a + i] / delta(dv, rt, ro, i, j) * J.vnorm[a + j]);
+        v = J.wz[a + i] / delta(dv, rt, ro, i, j) * J.vnorm[a + j];
     }
     J.Sb[(size_t)(a + i) * J.ldw + j] = v;
 }
@@ -767,9 +798,9 @@ __global__ void dc_assemble(const TrdJob *jobs, const MergeDesc *merges, int pin
     const int a = M.a, nm = M.n1 + M.n2, k = J.mstate[4 * a + 0], ldw = J.ldw;
     const int r = blockIdx.y, p = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= nm || p >= nm) return;
-    float *Zd = ping ? J.Z0 : J.Z1;                 // destination = the other buffer
+    double *Zd = ping ? J.Z0 : J.Z1;                // destination = the other buffer
     const int src = J.srcpos[a + p];
-    const float v = src < k ? J.Tmp[(size_t)(a + r) * ldw + src] : J.Qnd[(size_t)(a + r) * ldw + src];
+    const double v = src < k ? J.Tmp[(size_t)(a + r) * ldw + src] : J.Qnd[(size_t)(a + r) * ldw + src];
     Zd[(size_t)(a + r) * ldw + a + p] = v;
 }
 
@@ -802,17 +833,23 @@ __global__ void bt_larft(const TrdJob *jobs, const BtStep *steps) {
     }
     for (int idx = t; idx < kBt * kBt; idx += blockDim.x) {
         const int r = idx / kBt, c = idx % kBt;
-        J.Tb[idx] = (r < nr && c < nr) ? (float)T[r][c] : 0.f;
+        J.Tb[idx] = (r < nr && c < nr) ? T[r][c] : 0.0;
     }
 }
 
-__global__ void trd_output(const TrdJob *jobs, int ping) {
-    const TrdJob &J = jobs[blockIdx.z];
-    const int r = blockIdx.y, c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= J.n || c >= J.n) return;
-    const float *Z = ping ? J.Z1 : J.Z0;
-    J.Q[(size_t)r * J.ldQ + c] = Z[(size_t)r * J.ldw + c];
-    if (r == 0) J.evals[c] = (float)fmax(J.D[c], 0.0);
+// Eigenvectors of T after the last merge level: level l writes Z0 (l even) / Z1 (l odd).
+__host__ __device__ inline double *final_z(const TrdJob &J) { return (J.levels & 1) ? J.Z1 : J.Z0; }
+
+__global__ void trd_output(const TrdJob *jobs) {
+    const TrdJob &J = jobs[blockIdx.y];
+    const double *Z = final_z(J);
+    const long long total = (long long)J.n * J.n;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const int r = (int)(e / J.n), c = (int)(e % J.n);
+        J.Q[(size_t)r * J.ldQ + c] = (float)Z[(size_t)r * J.ldw + c];
+        if (r == 0) J.evals[c] = (float)fmax(J.D[c], 0.0);
+    }
 }
 
 __global__ void trd_zero_info(const TrdJob *jobs) {
@@ -885,15 +922,15 @@ Plan plan(const int32_t *dims, int count) {
         TAKE(Vb, float, sq);
         TAKE(VW, float, (size_t)n * 64);
         TAKE(WV, float, (size_t)n * 64);
-        TAKE(Z0, float, sq);
-        TAKE(Z1, float, sq);
-        TAKE(Qnd, float, sq);
-        TAKE(Tmp, float, sq);
-        J.Sb = J.A;
-        TAKE(Yb, float, (size_t)kBt * ldw);
-        TAKE(Y2b, float, (size_t)kBt * ldw);
-        TAKE(Gb, float, kBt * kBt);
-        TAKE(Tb, float, kBt * kBt);
+        TAKE(Z0, double, sq);
+        TAKE(Z1, double, sq);
+        TAKE(Qnd, double, sq);
+        TAKE(Tmp, double, sq);
+        TAKE(Sb, double, sq);
+        TAKE(Yb, double, (size_t)kBt * ldw);
+        TAKE(Y2b, double, (size_t)kBt * ldw);
+        TAKE(Gb, double, kBt * kBt);
+        TAKE(Tb, double, kBt * kBt);
         TAKE(d, double, n);
         TAKE(e, double, n);
         TAKE(tau, double, n);
@@ -1036,7 +1073,7 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
     }
     trd_zero_info<<<count, 32, 0, s>>>(djobs);
     KFAC_LAUNCHED();
-    std::vector<GemmDesc> gd;
+    std::vector<Gemm64Desc> gd;
     if (mode != TRD_DEBUG_STEDC) {
     trd_init<<<dim3(std::min(2048, cdiv((long long)max_n * ldw_for(max_n), 256)), count), 256, 0, s>>>(djobs);
     KFAC_LAUNCHED();
@@ -1050,16 +1087,22 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
     const size_t smem = (size_t)(round_up(max_n, 4) + 8) * sizeof(float);
     const int cap = panel_capacity(smem);
     static PanelLaunch PL;
-    for (int p0 = 0; p0 < max_n; p0 += kNb) {
-        std::vector<int> act;
+    // Staggered schedule: factor j (P_j panels) starts at launch P_max - P_j, so all factors finish
+    // together and the small ones share the GPU with the big ones' small trailing matrices.
+    int pmax = 0;
+    for (int i = 0; i < count; ++i) pmax = std::max(pmax, cdiv(P.jobs[i].n, kNb));
+    for (int t = 0; t < pmax; ++t) {
+        std::vector<int> act, pst;
         double wsum = 0.0;
-        for (int i = 0; i < count; ++i)
-            if (P.jobs[i].n > p0) {
-                act.push_back(i);
-                const double m = P.jobs[i].n - p0;
-                wsum += m * m;
-            }
-        if (act.empty()) break;
+        for (int i = 0; i < count; ++i) {
+            const int pidx = t - (pmax - cdiv(P.jobs[i].n, kNb));
+            if (pidx < 0) continue;
+            act.push_back(i);
+            pst.push_back(pidx * kNb);
+            const double m = P.jobs[i].n - pidx * kNb;
+            wsum += m * m;
+        }
+        if (act.empty()) continue;
         const int na = (int)act.size();
         if (na > cap) {
             set_error("trd: more active factors than co-resident CTAs");
@@ -1069,7 +1112,7 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
         std::vector<int> nc(na, 1);
         int spare = cap - na;
         for (int q = 0; q < na; ++q) {
-            const double m = P.jobs[act[q]].n - p0;
+            const double m = P.jobs[act[q]].n - pst[q];
             int want = (int)std::floor((cap - na) * (m * m) / wsum);
             want = std::min(want, std::max(0, (int)(m / 16) - 1));
             want = std::min(want, spare);
@@ -1077,11 +1120,11 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
             spare -= want;
         }
         PL.jobs = djobs;
-        PL.p0 = p0;
         PL.count = na;
         int tot = 0;
         for (int q = 0; q < na; ++q) {
             PL.job[q] = act[q];
+            PL.p0[q] = pst[q];
             PL.cta_begin[q] = tot;
             tot += nc[q];
         }
@@ -1093,20 +1136,20 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
         KFAC_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)trd_panel, dim3(tot), dim3(kTrdThreads), args, smem, s));
         KFAC_LAUNCHED();
         gd.clear();
-        const int q0 = p0 + kNb;
         for (int q = 0; q < na; ++q) {
             const TrdJob &J = P.jobs[act[q]];
+            const int q0 = pst[q] + kNb;
             if (J.n <= q0) continue;
-            GemmDesc g{};
+            Gemm64Desc g{};
             g.M = g.N = J.n - q0;
             g.K = 2 * kNb;
-            g.A = J.VW + (size_t)q0 * 64; g.lda = 64; g.trans_a = 0;
-            g.B = J.WV + (size_t)q0 * 64; g.ldb = 64; g.trans_b = 1;
-            g.C = J.A + (size_t)q0 * J.ldw + q0; g.ldc = J.ldw;
+            g.A = J.VW + (size_t)q0 * 64; g.ta = DT_F32; g.lda = 64; g.trans_a = 0;
+            g.B = J.WV + (size_t)q0 * 64; g.tb = DT_F32; g.ldb = 64; g.trans_b = 1;
+            g.C = J.A + (size_t)q0 * J.ldw + q0; g.tc = DT_F32; g.ldc = J.ldw;
             g.epi = EPI_SUB;
             gd.push_back(g);
         }
-        if (!gd.empty()) RET_OK(gemm_grouped(gd.data(), (int)gd.size(), 0.f, s));
+        if (!gd.empty()) RET_OK(gemm64_grouped(gd.data(), (int)gd.size(), s));
     }
 
     }   // mode != TRD_DEBUG_STEDC
@@ -1126,7 +1169,7 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
         dc_leaf<<<cdiv((long long)P.leaves.size(), 4), 128, 0, s>>>(djobs, dleaves, (int)P.leaves.size());
         KFAC_LAUNCHED();
     }
-    int ping = 0;                  // current eigenvectors in Z0 (ping = 0) or Z1 (ping = 1)
+    int ping = 0;                  // level l reads Z0 (l odd) / Z1 (l even) for every factor
     size_t moff = 0;
     for (size_t l = 0; l < P.merges.size(); ++l) {
         const auto &lv = P.merges[l];
@@ -1152,16 +1195,16 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
         gd.clear();
         for (auto &m : lv) {
             const TrdJob &J = P.jobs[m.job];
-            GemmDesc g{};
+            Gemm64Desc g{};
             const int nm = m.n1 + m.n2;
             g.M = nm; g.N = nm; g.K = nm;
-            g.A = J.Qnd + (size_t)m.a * J.ldw; g.lda = J.ldw;
-            g.B = J.Sb + (size_t)m.a * J.ldw; g.ldb = J.ldw;
-            g.C = J.Tmp + (size_t)m.a * J.ldw; g.ldc = J.ldw;
+            g.A = J.Qnd + (size_t)m.a * J.ldw; g.ta = DT_F64; g.lda = J.ldw;
+            g.B = J.Sb + (size_t)m.a * J.ldw; g.tb = DT_F64; g.ldb = J.ldw;
+            g.C = J.Tmp + (size_t)m.a * J.ldw; g.tc = DT_F64; g.ldc = J.ldw;
             g.dyn = J.mstate + 4 * m.a + 2;
             gd.push_back(g);
         }
-        RET_OK(gemm_grouped(gd.data(), (int)gd.size(), 0.f, s));
+        RET_OK(gemm64_grouped(gd.data(), (int)gd.size(), s));
         dc_rank<<<dim3(cdiv(nmax, 128), nmg), 128, 0, s>>>(djobs, dm);
         KFAC_LAUNCHED();
         dc_assemble<<<dim3(cdiv(nmax, 128), nmax, nmg), 128, 0, s>>>(djobs, dm, ping);
@@ -1174,46 +1217,46 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
     for (auto &stp : P.bt) {
         if (mode == TRD_DEBUG_STEDC) break;
         const int ns = (int)stp.size();
-        std::vector<GemmDesc> g1, g2, g3;
+        std::vector<Gemm64Desc> g1, g2, g3;
         for (auto &b : stp) {
             const TrdJob &J = P.jobs[b.job];
             const int m = J.n - b.b0 - 1;
             const float *V = J.Vb + (size_t)(b.b0 + 1) * J.ldw + b.b0;
-            float *X = (ping ? J.Z1 : J.Z0) + (size_t)(b.b0 + 1) * J.ldw;
-            GemmDesc g{};
+            double *X = final_z(J) + (size_t)(b.b0 + 1) * J.ldw;
+            Gemm64Desc g{};
             g.M = b.nr; g.N = b.nr; g.K = m;                     // G = V^T V
-            g.A = V; g.lda = J.ldw; g.trans_a = 1;
-            g.B = V; g.ldb = J.ldw;
-            g.C = J.Gb; g.ldc = kBt;
+            g.A = V; g.ta = DT_F32; g.lda = J.ldw; g.trans_a = 1;
+            g.B = V; g.tb = DT_F32; g.ldb = J.ldw;
+            g.C = J.Gb; g.tc = DT_F64; g.ldc = kBt;
             g1.push_back(g);
-            GemmDesc h{};
+            Gemm64Desc h{};
             h.M = b.nr; h.N = J.n; h.K = m;                      // Y = V^T X
-            h.A = V; h.lda = J.ldw; h.trans_a = 1;
-            h.B = X; h.ldb = J.ldw;
-            h.C = J.Yb; h.ldc = J.ldw;
+            h.A = V; h.ta = DT_F32; h.lda = J.ldw; h.trans_a = 1;
+            h.B = X; h.tb = DT_F64; h.ldb = J.ldw;
+            h.C = J.Yb; h.tc = DT_F64; h.ldc = J.ldw;
             g1.push_back(h);
-            GemmDesc u{};
+            Gemm64Desc u{};
             u.M = b.nr; u.N = J.n; u.K = b.nr;                   // Y2 = T Y
-            u.A = J.Tb; u.lda = kBt;
-            u.B = J.Yb; u.ldb = J.ldw;
-            u.C = J.Y2b; u.ldc = J.ldw;
+            u.A = J.Tb; u.ta = DT_F64; u.lda = kBt;
+            u.B = J.Yb; u.tb = DT_F64; u.ldb = J.ldw;
+            u.C = J.Y2b; u.tc = DT_F64; u.ldc = J.ldw;
             g2.push_back(u);
-            GemmDesc v{};
+            Gemm64Desc v{};
             v.M = m; v.N = J.n; v.K = b.nr;                      // X -= V Y2
-            v.A = V; v.lda = J.ldw;
-            v.B = J.Y2b; v.ldb = J.ldw;
-            v.C = X; v.ldc = J.ldw;
+            v.A = V; v.ta = DT_F32; v.lda = J.ldw;
+            v.B = J.Y2b; v.tb = DT_F64; v.ldb = J.ldw;
+            v.C = X; v.tc = DT_F64; v.ldc = J.ldw;
             v.epi = EPI_SUB;
             g3.push_back(v);
         }
-        RET_OK(gemm_grouped(g1.data(), (int)g1.size(), 0.f, s));
+        RET_OK(gemm64_grouped(g1.data(), (int)g1.size(), s));
         bt_larft<<<ns, kBt, kLarftSmem, s>>>(djobs, dbt + boff);
         KFAC_LAUNCHED();
-        RET_OK(gemm_grouped(g2.data(), (int)g2.size(), 0.f, s));
-        RET_OK(gemm_grouped(g3.data(), (int)g3.size(), 0.f, s));
+        RET_OK(gemm64_grouped(g2.data(), (int)g2.size(), s));
+        RET_OK(gemm64_grouped(g3.data(), (int)g3.size(), s));
         boff += ns;
     }
-    trd_output<<<dim3(cdiv(max_n, 128), max_n, count), 128, 0, s>>>(djobs, ping);
+    trd_output<<<dim3(std::min(1024, cdiv((long long)max_n * max_n, 256)), count), 256, 0, s>>>(djobs);
     KFAC_LAUNCHED();
     if (mode == TRD_DEBUG_STEDC)
         KFAC_CUDA_TRY(cudaMemcpyAsync(dbg_d, P.jobs[0].D, sizeof(double) * P.jobs[0].n, cudaMemcpyDeviceToDevice, s));

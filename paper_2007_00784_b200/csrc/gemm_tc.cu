@@ -154,10 +154,6 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
         : "memory");
 }
 
-// Round an fp32 value to the nearest TF32 (10-bit mantissa), ties away from zero; exact in fp32.
-__device__ __forceinline__ float tf32_rn(float x) {
-    return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
-}
 
 // ------------------------------------------------------- shared pieces --
 struct Smem {
@@ -215,7 +211,16 @@ __device__ __forceinline__ void teardown(uint32_t tmem, int warp) {
     }
 }
 
-// hi = rn_tf32(x) in place, lo = rn_tf32(x - hi): 3xTF32 operands, both exact TF32 values.
+// Round an fp32 value to the nearest TF32 (10-bit mantissa), ties away from zero; exact in fp32.
+__device__ __forceinline__ float tf32_rn(float x) {
+    return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+}
+
+// hi = rn_tf32(x) in place, lo = rn_tf32(x - hi): 3xTF32 operands, both exact TF32 values, so the
+// dropped terms (lo*lo and the rounding of lo) are < 2^-22 relative per product.  (Feeding the raw
+// tile as hi and writing only lo = x - trunc(x) would save the in-place write, but the hardware
+// truncation makes |lo| up to 2^-10|x| and the product error 4x larger -- too much for the
+// 1/damping amplification on rank-deficient layers.)
 __device__ __forceinline__ void split_region(uint8_t *raw, uint8_t *lo_base, int n_f4, int t) {
     float4 *hi = reinterpret_cast<float4 *>(raw);
     float4 *lo = reinterpret_cast<float4 *>(lo_base);
@@ -422,12 +427,12 @@ __device__ __forceinline__ void syrk_issue(const FactorJob &J, const Smem &S, in
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
         const int k = t / 32 + 4 * j;
-        const long long r = r0 + k;
+        const int r = (int)(r0 + k);
         const bool rv = r < r_end;
         int img = 0, oh = 0, ow = 0;
         if (J.is_a && rv) {
-            img = (int)(r / hw);
-            const int p = (int)(r - (long long)img * hw);
+            img = r / hw;
+            const int p = r - img * hw;
             oh = p / J.w_out;
             ow = p - oh * J.w_out;
         }
@@ -445,7 +450,7 @@ __device__ __forceinline__ void syrk_issue(const FactorJob &J, const Smem &S, in
             uint32_t bytes = 0;
             if (rv && c.kind == 0) {
                 if (!J.is_a) {
-                    src = J.src + r * J.c_in + c.off;
+                    src = J.src + (long long)r * J.c_in + c.off;
                     bytes = 16;
                 } else {
                     // c.off already holds (kh * w_in + kw) * c_in + channel (receptive-field offset)
@@ -490,6 +495,13 @@ __global__ void __launch_bounds__(NT, 1) syrk_tc_kernel(const __grid_constant__ 
             cp_async_arrive(S.raw_full + 8 * p);
         }
         for (int kb = 0; kb < nk; ++kb) {
+            // split k-block kb first (overlaps the MMA of kb-1), then refill the stage that
+            // MMA kb-1 releases with k-block kb + kRaw - 1
+            const int s = kb % kRaw, l = kb % kLo;
+            mbar_wait(S.raw_full + 8 * s, (kb / kRaw) & 1);
+            if (kb >= kLo) mbar_wait(S.lo_empty + 8 * l, ((kb / kLo) - 1) & 1);
+            split_region(S.raw(s), S.lo(l), n_f4, t);
+            mbar_arrive(S.ready + 8 * s);
             const int nxt = kb + kRaw - 1;
             if (nxt < nk) {
                 const int s2 = nxt % kRaw;
@@ -497,11 +509,6 @@ __global__ void __launch_bounds__(NT, 1) syrk_tc_kernel(const __grid_constant__ 
                 syrk_issue(J, S, s2, r_begin + (long long)nxt * BK, r_end, ci, cc, t, diag);
                 cp_async_arrive(S.raw_full + 8 * s2);
             }
-            const int s = kb % kRaw, l = kb % kLo;
-            mbar_wait(S.raw_full + 8 * s, (kb / kRaw) & 1);
-            if (kb >= kLo) mbar_wait(S.lo_empty + 8 * l, ((kb / kLo) - 1) & 1);
-            split_region(S.raw(s), S.lo(l), n_f4, t);
-            mbar_arrive(S.ready + 8 * s);
         }
     } else if (warp < W_TMA) {
         const int wq = warp - W_DRAIN0;

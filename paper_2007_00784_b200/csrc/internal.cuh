@@ -52,6 +52,24 @@ bool gemm_tc_supported(const GemmDesc &d);
 // Dispatch each descriptor to the tensor-core or SIMT engine.
 kfac_status_t gemm_grouped(const GemmDesc *descs, int count, float damping, cudaStream_t s);
 
+// fp64-accumulating SIMT grouped GEMM (eigensolver internals, gemm_f64.cu):
+// C (dtype tc) = op(A) op(B)  or  C -= op(A) op(B)  (epi EPI_SUB), operands fp32 or fp64.
+enum DType : int { DT_F32 = 0, DT_F64 = 1 };
+struct Gemm64Desc {
+    const void *A;
+    const void *B;
+    void *C;
+    const int *dyn;          // optional device {N_eff, K_eff}
+    int ta, tb, tc;          // DType of A, B, C
+    int M, N, K;
+    int lda, ldb, ldc;
+    int trans_a, trans_b, epi;
+    int lower;               // skip 128x128 tiles strictly above the diagonal
+    int tile_begin;          // filled by the launcher
+};
+constexpr int kGemm64MaxDescs = 256;
+kfac_status_t gemm64_grouped(const Gemm64Desc *descs, int count, cudaStream_t s);
+
 // ------------------------------------------------------------ factor SYRK --
 // One Kronecker factor of one layer: F_batch = X^T X / n over the n rows of X, where X is
 // [im2col(act) | 1] (A factor, Eq. 5) or the output gradients (G factor).  The upper 128x128

@@ -33,6 +33,9 @@ def lib():
     L.kfac_debug_tridiag.restype = C.c_int
     L.kfac_debug_stedc.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
     L.kfac_debug_stedc.restype = C.c_int
+    L.kfac_debug_gemm64.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_int,
+                                    C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p]
+    L.kfac_debug_gemm64.restype = C.c_int
     return _lib
 
 
@@ -64,6 +67,36 @@ def test_gemm_sub_epilogue(lib, engine, M, N, K):
     ref = C0.astype(np.float32).astype(np.float64) - A.astype(np.float32).astype(np.float64) @ B.astype(np.float32).astype(np.float64)
     got = c[:, :N].double().cpu().numpy()
     assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < 2e-6
+
+
+@pytest.mark.parametrize("dts", [(0, 0, 0), (0, 1, 1), (1, 1, 1), (1, 0, 0)])
+@pytest.mark.parametrize("ta,tb", [(0, 0), (1, 0), (0, 1), (1, 1)])
+@pytest.mark.parametrize("epi", [0, 3])
+def test_gemm64(lib, dts, ta, tb, epi):
+    """fp64-accumulating SIMT GEMM of the eigensolver: fp64 products of the (fp32 or fp64)
+    operands, one rounding to the output type -> relF <= 1e-14 (fp64 out) / 2^-24 (fp32 out)."""
+    M, N, K = 150, 131, 77
+    rng = np.random.default_rng(ta * 2 + tb + 10 * epi)
+    dt = lambda c: torch.float64 if c else torch.float32
+    A = rng.standard_normal((K, M) if ta else (M, K))
+    B = rng.standard_normal((N, K) if tb else (K, N))
+    C0 = rng.standard_normal((M, N))
+    a = torch.from_numpy(A).to(dt(dts[0])).cuda()
+    b = torch.from_numpy(B).to(dt(dts[1])).cuda()
+    c = torch.from_numpy(C0).to(dt(dts[2])).cuda()
+    st = lib.lib.kfac_debug_gemm64(a.data_ptr(), dts[0], a.stride(0), ta, b.data_ptr(), dts[1], b.stride(0), tb,
+                                   c.data_ptr(), dts[2], c.stride(0), M, N, K, epi, None)
+    assert st == 0
+    torch.cuda.synchronize()
+    opA = a.double().cpu().numpy()
+    opB = b.double().cpu().numpy()
+    opA = opA.T if ta else opA
+    opB = opB.T if tb else opB
+    c0 = torch.from_numpy(C0).to(dt(dts[2])).double().numpy()
+    ref = c0 - opA @ opB if epi == 3 else opA @ opB
+    got = c.double().cpu().numpy()
+    tol = 1e-14 if dts[2] == 1 else 1.2e-7
+    assert np.linalg.norm(got - ref) / np.linalg.norm(ref) <= tol
 
 
 def _wishart(rng, n, rows, bias=True):
@@ -167,3 +200,25 @@ def test_compute_eigen_tridiag(lib, n, rows):
     assert np.abs(Qn.T @ Qn - np.eye(n)).max() <= 2e-5
     rec = (Qn * vn) @ Qn.T
     assert np.linalg.norm(rec - F64) / np.linalg.norm(F64) <= 1e-5
+
+
+def test_compute_eigen_tridiag_batched(lib):
+    """Several factors with different D&C depths and panel counts in one call (per-factor
+    ping-pong parity of the merge levels, CTA groups of the reduction, blocks of the
+    back-transformation)."""
+    dims = [33, 64, 65, 300, 1100, 97]
+    rng = np.random.default_rng(11)
+    Fs = [_wishart(rng, n, max(8, n // 3)).astype(np.float32) for n in dims]
+    fd = [_dev(F) for F in Fs]
+    Q = [torch.zeros_like(f) for f in fd]
+    v = [torch.zeros(n, device="cuda") for n in dims]
+    info = torch.full((len(dims),), -7, dtype=torch.int32, device="cuda")
+    lib.kfac_compute_eigen(fd, Q, v, info=info, flags=4)
+    torch.cuda.synchronize()
+    assert (info.cpu().numpy() == 0).all()
+    for n, F, q, w in zip(dims, Fs, Q, v):
+        Qn = q[:, :n].double().cpu().numpy()
+        wn = w.double().cpu().numpy()
+        F64 = F.astype(np.float64)
+        assert np.abs(Qn.T @ Qn - np.eye(n)).max() <= 2e-5, n
+        assert np.linalg.norm((Qn * wn) @ Qn.T - F64) / np.linalg.norm(F64) <= 1e-5, n
