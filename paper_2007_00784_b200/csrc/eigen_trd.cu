@@ -47,7 +47,10 @@ constexpr int kTrdWarps = kTrdThreads / 32;
 constexpr int kPart = 2 * kNb + 2;      // per-CTA partials: V^T v, W^T v, ||x||^2, w^T v
 constexpr int kMaxGroupCtas = 512;
 constexpr int kLeaf = 32;               // D&C leaf size
-constexpr int kBt = 128;                // reflectors per back-transformation block
+constexpr int kSymvR = 64;              // symv tile rows (lower triangle only)
+constexpr int kSymvC = 128;             // symv tile columns (one float4 per lane)
+constexpr int kBt = 512;                // reflectors per back-transformation block
+constexpr int kTs = 128;                // dlarft sub-block (T built recursively from 128-blocks)
 constexpr double kEps = 1.1102230246251565e-16;   // 2^-53, LAPACK dlamch('E')
 
 // ----------------------------------------------------------------- job --
@@ -63,6 +66,7 @@ struct TrdJob {
     double *Sb;        // n x ldw D&C secular eigenvectors S
     double *Yb, *Y2b;  // kBt x ldw back-transformation scratch
     double *Gb, *Tb;   // kBt x kBt Gram matrix V^T V and WY factor T
+    double *Wt;        // kBt x kBt scratch for the recursive T
     double *d, *e, *tau;       // tridiagonal T and reflector scalars
     double *x, *y;             // corrected column / mat-vec result (sytrd)
     double *D;                 // current eigenvalues of the D&C subproblems
@@ -74,6 +78,9 @@ struct TrdJob {
     int *mstate;               // per merge: {k, nrot, k, k} (k twice: GEMM dynamic N, K)
     double *mscal;             // per merge: {rho2, tol}
     double *part;              // kMaxGroupCtas x kPart
+    double *DP;                // symv direct partials  [n][ldp]  (row, 128-column chunk)
+    double *TP;                // symv transposed partials [n/64][ldw] (64-row block, column)
+    int ldp;
     unsigned *bar;
     int n, ldF, ldQ, ldw;
     int levels;                // D&C merge levels (n <= kLeaf -> 0)
@@ -111,6 +118,17 @@ __device__ __forceinline__ double block_sum(double v, double *sh) {
     __syncthreads();
     double s = 0.0;
     for (int i = 0; i < (int)(blockDim.x / 32); ++i) s += sh[i];
+    return s;
+}
+
+// Fixed-order sum over the group's CTAs of one partial column, by one warp (lane-strided partial
+// sums, then a butterfly): independent loads instead of a chain of nc dependent L2 round trips.
+__device__ __forceinline__ double warp_part_sum(const double *part, int col, int nc, int lane) {
+    double s = 0.0;
+#pragma unroll 4
+    for (int q = lane; q < nc; q += 32) s += ldcg(part + (size_t)q * kPart + col);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     return s;
 }
 
@@ -191,23 +209,27 @@ __global__ void __launch_bounds__(kTrdThreads, 1) trd_panel(const __grid_constan
         int lo, hi;
         part_range(k, n, c, nc, lo, hi);
         double s2 = 0.0;
-        for (int r = lo + t; r < hi; r += kTrdThreads) {
-            double cv = A[(size_t)k * ldw + r];
-            const float *vr = VW + (size_t)r * 64;
-            for (int q = 0; q < i; ++q)
-                cv -= (double)ldcg(vr + q) * rowW[q] + (double)ldcg(vr + kNb + q) * rowV[q];
-            if (r == k) J.d[k] = cv;
-            else __stcg(J.x + r, cv);
-            if (r >= k + 2) s2 += cv * cv;
+        for (int r = lo + warp; r < hi; r += kTrdWarps) {       // one warp per row, lane q = panel column
+            double corr = 0.0;
+            if (lane < i)
+                corr = (double)ldcg(VW + (size_t)r * 64 + lane) * rowW[lane] +
+                       (double)ldcg(VW + (size_t)r * 64 + kNb + lane) * rowV[lane];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) corr += __shfl_xor_sync(0xffffffffu, corr, o);
+            if (lane == 0) {
+                const double cv = (double)A[(size_t)r * ldw + k] - corr;   // column k (lower triangle kept)
+                if (r == k) J.d[k] = cv;
+                else __stcg(J.x + r, cv);
+                if (r >= k + 2) s2 += cv * cv;
+            }
         }
         s2 = block_sum(s2, sh);
         if (t == 0) __stcg(part + (size_t)c * kPart + 2 * kNb, s2);
         group_barrier(J.bar, target, nc);
         if (k == n - 1) break;
         // ---------------- phase B (rows [k+1, n)) ----------------
-        if (t == 0) {
-            double nrm2 = 0.0;
-            for (int q = 0; q < nc; ++q) nrm2 += ldcg(part + (size_t)q * kPart + 2 * kNb);
+        if (warp == 0) {
+            const double nrm2 = warp_part_sum(part, 2 * kNb, nc, lane);
             const double alpha = ldcg(J.x + k + 1);
             double tau = 0.0, beta = alpha, scale = 0.0;
             if (nrm2 > 0.0) {
@@ -215,18 +237,21 @@ __global__ void __launch_bounds__(kTrdThreads, 1) trd_panel(const __grid_constan
                 tau = (beta - alpha) / beta;
                 scale = 1.0 / (alpha - beta);
             }
-            scal[0] = tau;
-            scal[1] = scale;
-            if (c == 0) {
-                J.e[k] = beta;
-                J.tau[k] = tau;
+            if (lane == 0) {
+                scal[0] = tau;
+                scal[1] = scale;
+                if (c == 0) {
+                    J.e[k] = beta;
+                    J.tau[k] = tau;
+                }
             }
         }
         __syncthreads();
         const double tau = scal[0], scale = scal[1];
         const int c0 = (k + 1) & ~3;
-        const int nv4 = (n - c0 + 3) >> 2;           // float4 count from c0
-        for (int j = t; j < nv4 * 4; j += kTrdThreads) {
+        const int nvp = (n - c0 + kSymvC - 1) / kSymvC * kSymvC;   // v padded to whole column chunks
+#pragma unroll 4
+        for (int j = t; j < nvp; j += kTrdThreads) {
             const int col = c0 + j;
             float v = 0.f;
             if (col == k + 1) v = 1.f;
@@ -241,53 +266,79 @@ __global__ void __launch_bounds__(kTrdThreads, 1) trd_panel(const __grid_constan
             VW[(size_t)r * 64 + i] = v;
             WV[(size_t)r * 64 + kNb + i] = v;
         }
-        // symmetric mat-vec (one warp per pair of rows, 8 float4 loads in flight per lane) + panel
-        // dot partials (lane q -> panel column q)
+        // panel dot partials over the owned rows (lane q -> panel column q)
         double pa = 0.0, pb = 0.0;
-        const float4 *v4 = reinterpret_cast<const float4 *>(vsm);
-        for (int r = lo + 2 * warp; r < hi; r += 2 * kTrdWarps) {
-            const bool two = r + 1 < hi;
-            const float4 *a0 = reinterpret_cast<const float4 *>(A + (size_t)r * ldw + c0);
-            const float4 *a1 = two ? a0 + ldw / 4 : a0;
-            double s0 = 0.0, s1 = 0.0;
-            int q = lane;
-            for (; q + 96 < nv4; q += 128) {
-                float4 x[4], z[4];
+        if (lane < i)
+            for (int r = lo + warp; r < hi; r += kTrdWarps) {
+                const double vr = vsm[r - c0];
+                pa += (double)ldcg(VW + (size_t)r * 64 + lane) * vr;
+                pb += (double)ldcg(VW + (size_t)r * 64 + kNb + lane) * vr;
+            }
+        // symmetric mat-vec over the lower triangle of A_p[k+1:n, k+1:n] in 64 x 128 tiles (one warp
+        // per tile, every tile of the group's factor spread over its warps): each tile adds its
+        // row sums to DP[row][chunk] and its column sums (the mirrored upper triangle) to
+        // TP[block][column]; phase C sums both in a fixed order, so every element is read once.
+        {
+            const int r00 = k + 1, nrb = (n - r00 + kSymvR - 1) / kSymvR;
+            auto cnt = [&](int b) { return (min(n, r00 + kSymvR * (b + 1)) - 1 - c0) / kSymvC + 1; };
+            int total = 0;
+            for (int b = 0; b < nrb; ++b) total += cnt(b);
+            const int W = nc * kTrdWarps;
+            int b = 0, base = 0;
+            const float4 *v4 = reinterpret_cast<const float4 *>(vsm);
+            for (int it = c * kTrdWarps + warp; it < total; it += W) {
+                while (it >= base + cnt(b)) { base += cnt(b); ++b; }
+                const int j = it - base;
+                const int r0 = r00 + kSymvR * b, r1 = min(n, r0 + kSymvR);
+                const int cc = c0 + kSymvC * j + 4 * lane;
+                const float4 v = v4[(cc - c0) >> 2];
+                double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
+                for (int r = r0; r < r1; r += 8) {
+                    // 8 rows: 8 float4 loads in flight per lane, then a butterfly reduce-scatter of
+                    // the 8 row partials (9 shuffles instead of 40)
+                    float4 a[8];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    x[u] = __ldg(a0 + q + 32 * u);
-                    z[u] = __ldg(a1 + q + 32 * u);
-                }
+                    for (int u = 0; u < 8; ++u) {
+                        const int rr = r + u;
+                        a[u] = (rr < r1 && cc <= rr) ? __ldg(reinterpret_cast<const float4 *>(A + (size_t)rr * ldw + cc))
+                                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+                    }
+                    double p[8];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const float4 v = v4[q + 32 * u];
-                    s0 += (double)x[u].x * v.x + (double)x[u].y * v.y + (double)x[u].z * v.z + (double)x[u].w * v.w;
-                    s1 += (double)z[u].x * v.x + (double)z[u].y * v.y + (double)z[u].z * v.z + (double)z[u].w * v.w;
-                }
-            }
-            for (; q < nv4; q += 32) {
-                const float4 x = __ldg(a0 + q), z = __ldg(a1 + q), v = v4[q];
-                s0 += (double)x.x * v.x + (double)x.y * v.y + (double)x.z * v.z + (double)x.w * v.w;
-                s1 += (double)z.x * v.x + (double)z.y * v.y + (double)z.z * v.z + (double)z.w * v.w;
-            }
+                    for (int u = 0; u < 8; ++u) {
+                        const int rr = r + u;
+                        const double ax = cc <= rr ? a[u].x : 0.0, ay = cc + 1 <= rr ? a[u].y : 0.0;
+                        const double az = cc + 2 <= rr ? a[u].z : 0.0, aw = cc + 3 <= rr ? a[u].w : 0.0;
+                        p[u] = ax * v.x + ay * v.y + az * v.z + aw * v.w;
+                        const double vr = rr < r1 ? (double)vsm[rr - c0] : 0.0;
+                        t0 += (cc < rr ? ax : 0.0) * vr;
+                        t1 += (cc + 1 < rr ? ay : 0.0) * vr;
+                        t2 += (cc + 2 < rr ? az : 0.0) * vr;
+                        t3 += (cc + 3 < rr ? aw : 0.0) * vr;
+                    }
+                    const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4;
+                    double q4[4], q2[2];
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                s0 += __shfl_xor_sync(0xffffffffu, s0, o);
-                s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-            }
-            if (lane == 0) {
-                __stcg(J.y + r, s0);
-                if (two) __stcg(J.y + r + 1, s1);
-            }
-            if (lane < i) {
-                const double v0 = vsm[r - c0];
-                pa += (double)ldcg(VW + (size_t)r * 64 + lane) * v0;
-                pb += (double)ldcg(VW + (size_t)r * 64 + kNb + lane) * v0;
-                if (two) {
-                    const double v1 = vsm[r + 1 - c0];
-                    pa += (double)ldcg(VW + (size_t)(r + 1) * 64 + lane) * v1;
-                    pb += (double)ldcg(VW + (size_t)(r + 1) * 64 + kNb + lane) * v1;
+                    for (int u = 0; u < 4; ++u) {
+                        const double send = h16 ? p[u] : p[u + 4], keep = h16 ? p[u + 4] : p[u];
+                        q4[u] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+                    }
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        const double send = h8 ? q4[u] : q4[u + 2], keep = h8 ? q4[u + 2] : q4[u];
+                        q2[u] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+                    }
+                    double sd = (h4 ? q2[1] : q2[0]) + __shfl_xor_sync(0xffffffffu, h4 ? q2[0] : q2[1], 4);
+                    sd += __shfl_xor_sync(0xffffffffu, sd, 2);
+                    sd += __shfl_xor_sync(0xffffffffu, sd, 1);
+                    const int rr = r + (h16 ? 4 : 0) + (h8 ? 2 : 0) + (h4 ? 1 : 0);
+                    if ((lane & 3) == 0 && rr < r1) __stcg(J.DP + (size_t)rr * J.ldp + j, sd);
                 }
+                double *tp = J.TP + (size_t)b * ldw + cc;
+                if (cc < n) __stcg(tp, t0);
+                if (cc + 1 < n) __stcg(tp + 1, t1);
+                if (cc + 2 < n) __stcg(tp + 2, t2);
+                if (cc + 3 < n) __stcg(tp + 3, t3);
             }
         }
         red[warp][lane] = pa;
@@ -300,30 +351,39 @@ __global__ void __launch_bounds__(kTrdThreads, 1) trd_panel(const __grid_constan
         }
         group_barrier(J.bar, target, nc);
         // ---------------- phase C ----------------
-        if (t < 2 * kNb) {
-            double s = 0.0;
-            if ((t % kNb) < i)
-                for (int q = 0; q < nc; ++q) s += ldcg(part + (size_t)q * kPart + t);
-            ab[t] = s;
+        for (int col = warp; col < 2 * kNb; col += kTrdWarps) {
+            const double sum = (col % kNb) < i ? warp_part_sum(part, col, nc, lane) : 0.0;
+            if (lane == 0) ab[col] = sum;
         }
         __syncthreads();
         double wv = 0.0;
-        for (int r = lo + t; r < hi; r += kTrdThreads) {
-            double yr = ldcg(J.y + r);
-            const float *vr = VW + (size_t)r * 64;
-            for (int q = 0; q < i; ++q) yr -= (double)ldcg(vr + kNb + q) * ab[q] + (double)ldcg(vr + q) * ab[kNb + q];
-            const double w = tau * yr;
-            __stcg(J.y + r, w);
-            wv += w * (double)vsm[r - c0];
+        {
+            const int nrb = (n - (k + 1) + kSymvR - 1) / kSymvR;
+            for (int r = lo + warp; r < hi; r += kTrdWarps) {   // one warp per row
+                const int b = (r - (k + 1)) / kSymvR;
+                const int nj = (min(n, k + 1 + kSymvR * (b + 1)) - 1 - c0) / kSymvC + 1;
+                double yr = 0.0;
+                for (int jj = lane; jj < nj; jj += 32) yr += ldcg(J.DP + (size_t)r * J.ldp + jj);
+                for (int bb = b + lane; bb < nrb; bb += 32) yr += ldcg(J.TP + (size_t)bb * ldw + r);
+                if (lane < i)
+                    yr -= (double)ldcg(VW + (size_t)r * 64 + kNb + lane) * ab[lane] +
+                          (double)ldcg(VW + (size_t)r * 64 + lane) * ab[kNb + lane];
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) yr += __shfl_xor_sync(0xffffffffu, yr, o);
+                if (lane == 0) {
+                    const double w = tau * yr;
+                    __stcg(J.y + r, w);
+                    wv += w * (double)vsm[r - c0];
+                }
+            }
         }
         wv = block_sum(wv, sh);
         if (t == 0) __stcg(part + (size_t)c * kPart + 2 * kNb + 1, wv);
         group_barrier(J.bar, target, nc);
         // ---------------- phase D ----------------
-        if (t == 0) {
-            double s = 0.0;
-            for (int q = 0; q < nc; ++q) s += ldcg(part + (size_t)q * kPart + 2 * kNb + 1);
-            scal[2] = -0.5 * tau * s;
+        if (warp == 0) {
+            const double sum = warp_part_sum(part, 2 * kNb + 1, nc, lane);
+            if (lane == 0) scal[2] = -0.5 * tau * sum;
         }
         __syncthreads();
         const double alpha2 = scal[2];
@@ -805,35 +865,41 @@ __global__ void dc_assemble(const TrdJob *jobs, const MergeDesc *merges, int pin
 }
 
 // ------------------------------------------------- back-transformation --
-// T (upper triangular, kBt x kBt) of H_b0 ... H_{b0+nr-1} = I - V T V^T from G = V^T V
-// (LAPACK dlarft, forward / columnwise): T_jj = tau_j, T[0:j, j] = -tau_j T[0:j, 0:j] G[0:j, j].
+// T (upper triangular) of H_b0 ... H_{b0+nr-1} = I - V T V^T from G = V^T V (LAPACK dlarft,
+// forward / columnwise): T_jj = tau_j, T[0:j, j] = -tau_j T[0:j, 0:j] G[0:j, j].  This kernel builds
+// one 128x128 diagonal block per CTA (blockIdx.x = 4 step-entry + sub-block) and zeroes the rest of
+// its block row; the off-diagonal blocks follow from T12 = -T1 (V1^T V2) T2 (two GEMMs per level).
 struct BtStep {
     int job, b0, nr;
 };
-constexpr size_t kLarftSmem = sizeof(double) * (kBt * (kBt + 1) + kBt);
+constexpr size_t kLarftSmem = sizeof(double) * (kTs * (kTs + 1) + kTs);
 __global__ void bt_larft(const TrdJob *jobs, const BtStep *steps) {
     extern __shared__ double bt_smem[];
-    double (*T)[kBt + 1] = reinterpret_cast<double (*)[kBt + 1]>(bt_smem);
-    double *gcol = bt_smem + kBt * (kBt + 1);
-    const BtStep S = steps[blockIdx.x];
+    double (*T)[kTs + 1] = reinterpret_cast<double (*)[kTs + 1]>(bt_smem);
+    double *gcol = bt_smem + kTs * (kTs + 1);
+    const BtStep S = steps[blockIdx.x / (kBt / kTs)];
+    const int sb = blockIdx.x % (kBt / kTs);
     const TrdJob &J = jobs[S.job];
-    const int nr = S.nr, t = threadIdx.x;
+    const int o = sb * kTs, nr = min(kTs, S.nr - o), t = threadIdx.x;
+    if (nr <= 0) return;
     for (int j = 0; j < nr; ++j) {
-        const double tj = J.tau[S.b0 + j];
-        if (t < j) gcol[t] = J.Gb[t * kBt + j];
+        const double tj = J.tau[S.b0 + o + j];
+        if (t < j) gcol[t] = J.Gb[(size_t)(o + t) * kBt + o + j];
         __syncthreads();
-        double s = 0.0;
+        double acc = 0.0;
         if (t < j)
-            for (int l = t; l < j; ++l) s += T[t][l] * gcol[l];
+            for (int l = t; l < j; ++l) acc += T[t][l] * gcol[l];
         __syncthreads();
-        if (t < j) T[t][j] = -tj * s;
+        if (t < j) T[t][j] = -tj * acc;
         if (t == j) T[j][j] = tj;
-        if (t > j && t < kBt) T[t][j] = 0.0;
+        if (t > j && t < kTs) T[t][j] = 0.0;
         __syncthreads();
     }
-    for (int idx = t; idx < kBt * kBt; idx += blockDim.x) {
+    for (int idx = t; idx < kTs * kBt; idx += blockDim.x) {
         const int r = idx / kBt, c = idx % kBt;
-        J.Tb[idx] = (r < nr && c < nr) ? T[r][c] : 0.0;
+        double v = 0.0;
+        if (r < nr && c >= o && c < o + nr) v = T[r][c - o];
+        J.Tb[(size_t)(o + r) * kBt + c] = v;
     }
 }
 
@@ -931,6 +997,7 @@ Plan plan(const int32_t *dims, int count) {
         TAKE(Y2b, double, (size_t)kBt * ldw);
         TAKE(Gb, double, kBt * kBt);
         TAKE(Tb, double, kBt * kBt);
+        TAKE(Wt, double, kBt * kBt);
         TAKE(d, double, n);
         TAKE(e, double, n);
         TAKE(tau, double, n);
@@ -953,6 +1020,9 @@ Plan plan(const int32_t *dims, int count) {
         TAKE(mstate, int, 4 * (size_t)n);
         TAKE(mscal, double, 2 * (size_t)n);
         TAKE(part, double, (size_t)kMaxGroupCtas * kPart);
+        J.ldp = cdiv(n + 3, kSymvC) + 1;
+        TAKE(DP, double, (size_t)n * J.ldp);
+        TAKE(TP, double, (size_t)cdiv(n, kSymvR) * ldw);
         TAKE(bar, unsigned, 64);
 #undef TAKE
         // leaves and merges
@@ -1053,6 +1123,7 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
         J.rorg = rebase(J.rorg, base); J.rot_p = rebase(J.rot_p, base); J.rot_j = rebase(J.rot_j, base);
         J.srcpos = rebase(J.srcpos, base); J.mstate = rebase(J.mstate, base); J.mscal = rebase(J.mscal, base);
         J.part = rebase(J.part, base); J.bar = rebase(J.bar, base);
+        J.DP = rebase(J.DP, base); J.TP = rebase(J.TP, base); J.Wt = rebase(J.Wt, base);
         max_n = std::max(max_n, J.n);
     }
     TrdJob *djobs = reinterpret_cast<TrdJob *>(base + P.table_off);
@@ -1084,7 +1155,7 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
         KFAC_CUDA_TRY(cudaFuncSetAttribute(bt_larft, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLarftSmem));
         attr = true;
     }
-    const size_t smem = (size_t)(round_up(max_n, 4) + 8) * sizeof(float);
+    const size_t smem = (size_t)(round_up(max_n, kSymvC) + kSymvC + 8) * sizeof(float);
     const int cap = panel_capacity(smem);
     static PanelLaunch PL;
     // Staggered schedule: factor j (P_j panels) starts at launch P_max - P_j, so all factors finish
@@ -1147,6 +1218,7 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
             g.B = J.WV + (size_t)q0 * 64; g.tb = DT_F32; g.ldb = 64; g.trans_b = 1;
             g.C = J.A + (size_t)q0 * J.ldw + q0; g.tc = DT_F32; g.ldc = J.ldw;
             g.epi = EPI_SUB;
+            g.lower = 1;                             // the reduction reads only the lower triangle
             gd.push_back(g);
         }
         if (!gd.empty()) RET_OK(gemm64_grouped(gd.data(), (int)gd.size(), s));
@@ -1250,8 +1322,36 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
             g3.push_back(v);
         }
         RET_OK(gemm64_grouped(g1.data(), (int)g1.size(), s));
-        bt_larft<<<ns, kBt, kLarftSmem, s>>>(djobs, dbt + boff);
+        bt_larft<<<ns * (kBt / kTs), kTs, kLarftSmem, s>>>(djobs, dbt + boff);
         KFAC_LAUNCHED();
+        // recursive off-diagonal blocks of T: level 1 pairs of 128-blocks, level 2 pair of 256-blocks
+        for (int lvl = 1; lvl <= 2; ++lvl) {
+            const int h = kTs << (lvl - 1);              // size of the halves being joined
+            std::vector<Gemm64Desc> ga, gb;
+            for (auto &b : stp) {
+                const TrdJob &J = P.jobs[b.job];
+                for (int o = 0; o + h < b.nr; o += 2 * h) {
+                    const int n1 = h, n2 = std::min(h, b.nr - o - h);
+                    Gemm64Desc x{};                      // Wt = T1 G12
+                    x.M = n1; x.N = n2; x.K = n1;
+                    x.A = J.Tb + (size_t)o * kBt + o; x.ta = DT_F64; x.lda = kBt;
+                    x.B = J.Gb + (size_t)o * kBt + o + h; x.tb = DT_F64; x.ldb = kBt;
+                    x.C = J.Wt + (size_t)o * kBt; x.tc = DT_F64; x.ldc = kBt;
+                    ga.push_back(x);
+                    Gemm64Desc y{};                      // T12 = 0 - Wt T2
+                    y.M = n1; y.N = n2; y.K = n2;
+                    y.A = J.Wt + (size_t)o * kBt; y.ta = DT_F64; y.lda = kBt;
+                    y.B = J.Tb + (size_t)(o + h) * kBt + o + h; y.tb = DT_F64; y.ldb = kBt;
+                    y.C = J.Tb + (size_t)o * kBt + o + h; y.tc = DT_F64; y.ldc = kBt;
+                    y.epi = EPI_SUB;
+                    gb.push_back(y);
+                }
+            }
+            if (!ga.empty()) {
+                RET_OK(gemm64_grouped(ga.data(), (int)ga.size(), s));
+                RET_OK(gemm64_grouped(gb.data(), (int)gb.size(), s));
+            }
+        }
         RET_OK(gemm64_grouped(g2.data(), (int)g2.size(), s));
         RET_OK(gemm64_grouped(g3.data(), (int)g3.size(), s));
         boff += ns;

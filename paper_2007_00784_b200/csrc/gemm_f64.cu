@@ -37,8 +37,8 @@ __device__ __forceinline__ double ld_any(const void *p, size_t i, int dt) {
 }
 
 __global__ void __launch_bounds__(NT, 1) gemm64_kernel(const __grid_constant__ Batch64 batch) {
-    __shared__ double As[2][BK][BM + 2];
-    __shared__ double Bs[2][BK][BN + 2];
+    __shared__ __align__(16) double As[2][BK][BM + 2];
+    __shared__ __align__(16) double Bs[2][BK][BN + 2];
     const int tile = blockIdx.x;
     const Gemm64Desc &d = batch.d[find_desc(batch, tile)];
     const int local = tile - d.tile_begin;
@@ -88,6 +88,8 @@ __global__ void __launch_bounds__(NT, 1) gemm64_kernel(const __grid_constant__ B
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
 
+    // thread (ty, tx) owns rows 2 ty + {0,1} + 32 i and columns 2 tx + {0,1} + 32 j (i, j < 4): the
+    // 16-byte shared loads of a quarter-warp then cover 128 contiguous bytes (no bank conflicts)
     const int ty = t / 16, tx = t % 16;
     const int nk = (Ke + BK - 1) / BK;
     if (nk > 0) {
@@ -103,10 +105,10 @@ __global__ void __launch_bounds__(NT, 1) gemm64_kernel(const __grid_constant__ B
             double a[8], b[8];
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-                a[i] = As[buf][k][ty * 4 + i];
-                a[4 + i] = As[buf][k][64 + ty * 4 + i];
-                b[i] = Bs[buf][k][tx * 4 + i];
-                b[4 + i] = Bs[buf][k][64 + tx * 4 + i];
+                const double2 av = *reinterpret_cast<const double2 *>(&As[buf][k][2 * ty + 32 * i]);
+                const double2 bv = *reinterpret_cast<const double2 *>(&Bs[buf][k][2 * tx + 32 * i]);
+                a[2 * i] = av.x; a[2 * i + 1] = av.y;
+                b[2 * i] = bv.x; b[2 * i + 1] = bv.y;
             }
 #pragma unroll
             for (int i = 0; i < 8; ++i)
@@ -121,11 +123,11 @@ __global__ void __launch_bounds__(NT, 1) gemm64_kernel(const __grid_constant__ B
 
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-        const int m = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
+        const int m = m0 + 2 * ty + (i & 1) + 32 * (i >> 1);
         if (m >= Me) continue;
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-            const int n = n0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + (j - 4));
+            const int n = n0 + 2 * tx + (j & 1) + 32 * (j >> 1);
             if (n >= Ne) continue;
             const size_t o = (size_t)m * d.ldc + n;
             if (d.tc == DT_F64) {
