@@ -57,7 +57,37 @@ __global__ void __launch_bounds__(NT, 1) gemm64_kernel(const __grid_constant__ B
     else           { b_r = t / 32; b_c = (t % 32) * 4; }    // B[k][n..n+4)
 
     double ra[4], rb[4];
+    // Each thread's 4 elements of an operand are contiguous in memory (k for a K-major operand,
+    // m/n otherwise): one 16-byte (fp32) or two 16-byte (fp64) loads when the run is in bounds
+    // and aligned, element loads at the edges.
+    const bool a_vec = ((d.lda & 3) == 0) && ((reinterpret_cast<uintptr_t>(d.A) & 15) == 0);
+    const bool b_vec = ((d.ldb & 3) == 0) && ((reinterpret_cast<uintptr_t>(d.B) & 15) == 0);
+    auto load4 = [&](const void *p, size_t i0, int dt, double (&r)[4]) {
+        if (dt == DT_F64) {
+            const double2 x = __ldg(reinterpret_cast<const double2 *>(static_cast<const double *>(p) + i0));
+            const double2 y = __ldg(reinterpret_cast<const double2 *>(static_cast<const double *>(p) + i0 + 2));
+            r[0] = x.x; r[1] = x.y; r[2] = y.x; r[3] = y.y;
+        } else {
+            const float4 x = __ldg(reinterpret_cast<const float4 *>(static_cast<const float *>(p) + i0));
+            r[0] = x.x; r[1] = x.y; r[2] = x.z; r[3] = x.w;
+        }
+    };
     auto load = [&](int k0) {
+        {
+            int m, k;
+            if (d.trans_a) { k = k0 + a_r; m = m0 + a_c; }
+            else           { m = m0 + a_r; k = k0 + a_c; }
+            const bool full = d.trans_a ? (k < Ke && m + 3 < Me) : (m < Me && k + 3 < Ke);
+            const bool fast_a = a_vec && full;
+            const bool fast_b = b_vec && (d.trans_b ? (n0 + b_r < Ne && k0 + b_c + 3 < Ke)
+                                                    : (k0 + b_r < Ke && n0 + b_c + 3 < Ne));
+            if (fast_a && fast_b) {
+                load4(d.A, d.trans_a ? (size_t)k * d.lda + m : (size_t)m * d.lda + k, d.ta, ra);
+                load4(d.B, d.trans_b ? (size_t)(n0 + b_r) * d.ldb + k0 + b_c : (size_t)(k0 + b_r) * d.ldb + n0 + b_c,
+                      d.tb, rb);
+                return;
+            }
+        }
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             int m, k;
@@ -121,21 +151,75 @@ __global__ void __launch_bounds__(NT, 1) gemm64_kernel(const __grid_constant__ B
         }
     }
 
+    // Epilogue.  Thread columns come in adjacent pairs (2 tx + {0,1} + 32 jj), so C is accessed as
+    // 8- or 16-byte pairs; for C -= AB the 16 pairs of four rows are all loaded before any is
+    // used or stored (independent loads in flight instead of one dependent round trip each).
+    const bool pair_ok = ((d.ldc & 1) == 0) &&
+                         ((reinterpret_cast<uintptr_t>(d.C) & (d.tc == DT_F64 ? 15 : 7)) == 0);
+    const bool sub = d.epi == EPI_SUB;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const int m = m0 + 2 * ty + (i & 1) + 32 * (i >> 1);
-        if (m >= Me) continue;
+    for (int h = 0; h < 2; ++h) {
+        double cv[4][4][2];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const int n = n0 + 2 * tx + (j & 1) + 32 * (j >> 1);
-            if (n >= Ne) continue;
-            const size_t o = (size_t)m * d.ldc + n;
-            if (d.tc == DT_F64) {
-                double *C = static_cast<double *>(d.C);
-                C[o] = d.epi == EPI_SUB ? C[o] - acc[i][j] : acc[i][j];
-            } else {
-                float *C = static_cast<float *>(d.C);
-                C[o] = d.epi == EPI_SUB ? (float)((double)C[o] - acc[i][j]) : (float)acc[i][j];
+        for (int ii = 0; ii < 4; ++ii) {
+            const int i = 4 * h + ii;
+            const int m = m0 + 2 * ty + (i & 1) + 32 * (i >> 1);
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {
+                const int n = n0 + 2 * tx + 32 * jj;
+                cv[ii][jj][0] = cv[ii][jj][1] = 0.0;
+                if (!sub || m >= Me || n >= Ne) continue;
+                const size_t o = (size_t)m * d.ldc + n;
+                if (d.tc == DT_F64) {
+                    const double *C = static_cast<const double *>(d.C);
+                    if (pair_ok && n + 1 < Ne) {
+                        const double2 v = __ldcg(reinterpret_cast<const double2 *>(C + o));
+                        cv[ii][jj][0] = v.x; cv[ii][jj][1] = v.y;
+                    } else {
+                        cv[ii][jj][0] = __ldcg(C + o);
+                        if (n + 1 < Ne) cv[ii][jj][1] = __ldcg(C + o + 1);
+                    }
+                } else {
+                    const float *C = static_cast<const float *>(d.C);
+                    if (pair_ok && n + 1 < Ne) {
+                        const float2 v = __ldcg(reinterpret_cast<const float2 *>(C + o));
+                        cv[ii][jj][0] = v.x; cv[ii][jj][1] = v.y;
+                    } else {
+                        cv[ii][jj][0] = __ldcg(C + o);
+                        if (n + 1 < Ne) cv[ii][jj][1] = __ldcg(C + o + 1);
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int ii = 0; ii < 4; ++ii) {
+            const int i = 4 * h + ii;
+            const int m = m0 + 2 * ty + (i & 1) + 32 * (i >> 1);
+            if (m >= Me) continue;
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {
+                const int n = n0 + 2 * tx + 32 * jj;
+                if (n >= Ne) continue;
+                const double r0 = sub ? cv[ii][jj][0] - acc[i][2 * jj] : acc[i][2 * jj];
+                const double r1 = sub ? cv[ii][jj][1] - acc[i][2 * jj + 1] : acc[i][2 * jj + 1];
+                const size_t o = (size_t)m * d.ldc + n;
+                if (d.tc == DT_F64) {
+                    double *C = static_cast<double *>(d.C);
+                    if (pair_ok && n + 1 < Ne) {
+                        *reinterpret_cast<double2 *>(C + o) = make_double2(r0, r1);
+                    } else {
+                        C[o] = r0;
+                        if (n + 1 < Ne) C[o + 1] = r1;
+                    }
+                } else {
+                    float *C = static_cast<float *>(d.C);
+                    if (pair_ok && n + 1 < Ne) {
+                        *reinterpret_cast<float2 *>(C + o) = make_float2((float)r0, (float)r1);
+                    } else {
+                        C[o] = (float)r0;
+                        if (n + 1 < Ne) C[o + 1] = (float)r1;
+                    }
+                }
             }
         }
     }

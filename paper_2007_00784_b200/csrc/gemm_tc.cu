@@ -63,10 +63,12 @@ struct __align__(64) TcBatch {
     TcDesc d[kMaxTc];
     int count;
     float damping;
+    int drain;            // k-blocks accumulated in TMEM per drain (>= 1)
 };
 
 struct SyrkBatch {
     int count;
+    int drain;
     FactorJob j[kMaxSyrk];
 };
 
@@ -244,39 +246,44 @@ __device__ __forceinline__ uint64_t operand_desc(uint32_t base, int kstep, int m
     return smem_desc(base + kstep * 1024, 4096, 512, 1);
 }
 
-// MMA issuer: for each k-block, the three 3xTF32 products into TMEM buffer (kb & 1).
-__device__ __forceinline__ void mma_loop(const Smem &S, uint32_t tmem, int nk, int a_mn, int b_mn, bool same_ab) {
+// MMA issuer: for each k-block, the three 3xTF32 products into TMEM buffer (segment & 1), where a
+// segment is `drain` consecutive k-blocks accumulated in TMEM before the drain warps take it.
+__device__ __forceinline__ void mma_loop(const Smem &S, uint32_t tmem, int nk, int a_mn, int b_mn, bool same_ab,
+                                         int drain) {
     const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
                            ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
     for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % kRaw, l = kb % kLo, b = kb & 1, u = kb >> 1;
+        const int s = kb % kRaw, l = kb % kLo;
+        const int seg = kb / drain, pos = kb - seg * drain, b = seg & 1, u = seg >> 1;
         mbar_wait(S.ready + 8 * s, (kb / kRaw) & 1);
-        if (u >= 1) mbar_wait(S.tempty + 8 * b, (u - 1) & 1);
+        if (pos == 0 && u >= 1) mbar_wait(S.tempty + 8 * b, (u - 1) & 1);
         tc_fence_after();
         const uint32_t a_hi = smem_u32(S.raw(s)), a_lo = smem_u32(S.lo(l));
         const uint32_t b_hi = same_ab ? a_hi : a_hi + kTileBytes, b_lo = same_ab ? a_lo : a_lo + kTileBytes;
         const uint32_t d = tmem + b * BN;
 #pragma unroll
         for (int ks = 0; ks < BK / 8; ++ks) {
-            mma_tf32(d, operand_desc(a_lo, ks, a_mn), operand_desc(b_hi, ks, b_mn), idesc, ks > 0 ? 1u : 0u);
+            mma_tf32(d, operand_desc(a_lo, ks, a_mn), operand_desc(b_hi, ks, b_mn), idesc, (ks > 0 || pos > 0) ? 1u : 0u);
             mma_tf32(d, operand_desc(a_hi, ks, a_mn), operand_desc(b_lo, ks, b_mn), idesc, 1u);
             mma_tf32(d, operand_desc(a_hi, ks, a_mn), operand_desc(b_hi, ks, b_mn), idesc, 1u);
         }
         mma_commit(S.raw_empty + 8 * s);
         mma_commit(S.lo_empty + 8 * l);
-        mma_commit(S.tfull + 8 * b);
+        if (pos == drain - 1 || kb == nk - 1) mma_commit(S.tfull + 8 * b);
     }
 }
 
-// Drain warps: every k-block's 128x128 partial product is added into fp32 registers with
-// IEEE rounding (the tensor-core accumulator truncates, so long accumulations stay in TMEM
-// for only 12 MMAs).  Thread (quarter wq, lane) owns row 32*wq + lane.
-__device__ __forceinline__ void drain_loop(const Smem &S, uint32_t tmem, int nk, int wq, float (&acc)[BN]) {
+// Drain warps: every segment's 128x128 partial product is added into fp32 registers with IEEE
+// rounding (the tensor-core accumulator truncates, so an accumulation stays in TMEM for only
+// 12 * drain MMAs).  Thread (quarter wq, lane) owns row 32*wq + lane.
+__device__ __forceinline__ void drain_loop(const Smem &S, uint32_t tmem, int nk, int wq, float (&acc)[BN],
+                                           int drain) {
 #pragma unroll
     for (int j = 0; j < BN; ++j) acc[j] = 0.f;
-    for (int kb = 0; kb < nk; ++kb) {
-        const int b = kb & 1;
-        mbar_wait(S.tfull + 8 * b, (kb >> 1) & 1);
+    const int nseg = (nk + drain - 1) / drain;
+    for (int sg = 0; sg < nseg; ++sg) {
+        const int b = sg & 1;
+        mbar_wait(S.tfull + 8 * b, (sg >> 1) & 1);
         tc_fence_after();
 #pragma unroll
         for (int c = 0; c < BN / 32; ++c) {
@@ -341,7 +348,7 @@ __global__ void __launch_bounds__(NT, 1) gemm_tc_kernel(const __grid_constant__ 
             }
         }
     } else if (warp == W_MMA) {
-        if (lane == 0) mma_loop(S, tmem, nk, d.a_mn, d.b_mn, false);
+        if (lane == 0) mma_loop(S, tmem, nk, d.a_mn, d.b_mn, false, batch.drain);
     } else if (warp < W_DRAIN0) {
         const int t = threadIdx.x;
         for (int kb = 0; kb < nk; ++kb) {
@@ -354,7 +361,7 @@ __global__ void __launch_bounds__(NT, 1) gemm_tc_kernel(const __grid_constant__ 
     } else {
         const int wq = warp - W_DRAIN0;
         float acc[BN];
-        drain_loop(S, tmem, nk, wq, acc);
+        drain_loop(S, tmem, nk, wq, acc, batch.drain);
         const int m = m0 + wq * 32 + lane;
         if (m < d.M) {
             const float vr = epi_uses_vectors(d.epi) ? d.vr[m] : 0.f;
@@ -418,25 +425,48 @@ __device__ __forceinline__ ChunkInfo chunk_info(const FactorJob &J, int c) {
     return ci;
 }
 
+// Geometry of one SYRK job, copied out of the (dynamically indexed) kernel parameters once.
+struct SyrkGeom {
+    const float *src;
+    int is_a, c_in, h_in, w_in, h_out, w_out, stride_h, stride_w, pad_h, pad_w;
+};
+
 // Producer warps 0-3: cp.async gathers of the 32-row k-block into raw stage s; the stage's
-// mbarrier completes when every producer thread's copies have landed.
-__device__ __forceinline__ void syrk_issue(const FactorJob &J, const Smem &S, int s, long long r0, long long r_end,
+// mbarrier completes when every producer thread's copies have landed.  Warp w fills rows
+// w + 4j (j < 8).  The row -> (image, output pixel) decomposition is done once per row by lanes
+// 0-7 in parallel and broadcast with shuffles (the integer divisions were the producer's
+// instruction-issue bottleneck); per (row, operand) only a bounds test and an add remain.
+__device__ __forceinline__ void syrk_issue(const SyrkGeom &G, const Smem &S, int s, long long r0, long long r_end,
                                            const ChunkInfo (&ci)[2], int cc, int t, bool diag) {
     const uint32_t st = smem_u32(S.raw(s));
-    const int hw = J.h_out * J.w_out;
+    const int warp = t / 32, lane = t % 32;
+    // lane j < 8 describes row r0 + warp + 4 j: element offset of its receptive-field origin and
+    // the origin's (ih0, iw0); invalid rows (past r_end) get ih0 = -32768 so every tap fails
+    int org = 0, ihw = 0;
+    {
+        const long long r = r0 + warp + 4 * (lane & 7);
+        const bool rv = r < r_end;
+        if (G.is_a) {
+            const int hw = G.h_out * G.w_out;
+            const int ri = rv ? (int)r : 0;
+            const int img = ri / hw;
+            const int p = ri - img * hw;
+            const int oh = p / G.w_out, ow = p - (p / G.w_out) * G.w_out;
+            const int ih0 = oh * G.stride_h - G.pad_h, iw0 = ow * G.stride_w - G.pad_w;
+            org = ((img * G.h_in + ih0) * G.w_in + iw0) * G.c_in;
+            ihw = rv ? (int)(((unsigned)ih0 << 16) | ((unsigned)iw0 & 0xffffu)) : (int)0x80000000;
+        } else {
+            org = rv ? (int)r * G.c_in : 0;
+            ihw = rv ? 0 : (int)0x80000000;
+        }
+    }
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-        const int k = t / 32 + 4 * j;
-        const int r = (int)(r0 + k);
-        const bool rv = r < r_end;
-        int img = 0, oh = 0, ow = 0;
-        if (J.is_a && rv) {
-            img = r / hw;
-            const int p = r - img * hw;
-            oh = p / J.w_out;
-            ow = p - oh * J.w_out;
-        }
-        const int ih0 = oh * J.stride_h - J.pad_h, iw0 = ow * J.stride_w - J.pad_w;
+        const int k = warp + 4 * j;
+        const int o = __shfl_sync(0xffffffffu, org, j);
+        const int hv = __shfl_sync(0xffffffffu, ihw, j);
+        const bool rv = hv != (int)0x80000000;
+        const int ih0 = hv >> 16, iw0 = (int)(short)(hv & 0xffff);
 #pragma unroll
         for (int op = 0; op < 2; ++op) {
             if (op == 1 && diag) break;
@@ -446,22 +476,12 @@ __device__ __forceinline__ void syrk_issue(const FactorJob &J, const Smem &S, in
                 cp_async16(dst, kBiasChunk, rv ? 16u : 0u);
                 continue;
             }
-            const float *src = J.src;
-            uint32_t bytes = 0;
-            if (rv && c.kind == 0) {
-                if (!J.is_a) {
-                    src = J.src + (long long)r * J.c_in + c.off;
-                    bytes = 16;
-                } else {
-                    // c.off already holds (kh * w_in + kw) * c_in + channel (receptive-field offset)
-                    const int ih = ih0 + c.kh, iw = iw0 + c.kw;
-                    if (ih >= 0 && ih < J.h_in && iw >= 0 && iw < J.w_in) {
-                        src = J.src + (((long long)img * J.h_in + ih0) * J.w_in + iw0) * J.c_in + c.off;
-                        bytes = 16;
-                    }
-                }
+            bool ok = rv && c.kind == 0;
+            if (G.is_a) {
+                // c.off holds (kh * w_in + kw) * c_in + channel (offset inside the receptive field)
+                ok = ok && (unsigned)(ih0 + c.kh) < (unsigned)G.h_in && (unsigned)(iw0 + c.kw) < (unsigned)G.w_in;
             }
-            cp_async16(dst, src, bytes);
+            cp_async16(dst, ok ? G.src + (o + c.off) : G.src, ok ? 16u : 0u);
         }
     }
 }
@@ -484,14 +504,16 @@ __global__ void __launch_bounds__(NT, 1) syrk_tc_kernel(const __grid_constant__ 
     const uint32_t tmem = *S.tmem_slot;
 
     if (warp == W_MMA) {
-        if (lane == 0) mma_loop(S, tmem, nk, 1, 1, diag);
+        if (lane == 0) mma_loop(S, tmem, nk, 1, 1, diag, batch.drain);
     } else if (warp < W_DRAIN0) {
         const int t = threadIdx.x, cc = t % 32;
         ChunkInfo ci[2] = {chunk_info(J, ti * BM + 4 * cc), chunk_info(J, tj * BM + 4 * cc)};
+        const SyrkGeom G{J.src, J.is_a, J.c_in, J.h_in, J.w_in, J.h_out, J.w_out,
+                         J.stride_h, J.stride_w, J.pad_h, J.pad_w};
         const int n_f4 = (diag ? 1 : 2) * kTileBytes / 16;
         // prologue: k-blocks 0 .. kRaw-2 in flight before the first split
         for (int p = 0; p < kRaw - 1 && p < nk; ++p) {
-            syrk_issue(J, S, p, r_begin + (long long)p * BK, r_end, ci, cc, t, diag);
+            syrk_issue(G, S, p, r_begin + (long long)p * BK, r_end, ci, cc, t, diag);
             cp_async_arrive(S.raw_full + 8 * p);
         }
         for (int kb = 0; kb < nk; ++kb) {
@@ -506,14 +528,14 @@ __global__ void __launch_bounds__(NT, 1) syrk_tc_kernel(const __grid_constant__ 
             if (nxt < nk) {
                 const int s2 = nxt % kRaw;
                 if (nxt >= kRaw) mbar_wait(S.raw_empty + 8 * s2, ((nxt / kRaw) - 1) & 1);
-                syrk_issue(J, S, s2, r_begin + (long long)nxt * BK, r_end, ci, cc, t, diag);
+                syrk_issue(G, S, s2, r_begin + (long long)nxt * BK, r_end, ci, cc, t, diag);
                 cp_async_arrive(S.raw_full + 8 * s2);
             }
         }
     } else if (warp < W_TMA) {
         const int wq = warp - W_DRAIN0;
         float acc[BN];
-        drain_loop(S, tmem, nk, wq, acc);
+        drain_loop(S, tmem, nk, wq, acc, batch.drain);
         float4 *dst = reinterpret_cast<float4 *>(J.partial + ((size_t)split * J.tiles + tau) * (BM * BN) +
                                                  (size_t)(wq * 32 + lane) * BN);
 #pragma unroll
@@ -551,6 +573,21 @@ bool make_map(CUtensorMap *map, const float *ptr, int rows, int cols, int ld, in
     return r == CUDA_SUCCESS;
 }
 
+// k-blocks per TMEM accumulation segment: KFAC_TC_DRAIN_GEMM / KFAC_TC_DRAIN_SYRK.
+int drain_env(const char *name, int dflt) {
+    const char *e = getenv(name);
+    const int v = e ? atoi(e) : dflt;
+    return v >= 1 ? v : 1;
+}
+int g_drain_gemm() {
+    static int v = drain_env("KFAC_TC_DRAIN_GEMM", 1);
+    return v;
+}
+int g_drain_syrk() {
+    static int v = drain_env("KFAC_TC_DRAIN_SYRK", 1);
+    return v;
+}
+
 bool g_tc_disabled() {
     static int v = -1;
     if (v < 0) {
@@ -580,6 +617,7 @@ kfac_status_t gemm_tc_grouped(const GemmDesc *descs, int count, float damping, c
         TcBatch b;
         memset(&b, 0, sizeof(b));
         b.damping = damping;
+        b.drain = g_drain_gemm();
         b.count = 0;
         int tiles = 0;
         for (int i = base; i < count && b.count < kMaxTc; ++i) {
@@ -616,6 +654,10 @@ bool syrk_tc_supported(const FactorJob &j) {
     if (j.d < 64 || j.n < 32) return false;               // small factors: SIMT tile
     if (j.c_in % 4 != 0) return false;                    // 16-byte gathers
     if (j.is_a && j.bias_col && j.patch_cols % 4 != 0) return false;
+    // 32-bit element offsets in the gather
+    const long long elems = j.is_a ? (long long)(j.n / ((long long)j.h_out * j.w_out)) * j.h_in * j.w_in * j.c_in
+                                   : j.n * j.c_in;
+    if (elems >= (1ll << 31) - 4096) return false;
     return aligned16(j.src);
 }
 
@@ -628,6 +670,7 @@ kfac_status_t syrk_tc_partial(const FactorJob *jobs, int count, cudaStream_t s) 
     for (int base = 0; base < count; base += kMaxSyrk) {
         SyrkBatch b;
         b.count = 0;
+        b.drain = g_drain_syrk();
         int items = 0;
         for (int i = base; i < count && b.count < kMaxSyrk; ++i) {
             FactorJob j = jobs[i];
