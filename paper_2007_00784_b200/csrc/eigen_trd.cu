@@ -79,8 +79,8 @@ struct TrdJob {
     double *mscal;             // per merge: {rho2, tol}
     double *part;              // kMaxGroupCtas x kPart
     double *DP;                // symv direct partials  [n][ldp]  (row, 128-column chunk)
-    double *TP;                // symv transposed partials [n/64][ldw] (64-row block, column)
-    int ldp;
+    double *TP;                // symv transposed partials [n][ldtp] (column, 64-row block)
+    int ldp, ldtp;
     unsigned *bar;
     int n, ldF, ldQ, ldw;
     int levels;                // D&C merge levels (n <= kLeaf -> 0)
@@ -95,15 +95,16 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
     return v;
 }
 
-// Barrier among the `nc` CTAs of one factor's group (counter zeroed before each launch).
+// Barrier among the `nc` CTAs of one factor's group (counter zeroed before each launch).  The
+// CTA's writes are ordered before thread 0's release add by bar.sync (cumulativity), and its
+// acquire poll orders the other CTAs' writes before everything after the closing bar.sync.
 __device__ __forceinline__ void group_barrier(unsigned *bar, unsigned &target, int nc) {
     __syncthreads();
     target += (unsigned)nc;
     if (threadIdx.x == 0) {
-        __threadfence();
-        atomicAdd(bar, 1u);
-        while (ld_acquire(bar) < target) __nanosleep(20);
-        __threadfence();
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+        while (ld_acquire(bar) < target) {
+        }
     }
     __syncthreads();
 }
@@ -161,6 +162,7 @@ struct PanelLaunch {
     int job[kMaxGroupCtas];
     int p0[kMaxGroupCtas];                 // panel start of each group's factor (staggered)
     int cta_begin[kMaxGroupCtas + 1];
+    int ring_off;                          // float offset of the symv prefetch ring in dynamic smem
 };
 
 // One panel of 32 columns (LAPACK dlatrd, lower) for every active factor.  Column k (i = k - p0):
@@ -194,6 +196,7 @@ __global__ void __launch_bounds__(kTrdThreads, 1) trd_panel(const __grid_constan
     float *VW = J.VW, *WV = J.WV;
     double *part = J.part;
     const int t = threadIdx.x, warp = t / 32, lane = t % 32;
+    const int ring_off = L.ring_off;                 // floats: symv prefetch ring after v
     unsigned target = 0;
     float w_next = 0.f;                              // W[k, i-1], computed redundantly
 
@@ -209,6 +212,7 @@ __global__ void __launch_bounds__(kTrdThreads, 1) trd_panel(const __grid_constan
         int lo, hi;
         part_range(k, n, c, nc, lo, hi);
         double s2 = 0.0;
+#pragma unroll 4
         for (int r = lo + warp; r < hi; r += kTrdWarps) {       // one warp per row, lane q = panel column
             double corr = 0.0;
             if (lane < i)
@@ -277,68 +281,108 @@ __global__ void __launch_bounds__(kTrdThreads, 1) trd_panel(const __grid_constan
         // symmetric mat-vec over the lower triangle of A_p[k+1:n, k+1:n] in 64 x 128 tiles (one warp
         // per tile, every tile of the group's factor spread over its warps): each tile adds its
         // row sums to DP[row][chunk] and its column sums (the mirrored upper triangle) to
-        // TP[block][column]; phase C sums both in a fixed order, so every element is read once.
+        // TP[column][block]; phase C sums both in a fixed order, so every element is read once.
+        // The warp walks its tiles as a stream of 8-row octets; every lane prefetches its own
+        // 16-byte chunk of the next octet with cp.async into a private two-stage ring (zero fill
+        // above the diagonal and past the last row), so the loads of octet q+1 are in flight while
+        // octet q is reduced.
         {
             const int r00 = k + 1, nrb = (n - r00 + kSymvR - 1) / kSymvR;
             auto cnt = [&](int b) { return (min(n, r00 + kSymvR * (b + 1)) - 1 - c0) / kSymvC + 1; };
             int total = 0;
             for (int b = 0; b < nrb; ++b) total += cnt(b);
             const int W = nc * kTrdWarps;
-            int b = 0, base = 0;
             const float4 *v4 = reinterpret_cast<const float4 *>(vsm);
-            for (int it = c * kTrdWarps + warp; it < total; it += W) {
-                while (it >= base + cnt(b)) { base += cnt(b); ++b; }
-                const int j = it - base;
+            float4 *ring = reinterpret_cast<float4 *>(vsm + ring_off) + (size_t)warp * (2 * 8 * 32) + lane;
+            // octet cursor: tile it (row block bq, chunk jq), first row rq
+            int it = c * kTrdWarps + warp, bq = 0, base = 0, jq = 0, rq = 0;
+            auto locate = [&]() {
+                while (bq < nrb && it >= base + cnt(bq)) { base += cnt(bq); ++bq; }
+                jq = it - base;
+                rq = r00 + kSymvR * bq;
+            };
+            auto issue = [&](int stage) {
+                const int rend = min(n, r00 + kSymvR * (bq + 1));
+                const int ccq = c0 + kSymvC * jq + 4 * lane;
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int rr = rq + u;
+                    const bool ok = rr < rend && ccq <= rr;
+                    const float *src = ok ? A + (size_t)rr * ldw + ccq : A;
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
+                                     (uint32_t)__cvta_generic_to_shared(ring + (stage * 8 + u) * 32)),
+                                 "l"(src), "r"(ok ? 16u : 0u)
+                                 : "memory");
+                }
+                asm volatile("cp.async.commit_group;" ::: "memory");
+            };
+            if (it < total) {
+                locate();
+                issue(0);
+            }
+            int stage = 0;
+            double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
+            while (it < total) {
+                // current octet
+                const int b = bq, j = jq, r = rq;
                 const int r0 = r00 + kSymvR * b, r1 = min(n, r0 + kSymvR);
                 const int cc = c0 + kSymvC * j + 4 * lane;
-                const float4 v = v4[(cc - c0) >> 2];
-                double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
-                for (int r = r0; r < r1; r += 8) {
-                    // 8 rows: 8 float4 loads in flight per lane, then a butterfly reduce-scatter of
-                    // the 8 row partials (9 shuffles instead of 40)
-                    float4 a[8];
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        const int rr = r + u;
-                        a[u] = (rr < r1 && cc <= rr) ? __ldg(reinterpret_cast<const float4 *>(A + (size_t)rr * ldw + cc))
-                                                     : make_float4(0.f, 0.f, 0.f, 0.f);
-                    }
-                    double p[8];
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        const int rr = r + u;
-                        const double ax = cc <= rr ? a[u].x : 0.0, ay = cc + 1 <= rr ? a[u].y : 0.0;
-                        const double az = cc + 2 <= rr ? a[u].z : 0.0, aw = cc + 3 <= rr ? a[u].w : 0.0;
-                        p[u] = ax * v.x + ay * v.y + az * v.z + aw * v.w;
-                        const double vr = rr < r1 ? (double)vsm[rr - c0] : 0.0;
-                        t0 += (cc < rr ? ax : 0.0) * vr;
-                        t1 += (cc + 1 < rr ? ay : 0.0) * vr;
-                        t2 += (cc + 2 < rr ? az : 0.0) * vr;
-                        t3 += (cc + 3 < rr ? aw : 0.0) * vr;
-                    }
-                    const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4;
-                    double q4[4], q2[2];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const double send = h16 ? p[u] : p[u + 4], keep = h16 ? p[u + 4] : p[u];
-                        q4[u] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-                    }
-#pragma unroll
-                    for (int u = 0; u < 2; ++u) {
-                        const double send = h8 ? q4[u] : q4[u + 2], keep = h8 ? q4[u + 2] : q4[u];
-                        q2[u] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-                    }
-                    double sd = (h4 ? q2[1] : q2[0]) + __shfl_xor_sync(0xffffffffu, h4 ? q2[0] : q2[1], 4);
-                    sd += __shfl_xor_sync(0xffffffffu, sd, 2);
-                    sd += __shfl_xor_sync(0xffffffffu, sd, 1);
-                    const int rr = r + (h16 ? 4 : 0) + (h8 ? 2 : 0) + (h4 ? 1 : 0);
-                    if ((lane & 3) == 0 && rr < r1) __stcg(J.DP + (size_t)rr * J.ldp + j, sd);
+                // advance the cursor and prefetch the next octet into the other stage
+                rq += 8;
+                if (rq >= r1) {
+                    it += W;
+                    if (it < total) locate();
                 }
-                double *tp = J.TP + (size_t)b * ldw + cc;
-                if (cc < n) __stcg(tp, t0);
-                if (cc + 1 < n) __stcg(tp + 1, t1);
-                if (cc + 2 < n) __stcg(tp + 2, t2);
-                if (cc + 3 < n) __stcg(tp + 3, t3);
+                const bool more = it < total;
+                if (more) {
+                    issue(stage ^ 1);
+                    asm volatile("cp.async.wait_group 1;" ::: "memory");
+                } else {
+                    asm volatile("cp.async.wait_group 0;" ::: "memory");
+                }
+                const float4 v = v4[(cc - c0) >> 2];
+                float4 a[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) a[u] = ring[(stage * 8 + u) * 32];
+                stage ^= 1;
+                double p[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int rr = r + u;
+                    const double ax = cc <= rr ? a[u].x : 0.0, ay = cc + 1 <= rr ? a[u].y : 0.0;
+                    const double az = cc + 2 <= rr ? a[u].z : 0.0, aw = cc + 3 <= rr ? a[u].w : 0.0;
+                    p[u] = ax * v.x + ay * v.y + az * v.z + aw * v.w;
+                    const double vr = rr < r1 ? (double)vsm[rr - c0] : 0.0;
+                    t0 += (cc < rr ? ax : 0.0) * vr;
+                    t1 += (cc + 1 < rr ? ay : 0.0) * vr;
+                    t2 += (cc + 2 < rr ? az : 0.0) * vr;
+                    t3 += (cc + 3 < rr ? aw : 0.0) * vr;
+                }
+                // butterfly reduce-scatter of the 8 row partials (9 shuffles instead of 40)
+                const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4;
+                double q4[4], q2[2];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const double send = h16 ? p[u] : p[u + 4], keep = h16 ? p[u + 4] : p[u];
+                    q4[u] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+                }
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const double send = h8 ? q4[u] : q4[u + 2], keep = h8 ? q4[u + 2] : q4[u];
+                    q2[u] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+                }
+                double sd = (h4 ? q2[1] : q2[0]) + __shfl_xor_sync(0xffffffffu, h4 ? q2[0] : q2[1], 4);
+                sd += __shfl_xor_sync(0xffffffffu, sd, 2);
+                sd += __shfl_xor_sync(0xffffffffu, sd, 1);
+                const int rs = r + (h16 ? 4 : 0) + (h8 ? 2 : 0) + (h4 ? 1 : 0);
+                if ((lane & 3) == 0 && rs < r1) __stcg(J.DP + (size_t)rs * J.ldp + j, sd);
+                if (r + 8 >= r1) {                   // tile done: its column sums
+                    if (cc < n) __stcg(J.TP + (size_t)cc * J.ldtp + b, t0);
+                    if (cc + 1 < n) __stcg(J.TP + (size_t)(cc + 1) * J.ldtp + b, t1);
+                    if (cc + 2 < n) __stcg(J.TP + (size_t)(cc + 2) * J.ldtp + b, t2);
+                    if (cc + 3 < n) __stcg(J.TP + (size_t)(cc + 3) * J.ldtp + b, t3);
+                    t0 = t1 = t2 = t3 = 0.0;
+                }
             }
         }
         red[warp][lane] = pa;
@@ -359,12 +403,13 @@ __global__ void __launch_bounds__(kTrdThreads, 1) trd_panel(const __grid_constan
         double wv = 0.0;
         {
             const int nrb = (n - (k + 1) + kSymvR - 1) / kSymvR;
+#pragma unroll 2
             for (int r = lo + warp; r < hi; r += kTrdWarps) {   // one warp per row
                 const int b = (r - (k + 1)) / kSymvR;
                 const int nj = (min(n, k + 1 + kSymvR * (b + 1)) - 1 - c0) / kSymvC + 1;
                 double yr = 0.0;
                 for (int jj = lane; jj < nj; jj += 32) yr += ldcg(J.DP + (size_t)r * J.ldp + jj);
-                for (int bb = b + lane; bb < nrb; bb += 32) yr += ldcg(J.TP + (size_t)bb * ldw + r);
+                for (int bb = b + lane; bb < nrb; bb += 32) yr += ldcg(J.TP + (size_t)r * J.ldtp + bb);
                 if (lane < i)
                     yr -= (double)ldcg(VW + (size_t)r * 64 + kNb + lane) * ab[lane] +
                           (double)ldcg(VW + (size_t)r * 64 + lane) * ab[kNb + lane];
@@ -1022,7 +1067,8 @@ Plan plan(const int32_t *dims, int count) {
         TAKE(part, double, (size_t)kMaxGroupCtas * kPart);
         J.ldp = cdiv(n + 3, kSymvC) + 1;
         TAKE(DP, double, (size_t)n * J.ldp);
-        TAKE(TP, double, (size_t)cdiv(n, kSymvR) * ldw);
+        J.ldtp = cdiv(n, kSymvR) + 1;
+        TAKE(TP, double, (size_t)n * J.ldtp);
         TAKE(bar, unsigned, 64);
 #undef TAKE
         // leaves and merges
@@ -1155,7 +1201,8 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
         KFAC_CUDA_TRY(cudaFuncSetAttribute(bt_larft, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLarftSmem));
         attr = true;
     }
-    const size_t smem = (size_t)(round_up(max_n, kSymvC) + kSymvC + 8) * sizeof(float);
+    const int ring_off = (int)round_up(round_up(max_n, kSymvC) + kSymvC + 8, 64);
+    const size_t smem = (size_t)ring_off * sizeof(float) + (size_t)kTrdWarps * 2 * 8 * 32 * sizeof(float4);
     const int cap = panel_capacity(smem);
     static PanelLaunch PL;
     // Staggered schedule: factor j (P_j panels) starts at launch P_max - P_j, so all factors finish
@@ -1192,6 +1239,7 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
         }
         PL.jobs = djobs;
         PL.count = na;
+        PL.ring_off = ring_off;
         int tot = 0;
         for (int q = 0; q < na; ++q) {
             PL.job[q] = act[q];

@@ -36,6 +36,84 @@ __device__ __forceinline__ double ld_any(const void *p, size_t i, int dt) {
     return dt == DT_F64 ? __ldg(static_cast<const double *>(p) + i) : (double)__ldg(static_cast<const float *>(p) + i);
 }
 
+// Epilogue shared by both kernels.  Thread (ty, tx) owns rows 2 ty + {0,1} + 32 i' and columns
+// 2 tx + {0,1} + 32 j'; acc[i][j] with i = 2 i' + {0,1}, j = 2 j' + {0,1}.
+__device__ __forceinline__ void epilogue(const Gemm64Desc &d, int m0, int n0, int Me, int Ne, int ty, int tx,
+                                         const double (&acc)[8][8]) {
+    // Epilogue.  Thread columns come in adjacent pairs (2 tx + {0,1} + 32 jj), so C is accessed as
+    // 8- or 16-byte pairs; for C -= AB the 16 pairs of four rows are all loaded before any is
+    // used or stored (independent loads in flight instead of one dependent round trip each).
+    const bool pair_ok = ((d.ldc & 1) == 0) &&
+                         ((reinterpret_cast<uintptr_t>(d.C) & (d.tc == DT_F64 ? 15 : 7)) == 0);
+    const bool sub = d.epi == EPI_SUB;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        double cv[4][4][2];
+#pragma unroll
+        for (int ii = 0; ii < 4; ++ii) {
+            const int i = 4 * h + ii;
+            const int m = m0 + 2 * ty + (i & 1) + 32 * (i >> 1);
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {
+                const int n = n0 + 2 * tx + 32 * jj;
+                cv[ii][jj][0] = cv[ii][jj][1] = 0.0;
+                if (!sub || m >= Me || n >= Ne) continue;
+                const size_t o = (size_t)m * d.ldc + n;
+                if (d.tc == DT_F64) {
+                    const double *C = static_cast<const double *>(d.C);
+                    if (pair_ok && n + 1 < Ne) {
+                        const double2 v = __ldcg(reinterpret_cast<const double2 *>(C + o));
+                        cv[ii][jj][0] = v.x; cv[ii][jj][1] = v.y;
+                    } else {
+                        cv[ii][jj][0] = __ldcg(C + o);
+                        if (n + 1 < Ne) cv[ii][jj][1] = __ldcg(C + o + 1);
+                    }
+                } else {
+                    const float *C = static_cast<const float *>(d.C);
+                    if (pair_ok && n + 1 < Ne) {
+                        const float2 v = __ldcg(reinterpret_cast<const float2 *>(C + o));
+                        cv[ii][jj][0] = v.x; cv[ii][jj][1] = v.y;
+                    } else {
+                        cv[ii][jj][0] = __ldcg(C + o);
+                        if (n + 1 < Ne) cv[ii][jj][1] = __ldcg(C + o + 1);
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int ii = 0; ii < 4; ++ii) {
+            const int i = 4 * h + ii;
+            const int m = m0 + 2 * ty + (i & 1) + 32 * (i >> 1);
+            if (m >= Me) continue;
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {
+                const int n = n0 + 2 * tx + 32 * jj;
+                if (n >= Ne) continue;
+                const double r0 = sub ? cv[ii][jj][0] - acc[i][2 * jj] : acc[i][2 * jj];
+                const double r1 = sub ? cv[ii][jj][1] - acc[i][2 * jj + 1] : acc[i][2 * jj + 1];
+                const size_t o = (size_t)m * d.ldc + n;
+                if (d.tc == DT_F64) {
+                    double *C = static_cast<double *>(d.C);
+                    if (pair_ok && n + 1 < Ne) {
+                        *reinterpret_cast<double2 *>(C + o) = make_double2(r0, r1);
+                    } else {
+                        C[o] = r0;
+                        if (n + 1 < Ne) C[o + 1] = r1;
+                    }
+                } else {
+                    float *C = static_cast<float *>(d.C);
+                    if (pair_ok && n + 1 < Ne) {
+                        *reinterpret_cast<float2 *>(C + o) = make_float2((float)r0, (float)r1);
+                    } else {
+                        C[o] = (float)r0;
+                        if (n + 1 < Ne) C[o + 1] = (float)r1;
+                    }
+                }
+            }
+        }
+    }
+}
+
 __global__ void __launch_bounds__(NT, 1) gemm64_kernel(const __grid_constant__ Batch64 batch) {
     __shared__ __align__(16) double As[2][BK][BM + 2];
     __shared__ __align__(16) double Bs[2][BK][BN + 2];
@@ -151,78 +229,7 @@ __global__ void __launch_bounds__(NT, 1) gemm64_kernel(const __grid_constant__ B
         }
     }
 
-    // Epilogue.  Thread columns come in adjacent pairs (2 tx + {0,1} + 32 jj), so C is accessed as
-    // 8- or 16-byte pairs; for C -= AB the 16 pairs of four rows are all loaded before any is
-    // used or stored (independent loads in flight instead of one dependent round trip each).
-    const bool pair_ok = ((d.ldc & 1) == 0) &&
-                         ((reinterpret_cast<uintptr_t>(d.C) & (d.tc == DT_F64 ? 15 : 7)) == 0);
-    const bool sub = d.epi == EPI_SUB;
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        double cv[4][4][2];
-#pragma unroll
-        for (int ii = 0; ii < 4; ++ii) {
-            const int i = 4 * h + ii;
-            const int m = m0 + 2 * ty + (i & 1) + 32 * (i >> 1);
-#pragma unroll
-            for (int jj = 0; jj < 4; ++jj) {
-                const int n = n0 + 2 * tx + 32 * jj;
-                cv[ii][jj][0] = cv[ii][jj][1] = 0.0;
-                if (!sub || m >= Me || n >= Ne) continue;
-                const size_t o = (size_t)m * d.ldc + n;
-                if (d.tc == DT_F64) {
-                    const double *C = static_cast<const double *>(d.C);
-                    if (pair_ok && n + 1 < Ne) {
-                        const double2 v = __ldcg(reinterpret_cast<const double2 *>(C + o));
-                        cv[ii][jj][0] = v.x; cv[ii][jj][1] = v.y;
-                    } else {
-                        cv[ii][jj][0] = __ldcg(C + o);
-                        if (n + 1 < Ne) cv[ii][jj][1] = __ldcg(C + o + 1);
-                    }
-                } else {
-                    const float *C = static_cast<const float *>(d.C);
-                    if (pair_ok && n + 1 < Ne) {
-                        const float2 v = __ldcg(reinterpret_cast<const float2 *>(C + o));
-                        cv[ii][jj][0] = v.x; cv[ii][jj][1] = v.y;
-                    } else {
-                        cv[ii][jj][0] = __ldcg(C + o);
-                        if (n + 1 < Ne) cv[ii][jj][1] = __ldcg(C + o + 1);
-                    }
-                }
-            }
-        }
-#pragma unroll
-        for (int ii = 0; ii < 4; ++ii) {
-            const int i = 4 * h + ii;
-            const int m = m0 + 2 * ty + (i & 1) + 32 * (i >> 1);
-            if (m >= Me) continue;
-#pragma unroll
-            for (int jj = 0; jj < 4; ++jj) {
-                const int n = n0 + 2 * tx + 32 * jj;
-                if (n >= Ne) continue;
-                const double r0 = sub ? cv[ii][jj][0] - acc[i][2 * jj] : acc[i][2 * jj];
-                const double r1 = sub ? cv[ii][jj][1] - acc[i][2 * jj + 1] : acc[i][2 * jj + 1];
-                const size_t o = (size_t)m * d.ldc + n;
-                if (d.tc == DT_F64) {
-                    double *C = static_cast<double *>(d.C);
-                    if (pair_ok && n + 1 < Ne) {
-                        *reinterpret_cast<double2 *>(C + o) = make_double2(r0, r1);
-                    } else {
-                        C[o] = r0;
-                        if (n + 1 < Ne) C[o + 1] = r1;
-                    }
-                } else {
-                    float *C = static_cast<float *>(d.C);
-                    if (pair_ok && n + 1 < Ne) {
-                        *reinterpret_cast<float2 *>(C + o) = make_float2((float)r0, (float)r1);
-                    } else {
-                        C[o] = (float)r0;
-                        if (n + 1 < Ne) C[o + 1] = (float)r1;
-                    }
-                }
-            }
-        }
-    }
+    epilogue(d, m0, n0, Me, Ne, ty, tx, acc);
 }
 
 }  // namespace
