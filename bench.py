@@ -71,6 +71,14 @@ def peaks():
         return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, src="fallback")
 
 
+PROF_CLASSES = (1, 2, 3, 4)     # KFAC_PROF_* in include/kfac.h
+PROF_NAMES = {1: ("trd_panel (Householder tridiagonalisation panel: lower-triangle symv, "
+                  "4 B per trailing-matrix element per column)", "hbm"),
+              2: ("gemm64 (fp64-accumulating eigensolver GEMMs)", "alu"),
+              3: ("syrk_tc_kernel (factor SYRK, tcgen05 3xTF32)", "tensor"),
+              4: ("gemm_tc_kernel (preconditioning GEMMs, tcgen05 3xTF32)", "tensor")}
+
+
 # ---------------------------------------------------------------- clocks ------
 class ClockSampler:
     def __init__(self, idx):
@@ -251,7 +259,22 @@ def run_ours(args):
     barrier()
     cold_ms = cold[0][0].elapsed_time(cold[0][3])
     cold_eig_ms = cold[0][1].elapsed_time(cold[0][2])
+    # Probe steps (untimed): one step with each instrumented kernel class armed, to find the
+    # kernel that dominates the step; that class stays armed (CUDA events around each of its
+    # launches, on its launch stream) during the timed region for the roofline below.
+    probe = {}
+    for j, kc in enumerate(PROF_CLASSES):
+        _lib.kfac_profile_start(kc)
+        one_step(args.warmup + j, first=False, warm=True)
+        probe[kc] = _lib.kfac_profile_stop()[0]
+    if world > 1:       # same class on every rank: max over ranks of each probe
+        pv = torch.tensor([probe[k] for k in PROF_CLASSES], dtype=torch.float64, device="cuda")
+        dist.all_reduce(pv, op=dist.ReduceOp.MAX)
+        probe = dict(zip(PROF_CLASSES, pv.tolist()))
+    dom_class = max(probe, key=probe.get)
+    barrier()
     n0 = _lib.kfac_launch_count()
+    _lib.kfac_profile_start(dom_class)
     log = []
     with ClockSampler(local) as clk:
         t0, t1 = ev(), ev()
@@ -262,6 +285,7 @@ def run_ours(args):
         t1.record(stream)
         barrier()
     launches = _lib.kfac_launch_count() - n0
+    prof_ms, prof_n, prof_bytes, prof_flops = _lib.kfac_profile_stop()
     ms = t0.elapsed_time(t1) / args.steps
     stages = {"factors": float(np.mean([e[0].elapsed_time(e[1]) for e in log])),
               "eigen": float(np.mean([e[1].elapsed_time(e[2]) for e in log])),
@@ -321,22 +345,26 @@ def run_ours(args):
         pk = peaks()
         tf32_peak = pk["bf16"] * (1.1 / 2.25)              # guide's nominal tf32/bf16 ratio
         fp64_peak = 148 * 64 * 2 * 1.965e9 / 1e12          # 64 FP64 FMA/clk/SM x 1965 MHz
-        dom = max(stages, key=stages.get)
-        if dom == "eigen":
-            ach = wm["eig_flops"] / (stages["eigen"] * 1e-3) / 1e12
+        hbm_peak = pk["hbm"]
+        per_launch_ms = prof_ms / max(prof_n, 1)
+        kname, bound = PROF_NAMES[dom_class]
+        if bound == "hbm":
+            ach = prof_bytes / max(prof_n, 1) / (per_launch_ms * 1e-3) / 1e9
+            roof = {"bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
+                    "peak_source": f"{pk['src']} HBM copy bandwidth"}
+        elif bound == "alu":
+            ach = prof_flops / max(prof_n, 1) / (per_launch_ms * 1e-3) / 1e12
             roof = {"bound": "alu", "achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s",
-                    "kernel": "eig_round (fp64 one-sided Jacobi; conventional 9d^3 flops per factor)",
                     "peak_source": "148 SMs x 64 fp64 FMA/clk x 2 x 1965 MHz (derived, DESIGN.md)"}
-        elif dom == "factors":
-            ach = wm["fac_flops"] / (stages["factors"] * 1e-3) / 1e12
-            roof = {"bound": "tensor", "achieved": ach, "peak": tf32_peak / 3, "unit": "TFLOP/s",
-                    "kernel": "syrk_tc_kernel (factor stage, 3xTF32)",
-                    "peak_source": f"{pk['src']} bf16 x 1.1/2.25 tf32 ratio / 3 products"}
         else:
-            ach = wm["pc_flops"] / (stages["precond"] * 1e-3) / 1e12
+            ach = prof_flops / max(prof_n, 1) / (per_launch_ms * 1e-3) / 1e12
             roof = {"bound": "tensor", "achieved": ach, "peak": tf32_peak / 3, "unit": "TFLOP/s",
-                    "kernel": "gemm_tc_kernel (precondition stage, 3xTF32)",
-                    "peak_source": f"{pk['src']} bf16 x 1.1/2.25 tf32 ratio / 3 products"}
+                    "peak_source": f"{pk['src']} bf16 x 1.1/2.25 tf32 ratio / 3 products (3xTF32)"}
+        roof.update({"kernel": kname, "launches_timed": prof_n, "avg_launch_ms": per_launch_ms,
+                     "share_of_step": prof_ms / args.steps / ms,
+                     "algorithmic_per_launch": {"bytes": prof_bytes / max(prof_n, 1),
+                                                "flops": prof_flops / max(prof_n, 1)},
+                     "probe_ms_per_step": {PROF_NAMES[k][0]: v for k, v in probe.items()}})
         roof["frac"] = roof["achieved"] / roof["peak"]
         roof["traffic"] = None
         tensor_tflops = (wm["fac_flops"] + wm["pc_flops"]) / ((stages["factors"] + stages["precond"]) * 1e-3) / 1e12

@@ -176,6 +176,20 @@ const char *kfac_last_error(void);
 uint64_t kfac_launch_count(void);
 int32_t kfac_version(void);
 
+/* ---- Instrumentation (bench.py's roofline).  kfac_profile_start(k) arms per-launch timing of one
+ * kernel class k (KFAC_PROF_*): every launch of that class records a CUDA event pair on the
+ * stream it is launched on and adds its algorithmic bytes and flops.
+ * kfac_profile_stop synchronises those events and returns the summed device time (ms), the
+ * launch count and the algorithmic bytes/flops, then disarms.  Host only; at most one class at
+ * a time; not for use inside CUDA-graph capture.  Returns KFAC_ERR_INVALID_VALUE for an unknown
+ * class or null outputs. */
+#define KFAC_PROF_TRD_PANEL 1   /* Householder tridiagonalisation panel (trd_panel)        */
+#define KFAC_PROF_GEMM64 2      /* fp64-accumulating GEMMs of the eigensolver (gemm64_*)    */
+#define KFAC_PROF_SYRK_TC 3     /* tcgen05 factor SYRK (syrk_tc_kernel)                     */
+#define KFAC_PROF_GEMM_TC 4     /* tcgen05 preconditioning GEMMs (gemm_tc_kernel)           */
+kfac_status_t kfac_profile_start(int32_t kernel_class);
+kfac_status_t kfac_profile_stop(double *ms, int64_t *launches, double *bytes, double *flops);
+
 #ifdef __cplusplus
 }
 #endif

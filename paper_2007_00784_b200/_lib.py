@@ -64,8 +64,11 @@ def _load():
     L.kfac_last_error.restype = C.c_char_p
     L.kfac_launch_count.restype = C.c_uint64
     L.kfac_version.restype = C.c_int32
+    L.kfac_profile_start.argtypes = [C.c_int32]
+    L.kfac_profile_stop.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_int64), C.POINTER(C.c_double),
+                                    C.POINTER(C.c_double)]
     for f in ("kfac_layer_dims", "kfac_update_factors", "kfac_compute_eigen", "kfac_compute_inverse",
-              "kfac_precondition", "kfac_kl_clip", "kfac_assign"):
+              "kfac_precondition", "kfac_kl_clip", "kfac_assign", "kfac_profile_start", "kfac_profile_stop"):
         getattr(L, f).restype = C.c_int
     return L
 
@@ -77,7 +80,8 @@ EXPORTED = ("kfac_layer_dims", "kfac_update_factors_workspace_size", "kfac_updat
             "kfac_compute_inverse_workspace_size", "kfac_compute_inverse",
             "kfac_precondition_workspace_size", "kfac_precondition",
             "kfac_kl_clip_workspace_size", "kfac_kl_clip", "kfac_assign",
-            "kfac_status_string", "kfac_last_error", "kfac_launch_count", "kfac_version")
+            "kfac_status_string", "kfac_last_error", "kfac_launch_count", "kfac_version",
+            "kfac_profile_start", "kfac_profile_stop")
 
 
 def _check(status: int, fn: str):
@@ -228,3 +232,17 @@ def kfac_assign(dims, layer_of, num_layers: int, world_size: int, policy: int):
 
 def kfac_launch_count() -> int:
     return int(lib.kfac_launch_count())
+
+
+PROF_TRD_PANEL, PROF_GEMM64, PROF_SYRK_TC, PROF_GEMM_TC = 1, 2, 3, 4
+
+
+def kfac_profile_start(kernel_class: int):
+    _check(lib.kfac_profile_start(int(kernel_class)), "kfac_profile_start")
+
+
+def kfac_profile_stop():
+    """-> (device ms summed over the armed class's launches, launches, algorithmic bytes, flops)."""
+    ms, n, by, fl = C.c_double(), C.c_int64(), C.c_double(), C.c_double()
+    _check(lib.kfac_profile_stop(C.byref(ms), C.byref(n), C.byref(by), C.byref(fl)), "kfac_profile_stop")
+    return ms.value, n.value, by.value, fl.value

@@ -71,4 +71,9 @@ struct WsArena {
 
 int num_sms();   // cached multiprocessor count of the current device
 
+// Per-launch instrumentation (kfac_profile_start/stop).  prof_begin returns a slot (< 0 when the
+// class is not armed); prof_end records the closing event and the launch's algorithmic work.
+int prof_begin(int kernel_class, cudaStream_t s);
+void prof_end(int slot, cudaStream_t s, double bytes, double flops);
+
 }  // namespace kfac

@@ -212,15 +212,23 @@ __global__ void __launch_bounds__(kTrdThreads, 1) trd_panel(const __grid_constan
         int lo, hi;
         part_range(k, n, c, nc, lo, hi);
         double s2 = 0.0;
-#pragma unroll 4
-        for (int r = lo + warp; r < hi; r += kTrdWarps) {       // one warp per row, lane q = panel column
+        const int sub = lane >> 3, sl = lane & 7;          // 8 lanes per row, 4 rows per warp
+        for (int r0 = lo + 4 * warp; r0 < hi; r0 += 4 * kTrdWarps) {
+            // lane sl covers panel columns q = 4 sl .. 4 sl + 3 (< i) with one float4 of V and of W
+            const int r = r0 + sub;
             double corr = 0.0;
-            if (lane < i)
-                corr = (double)ldcg(VW + (size_t)r * 64 + lane) * rowW[lane] +
-                       (double)ldcg(VW + (size_t)r * 64 + kNb + lane) * rowV[lane];
+            if (r < hi && 4 * sl < i) {
+                const float4 vv = __ldcg(reinterpret_cast<const float4 *>(VW + (size_t)r * 64) + sl);
+                const float4 ww = __ldcg(reinterpret_cast<const float4 *>(VW + (size_t)r * 64 + kNb) + sl);
+                const float v4[4] = {vv.x, vv.y, vv.z, vv.w}, w4[4] = {ww.x, ww.y, ww.z, ww.w};
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) corr += __shfl_xor_sync(0xffffffffu, corr, o);
-            if (lane == 0) {
+                for (int u = 0; u < 4; ++u)
+                    if (4 * sl + u < i) corr += (double)v4[u] * rowW[4 * sl + u] + (double)w4[u] * rowV[4 * sl + u];
+            }
+            corr += __shfl_xor_sync(0xffffffffu, corr, 4);
+            corr += __shfl_xor_sync(0xffffffffu, corr, 2);
+            corr += __shfl_xor_sync(0xffffffffu, corr, 1);
+            if (sl == 0 && r < hi) {
                 const double cv = (double)A[(size_t)r * ldw + k] - corr;   // column k (lower triangle kept)
                 if (r == k) J.d[k] = cv;
                 else __stcg(J.x + r, cv);
@@ -403,19 +411,28 @@ __global__ void __launch_bounds__(kTrdThreads, 1) trd_panel(const __grid_constan
         double wv = 0.0;
         {
             const int nrb = (n - (k + 1) + kSymvR - 1) / kSymvR;
-#pragma unroll 2
-            for (int r = lo + warp; r < hi; r += kTrdWarps) {   // one warp per row
-                const int b = (r - (k + 1)) / kSymvR;
-                const int nj = (min(n, k + 1 + kSymvR * (b + 1)) - 1 - c0) / kSymvC + 1;
+            const int sub = lane >> 3, sl = lane & 7;      // 8 lanes per row, 4 rows per warp
+            for (int r0 = lo + 4 * warp; r0 < hi; r0 += 4 * kTrdWarps) {
+                const int r = r0 + sub;
                 double yr = 0.0;
-                for (int jj = lane; jj < nj; jj += 32) yr += ldcg(J.DP + (size_t)r * J.ldp + jj);
-                for (int bb = b + lane; bb < nrb; bb += 32) yr += ldcg(J.TP + (size_t)r * J.ldtp + bb);
-                if (lane < i)
-                    yr -= (double)ldcg(VW + (size_t)r * 64 + kNb + lane) * ab[lane] +
-                          (double)ldcg(VW + (size_t)r * 64 + lane) * ab[kNb + lane];
+                if (r < hi) {
+                    const int b = (r - (k + 1)) / kSymvR;
+                    const int nj = (min(n, k + 1 + kSymvR * (b + 1)) - 1 - c0) / kSymvC + 1;
+                    for (int jj = sl; jj < nj; jj += 8) yr += ldcg(J.DP + (size_t)r * J.ldp + jj);
+                    for (int bb = b + sl; bb < nrb; bb += 8) yr += ldcg(J.TP + (size_t)r * J.ldtp + bb);
+                    if (4 * sl < i) {
+                        const float4 vv = __ldcg(reinterpret_cast<const float4 *>(VW + (size_t)r * 64) + sl);
+                        const float4 ww = __ldcg(reinterpret_cast<const float4 *>(VW + (size_t)r * 64 + kNb) + sl);
+                        const float v4[4] = {vv.x, vv.y, vv.z, vv.w}, w4[4] = {ww.x, ww.y, ww.z, ww.w};
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) yr += __shfl_xor_sync(0xffffffffu, yr, o);
-                if (lane == 0) {
+                        for (int u = 0; u < 4; ++u)
+                            if (4 * sl + u < i) yr -= (double)w4[u] * ab[4 * sl + u] + (double)v4[u] * ab[kNb + 4 * sl + u];
+                    }
+                }
+                yr += __shfl_xor_sync(0xffffffffu, yr, 4);
+                yr += __shfl_xor_sync(0xffffffffu, yr, 2);
+                yr += __shfl_xor_sync(0xffffffffu, yr, 1);
+                if (sl == 0 && r < hi) {
                     const double w = tau * yr;
                     __stcg(J.y + r, w);
                     wv += w * (double)vsm[r - c0];
@@ -1003,6 +1020,7 @@ int ldw_for(int n) { return (int)round_up((size_t)n, 32); }
 struct Plan {
     std::vector<TrdJob> jobs;
     size_t bytes = 0, table_off = 0, leaf_off = 0, merge_off = 0, bt_off = 0;
+    size_t bar_off = 0;                               // all factors' group-barrier counters (64 B apart)
     std::vector<LeafDesc> leaves;
     std::vector<std::vector<MergeDesc>> merges;       // per level (1..maxL)
     std::vector<std::vector<BtStep>> bt;              // per back-transform step
@@ -1069,7 +1087,6 @@ Plan plan(const int32_t *dims, int count) {
         TAKE(DP, double, (size_t)n * J.ldp);
         J.ldtp = cdiv(n, kSymvR) + 1;
         TAKE(TP, double, (size_t)n * J.ldtp);
-        TAKE(bar, unsigned, 64);
 #undef TAKE
         // leaves and merges
         const int nleaf = 1 << J.levels;
@@ -1098,6 +1115,9 @@ Plan plan(const int32_t *dims, int count) {
             P.bt[s].push_back({i, b0, std::min(kBt, nref - b0)});
         }
     }
+    P.bar_off = take((size_t)count * 64);
+    for (int i = 0; i < count; ++i)
+        P.jobs[i].bar = reinterpret_cast<unsigned *>(P.bar_off + 64 * (size_t)i);   // offset, rebased later
     P.leaf_off = take(P.leaves.size() * sizeof(LeafDesc));
     P.merge_off = take(nmerge_total * sizeof(MergeDesc));
     size_t nbt = 0;
@@ -1248,12 +1268,25 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
             tot += nc[q];
         }
         PL.cta_begin[na] = tot;
-        for (int q = 0; q < na; ++q) {
-            KFAC_CUDA_TRY(cudaMemsetAsync(P.jobs[act[q]].bar, 0, sizeof(unsigned), s));
-        }
+        KFAC_CUDA_TRY(cudaMemsetAsync(base + P.bar_off, 0, (size_t)count * 64, s));   // every counter, one call
         void *args[] = {&PL};
+        const int prof = prof_begin(KFAC_PROF_TRD_PANEL, s);
         KFAC_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)trd_panel, dim3(tot), dim3(kTrdThreads), args, smem, s));
         KFAC_LAUNCHED();
+        if (prof >= 0) {
+            // algorithmic work: per column k, the lower triangle of the m x m trailing matrix
+            // (m = n - k - 1) read once (4 B per element) and 2 m^2 flops of the mat-vec
+            double by = 0.0, fl = 0.0;
+            for (int q = 0; q < na; ++q) {
+                const int n = P.jobs[act[q]].n;
+                for (int k = pst[q]; k < std::min(n - 1, pst[q] + kNb); ++k) {
+                    const double m = n - k - 1;
+                    by += 4.0 * m * (m + 1) / 2;
+                    fl += 2.0 * m * m;
+                }
+            }
+            prof_end(prof, s, by, fl);
+        }
         gd.clear();
         for (int q = 0; q < na; ++q) {
             const TrdJob &J = P.jobs[act[q]];

@@ -11,6 +11,7 @@
 // memory as fp64 (operands converted once when staged), register prefetch of the next slab.
 #include "internal.cuh"
 
+#include <cstdlib>
 #include <vector>
 
 namespace kfac {
@@ -36,10 +37,10 @@ __device__ __forceinline__ double ld_any(const void *p, size_t i, int dt) {
     return dt == DT_F64 ? __ldg(static_cast<const double *>(p) + i) : (double)__ldg(static_cast<const float *>(p) + i);
 }
 
-// Epilogue shared by both kernels.  Thread (ty, tx) owns rows 2 ty + {0,1} + 32 i' and columns
-// 2 tx + {0,1} + 32 j'; acc[i][j] with i = 2 i' + {0,1}, j = 2 j' + {0,1}.
-__device__ __forceinline__ void epilogue(const Gemm64Desc &d, int m0, int n0, int Me, int Ne, int ty, int tx,
-                                         const double (&acc)[8][8]) {
+// Epilogue shared by both kernels: the thread owns rows rows[i] (i < 8) and column pairs
+// (cols[jj], cols[jj] + 1) (jj < 4); acc[i][2 jj + e] is element (rows[i], cols[jj] + e).
+__device__ __forceinline__ void epilogue(const Gemm64Desc &d, int Me, int Ne, const int (&rows)[8],
+                                         const int (&cols)[4], const double (&acc)[8][8]) {
     // Epilogue.  Thread columns come in adjacent pairs (2 tx + {0,1} + 32 jj), so C is accessed as
     // 8- or 16-byte pairs; for C -= AB the 16 pairs of four rows are all loaded before any is
     // used or stored (independent loads in flight instead of one dependent round trip each).
@@ -52,10 +53,10 @@ __device__ __forceinline__ void epilogue(const Gemm64Desc &d, int m0, int n0, in
 #pragma unroll
         for (int ii = 0; ii < 4; ++ii) {
             const int i = 4 * h + ii;
-            const int m = m0 + 2 * ty + (i & 1) + 32 * (i >> 1);
+            const int m = rows[i];
 #pragma unroll
             for (int jj = 0; jj < 4; ++jj) {
-                const int n = n0 + 2 * tx + 32 * jj;
+                const int n = cols[jj];
                 cv[ii][jj][0] = cv[ii][jj][1] = 0.0;
                 if (!sub || m >= Me || n >= Ne) continue;
                 const size_t o = (size_t)m * d.ldc + n;
@@ -83,11 +84,11 @@ __device__ __forceinline__ void epilogue(const Gemm64Desc &d, int m0, int n0, in
 #pragma unroll
         for (int ii = 0; ii < 4; ++ii) {
             const int i = 4 * h + ii;
-            const int m = m0 + 2 * ty + (i & 1) + 32 * (i >> 1);
+            const int m = rows[i];
             if (m >= Me) continue;
 #pragma unroll
             for (int jj = 0; jj < 4; ++jj) {
-                const int n = n0 + 2 * tx + 32 * jj;
+                const int n = cols[jj];
                 if (n >= Ne) continue;
                 const double r0 = sub ? cv[ii][jj][0] - acc[i][2 * jj] : acc[i][2 * jj];
                 const double r1 = sub ? cv[ii][jj][1] - acc[i][2 * jj + 1] : acc[i][2 * jj + 1];
@@ -229,7 +230,161 @@ __global__ void __launch_bounds__(NT, 1) gemm64_kernel(const __grid_constant__ B
         }
     }
 
-    epilogue(d, m0, n0, Me, Ne, ty, tx, acc);
+    int rows[8], cols[4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) rows[i] = m0 + 2 * ty + (i & 1) + 32 * (i >> 1);
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) cols[jj] = n0 + 2 * tx + 32 * jj;
+    epilogue(d, Me, Ne, rows, cols, acc);
+}
+
+
+// ------------------------------------------------------- pipelined DMMA kernel --
+// Same 128 x 128 output tile, K staged 16 at a time: every slab is copied raw (fp32 or fp64, in
+// the operand's own layout) into one of kStages shared-memory stages with cp.async -- kStages-1
+// slabs in flight while one is computed -- then converted once to fp64 tiles T[k][mn] (row
+// stride kTs = 136 doubles, so the 8x4 fragment loads below hit every bank exactly twice).  The
+// products run on the fp64 tensor cores: mma.sync m8n8k4 f64 (DMMA; fp64 products, fp64
+// accumulation -- the same arithmetic as DFMA, at the tensor pipe's rate).  Warp w owns the
+// 64 x 32 block (rows 64 (w / 4), columns 32 (w % 4)) as 8 x 4 DMMA tiles.  Used when every
+// operand's rows are 16-byte aligned.
+constexpr int PBK = 16, kStages = 3, kTs = BM + 8;
+constexpr int kRawBytes = BM * PBK * 8;                           // one operand slab, fp64 worst case
+constexpr int kPipeSmem = kStages * 2 * kRawBytes + 2 * PBK * kTs * 8 + 64;
+
+// Raw slab of one operand: "outer" rows of "inner" contiguous elements.  MN-contiguous operands
+// (A^T stored k x m, B stored k x n) have outer = k, inner = mn; K-contiguous ones the reverse.
+struct RawOp {
+    const char *base;     // element (0, 0) of the operand
+    size_t ld_bytes;      // bytes between outer rows
+    int es;               // element size
+    int mn_inner;         // 1: inner = mn (128 wide), outer = k (16); 0: inner = k, outer = mn
+    int mn0, mn_lim, k_lim;
+};
+
+__device__ __forceinline__ void issue_raw(const RawOp &o, uint32_t dst, int k0, int t) {
+    const int inner = o.mn_inner ? BM : PBK, outer = o.mn_inner ? PBK : BM;
+    const int epc = 16 / o.es;                         // elements per 16-byte chunk
+    const int cpr = inner / epc;                       // chunks per outer row
+    const int nchunk = outer * cpr;
+    for (int c = t; c < nchunk; c += NT) {
+        const int r = c / cpr, i0 = (c - r * cpr) * epc;
+        const int og = o.mn_inner ? k0 + r : o.mn0 + r;          // global outer index
+        const int ig = o.mn_inner ? o.mn0 + i0 : k0 + i0;        // global inner index
+        const int olim = o.mn_inner ? o.k_lim : o.mn_lim, ilim = o.mn_inner ? o.mn_lim : o.k_lim;
+        int valid = (og < olim) ? min(epc, ilim - ig) : 0;
+        valid = max(valid, 0);
+        const char *src = valid ? o.base + (size_t)og * o.ld_bytes + (size_t)ig * o.es : o.base;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst + (uint32_t)(r * inner + i0) * o.es),
+                     "l"(src), "r"((uint32_t)(valid * o.es))
+                     : "memory");
+    }
+}
+
+// raw slab -> fp64 tile T[k][mn] (row stride kTs)
+__device__ __forceinline__ void convert_raw(const RawOp &o, const char *raw, double *T, int t) {
+    for (int e = t; e < BM * PBK; e += NT) {
+        int k, mn;
+        if (o.mn_inner) { k = e / BM; mn = e % BM; }
+        else            { mn = e / PBK; k = e % PBK; }
+        const double v = o.es == 8 ? reinterpret_cast<const double *>(raw)[e]
+                                   : (double)reinterpret_cast<const float *>(raw)[e];
+        T[k * kTs + mn] = v;
+    }
+}
+
+__device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(NT, 1) gemm64_pipe_kernel(const __grid_constant__ Batch64 batch) {
+    // dynamic shared memory is 16-byte aligned; keep every pointer derived from the __shared__
+    // symbol so the compiler emits LDS/STS (a uintptr round trip would make them generic loads)
+    extern __shared__ __align__(16) double smem_d[];
+    const int tile = blockIdx.x;
+    const Gemm64Desc &d = batch.d[find_desc(batch, tile)];
+    const int local = tile - d.tile_begin;
+    const int tiles_n = (d.N + BN - 1) / BN;
+    const int m0 = (local / tiles_n) * BM, n0 = (local % tiles_n) * BN;
+    const int Me = d.M, Ne = d.dyn ? min(d.N, d.dyn[0]) : d.N, Ke = d.dyn ? min(d.K, d.dyn[1]) : d.K;
+    if (n0 >= Ne) return;
+    if (d.lower && n0 >= m0 + BM) return;            // block strictly above the diagonal
+    const int t = threadIdx.x, warp = t / 32, lane = t % 32;
+    char *raw = reinterpret_cast<char *>(smem_d);
+    double *As = smem_d + kStages * 2 * kRawBytes / 8;
+    double *Bs = As + PBK * kTs;
+    const uint32_t raw_s = (uint32_t)__cvta_generic_to_shared(raw);
+
+    RawOp oa, ob;
+    oa.base = static_cast<const char *>(d.A); oa.es = d.ta == DT_F64 ? 8 : 4;
+    oa.ld_bytes = (size_t)d.lda * oa.es; oa.mn_inner = d.trans_a; oa.mn0 = m0; oa.mn_lim = Me; oa.k_lim = Ke;
+    ob.base = static_cast<const char *>(d.B); ob.es = d.tb == DT_F64 ? 8 : 4;
+    ob.ld_bytes = (size_t)d.ldb * ob.es; ob.mn_inner = !d.trans_b; ob.mn0 = n0; ob.mn_lim = Ne; ob.k_lim = Ke;
+
+    double acc[8][8];                          // [mi][2 ni + e]
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
+    const int wm = (warp >> 2) * 64, wn = (warp & 3) * 32, g = lane >> 2, q = lane & 3;
+    const int nk = (Ke + PBK - 1) / PBK;
+    auto issue = [&](int kt) {
+        if (kt < nk) {
+            const uint32_t st = raw_s + (uint32_t)((kt % kStages) * 2 * kRawBytes);
+            issue_raw(oa, st, kt * PBK, t);
+            issue_raw(ob, st + kRawBytes, kt * PBK, t);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+#pragma unroll
+    for (int s = 0; s < kStages - 1; ++s) issue(s);
+    for (int kt = 0; kt < nk; ++kt) {
+        asm volatile("cp.async.wait_group %0;" ::"n"(kStages - 2) : "memory");
+        __syncthreads();                        // slab kt landed everywhere; previous compute done
+        const char *st = raw + (kt % kStages) * 2 * kRawBytes;
+        convert_raw(oa, st, As, t);
+        convert_raw(ob, st + kRawBytes, Bs, t);
+        __syncthreads();
+        issue(kt + kStages - 1);                // into the stage converted in iteration kt - 1
+#pragma unroll
+        for (int kk = 0; kk < PBK; kk += 4) {
+            // A fragment (8 x 4, row-major): element (g, q); B fragment (4 x 8, col): element (q, g)
+            double a[8], b[4];
+#pragma unroll
+            for (int mi = 0; mi < 8; ++mi) a[mi] = As[(kk + q) * kTs + wm + mi * 8 + g];
+#pragma unroll
+            for (int ni = 0; ni < 4; ++ni) b[ni] = Bs[(kk + q) * kTs + wn + ni * 8 + g];
+#pragma unroll
+            for (int mi = 0; mi < 8; ++mi)
+#pragma unroll
+                for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][2 * ni], acc[mi][2 * ni + 1], a[mi], b[ni]);
+        }
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    // accumulator (mi, ni): rows wm + 8 mi + g, columns wn + 8 ni + 2 q + {0, 1}
+    int rows[8], cols[4];
+#pragma unroll
+    for (int mi = 0; mi < 8; ++mi) rows[mi] = m0 + wm + mi * 8 + g;
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) cols[ni] = n0 + wn + ni * 8 + 2 * q;
+    epilogue(d, Me, Ne, rows, cols, acc);
+}
+
+bool g_pipe_disabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("KFAC_GEMM64_NOPIPE");
+        v = (e && e[0] == '1') ? 1 : 0;
+    }
+    return v == 1;
+}
+
+bool pipe_ok(const Gemm64Desc &g) {
+    const int ea = g.ta == DT_F64 ? 8 : 4, eb = g.tb == DT_F64 ? 8 : 4;
+    return (reinterpret_cast<uintptr_t>(g.A) % 16 == 0) && (reinterpret_cast<uintptr_t>(g.B) % 16 == 0) &&
+           ((size_t)g.lda * ea) % 16 == 0 && ((size_t)g.ldb * eb) % 16 == 0;
 }
 
 }  // namespace
@@ -248,8 +403,32 @@ kfac_status_t gemm64_grouped(const Gemm64Desc *descs, int count, cudaStream_t s)
             ++b.count;
         }
         if (b.count == 0) continue;
-        gemm64_kernel<<<tiles, NT, 0, s>>>(b);
+        const int prof = prof_begin(KFAC_PROF_GEMM64, s);
+        bool pipe = !g_pipe_disabled();
+        for (int i = 0; i < b.count && pipe; ++i) pipe = pipe_ok(b.d[i]);
+        if (pipe) {
+            static bool attr = false;
+            if (!attr) {
+                KFAC_CUDA_TRY(cudaFuncSetAttribute(gemm64_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   kPipeSmem));
+                attr = true;
+            }
+            gemm64_pipe_kernel<<<tiles, NT, kPipeSmem, s>>>(b);
+        } else {
+            gemm64_kernel<<<tiles, NT, 0, s>>>(b);
+        }
         KFAC_LAUNCHED();
+        if (prof >= 0) {
+            double by = 0.0, fl = 0.0;
+            for (int i = 0; i < b.count; ++i) {
+                const Gemm64Desc &g = b.d[i];
+                const double ea = g.ta == DT_F64 ? 8 : 4, eb = g.tb == DT_F64 ? 8 : 4, ec = g.tc == DT_F64 ? 8 : 4;
+                const double mn = g.lower ? 0.5 * g.M * (g.N + 1.0) : (double)g.M * g.N;
+                fl += 2.0 * mn * g.K;
+                by += (double)g.M * g.K * ea + (double)g.N * g.K * eb + mn * ec * (g.epi == EPI_SUB ? 2 : 1);
+            }
+            prof_end(prof, s, by, fl);
+        }
     }
     return KFAC_OK;
 }

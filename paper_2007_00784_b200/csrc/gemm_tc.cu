@@ -162,13 +162,17 @@ struct Smem {
     uint8_t *base;       // kRaw raw stages, then kLo lo stages (each A tile + B tile)
     uint32_t raw_full, ready, raw_empty, lo_empty, tfull, tempty;   // barrier arrays (8 B stride)
     uint32_t *tmem_slot;
+    int2 *rowtab;        // SYRK producer: per warp 8 (origin offset, packed ih0/iw0) row descriptors
     __device__ __forceinline__ uint8_t *raw(int s) const { return base + s * kStageBytes; }
     __device__ __forceinline__ uint8_t *lo(int l) const { return base + (kRaw + l) * kStageBytes; }
 };
 
 __device__ __forceinline__ Smem carve(uint8_t *smem_raw) {
     Smem s;
-    s.base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // align by an integer offset on the __shared__ array itself (a uintptr round trip would turn
+    // every later access into a generic LD/ST instead of LDS/STS)
+    const uint32_t a0 = smem_u32(smem_raw);
+    s.base = smem_raw + (((a0 + 1023u) & ~1023u) - a0);
     uint64_t *bars = reinterpret_cast<uint64_t *>(s.base + (kRaw + kLo) * kStageBytes);
     s.raw_full = smem_u32(bars);
     s.ready = smem_u32(bars + kRaw);
@@ -177,6 +181,7 @@ __device__ __forceinline__ Smem carve(uint8_t *smem_raw) {
     s.tfull = smem_u32(bars + 3 * kRaw + kLo);
     s.tempty = smem_u32(bars + 3 * kRaw + kLo + 2);
     s.tmem_slot = reinterpret_cast<uint32_t *>(bars + 3 * kRaw + kLo + 4);
+    s.rowtab = reinterpret_cast<int2 *>(bars + 32);      // bytes 256..511 of the barrier area
     return s;
 }
 
@@ -434,8 +439,9 @@ struct SyrkGeom {
 // Producer warps 0-3: cp.async gathers of the 32-row k-block into raw stage s; the stage's
 // mbarrier completes when every producer thread's copies have landed.  Warp w fills rows
 // w + 4j (j < 8).  The row -> (image, output pixel) decomposition is done once per row by lanes
-// 0-7 in parallel and broadcast with shuffles (the integer divisions were the producer's
-// instruction-issue bottleneck); per (row, operand) only a bounds test and an add remain.
+// 0-7 in parallel and broadcast through a per-warp shared-memory table (the integer divisions
+// were the producer's instruction-issue bottleneck); per (row, operand) only a bounds test and
+// an add remain.
 __device__ __forceinline__ void syrk_issue(const SyrkGeom &G, const Smem &S, int s, long long r0, long long r_end,
                                            const ChunkInfo (&ci)[2], int cc, int t, bool diag) {
     const uint32_t st = smem_u32(S.raw(s));
@@ -460,11 +466,15 @@ __device__ __forceinline__ void syrk_issue(const SyrkGeom &G, const Smem &S, int
             ihw = rv ? 0 : (int)0x80000000;
         }
     }
+    int2 *tab = S.rowtab + warp * 8;
+    __syncwarp();                                     // previous k-block's reads are done
+    if (lane < 8) tab[lane] = make_int2(org, ihw);
+    __syncwarp();
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
         const int k = warp + 4 * j;
-        const int o = __shfl_sync(0xffffffffu, org, j);
-        const int hv = __shfl_sync(0xffffffffu, ihw, j);
+        const int2 rd = tab[j];
+        const int o = rd.x, hv = rd.y;
         const bool rv = hv != (int)0x80000000;
         const int ih0 = hv >> 16, iw0 = (int)(short)(hv & 0xffff);
 #pragma unroll
@@ -643,8 +653,18 @@ kfac_status_t gemm_tc_grouped(const GemmDesc *descs, int count, float damping, c
             ++b.count;
         }
         if (!b.count) continue;
+        const int prof = prof_begin(KFAC_PROF_GEMM_TC, s);
         gemm_tc_kernel<<<tiles, NT, kSmemBytes, s>>>(b);
         KFAC_LAUNCHED();
+        if (prof >= 0) {
+            double by = 0.0, fl = 0.0;
+            for (int i = 0; i < b.count; ++i) {
+                const TcDesc &g = b.d[i];
+                fl += 2.0 * g.M * g.N * g.K;
+                by += 4.0 * ((double)g.M * g.K + (double)g.K * g.N + (double)g.M * g.N);
+            }
+            prof_end(prof, s, by, fl);
+        }
     }
     return KFAC_OK;
 }
@@ -678,8 +698,22 @@ kfac_status_t syrk_tc_partial(const FactorJob *jobs, int count, cudaStream_t s) 
             items += j.tiles * j.splits;
             b.j[b.count++] = j;
         }
+        const int prof = prof_begin(KFAC_PROF_SYRK_TC, s);
         syrk_tc_kernel<<<items, NT, kSmemBytes, s>>>(b);
         KFAC_LAUNCHED();
+        if (prof >= 0) {
+            // algorithmic work of the factors in this launch: n d (d + 1) flops (upper triangle incl.
+            // diagonal); bytes: the input tensor read once + the fp32 partial tiles
+            double by = 0.0, fl = 0.0;
+            for (int i = 0; i < b.count; ++i) {
+                const FactorJob &j = b.j[i];
+                fl += (double)j.n * j.d * (j.d + 1.0);
+                const double in = j.is_a ? (double)(j.n / ((long long)j.h_out * j.w_out)) * j.h_in * j.w_in * j.c_in
+                                         : (double)j.n * j.c_in;
+                by += 4.0 * in + 4.0 * (double)j.splits * j.tiles * BM * BN;
+            }
+            prof_end(prof, s, by, fl);
+        }
     }
     return KFAC_OK;
 }

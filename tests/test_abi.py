@@ -96,3 +96,12 @@ def test_call_validation_before_launch(L):
     assert lib.kfac_status_string(st) == b"KFAC_ERR_INVALID_VALUE"             # unknown mode
     assert L.kfac_launch_count() == n0
     assert lib.kfac_last_error()
+
+
+def test_profile_hook_host_side(L):
+    """Instrumentation entry points: argument validation and an empty (no launch) window."""
+    assert L.lib.kfac_profile_start(0) != 0
+    assert L.lib.kfac_profile_start(99) != 0
+    L.kfac_profile_start(L.PROF_TRD_PANEL)
+    ms, n, by, fl = L.kfac_profile_stop()
+    assert (ms, n, by, fl) == (0.0, 0, 0.0, 0.0)

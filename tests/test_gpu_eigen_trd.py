@@ -72,18 +72,31 @@ def test_gemm_sub_epilogue(lib, engine, M, N, K):
 @pytest.mark.parametrize("dts", [(0, 0, 0), (0, 1, 1), (1, 1, 1), (1, 0, 0)])
 @pytest.mark.parametrize("ta,tb", [(0, 0), (1, 0), (0, 1), (1, 1)])
 @pytest.mark.parametrize("epi", [0, 3])
-def test_gemm64(lib, dts, ta, tb, epi):
+@pytest.mark.parametrize("padded", [False, True])
+def test_gemm64(lib, dts, ta, tb, epi, padded):
     """fp64-accumulating SIMT GEMM of the eigensolver: fp64 products of the (fp32 or fp64)
-    operands, one rounding to the output type -> relF <= 1e-14 (fp64 out) / 2^-24 (fp32 out)."""
+    operands, one rounding to the output type -> relF <= 1e-14 (fp64 out) / 2^-24 (fp32 out).
+    padded: leading dimensions rounded up to 16 bytes, which selects the cp.async pipelined
+    kernel (K = 77 leaves a ragged last slab and a partial 16-byte chunk)."""
     M, N, K = 150, 131, 77
     rng = np.random.default_rng(ta * 2 + tb + 10 * epi)
     dt = lambda c: torch.float64 if c else torch.float32
+
+    def dev(x, code):
+        t = torch.from_numpy(x).to(dt(code))
+        if not padded:
+            return t.cuda()
+        ld = (x.shape[1] + 3) // 4 * 4
+        buf = torch.zeros((x.shape[0], ld), dtype=dt(code), device="cuda")
+        buf[:, :x.shape[1]] = t.cuda()
+        return buf[:, :x.shape[1]]
+
     A = rng.standard_normal((K, M) if ta else (M, K))
     B = rng.standard_normal((N, K) if tb else (K, N))
     C0 = rng.standard_normal((M, N))
-    a = torch.from_numpy(A).to(dt(dts[0])).cuda()
-    b = torch.from_numpy(B).to(dt(dts[1])).cuda()
-    c = torch.from_numpy(C0).to(dt(dts[2])).cuda()
+    a = dev(A, dts[0])
+    b = dev(B, dts[1])
+    c = dev(C0, dts[2])
     st = lib.lib.kfac_debug_gemm64(a.data_ptr(), dts[0], a.stride(0), ta, b.data_ptr(), dts[1], b.stride(0), tb,
                                    c.data_ptr(), dts[2], c.stride(0), M, N, K, epi, None)
     assert st == 0
