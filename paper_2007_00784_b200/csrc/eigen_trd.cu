@@ -49,6 +49,7 @@ constexpr int kMaxGroupCtas = 512;
 constexpr int kLeaf = 32;               // D&C leaf size
 constexpr int kSymvR = 64;              // symv tile rows (lower triangle only)
 constexpr int kSymvC = 128;             // symv tile columns (one float4 per lane)
+constexpr int kMaxRb = 256;             // symv row blocks: n <= 16384 = 256 x 64
 constexpr int kBt = 512;                // reflectors per back-transformation block
 constexpr int kTs = 128;                // dlarft sub-block (T built recursively from 128-blocks)
 constexpr double kEps = 1.1102230246251565e-16;   // 2^-53, LAPACK dlamch('E')
@@ -179,6 +180,7 @@ __global__ void __launch_bounds__(kTrdThreads, 1) trd_panel(const __grid_constan
     __shared__ double ab[2 * kNb];                   // (V^T v, W^T v)
     __shared__ float rowV[kNb], rowW[kNb];           // V[k, <i], W[k, <i]
     __shared__ double scal[4];
+    __shared__ int tpre[kMaxRb + 1];                 // symv tile prefix per row block
 
     int g = 0;
     {
@@ -270,6 +272,31 @@ __global__ void __launch_bounds__(kTrdThreads, 1) trd_panel(const __grid_constan
             else if (col > k + 1 && col < n) v = (float)(ldcg(J.x + col) * scale);
             vsm[j] = v;
         }
+        if (warp == 0) {
+            // tile prefix of the symv: tpre[b] = number of 64 x 128 lower-triangle tiles in row
+            // blocks < b (block b spans chunks c0 .. its last row), for the warps' tile cursors
+            const int r00 = k + 1, nrb = (n - r00 + kSymvR - 1) / kSymvR;
+            int loc[kMaxRb / 32], run = 0;
+#pragma unroll
+            for (int u = 0; u < kMaxRb / 32; ++u) {
+                const int b = lane * (kMaxRb / 32) + u;
+                run += b < nrb ? (min(n, r00 + kSymvR * (b + 1)) - 1 - c0) / kSymvC + 1 : 0;
+                loc[u] = run;
+            }
+            int incl = run;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            const int excl = incl - run;
+#pragma unroll
+            for (int u = 0; u < kMaxRb / 32; ++u) {
+                const int b = lane * (kMaxRb / 32) + u;
+                if (b < nrb) tpre[b + 1] = excl + loc[u];
+            }
+            if (lane == 0) tpre[0] = 0;
+        }
         __syncthreads();
         part_range(k + 1, n, c, nc, lo, hi);
         for (int r = lo + t; r < hi; r += kTrdThreads) {
@@ -296,16 +323,20 @@ __global__ void __launch_bounds__(kTrdThreads, 1) trd_panel(const __grid_constan
         // octet q is reduced.
         {
             const int r00 = k + 1, nrb = (n - r00 + kSymvR - 1) / kSymvR;
-            auto cnt = [&](int b) { return (min(n, r00 + kSymvR * (b + 1)) - 1 - c0) / kSymvC + 1; };
-            int total = 0;
-            for (int b = 0; b < nrb; ++b) total += cnt(b);
+            const int total = tpre[nrb];
             const int W = nc * kTrdWarps;
             const float4 *v4 = reinterpret_cast<const float4 *>(vsm);
             float4 *ring = reinterpret_cast<float4 *>(vsm + ring_off) + (size_t)warp * (2 * 8 * 32) + lane;
             // octet cursor: tile it (row block bq, chunk jq), first row rq
             int it = c * kTrdWarps + warp, bq = 0, base = 0, jq = 0, rq = 0;
-            auto locate = [&]() {
-                while (bq < nrb && it >= base + cnt(bq)) { base += cnt(bq); ++bq; }
+            auto locate = [&]() {                    // last row block with tpre[bq] <= it
+                int lo2 = bq, hi2 = nrb - 1;
+                while (lo2 < hi2) {
+                    const int mid = (lo2 + hi2 + 1) >> 1;
+                    if (tpre[mid] <= it) lo2 = mid; else hi2 = mid - 1;
+                }
+                bq = lo2;
+                base = tpre[bq];
                 jq = it - base;
                 rq = r00 + kSymvR * bq;
             };
@@ -403,9 +434,15 @@ __global__ void __launch_bounds__(kTrdThreads, 1) trd_panel(const __grid_constan
         }
         group_barrier(J.bar, target, nc);
         // ---------------- phase C ----------------
-        for (int col = warp; col < 2 * kNb; col += kTrdWarps) {
-            const double sum = (col % kNb) < i ? warp_part_sum(part, col, nc, lane) : 0.0;
-            if (lane == 0) ab[col] = sum;
+        {   // (V^T v, W^T v): 8 consecutive threads per panel column sum the group's CTA partials
+            const int col = t >> 3, sub = t & 7;           // 64 columns x 8 = 512 threads
+            double sum = 0.0;
+            if ((col % kNb) < i)
+                for (int q = sub; q < nc; q += 8) sum += ldcg(part + (size_t)q * kPart + col);
+            sum += __shfl_xor_sync(0xffffffffu, sum, 4);
+            sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+            sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+            if (sub == 0) ab[col] = sum;
         }
         __syncthreads();
         double wv = 0.0;

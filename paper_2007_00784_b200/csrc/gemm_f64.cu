@@ -248,9 +248,11 @@ __global__ void __launch_bounds__(NT, 1) gemm64_kernel(const __grid_constant__ B
 // accumulation -- the same arithmetic as DFMA, at the tensor pipe's rate).  Warp w owns the
 // 64 x 32 block (rows 64 (w / 4), columns 32 (w % 4)) as 8 x 4 DMMA tiles.  Used when every
 // operand's rows are 16-byte aligned.
-constexpr int PBK = 16, kStages = 3, kTs = BM + 8;
-constexpr int kRawBytes = BM * PBK * 8;                           // one operand slab, fp64 worst case
-constexpr int kPipeSmem = kStages * 2 * kRawBytes + 2 * PBK * kTs * 8 + 64;
+constexpr int PBK = 16, kStages = 3, kPM = 64;                 // pipelined tile: kPM x BN
+constexpr int kPT = kPM * 2;                                      // 4 warps, each 64 x 32
+constexpr int kTsA = kPM + 8, kTsB = BN + 8;                      // fp64 tile row strides
+constexpr int kRawA = kPM * PBK * 8, kRawB = BN * PBK * 8;        // raw slabs, fp64 worst case
+constexpr int kPipeSmem = kStages * (kRawA + kRawB) + PBK * (kTsA + kTsB) * 8 + 64;
 
 // Raw slab of one operand: "outer" rows of "inner" contiguous elements.  MN-contiguous operands
 // (A^T stored k x m, B stored k x n) have outer = k, inner = mn; K-contiguous ones the reverse.
@@ -258,16 +260,17 @@ struct RawOp {
     const char *base;     // element (0, 0) of the operand
     size_t ld_bytes;      // bytes between outer rows
     int es;               // element size
-    int mn_inner;         // 1: inner = mn (128 wide), outer = k (16); 0: inner = k, outer = mn
+    int mn_inner;         // 1: inner = mn (ext wide), outer = k (16); 0: inner = k, outer = mn
+    int ext;              // mn extent of the tile (kPM for A, BN for B)
     int mn0, mn_lim, k_lim;
 };
 
 __device__ __forceinline__ void issue_raw(const RawOp &o, uint32_t dst, int k0, int t) {
-    const int inner = o.mn_inner ? BM : PBK, outer = o.mn_inner ? PBK : BM;
+    const int inner = o.mn_inner ? o.ext : PBK, outer = o.mn_inner ? PBK : o.ext;
     const int epc = 16 / o.es;                         // elements per 16-byte chunk
     const int cpr = inner / epc;                       // chunks per outer row
     const int nchunk = outer * cpr;
-    for (int c = t; c < nchunk; c += NT) {
+    for (int c = t; c < nchunk; c += kPT) {
         const int r = c / cpr, i0 = (c - r * cpr) * epc;
         const int og = o.mn_inner ? k0 + r : o.mn0 + r;          // global outer index
         const int ig = o.mn_inner ? o.mn0 + i0 : k0 + i0;        // global inner index
@@ -281,15 +284,15 @@ __device__ __forceinline__ void issue_raw(const RawOp &o, uint32_t dst, int k0, 
     }
 }
 
-// raw slab -> fp64 tile T[k][mn] (row stride kTs)
-__device__ __forceinline__ void convert_raw(const RawOp &o, const char *raw, double *T, int t) {
-    for (int e = t; e < BM * PBK; e += NT) {
+// raw slab -> fp64 tile T[k][mn] (row stride ts)
+__device__ __forceinline__ void convert_raw(const RawOp &o, const char *raw, double *T, int ts, int t) {
+    for (int e = t; e < o.ext * PBK; e += kPT) {
         int k, mn;
-        if (o.mn_inner) { k = e / BM; mn = e % BM; }
+        if (o.mn_inner) { k = e / o.ext; mn = e - k * o.ext; }
         else            { mn = e / PBK; k = e % PBK; }
         const double v = o.es == 8 ? reinterpret_cast<const double *>(raw)[e]
                                    : (double)reinterpret_cast<const float *>(raw)[e];
-        T[k * kTs + mn] = v;
+        T[k * ts + mn] = v;
     }
 }
 
@@ -299,7 +302,9 @@ __device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b)
                  : "d"(a), "d"(b));
 }
 
-__global__ void __launch_bounds__(NT, 1) gemm64_pipe_kernel(const __grid_constant__ Batch64 batch) {
+// kPM x BN output tile, 4 warps (warp w: columns 32 w .. 32 w + 31, all kPM rows), so two CTAs
+// share an SM and one's staging/barriers overlap the other's tensor-core work.
+__global__ void __launch_bounds__(kPT, 2) gemm64_pipe_kernel(const __grid_constant__ Batch64 batch) {
     // dynamic shared memory is 16-byte aligned; keep every pointer derived from the __shared__
     // symbol so the compiler emits LDS/STS (a uintptr round trip would make them generic loads)
     extern __shared__ __align__(16) double smem_d[];
@@ -307,20 +312,20 @@ __global__ void __launch_bounds__(NT, 1) gemm64_pipe_kernel(const __grid_constan
     const Gemm64Desc &d = batch.d[find_desc(batch, tile)];
     const int local = tile - d.tile_begin;
     const int tiles_n = (d.N + BN - 1) / BN;
-    const int m0 = (local / tiles_n) * BM, n0 = (local % tiles_n) * BN;
+    const int m0 = (local / tiles_n) * kPM, n0 = (local % tiles_n) * BN;
     const int Me = d.M, Ne = d.dyn ? min(d.N, d.dyn[0]) : d.N, Ke = d.dyn ? min(d.K, d.dyn[1]) : d.K;
     if (n0 >= Ne) return;
-    if (d.lower && n0 >= m0 + BM) return;            // block strictly above the diagonal
+    if (d.lower && n0 >= m0 + kPM) return;           // block strictly above the diagonal
     const int t = threadIdx.x, warp = t / 32, lane = t % 32;
     char *raw = reinterpret_cast<char *>(smem_d);
-    double *As = smem_d + kStages * 2 * kRawBytes / 8;
-    double *Bs = As + PBK * kTs;
+    double *As = smem_d + kStages * (kRawA + kRawB) / 8;
+    double *Bs = As + PBK * kTsA;
     const uint32_t raw_s = (uint32_t)__cvta_generic_to_shared(raw);
 
     RawOp oa, ob;
-    oa.base = static_cast<const char *>(d.A); oa.es = d.ta == DT_F64 ? 8 : 4;
+    oa.base = static_cast<const char *>(d.A); oa.es = d.ta == DT_F64 ? 8 : 4; oa.ext = kPM;
     oa.ld_bytes = (size_t)d.lda * oa.es; oa.mn_inner = d.trans_a; oa.mn0 = m0; oa.mn_lim = Me; oa.k_lim = Ke;
-    ob.base = static_cast<const char *>(d.B); ob.es = d.tb == DT_F64 ? 8 : 4;
+    ob.base = static_cast<const char *>(d.B); ob.es = d.tb == DT_F64 ? 8 : 4; ob.ext = BN;
     ob.ld_bytes = (size_t)d.ldb * ob.es; ob.mn_inner = !d.trans_b; ob.mn0 = n0; ob.mn_lim = Ne; ob.k_lim = Ke;
 
     double acc[8][8];                          // [mi][2 ni + e]
@@ -328,13 +333,13 @@ __global__ void __launch_bounds__(NT, 1) gemm64_pipe_kernel(const __grid_constan
     for (int i = 0; i < 8; ++i)
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
-    const int wm = (warp >> 2) * 64, wn = (warp & 3) * 32, g = lane >> 2, q = lane & 3;
+    const int wn = warp * 32, g = lane >> 2, q = lane & 3;
     const int nk = (Ke + PBK - 1) / PBK;
     auto issue = [&](int kt) {
         if (kt < nk) {
-            const uint32_t st = raw_s + (uint32_t)((kt % kStages) * 2 * kRawBytes);
+            const uint32_t st = raw_s + (uint32_t)((kt % kStages) * (kRawA + kRawB));
             issue_raw(oa, st, kt * PBK, t);
-            issue_raw(ob, st + kRawBytes, kt * PBK, t);
+            issue_raw(ob, st + kRawA, kt * PBK, t);
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
@@ -343,9 +348,9 @@ __global__ void __launch_bounds__(NT, 1) gemm64_pipe_kernel(const __grid_constan
     for (int kt = 0; kt < nk; ++kt) {
         asm volatile("cp.async.wait_group %0;" ::"n"(kStages - 2) : "memory");
         __syncthreads();                        // slab kt landed everywhere; previous compute done
-        const char *st = raw + (kt % kStages) * 2 * kRawBytes;
-        convert_raw(oa, st, As, t);
-        convert_raw(ob, st + kRawBytes, Bs, t);
+        const char *st = raw + (kt % kStages) * (kRawA + kRawB);
+        convert_raw(oa, st, As, kTsA, t);
+        convert_raw(ob, st + kRawA, Bs, kTsB, t);
         __syncthreads();
         issue(kt + kStages - 1);                // into the stage converted in iteration kt - 1
 #pragma unroll
@@ -353,9 +358,9 @@ __global__ void __launch_bounds__(NT, 1) gemm64_pipe_kernel(const __grid_constan
             // A fragment (8 x 4, row-major): element (g, q); B fragment (4 x 8, col): element (q, g)
             double a[8], b[4];
 #pragma unroll
-            for (int mi = 0; mi < 8; ++mi) a[mi] = As[(kk + q) * kTs + wm + mi * 8 + g];
+            for (int mi = 0; mi < 8; ++mi) a[mi] = As[(kk + q) * kTsA + mi * 8 + g];
 #pragma unroll
-            for (int ni = 0; ni < 4; ++ni) b[ni] = Bs[(kk + q) * kTs + wn + ni * 8 + g];
+            for (int ni = 0; ni < 4; ++ni) b[ni] = Bs[(kk + q) * kTsB + wn + ni * 8 + g];
 #pragma unroll
             for (int mi = 0; mi < 8; ++mi)
 #pragma unroll
@@ -363,10 +368,10 @@ __global__ void __launch_bounds__(NT, 1) gemm64_pipe_kernel(const __grid_constan
         }
     }
     asm volatile("cp.async.wait_group 0;" ::: "memory");
-    // accumulator (mi, ni): rows wm + 8 mi + g, columns wn + 8 ni + 2 q + {0, 1}
+    // accumulator (mi, ni): rows 8 mi + g, columns wn + 8 ni + 2 q + {0, 1}
     int rows[8], cols[4];
 #pragma unroll
-    for (int mi = 0; mi < 8; ++mi) rows[mi] = m0 + wm + mi * 8 + g;
+    for (int mi = 0; mi < 8; ++mi) rows[mi] = m0 + mi * 8 + g;
 #pragma unroll
     for (int ni = 0; ni < 4; ++ni) cols[ni] = n0 + wn + ni * 8 + 2 * q;
     epilogue(d, Me, Ne, rows, cols, acc);
@@ -390,22 +395,25 @@ bool pipe_ok(const Gemm64Desc &g) {
 }  // namespace
 
 kfac_status_t gemm64_grouped(const Gemm64Desc *descs, int count, cudaStream_t s) {
-    for (int base = 0; base < count; base += kGemm64MaxDescs) {
+    for (int base = 0, end = 0; base < count; base = end) {
         static Batch64 b;       // host staging; parameters are copied at launch
         b.count = 0;
-        int tiles = 0;
-        for (int i = base; i < count && b.count < kGemm64MaxDescs; ++i) {
+        end = base;
+        bool pipe = !g_pipe_disabled();
+        for (int i = base; i < count && b.count < kGemm64MaxDescs; ++i, ++end) {
             const Gemm64Desc &g = descs[i];
             if (g.M <= 0 || g.N <= 0) continue;
-            b.d[b.count] = g;
-            b.d[b.count].tile_begin = tiles;
-            tiles += cdiv(g.M, BM) * cdiv(g.N, BN);
-            ++b.count;
+            b.d[b.count++] = g;
+            pipe = pipe && pipe_ok(g);
         }
         if (b.count == 0) continue;
+        const int tm = pipe ? kPM : BM;
+        int tiles = 0;
+        for (int i = 0; i < b.count; ++i) {
+            b.d[i].tile_begin = tiles;
+            tiles += cdiv(b.d[i].M, tm) * cdiv(b.d[i].N, BN);
+        }
         const int prof = prof_begin(KFAC_PROF_GEMM64, s);
-        bool pipe = !g_pipe_disabled();
-        for (int i = 0; i < b.count && pipe; ++i) pipe = pipe_ok(b.d[i]);
         if (pipe) {
             static bool attr = false;
             if (!attr) {
@@ -413,7 +421,7 @@ kfac_status_t gemm64_grouped(const Gemm64Desc *descs, int count, cudaStream_t s)
                                                    kPipeSmem));
                 attr = true;
             }
-            gemm64_pipe_kernel<<<tiles, NT, kPipeSmem, s>>>(b);
+            gemm64_pipe_kernel<<<tiles, kPT, kPipeSmem, s>>>(b);
         } else {
             gemm64_kernel<<<tiles, NT, 0, s>>>(b);
         }
