@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(kTrdThreads, 1) trd_panel(const __grid_constan
     __shared__ double red[kTrdWarps][2 * kNb];
     __shared__ double ab[2 * kNb];                   // (V^T v, W^T v)
     __shared__ float rowV[kNb], rowW[kNb];           // V[k, <i], W[k, <i]
-    __shared__ double scal[4];
+    __shared__ double scal[8];
     __shared__ int tpre[kMaxRb + 1];                 // symv tile prefix per row block
 
     int g = 0;
@@ -201,17 +201,25 @@ __global__ void __launch_bounds__(kTrdThreads, 1) trd_panel(const __grid_constan
     const int ring_off = L.ring_off;                 // floats: symv prefetch ring after v
     unsigned target = 0;
     float w_next = 0.f;                              // W[k, i-1], computed redundantly
+    // Column k's phase A (its corrected column and diagonal) is folded into column k-1's phase C
+    // whenever both lie in the same panel: there every row's c_r = f_r - v_r beta with f_r known
+    // before the barrier and beta = w_k + 2 alpha after it (see phase C); ||x||^2 is then summed
+    // by every CTA from the full x in phase B.  Columns 1..31 of a panel need two group barriers
+    // instead of three.
+    bool merged = false;
+    double m_beta = 0.0;                             // beta of the merged column
 
     for (int i = 0; i < kNb; ++i) {
         const int k = p0 + i;
         if (k >= n) break;
+        int lo, hi;
         // ---------------- phase A (rows [k, n)) ----------------
+        if (!merged) {
         if (t < i) {
             rowV[t] = ldcg(VW + (size_t)k * 64 + t);
             rowW[t] = (t == i - 1) ? w_next : ldcg(VW + (size_t)k * 64 + kNb + t);
         }
         __syncthreads();
-        int lo, hi;
         part_range(k, n, c, nc, lo, hi);
         double s2 = 0.0;
         const int sub = lane >> 3, sl = lane & 7;          // 8 lanes per row, 4 rows per warp
@@ -240,11 +248,27 @@ __global__ void __launch_bounds__(kTrdThreads, 1) trd_panel(const __grid_constan
         s2 = block_sum(s2, sh);
         if (t == 0) __stcg(part + (size_t)c * kPart + 2 * kNb, s2);
         group_barrier(J.bar, target, nc);
+        }   // !merged
         if (k == n - 1) break;
         // ---------------- phase B (rows [k+1, n)) ----------------
+        // x_r = J.x[r] (phase A), or f_r - v'_r beta with v' = V[:, i-1] (merged)
+        auto xval = [&](int r) -> double {
+            return merged ? ldcg(J.x + r) - m_beta * (double)ldcg(VW + (size_t)r * 64 + (i - 1)) : ldcg(J.x + r);
+        };
+        double m_nrm2 = 0.0;
+        if (merged) {
+            // ||x||^2 over rows k+2.. computed by every CTA from the full x (the same loads and the
+            // same fixed-order reduction in every CTA, so all CTAs agree bit for bit)
+            double q2 = 0.0;
+            for (int r = k + 2 + t; r < n; r += kTrdThreads) {
+                const double xr = xval(r);
+                q2 += xr * xr;
+            }
+            m_nrm2 = block_sum(q2, sh);
+        }
         if (warp == 0) {
-            const double nrm2 = warp_part_sum(part, 2 * kNb, nc, lane);
-            const double alpha = ldcg(J.x + k + 1);
+            const double nrm2 = merged ? m_nrm2 : warp_part_sum(part, 2 * kNb, nc, lane);
+            const double alpha = xval(k + 1);
             double tau = 0.0, beta = alpha, scale = 0.0;
             if (nrm2 > 0.0) {
                 beta = -copysign(sqrt(alpha * alpha + nrm2), alpha);
@@ -269,7 +293,7 @@ __global__ void __launch_bounds__(kTrdThreads, 1) trd_panel(const __grid_constan
             const int col = c0 + j;
             float v = 0.f;
             if (col == k + 1) v = 1.f;
-            else if (col > k + 1 && col < n) v = (float)(ldcg(J.x + col) * scale);
+            else if (col > k + 1 && col < n) v = (float)(xval(col) * scale);
             vsm[j] = v;
         }
         if (warp == 0) {
@@ -444,6 +468,12 @@ __global__ void __launch_bounds__(kTrdThreads, 1) trd_panel(const __grid_constan
             sum += __shfl_xor_sync(0xffffffffu, sum, 1);
             if (sub == 0) ab[col] = sum;
         }
+        // merge column k+1's phase A into this phase C (same panel, same row ownership)
+        const bool mnext = (i + 1 < kNb) && (k + 1 < n);
+        if (mnext && t < i) {          // V[k+1, q], W[k+1, q] (q < i: final since earlier barriers)
+            rowV[t] = ldcg(VW + (size_t)(k + 1) * 64 + t);
+            rowW[t] = ldcg(VW + (size_t)(k + 1) * 64 + kNb + t);
+        }
         __syncthreads();
         double wv = 0.0;
         {
@@ -451,7 +481,7 @@ __global__ void __launch_bounds__(kTrdThreads, 1) trd_panel(const __grid_constan
             const int sub = lane >> 3, sl = lane & 7;      // 8 lanes per row, 4 rows per warp
             for (int r0 = lo + 4 * warp; r0 < hi; r0 += 4 * kTrdWarps) {
                 const int r = r0 + sub;
-                double yr = 0.0;
+                double yr = 0.0, corr = 0.0;
                 if (r < hi) {
                     const int b = (r - (k + 1)) / kSymvR;
                     const int nj = (min(n, k + 1 + kSymvR * (b + 1)) - 1 - c0) / kSymvC + 1;
@@ -463,29 +493,51 @@ __global__ void __launch_bounds__(kTrdThreads, 1) trd_panel(const __grid_constan
                         const float v4[4] = {vv.x, vv.y, vv.z, vv.w}, w4[4] = {ww.x, ww.y, ww.z, ww.w};
 #pragma unroll
                         for (int u = 0; u < 4; ++u)
-                            if (4 * sl + u < i) yr -= (double)w4[u] * ab[4 * sl + u] + (double)v4[u] * ab[kNb + 4 * sl + u];
+                            if (4 * sl + u < i) {
+                                yr -= (double)w4[u] * ab[4 * sl + u] + (double)v4[u] * ab[kNb + 4 * sl + u];
+                                corr += (double)v4[u] * rowW[4 * sl + u] + (double)w4[u] * rowV[4 * sl + u];
+                            }
                     }
                 }
                 yr += __shfl_xor_sync(0xffffffffu, yr, 4);
                 yr += __shfl_xor_sync(0xffffffffu, yr, 2);
                 yr += __shfl_xor_sync(0xffffffffu, yr, 1);
+                if (mnext) {
+                    corr += __shfl_xor_sync(0xffffffffu, corr, 4);
+                    corr += __shfl_xor_sync(0xffffffffu, corr, 2);
+                    corr += __shfl_xor_sync(0xffffffffu, corr, 1);
+                }
                 if (sl == 0 && r < hi) {
                     const double w = tau * yr;
+                    const double vr = (double)vsm[r - c0];
                     __stcg(J.y + r, w);
-                    wv += w * (double)vsm[r - c0];
+                    wv += w * vr;
+                    if (mnext) {
+                        // column k+1 before its last correction term:
+                        //   c_r = A_p[r, k+1] - sum_{q<i} (V[r,q] W[k+1,q] + W[r,q] V[k+1,q])
+                        //         - (V[r,i] W[k+1,i] + W[r,i] V[k+1,i])
+                        // with V[:, i] = v (v_{k+1} = 1) and W[:, i] = w + alpha v, the last term is
+                        // w_r + v_r (w_{k+1} + 2 alpha), so c_r = f_r - v_r beta:
+                        __stcg(J.x + r, (double)A[(size_t)r * ldw + k + 1] - corr - w);
+                    }
                 }
             }
         }
         wv = block_sum(wv, sh);
         if (t == 0) __stcg(part + (size_t)c * kPart + 2 * kNb + 1, wv);
         group_barrier(J.bar, target, nc);
-        // ---------------- phase D ----------------
+        // ---------------- phase D (+ the merged phase A of column k+1) ----------------
         if (warp == 0) {
             const double sum = warp_part_sum(part, 2 * kNb + 1, nc, lane);
             if (lane == 0) scal[2] = -0.5 * tau * sum;
         }
         __syncthreads();
         const double alpha2 = scal[2];
+        if (mnext) {
+            m_beta = ldcg(J.y + k + 1) + 2.0 * alpha2;                 // w_{k+1} + 2 alpha
+            if (c == 0 && t == 0) J.d[k + 1] = ldcg(J.x + k + 1) - m_beta;   // f_{k+1} - v_{k+1} beta
+        }
+        merged = mnext;
         for (int r = lo + t; r < hi; r += kTrdThreads) {
             const float w = (float)(ldcg(J.y + r) + alpha2 * (double)vsm[r - c0]);
             VW[(size_t)r * 64 + kNb + i] = w;

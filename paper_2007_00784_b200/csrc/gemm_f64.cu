@@ -248,11 +248,12 @@ __global__ void __launch_bounds__(NT, 1) gemm64_kernel(const __grid_constant__ B
 // accumulation -- the same arithmetic as DFMA, at the tensor pipe's rate).  Warp w owns the
 // 64 x 32 block (rows 64 (w / 4), columns 32 (w % 4)) as 8 x 4 DMMA tiles.  Used when every
 // operand's rows are 16-byte aligned.
-constexpr int PBK = 16, kStages = 3, kPM = 64;                 // pipelined tile: kPM x BN
+constexpr int PBK = 16, kStages = 2, kPM = 64;                 // pipelined tile: kPM x BN
 constexpr int kPT = kPM * 2;                                      // 4 warps, each 64 x 32
 constexpr int kTsA = kPM + 8, kTsB = BN + 8;                      // fp64 tile row strides
 constexpr int kRawA = kPM * PBK * 8, kRawB = BN * PBK * 8;        // raw slabs, fp64 worst case
-constexpr int kPipeSmem = kStages * (kRawA + kRawB) + PBK * (kTsA + kTsB) * 8 + 64;
+constexpr int kTileD = PBK * (kTsA + kTsB);                       // doubles per fp64 tile pair
+constexpr int kPipeSmem = kStages * (kRawA + kRawB) + 2 * kTileD * 8 + 64;
 
 // Raw slab of one operand: "outer" rows of "inner" contiguous elements.  MN-contiguous operands
 // (A^T stored k x m, B stored k x n) have outer = k, inner = mn; K-contiguous ones the reverse.
@@ -318,8 +319,7 @@ __global__ void __launch_bounds__(kPT, 2) gemm64_pipe_kernel(const __grid_consta
     if (d.lower && n0 >= m0 + kPM) return;           // block strictly above the diagonal
     const int t = threadIdx.x, warp = t / 32, lane = t % 32;
     char *raw = reinterpret_cast<char *>(smem_d);
-    double *As = smem_d + kStages * (kRawA + kRawB) / 8;
-    double *Bs = As + PBK * kTsA;
+    double *tiles = smem_d + kStages * (kRawA + kRawB) / 8;     // two fp64 tile pairs (A, B)
     const uint32_t raw_s = (uint32_t)__cvta_generic_to_shared(raw);
 
     RawOp oa, ob;
@@ -335,24 +335,34 @@ __global__ void __launch_bounds__(kPT, 2) gemm64_pipe_kernel(const __grid_consta
         for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
     const int wn = warp * 32, g = lane >> 2, q = lane & 3;
     const int nk = (Ke + PBK - 1) / PBK;
-    auto issue = [&](int kt) {
+    auto issue = [&](int kt) {                 // slab kt -> raw stage kt & 1
         if (kt < nk) {
-            const uint32_t st = raw_s + (uint32_t)((kt % kStages) * (kRawA + kRawB));
+            const uint32_t st = raw_s + (uint32_t)((kt & 1) * (kRawA + kRawB));
             issue_raw(oa, st, kt * PBK, t);
             issue_raw(ob, st + kRawA, kt * PBK, t);
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
-#pragma unroll
-    for (int s = 0; s < kStages - 1; ++s) issue(s);
+    auto convert = [&](int kt) {               // raw stage kt & 1 -> tile pair kt & 1
+        const char *st = raw + (kt & 1) * (kRawA + kRawB);
+        double *T = tiles + (kt & 1) * kTileD;
+        convert_raw(oa, st, T, kTsA, t);
+        convert_raw(ob, st + kRawA, T + PBK * kTsA, kTsB, t);
+    };
+    // Software pipeline, one barrier per slab: iteration kt converts slab kt+1 (its copies landed)
+    // into the other tile pair and refills the raw stage of slab kt with slab kt+2, then runs the
+    // DMMAs of slab kt -- warps still converting overlap warps already multiplying.
+    issue(0);
+    issue(1);
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    __syncthreads();
+    if (nk > 0) convert(0);
     for (int kt = 0; kt < nk; ++kt) {
-        asm volatile("cp.async.wait_group %0;" ::"n"(kStages - 2) : "memory");
-        __syncthreads();                        // slab kt landed everywhere; previous compute done
-        const char *st = raw + (kt % kStages) * (kRawA + kRawB);
-        convert_raw(oa, st, As, kTsA, t);
-        convert_raw(ob, st + kRawA, Bs, kTsB, t);
-        __syncthreads();
-        issue(kt + kStages - 1);                // into the stage converted in iteration kt - 1
+        asm volatile("cp.async.wait_group 0;" ::: "memory");    // slab kt+1 (this thread's copies)
+        __syncthreads();       // all copies of kt+1 landed; convert(kt) done; compute(kt-1) done
+        if (kt + 1 < nk) convert(kt + 1);
+        issue(kt + 2);                          // raw stage of slab kt: converted last iteration
+        const double *As = tiles + (kt & 1) * kTileD, *Bs = As + PBK * kTsA;
 #pragma unroll
         for (int kk = 0; kk < PBK; kk += 4) {
             // A fragment (8 x 4, row-major): element (g, q); B fragment (4 x 8, col): element (q, g)
