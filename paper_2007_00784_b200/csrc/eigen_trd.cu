@@ -42,7 +42,11 @@ kfac_status_t trd_run(const float *const *F, const int32_t *dims, const int32_t 
 namespace {
 
 constexpr int kNb = 32;                 // panel width (reflectors per syr2k)
-constexpr int kTrdThreads = 512;
+#ifndef KFAC_TRD_THREADS
+#define KFAC_TRD_THREADS 512
+#endif
+constexpr int kTrdThreads = KFAC_TRD_THREADS;   // 512 (256 with two CTAs per SM measured slower)
+constexpr int kTrdCtasPerSm = 512 / kTrdThreads;
 constexpr int kTrdWarps = kTrdThreads / 32;
 constexpr int kPart = 2 * kNb + 2;      // per-CTA partials: V^T v, W^T v, ||x||^2, w^T v
 constexpr int kMaxGroupCtas = 512;
@@ -173,7 +177,7 @@ struct PanelLaunch {
 //   C: y -= W (V^T v) + V (W^T v);  w = tau y;  partial w^T v
 //   D: W[:, i] = w - (tau/2)(w^T v) v
 // so that after the panel A_p[q:n, q:n] - V W^T - W V^T is the reduced trailing matrix (q = p0+32).
-__global__ void __launch_bounds__(kTrdThreads, 1) trd_panel(const __grid_constant__ PanelLaunch L) {
+__global__ void __launch_bounds__(kTrdThreads, kTrdCtasPerSm) trd_panel(const __grid_constant__ PanelLaunch L) {
     extern __shared__ __align__(16) float vsm[];     // v, 4-aligned, zero padded
     __shared__ double sh[kTrdWarps];
     __shared__ double red[kTrdWarps][2 * kNb];
@@ -260,6 +264,7 @@ __global__ void __launch_bounds__(kTrdThreads, 1) trd_panel(const __grid_constan
             // ||x||^2 over rows k+2.. computed by every CTA from the full x (the same loads and the
             // same fixed-order reduction in every CTA, so all CTAs agree bit for bit)
             double q2 = 0.0;
+#pragma unroll 4
             for (int r = k + 2 + t; r < n; r += kTrdThreads) {
                 const double xr = xval(r);
                 q2 += xr * xr;
@@ -332,6 +337,7 @@ __global__ void __launch_bounds__(kTrdThreads, 1) trd_panel(const __grid_constan
         // panel dot partials over the owned rows (lane q -> panel column q)
         double pa = 0.0, pb = 0.0;
         if (lane < i)
+#pragma unroll 4
             for (int r = lo + warp; r < hi; r += kTrdWarps) {
                 const double vr = vsm[r - c0];
                 pa += (double)ldcg(VW + (size_t)r * 64 + lane) * vr;
@@ -458,14 +464,14 @@ __global__ void __launch_bounds__(kTrdThreads, 1) trd_panel(const __grid_constan
         }
         group_barrier(J.bar, target, nc);
         // ---------------- phase C ----------------
-        {   // (V^T v, W^T v): 8 consecutive threads per panel column sum the group's CTA partials
-            const int col = t >> 3, sub = t & 7;           // 64 columns x 8 = 512 threads
+        {   // (V^T v, W^T v): kTpc consecutive threads per panel column sum the group's CTA partials
+            constexpr int kTpc = kTrdThreads / (2 * kNb);
+            const int col = t / kTpc, sub = t % kTpc;
             double sum = 0.0;
             if ((col % kNb) < i)
-                for (int q = sub; q < nc; q += 8) sum += ldcg(part + (size_t)q * kPart + col);
-            sum += __shfl_xor_sync(0xffffffffu, sum, 4);
-            sum += __shfl_xor_sync(0xffffffffu, sum, 2);
-            sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+                for (int q = sub; q < nc; q += kTpc) sum += ldcg(part + (size_t)q * kPart + col);
+#pragma unroll
+            for (int o = kTpc / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
             if (sub == 0) ab[col] = sum;
         }
         // merge column k+1's phase A into this phase C (same panel, same row ownership)
@@ -485,8 +491,20 @@ __global__ void __launch_bounds__(kTrdThreads, 1) trd_panel(const __grid_constan
                 if (r < hi) {
                     const int b = (r - (k + 1)) / kSymvR;
                     const int nj = (min(n, k + 1 + kSymvR * (b + 1)) - 1 - c0) / kSymvC + 1;
-                    for (int jj = sl; jj < nj; jj += 8) yr += ldcg(J.DP + (size_t)r * J.ldp + jj);
-                    for (int bb = b + sl; bb < nrb; bb += 8) yr += ldcg(J.TP + (size_t)r * J.ldtp + bb);
+                    // independent loads in flight: 4-way unrolled with separate partial sums
+                    double y0 = 0.0, y1 = 0.0, y2 = 0.0, y3 = 0.0;
+                    const double *dp = J.DP + (size_t)r * J.ldp, *tp = J.TP + (size_t)r * J.ldtp;
+                    int jj = sl;
+                    for (; jj + 24 < nj; jj += 32) {
+                        y0 += ldcg(dp + jj); y1 += ldcg(dp + jj + 8); y2 += ldcg(dp + jj + 16); y3 += ldcg(dp + jj + 24);
+                    }
+                    for (; jj < nj; jj += 8) y0 += ldcg(dp + jj);
+                    int bb = b + sl;
+                    for (; bb + 24 < nrb; bb += 32) {
+                        y0 += ldcg(tp + bb); y1 += ldcg(tp + bb + 8); y2 += ldcg(tp + bb + 16); y3 += ldcg(tp + bb + 24);
+                    }
+                    for (; bb < nrb; bb += 8) y1 += ldcg(tp + bb);
+                    yr = (y0 + y1) + (y2 + y3);
                     if (4 * sl < i) {
                         const float4 vv = __ldcg(reinterpret_cast<const float4 *>(VW + (size_t)r * 64) + sl);
                         const float4 ww = __ldcg(reinterpret_cast<const float4 *>(VW + (size_t)r * 64 + kNb) + sl);
@@ -1221,6 +1239,15 @@ T *rebase(T *p, char *base) {
     return reinterpret_cast<T *>(base + reinterpret_cast<uintptr_t>(p));
 }
 
+bool trail_tc() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("KFAC_TRD_TRAIL_TC");
+        v = (e && e[0] == '1') ? 1 : 0;
+    }
+    return v == 1;
+}
+
 int panel_capacity(size_t smem) {
     static int cap = -1;
     static size_t cap_smem = 0;
@@ -1377,6 +1404,27 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
             prof_end(prof, s, by, fl);
         }
         gd.clear();
+        if (trail_tc()) {
+            // rank-64 trailing update on the tcgen05 3xTF32 engine (fp32-faithful products, fp32
+            // accumulation with IEEE drains; experiment switch KFAC_TRD_TRAIL_TC=1)
+            std::vector<GemmDesc> td;
+            for (int q = 0; q < na; ++q) {
+                const TrdJob &J = P.jobs[act[q]];
+                const int q0 = pst[q] + kNb;
+                if (J.n <= q0) continue;
+                GemmDesc g{};
+                g.M = g.N = J.n - q0;
+                g.K = 2 * kNb;
+                g.A = J.VW + (size_t)q0 * 64; g.lda = 64; g.trans_a = 0;
+                g.B = J.WV + (size_t)q0 * 64; g.ldb = 64; g.trans_b = 1;
+                g.C = J.A + (size_t)q0 * J.ldw + q0; g.ldc = J.ldw;
+                g.epi = EPI_SUB;
+                g.lower = 1;
+                td.push_back(g);
+            }
+            if (!td.empty()) RET_OK(gemm_grouped(td.data(), (int)td.size(), 0.f, s));
+            continue;
+        }
         for (int q = 0; q < na; ++q) {
             const TrdJob &J = P.jobs[act[q]];
             const int q0 = pst[q] + kNb;

@@ -55,7 +55,7 @@ struct TcDesc {
     const float *vc;
     const int *dyn;       // optional device {N_eff, K_eff}
     int M, N, K, ldc;
-    int a_mn, b_mn, epi;
+    int a_mn, b_mn, epi, lower;
     int tile_begin, tiles_n;
 };
 
@@ -333,6 +333,7 @@ __global__ void __launch_bounds__(NT, 1) gemm_tc_kernel(const __grid_constant__ 
     const int Ne = d.dyn ? min(d.N, d.dyn[0]) : d.N, Ke = d.dyn ? min(d.K, d.dyn[1]) : d.K;
     const int nk = (Ke + BK - 1) / BK;
     if (n0 >= Ne || nk <= 0) return;          // whole CTA exits before any barrier / TMEM setup
+    if (d.lower && n0 >= m0 + BM) return;     // strictly above the diagonal (symmetric update)
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     if (warp == W_TMA && lane == 0) {
         prefetch_map(&d.ta);
@@ -386,6 +387,230 @@ __global__ void __launch_bounds__(NT, 1) gemm_tc_kernel(const __grid_constant__ 
         }
     }
     teardown(tmem, warp);
+}
+
+
+// --------------------------------------------------- planes GEMM kernel --
+// Operands arrive pre-split as TF32 planes (hi, lo), so there is no split pass: per k-block the
+// TMA warp loads four 16 KB tiles [A_hi | B_hi | A_lo | B_lo] into one of kPS stages, the MMA
+// thread issues the three products straight from them, the drain warps accumulate the TMEM
+// segments in fp32 registers and the epilogue leaves through shared memory in coalesced 512-byte
+// rows (optionally as hi/lo planes again, for the next GEMM of the chain).
+constexpr int kPS = 3;                                  // stages of 64 KB
+constexpr int kPlaneStage = 4 * kTileBytes;
+constexpr int kEpiStride = 132;                         // staging row stride (floats), 16-B aligned
+
+struct __align__(64) TcPlanesBatch {
+    TcDesc d[kMaxTc];
+    CUtensorMap ta_lo[kMaxTc];
+    CUtensorMap tb_lo[kMaxTc];
+    float *c_lo[kMaxTc];
+    int count;
+    float damping;
+    int drain;
+};
+
+__device__ __forceinline__ int find_desc_p(const TcPlanesBatch &b, int tile) {
+    int lo = 0, hi = b.count - 1;
+    while (lo < hi) {
+        int mid = (lo + hi + 1) >> 1;
+        if (b.d[mid].tile_begin <= tile) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+__global__ void __launch_bounds__(NT, 1) gemm_tc_planes_kernel(const __grid_constant__ TcPlanesBatch batch) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    const uint32_t a0 = smem_u32(smem_raw);
+    uint8_t *base = smem_raw + (((a0 + 1023u) & ~1023u) - a0);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(base + kPS * kPlaneStage);
+    const uint32_t full = smem_u32(bars), empty = smem_u32(bars + kPS);
+    Smem S;                                             // drain_loop's view: TMEM barriers only
+    S.base = base;
+    S.tfull = smem_u32(bars + 2 * kPS);
+    S.tempty = smem_u32(bars + 2 * kPS + 2);
+    S.tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * kPS + 4);
+
+    const int di = find_desc_p(batch, blockIdx.x);
+    const TcDesc &d = batch.d[di];
+    const int local = blockIdx.x - d.tile_begin;
+    const int m0 = (local / d.tiles_n) * BM, n0 = (local % d.tiles_n) * BN;
+    const int Ne = d.dyn ? min(d.N, d.dyn[0]) : d.N, Ke = d.dyn ? min(d.K, d.dyn[1]) : d.K;
+    const int nk = (Ke + BK - 1) / BK;
+    if (n0 >= Ne || nk <= 0) return;
+    if (d.lower && n0 >= m0 + BM) return;
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kPS; ++i) {
+            mbar_init(full + 8 * i, 1);
+            mbar_init(empty + 8 * i, 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(S.tfull + 8 * b, 1);
+            mbar_init(S.tempty + 8 * b, 128);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == W_TMA) {
+        if (lane == 0) {
+            prefetch_map(&d.ta); prefetch_map(&d.tb);
+            prefetch_map(&batch.ta_lo[di]); prefetch_map(&batch.tb_lo[di]);
+        }
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(S.tmem_slot)),
+                     "r"(kTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *S.tmem_slot;
+
+    if (warp == W_TMA) {
+        if (lane == 0) {
+            for (int kb = 0; kb < nk; ++kb) {
+                const int s = kb % kPS;
+                if (kb >= kPS) mbar_wait(empty + 8 * s, ((kb / kPS) - 1) & 1);
+                const uint32_t st = smem_u32(base + s * kPlaneStage);
+                mbar_expect_tx(full + 8 * s, kPlaneStage);
+                load_tile(st, &d.ta, full + 8 * s, m0, kb * BK, d.a_mn);
+                load_tile(st + kTileBytes, &d.tb, full + 8 * s, n0, kb * BK, d.b_mn);
+                load_tile(st + 2 * kTileBytes, &batch.ta_lo[di], full + 8 * s, m0, kb * BK, d.a_mn);
+                load_tile(st + 3 * kTileBytes, &batch.tb_lo[di], full + 8 * s, n0, kb * BK, d.b_mn);
+            }
+        }
+    } else if (warp == W_MMA) {
+        if (lane == 0) {
+            const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)d.a_mn << 15) |
+                                   ((uint32_t)d.b_mn << 16) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+            const int drain = batch.drain;
+            for (int kb = 0; kb < nk; ++kb) {
+                const int s = kb % kPS;
+                const int seg = kb / drain, pos = kb - seg * drain, b = seg & 1, u = seg >> 1;
+                mbar_wait(full + 8 * s, (kb / kPS) & 1);
+                if (pos == 0 && u >= 1) mbar_wait(S.tempty + 8 * b, (u - 1) & 1);
+                tc_fence_after();
+                const uint32_t st = smem_u32(base + s * kPlaneStage);
+                const uint32_t a_hi = st, b_hi = st + kTileBytes, a_lo = st + 2 * kTileBytes, b_lo = st + 3 * kTileBytes;
+                const uint32_t dt = tmem + b * BN;
+#pragma unroll
+                for (int ks = 0; ks < BK / 8; ++ks) {
+                    mma_tf32(dt, operand_desc(a_lo, ks, d.a_mn), operand_desc(b_hi, ks, d.b_mn), idesc,
+                             (ks > 0 || pos > 0) ? 1u : 0u);
+                    mma_tf32(dt, operand_desc(a_hi, ks, d.a_mn), operand_desc(b_lo, ks, d.b_mn), idesc, 1u);
+                    mma_tf32(dt, operand_desc(a_hi, ks, d.a_mn), operand_desc(b_hi, ks, d.b_mn), idesc, 1u);
+                }
+                mma_commit(empty + 8 * s);
+                if (pos == drain - 1 || kb == nk - 1) mma_commit(S.tfull + 8 * b);
+            }
+        }
+    } else if (warp >= W_DRAIN0 && warp < W_TMA) {
+        const int wq = warp - W_DRAIN0;
+        float acc[BN];
+        drain_loop(S, tmem, nk, wq, acc, batch.drain);
+        // every MMA has completed (the last tfull), so the stages are free: stage this warp's
+        // 32 x 128 block row-major, then leave in coalesced rows (lane -> 4 consecutive columns)
+        float *stg = reinterpret_cast<float *>(base) + wq * 32 * kEpiStride;
+#pragma unroll
+        for (int j = 0; j < BN / 4; ++j)
+            *reinterpret_cast<float4 *>(stg + lane * kEpiStride + 4 * j) =
+                make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
+        __syncwarp();
+        const int n = n0 + 4 * lane;
+        float vc[4] = {0.f, 0.f, 0.f, 0.f};
+        if (epi_uses_vectors(d.epi))
+#pragma unroll
+            for (int e = 0; e < 4; ++e) vc[e] = n + e < Ne ? d.vc[n + e] : 0.f;
+        float *clo = batch.c_lo[di];
+        const bool vec = n + 3 < Ne;
+        for (int r = 0; r < 32; ++r) {
+            const int m = m0 + wq * 32 + r;
+            if (m >= d.M) break;
+            const float4 a4 = *reinterpret_cast<const float4 *>(stg + r * kEpiStride + 4 * lane);
+            float v[4] = {a4.x, a4.y, a4.z, a4.w};
+            const float vr = epi_uses_vectors(d.epi) ? d.vr[m] : 0.f;
+            float *crow = d.C + (size_t)m * d.ldc;
+            float cin[4] = {0.f, 0.f, 0.f, 0.f};
+            if (d.epi == EPI_SUB) {
+                if (vec) {
+                    const float4 c4 = *reinterpret_cast<const float4 *>(crow + n);
+                    cin[0] = c4.x; cin[1] = c4.y; cin[2] = c4.z; cin[3] = c4.w;
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) if (n + e < Ne) cin[e] = crow[n + e];
+                }
+            }
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                if (d.epi == EPI_DIV_EIGEN) v[e] = v[e] / fmaxf(fmaf(vr, vc[e], batch.damping), 1e-12f);
+                else if (d.epi == EPI_DIV_FACTORED) v[e] = v[e] / fmaxf((vr + batch.damping) * (vc[e] + batch.damping), 1e-12f);
+                else if (d.epi == EPI_SUB) v[e] = cin[e] - v[e];
+            }
+            if (clo) {                                    // result as TF32 planes (next GEMM's operand)
+                float h[4], l[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    h[e] = tf32_rn(v[e]);
+                    l[e] = tf32_rn(v[e] - h[e]);
+                }
+                float *lrow = clo + (size_t)m * d.ldc;
+                if (vec) {
+                    *reinterpret_cast<float4 *>(crow + n) = make_float4(h[0], h[1], h[2], h[3]);
+                    *reinterpret_cast<float4 *>(lrow + n) = make_float4(l[0], l[1], l[2], l[3]);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e)
+                        if (n + e < Ne) { crow[n + e] = h[e]; lrow[n + e] = l[e]; }
+                }
+            } else if (vec) {
+                *reinterpret_cast<float4 *>(crow + n) = make_float4(v[0], v[1], v[2], v[3]);
+            } else {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) if (n + e < Ne) crow[n + e] = v[e];
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == W_TMA) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+    }
+}
+
+// x -> (rn_tf32(x), rn_tf32(x - hi)), float4 per thread, grid-stride over all jobs' rows.
+struct SplitBatch {
+    int count;
+    SplitJob j[64];
+    long long row_begin[65];
+};
+
+__global__ void __launch_bounds__(256) split_planes_kernel(const __grid_constant__ SplitBatch b) {
+    const long long total_rows = b.row_begin[b.count];
+    for (long long gr = blockIdx.x; gr < total_rows; gr += gridDim.x) {
+        int ji = 0;
+        while (ji + 1 < b.count && b.row_begin[ji + 1] <= gr) ++ji;
+        const SplitJob &J = b.j[ji];
+        const int r = (int)(gr - b.row_begin[ji]);
+        const float *src = J.src + (size_t)r * J.ld_src;
+        float *hi = J.hi + (size_t)r * J.ld_dst, *lo = J.lo + (size_t)r * J.ld_dst;
+        for (int c = 4 * threadIdx.x; c < J.cols; c += 4 * blockDim.x) {
+            float x[4] = {0.f, 0.f, 0.f, 0.f};
+            if (c + 3 < J.cols) {
+                const float4 v = __ldg(reinterpret_cast<const float4 *>(src + c));
+                x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
+            } else {
+                for (int e = 0; e < 4 && c + e < J.cols; ++e) x[e] = src[c + e];
+            }
+            float h[4], l[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                h[e] = tf32_rn(x[e]);
+                l[e] = tf32_rn(x[e] - h[e]);
+            }
+            *reinterpret_cast<float4 *>(hi + c) = make_float4(h[0], h[1], h[2], h[3]);
+            *reinterpret_cast<float4 *>(lo + c) = make_float4(l[0], l[1], l[2], l[3]);
+        }
+    }
 }
 
 // ------------------------------------------------------------ SYRK kernel --
@@ -645,7 +870,7 @@ kfac_status_t gemm_tc_grouped(const GemmDesc *descs, int count, float damping, c
                 set_error("cuTensorMapEncodeTiled failed");
                 return KFAC_ERR_CUDA;
             }
-            t.C = g.C; t.vr = g.vr; t.vc = g.vc; t.dyn = g.dyn;
+            t.C = g.C; t.vr = g.vr; t.vc = g.vc; t.dyn = g.dyn; t.lower = g.lower;
             t.M = g.M; t.N = g.N; t.K = g.K; t.ldc = g.ldc; t.epi = g.epi;
             t.tiles_n = cdiv(g.N, BN);
             t.tile_begin = tiles;
@@ -665,6 +890,82 @@ kfac_status_t gemm_tc_grouped(const GemmDesc *descs, int count, float damping, c
             }
             prof_end(prof, s, by, fl);
         }
+    }
+    return KFAC_OK;
+}
+
+
+kfac_status_t gemm_tc_planes_grouped(const GemmDesc *descs, int count, float damping, cudaStream_t s) {
+    static bool attr = false;
+    if (!attr) {
+        KFAC_CUDA_TRY(cudaFuncSetAttribute(gemm_tc_planes_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           kSmemBytes));
+        attr = true;
+    }
+    static_assert(kPS * kPlaneStage + 1024 + 2 * kPS * 8 + 64 <= kSmemBytes, "planes smem");
+    for (int base = 0; base < count; base += kMaxTc) {
+        static TcPlanesBatch b;
+        memset(&b, 0, sizeof(b));
+        b.damping = damping;
+        b.drain = g_drain_gemm();
+        int tiles = 0;
+        for (int i = base; i < count && b.count < kMaxTc; ++i) {
+            const GemmDesc &g = descs[i];
+            const int q = b.count;
+            TcDesc &t = b.d[q];
+            t.a_mn = g.trans_a ? 1 : 0;
+            t.b_mn = g.trans_b ? 0 : 1;
+            const CUtensorMapSwizzle kmaj = CU_TENSOR_MAP_SWIZZLE_128B, mnmaj = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
+            auto mapA = [&](CUtensorMap *m, const float *p) {
+                return t.a_mn ? make_map(m, p, g.K, g.M, g.lda, 32, 32, mnmaj) : make_map(m, p, g.M, g.K, g.lda, 32, 128, kmaj);
+            };
+            auto mapB = [&](CUtensorMap *m, const float *p) {
+                return t.b_mn ? make_map(m, p, g.K, g.N, g.ldb, 32, 32, mnmaj) : make_map(m, p, g.N, g.K, g.ldb, 32, 128, kmaj);
+            };
+            if (!(mapA(&t.ta, g.A) && mapB(&t.tb, g.B) && mapA(&b.ta_lo[q], g.A_lo) && mapB(&b.tb_lo[q], g.B_lo))) {
+                set_error("cuTensorMapEncodeTiled failed (planes)");
+                return KFAC_ERR_CUDA;
+            }
+            t.C = g.C; t.vr = g.vr; t.vc = g.vc; t.dyn = g.dyn; t.lower = g.lower;
+            t.M = g.M; t.N = g.N; t.K = g.K; t.ldc = g.ldc; t.epi = g.epi;
+            b.c_lo[q] = g.C_lo;
+            t.tiles_n = cdiv(g.N, BN);
+            t.tile_begin = tiles;
+            tiles += cdiv(g.M, BM) * t.tiles_n;
+            ++b.count;
+        }
+        if (!b.count) continue;
+        const int prof = prof_begin(KFAC_PROF_GEMM_TC, s);
+        gemm_tc_planes_kernel<<<tiles, NT, kSmemBytes, s>>>(b);
+        KFAC_LAUNCHED();
+        if (prof >= 0) {
+            double by = 0.0, fl = 0.0;
+            for (int i = 0; i < b.count; ++i) {
+                const TcDesc &g = b.d[i];
+                fl += 2.0 * g.M * g.N * g.K;
+                by += 4.0 * ((double)g.M * g.K + (double)g.K * g.N + (double)g.M * g.N);
+            }
+            prof_end(prof, s, by, fl);
+        }
+    }
+    return KFAC_OK;
+}
+
+kfac_status_t split_planes(const SplitJob *jobs, int count, cudaStream_t s) {
+    for (int base = 0; base < count; base += 64) {
+        SplitBatch b;
+        b.count = 0;
+        long long rows = 0;
+        for (int i = base; i < count && b.count < 64; ++i) {
+            b.j[b.count] = jobs[i];
+            b.row_begin[b.count] = rows;
+            rows += jobs[i].rows;
+            ++b.count;
+        }
+        b.row_begin[b.count] = rows;
+        if (rows == 0) continue;
+        split_planes_kernel<<<(int)std::min<long long>(rows, 4 * 148 * 8), 256, 0, s>>>(b);
+        KFAC_LAUNCHED();
     }
     return KFAC_OK;
 }

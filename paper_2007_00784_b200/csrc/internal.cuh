@@ -29,6 +29,12 @@ struct GemmDesc {
     int trans_a, trans_b, epi;
     int tile_begin;          // filled by the launcher
     const int *dyn;          // optional device {N_eff, K_eff}: the kernel clips N and K to them
+    int lower;               // tensor-core engine: skip 128x128 tiles strictly above the diagonal
+    // Pre-split operands (tensor-core "planes" engine, gemm_tc_planes_grouped): A/B are the TF32
+    // hi planes and A_lo/B_lo the lo planes (x = hi + lo, both exact TF32 values); C_lo non-null
+    // makes the epilogue write its result as planes too (C = hi, C_lo = lo).
+    const float *A_lo, *B_lo;
+    float *C_lo;
 };
 
 constexpr int kGemmMaxDescs = 64;
@@ -48,6 +54,16 @@ kfac_status_t gemm_simt_grouped(const GemmDesc *descs, int count, float damping,
 // KFAC_ERR_UNSUPPORTED if a descriptor does not meet its layout rules.
 kfac_status_t gemm_tc_grouped(const GemmDesc *descs, int count, float damping, cudaStream_t s);
 bool gemm_tc_supported(const GemmDesc &d);
+
+// Tensor-core engine on pre-split TF32 operand planes: TMA loads hi and lo tiles, no split pass.
+kfac_status_t gemm_tc_planes_grouped(const GemmDesc *descs, int count, float damping, cudaStream_t s);
+// x -> (hi, lo) TF32 planes of a rows x cols matrix (ld_src / ld_dst in floats, multiples of 4).
+struct SplitJob {
+    const float *src;
+    float *hi, *lo;
+    int rows, cols, ld_src, ld_dst;
+};
+kfac_status_t split_planes(const SplitJob *jobs, int count, cudaStream_t s);
 
 // Dispatch each descriptor to the tensor-core or SIMT engine.
 kfac_status_t gemm_grouped(const GemmDesc *descs, int count, float damping, cudaStream_t s);

@@ -12,13 +12,36 @@
 // by the last CTA (deterministic), nu computed on the device, then P *= nu (float4).
 #include "internal.cuh"
 
+#include <cstdlib>
 #include <vector>
 
 namespace kfac {
 
+static bool getenv_flag(const char *name) {
+    const char *e = getenv(name);
+    return e && e[0] == '1';
+}
+
+// Layers whose four GEMMs all run on the tensor cores (every dimension >= 64, 16-byte rows) use
+// the pre-split "planes" engine: Q_G, Q_A and the gradient are split once into TF32 hi/lo planes
+// and every intermediate (T, V2, U) leaves its GEMM's epilogue as planes, so no GEMM re-splits
+// an operand.  The others run the fp32 SIMT chain.
+static bool planes_layer(int dg, int da, int ldW, int ldQG, int ldQA) {
+    return !getenv_flag("KFAC_PRECOND_NO_PLANES") && dg >= 64 && da >= 64 && (ldW % 4) == 0 &&
+           (ldQG % 4) == 0 && (ldQA % 4) == 0;
+}
+
+static size_t layer_floats(int dg, int da) {
+    const size_t ldt = round_up(da, 4);
+    const size_t ldg = round_up(dg, 4);
+    // T, V (fp32 chain) or T, V, U planes (2 each) + Q_G, Q_A, grad planes (2 each)
+    return 2 * (3 * round_up((size_t)dg * ldt, 64) + round_up((size_t)dg * ldg, 64) +
+                round_up((size_t)da * ldt, 64) + round_up((size_t)dg * ldt, 64));
+}
+
 size_t precond_workspace_bytes(const int32_t *d_g, const int32_t *d_a, int nl, int mode) {
     size_t f = 0;
-    for (int l = 0; l < nl; ++l) f += 2 * round_up((size_t)d_g[l] * round_up(d_a[l], 4), 64);
+    for (int l = 0; l < nl; ++l) f += layer_floats(d_g[l], d_a[l]);
     (void)mode;
     return f * sizeof(float) + 256;
 }
@@ -29,63 +52,99 @@ kfac_status_t precond_run(const int32_t *d_g, const int32_t *d_a, int nl, const 
                           const float *const *vA, float damping, int mode, float *const *out,
                           void *ws, cudaStream_t s) {
     float *base = reinterpret_cast<float *>(round_up(reinterpret_cast<uintptr_t>(ws), 256));
-    std::vector<float *> T(nl), V(nl);
-    std::vector<int> ldt(nl);
+    // per layer: fp32 chain buffers T, V and (planes layers) the hi/lo planes
+    struct Buf {
+        float *T, *V;                                   // fp32 chain
+        float *Th, *Tl, *Vh, *Vl, *Uh, *Ul;             // planes chain
+        float *QGh, *QGl, *QAh, *QAl, *Wh, *Wl;         // split inputs
+        int ldt, ldg, planes;
+    };
+    std::vector<Buf> B(nl);
     size_t off = 0;
+    auto take = [&](size_t n) { float *p = base + off; off += round_up(n, 64); return p; };
+    std::vector<SplitJob> split;
     for (int l = 0; l < nl; ++l) {
-        ldt[l] = (int)round_up(d_a[l], 4);
-        T[l] = base + off;
-        off += round_up((size_t)d_g[l] * ldt[l], 64);
-        V[l] = base + off;
-        off += round_up((size_t)d_g[l] * ldt[l], 64);
+        Buf &b = B[l];
+        b.ldt = (int)round_up(d_a[l], 4);
+        b.ldg = (int)round_up(d_g[l], 4);
+        const size_t gt = (size_t)d_g[l] * b.ldt;
+        const size_t start = off;
+        b.planes = planes_layer(d_g[l], d_a[l], ldW[l], ldQG[l], ldQA[l]);
+        if (!b.planes) {
+            b.T = take(gt);
+            b.V = take(gt);
+        } else {
+            b.Th = take(gt); b.Tl = take(gt);
+            b.Vh = take(gt); b.Vl = take(gt);
+            b.Uh = take(gt); b.Ul = take(gt);
+            b.QGh = take((size_t)d_g[l] * b.ldg); b.QGl = take((size_t)d_g[l] * b.ldg);
+            b.QAh = take((size_t)d_a[l] * b.ldt); b.QAl = take((size_t)d_a[l] * b.ldt);
+            b.Wh = take(gt); b.Wl = take(gt);
+            split.push_back({QG[l], b.QGh, b.QGl, d_g[l], d_g[l], ldQG[l], b.ldg});
+            split.push_back({QA[l], b.QAh, b.QAl, d_a[l], d_a[l], ldQA[l], b.ldt});
+            split.push_back({grad[l], b.Wh, b.Wl, d_g[l], d_a[l], ldW[l], b.ldt});
+        }
+        off = start + layer_floats(d_g[l], d_a[l]);
     }
-    std::vector<GemmDesc> g(nl);
-    auto run = [&]() { return gemm_grouped(g.data(), nl, damping, s); };
     kfac_status_t st;
+    if (!split.empty() && (st = split_planes(split.data(), (int)split.size(), s)) != KFAC_OK) return st;
+
+    std::vector<GemmDesc> gs, gp;                   // fp32 chain (SIMT / split-in-kernel), planes chain
+    auto run = [&]() {
+        kfac_status_t r = KFAC_OK;
+        if (!gs.empty()) r = gemm_grouped(gs.data(), (int)gs.size(), damping, s);
+        if (r == KFAC_OK && !gp.empty()) r = gemm_tc_planes_grouped(gp.data(), (int)gp.size(), damping, s);
+        gs.clear();
+        gp.clear();
+        return r;
+    };
+    // one GEMM of the chain for layer l: op(A) op(B) -> C (fp32) or planes (Ch, Cl)
+    auto add = [&](int l, const float *A, const float *Al, int lda, int ta, const float *Bm, const float *Bl, int ldb,
+                   int tb, float *C, float *Cl, int ldc, int M, int N, int K, int epi) {
+        GemmDesc d{};
+        d.A = A; d.A_lo = Al; d.lda = lda; d.trans_a = ta;
+        d.B = Bm; d.B_lo = Bl; d.ldb = ldb; d.trans_b = tb;
+        d.C = C; d.C_lo = Cl; d.ldc = ldc; d.M = M; d.N = N; d.K = K; d.epi = epi;
+        if (epi_uses_vectors(epi)) { d.vr = vG[l]; d.vc = vA[l]; }
+        (B[l].planes ? gp : gs).push_back(d);
+    };
     if (mode == KFAC_PRECOND_INVERSE) {
         for (int l = 0; l < nl; ++l) {      // T = G_inv grad
-            GemmDesc d{};
-            d.A = QG[l]; d.lda = ldQG[l]; d.B = grad[l]; d.ldb = ldW[l]; d.C = T[l]; d.ldc = ldt[l];
-            d.M = d_g[l]; d.N = d_a[l]; d.K = d_g[l];
-            g[l] = d;
+            const Buf &b = B[l];
+            if (b.planes) add(l, b.QGh, b.QGl, b.ldg, 0, b.Wh, b.Wl, b.ldt, 0, b.Th, b.Tl, b.ldt, d_g[l], d_a[l], d_g[l], EPI_STORE);
+            else add(l, QG[l], nullptr, ldQG[l], 0, grad[l], nullptr, ldW[l], 0, b.T, nullptr, b.ldt, d_g[l], d_a[l], d_g[l], EPI_STORE);
         }
         if ((st = run()) != KFAC_OK) return st;
         for (int l = 0; l < nl; ++l) {      // P = T A_inv
-            GemmDesc d{};
-            d.A = T[l]; d.lda = ldt[l]; d.B = QA[l]; d.ldb = ldQA[l]; d.C = out[l]; d.ldc = ldW[l];
-            d.M = d_g[l]; d.N = d_a[l]; d.K = d_a[l];
-            g[l] = d;
+            const Buf &b = B[l];
+            if (b.planes) add(l, b.Th, b.Tl, b.ldt, 0, b.QAh, b.QAl, b.ldt, 0, out[l], nullptr, ldW[l], d_g[l], d_a[l], d_a[l], EPI_STORE);
+            else add(l, b.T, nullptr, b.ldt, 0, QA[l], nullptr, ldQA[l], 0, out[l], nullptr, ldW[l], d_g[l], d_a[l], d_a[l], EPI_STORE);
         }
         return run();
     }
+    const int div = mode == KFAC_PRECOND_EIGEN ? EPI_DIV_EIGEN : EPI_DIV_FACTORED;
     for (int l = 0; l < nl; ++l) {          // T = Q_G^T grad
-        GemmDesc d{};
-        d.A = QG[l]; d.lda = ldQG[l]; d.trans_a = 1; d.B = grad[l]; d.ldb = ldW[l];
-        d.C = T[l]; d.ldc = ldt[l]; d.M = d_g[l]; d.N = d_a[l]; d.K = d_g[l];
-        g[l] = d;
+        const Buf &b = B[l];
+        if (b.planes) add(l, b.QGh, b.QGl, b.ldg, 1, b.Wh, b.Wl, b.ldt, 0, b.Th, b.Tl, b.ldt, d_g[l], d_a[l], d_g[l], EPI_STORE);
+        else add(l, QG[l], nullptr, ldQG[l], 1, grad[l], nullptr, ldW[l], 0, b.T, nullptr, b.ldt, d_g[l], d_a[l], d_g[l], EPI_STORE);
     }
     if ((st = run()) != KFAC_OK) return st;
-    for (int l = 0; l < nl; ++l) {          // V2 = (T Q_A) / D
-        GemmDesc d{};
-        d.A = T[l]; d.lda = ldt[l]; d.B = QA[l]; d.ldb = ldQA[l]; d.C = V[l]; d.ldc = ldt[l];
-        d.M = d_g[l]; d.N = d_a[l]; d.K = d_a[l];
-        d.epi = mode == KFAC_PRECOND_EIGEN ? EPI_DIV_EIGEN : EPI_DIV_FACTORED;
-        d.vr = vG[l]; d.vc = vA[l];
-        g[l] = d;
+    for (int l = 0; l < nl; ++l) {          // V2 = (T Q_A) / D   (Eq. 14 in the epilogue)
+        const Buf &b = B[l];
+        if (b.planes) add(l, b.Th, b.Tl, b.ldt, 0, b.QAh, b.QAl, b.ldt, 0, b.Vh, b.Vl, b.ldt, d_g[l], d_a[l], d_a[l], div);
+        else add(l, b.T, nullptr, b.ldt, 0, QA[l], nullptr, ldQA[l], 0, b.V, nullptr, b.ldt, d_g[l], d_a[l], d_a[l], div);
     }
     if ((st = run()) != KFAC_OK) return st;
     for (int l = 0; l < nl; ++l) {          // U = Q_G V2
-        GemmDesc d{};
-        d.A = QG[l]; d.lda = ldQG[l]; d.B = V[l]; d.ldb = ldt[l]; d.C = T[l]; d.ldc = ldt[l];
-        d.M = d_g[l]; d.N = d_a[l]; d.K = d_g[l];
-        g[l] = d;
+        const Buf &b = B[l];
+        if (b.planes) add(l, b.QGh, b.QGl, b.ldg, 0, b.Vh, b.Vl, b.ldt, 0, b.Uh, b.Ul, b.ldt, d_g[l], d_a[l], d_g[l], EPI_STORE);
+        else add(l, QG[l], nullptr, ldQG[l], 0, b.V, nullptr, b.ldt, 0, b.T, nullptr, b.ldt, d_g[l], d_a[l], d_g[l], EPI_STORE);
     }
     if ((st = run()) != KFAC_OK) return st;
     for (int l = 0; l < nl; ++l) {          // P = U Q_A^T
-        GemmDesc d{};
-        d.A = T[l]; d.lda = ldt[l]; d.B = QA[l]; d.ldb = ldQA[l]; d.trans_b = 1;
-        d.C = out[l]; d.ldc = ldW[l]; d.M = d_g[l]; d.N = d_a[l]; d.K = d_a[l];
-        g[l] = d;
+        const Buf &b = B[l];
+        if (b.planes) add(l, b.Uh, b.Ul, b.ldt, 0, b.QAh, b.QAl, b.ldt, 1, out[l], nullptr, ldW[l], d_g[l], d_a[l], d_a[l], EPI_STORE);
+        else add(l, b.T, nullptr, b.ldt, 0, QA[l], nullptr, ldQA[l], 1, out[l], nullptr, ldW[l], d_g[l], d_a[l], d_a[l], EPI_STORE);
     }
     return run();
 }
