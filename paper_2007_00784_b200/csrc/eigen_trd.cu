@@ -65,6 +65,7 @@ struct TrdJob {
     int *info;
     float *A;          // n x ldw working matrix (full symmetric storage, pads zero)
     float *Vb;         // n x ldw reflectors: column k = v_k (v_k[k+1] = 1, zero above)
+    double *Vd;        // fp64 copy of Vb for the back-transformation GEMMs (all-fp64 DMMA kernel)
     float *VW, *WV;    // n x 64 panel buffers: [V | W] and [W | V] of the current panel
     double *Z0, *Z1;   // n x ldw eigenvectors of T (D&C ping-pong), fp64
     double *Qnd, *Tmp; // n x ldw D&C scratch (permuted/rotated columns, GEMM output)
@@ -1087,6 +1088,15 @@ __global__ void trd_output(const TrdJob *jobs) {
     }
 }
 
+// Vd = (double) Vb (exact), so every back-transformation GEMM has fp64 operands.
+__global__ void trd_vb_to_f64(const TrdJob *jobs) {
+    const TrdJob &J = jobs[blockIdx.y];
+    const long long total = (long long)J.n * J.ldw;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x)
+        J.Vd[e] = (double)J.Vb[e];
+}
+
 __global__ void trd_zero_info(const TrdJob *jobs) {
     const TrdJob &J = jobs[blockIdx.x];
     if (threadIdx.x == 0 && J.info) *J.info = 0;
@@ -1156,6 +1166,7 @@ Plan plan(const int32_t *dims, int count) {
 #define TAKE(field, T, cnt) J.field = reinterpret_cast<T *>(take(sizeof(T) * (size_t)(cnt)))
         TAKE(A, float, sq);
         TAKE(Vb, float, sq);
+        TAKE(Vd, double, sq);
         TAKE(VW, float, (size_t)n * 64);
         TAKE(WV, float, (size_t)n * 64);
         TAKE(Z0, double, sq);
@@ -1293,7 +1304,7 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
         J.F = F[i]; J.Q = Q[i]; J.evals = evals[i];
         J.info = info ? info + i : nullptr;
         J.ldF = ldF[i]; J.ldQ = ldQ[i];
-        J.A = rebase(J.A, base); J.Vb = rebase(J.Vb, base); J.VW = rebase(J.VW, base); J.WV = rebase(J.WV, base);
+        J.A = rebase(J.A, base); J.Vb = rebase(J.Vb, base); J.Vd = rebase(J.Vd, base); J.VW = rebase(J.VW, base); J.WV = rebase(J.WV, base);
         J.Z0 = rebase(J.Z0, base); J.Z1 = rebase(J.Z1, base); J.Qnd = rebase(J.Qnd, base);
         J.Tmp = rebase(J.Tmp, base); J.Sb = rebase(J.Sb, base); J.Yb = rebase(J.Yb, base);
         J.Y2b = rebase(J.Y2b, base); J.Gb = rebase(J.Gb, base); J.Tb = rebase(J.Tb, base);
@@ -1503,6 +1514,10 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
     }
 
     // ---- (3) back-transformation X = H Z, last block of reflectors first ----
+    if (mode != TRD_DEBUG_STEDC) {
+        trd_vb_to_f64<<<dim3(std::min(1024, cdiv((long long)max_n * ldw_for(max_n), 256)), count), 256, 0, s>>>(djobs);
+        KFAC_LAUNCHED();
+    }
     size_t boff = 0;
     for (auto &stp : P.bt) {
         if (mode == TRD_DEBUG_STEDC) break;
@@ -1511,17 +1526,17 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
         for (auto &b : stp) {
             const TrdJob &J = P.jobs[b.job];
             const int m = J.n - b.b0 - 1;
-            const float *V = J.Vb + (size_t)(b.b0 + 1) * J.ldw + b.b0;
+            const double *V = J.Vd + (size_t)(b.b0 + 1) * J.ldw + b.b0;
             double *X = final_z(J) + (size_t)(b.b0 + 1) * J.ldw;
             Gemm64Desc g{};
             g.M = b.nr; g.N = b.nr; g.K = m;                     // G = V^T V
-            g.A = V; g.ta = DT_F32; g.lda = J.ldw; g.trans_a = 1;
-            g.B = V; g.tb = DT_F32; g.ldb = J.ldw;
+            g.A = V; g.ta = DT_F64; g.lda = J.ldw; g.trans_a = 1;
+            g.B = V; g.tb = DT_F64; g.ldb = J.ldw;
             g.C = J.Gb; g.tc = DT_F64; g.ldc = kBt;
             g1.push_back(g);
             Gemm64Desc h{};
             h.M = b.nr; h.N = J.n; h.K = m;                      // Y = V^T X
-            h.A = V; h.ta = DT_F32; h.lda = J.ldw; h.trans_a = 1;
+            h.A = V; h.ta = DT_F64; h.lda = J.ldw; h.trans_a = 1;
             h.B = X; h.tb = DT_F64; h.ldb = J.ldw;
             h.C = J.Yb; h.tc = DT_F64; h.ldc = J.ldw;
             g1.push_back(h);
@@ -1533,7 +1548,7 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
             g2.push_back(u);
             Gemm64Desc v{};
             v.M = m; v.N = J.n; v.K = b.nr;                      // X -= V Y2
-            v.A = V; v.ta = DT_F32; v.lda = J.ldw;
+            v.A = V; v.ta = DT_F64; v.lda = J.ldw;
             v.B = J.Y2b; v.tb = DT_F64; v.ldb = J.ldw;
             v.C = X; v.tc = DT_F64; v.ldc = J.ldw;
             v.epi = EPI_SUB;

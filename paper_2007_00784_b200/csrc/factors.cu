@@ -14,6 +14,7 @@
 // for large factors.
 #include "internal.cuh"
 
+#include <cstdlib>
 #include <vector>
 
 namespace kfac {
@@ -223,7 +224,13 @@ __global__ void __launch_bounds__(256) syrk_reduce_kernel(const __grid_constant_
 struct Plan {
     std::vector<FactorJob> jobs;
     size_t partial_floats = 0;
+    size_t plane_floats = 0;        // TF32 hi/lo planes of the tensor-core jobs' inputs
 };
+
+// Elements of a job's input tensor (A: the NHWC activation, G: the n x c_out gradient rows).
+inline long long input_elems(const FactorJob &j) {
+    return j.is_a ? (j.n / ((long long)j.h_out * j.w_out)) * j.h_in * j.w_in * j.c_in : j.n * j.c_in;
+}
 
 Plan make_plan(const kfac_layer_t *layers, int nl, float *const *A, const int32_t *ldA,
                float *const *G, const int32_t *ldG, const float *const *act,
@@ -251,17 +258,27 @@ Plan make_plan(const kfac_layer_t *layers, int nl, float *const *A, const int32_
             j.tiles = j.t1d * (j.t1d + 1) / 2;
             j.partial = reinterpret_cast<float *>(p.partial_floats);   // offset, rebased later
             p.partial_floats += (size_t)j.splits * j.tiles * T * T;
+            if (syrk_tc_supported(j)) p.plane_floats += 2 * round_up((size_t)input_elems(j), 64);
             p.jobs.push_back(j);
         }
     }
     return p;
 }
 
+bool planes_disabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("KFAC_SYRK_NO_PLANES");
+        v = (e && e[0] == '1') ? 1 : 0;
+    }
+    return v == 1;
+}
+
 }  // namespace
 
 size_t factors_workspace_bytes(const kfac_layer_t *layers, int nl) {
     Plan p = make_plan(layers, nl, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
-    return p.partial_floats * sizeof(float) + 256;
+    return (p.partial_floats + p.plane_floats) * sizeof(float) + 512;
 }
 
 kfac_status_t factors_run(const kfac_layer_t *layers, int nl, const float *const *act,
@@ -271,9 +288,26 @@ kfac_status_t factors_run(const kfac_layer_t *layers, int nl, const float *const
     Plan p = make_plan(layers, nl, A, ldA, G, ldG, act, gout);
     float *base = reinterpret_cast<float *>(round_up(reinterpret_cast<uintptr_t>(ws), 256));
     for (auto &j : p.jobs) j.partial = base + reinterpret_cast<uintptr_t>(j.partial);
-    // Partial SYRKs: tcgen05 3xTF32 for the factors it supports, the SIMT tile for the rest.
+    // Partial SYRKs: tcgen05 3xTF32 for the factors it supports, the SIMT tile for the rest.  The
+    // tensor-core jobs' inputs are first split once into TF32 hi/lo planes (one elementwise pass),
+    // so the SYRK kernel gathers both planes and never splits in shared memory.
     std::vector<FactorJob> tc, simt;
     for (auto &j : p.jobs) (syrk_tc_supported(j) ? tc : simt).push_back(j);
+    if (!tc.empty() && !planes_disabled()) {
+        float *pl = base + round_up(p.partial_floats, 64);
+        std::vector<SplitJob> sj;
+        for (auto &j : tc) {
+            const size_t e = round_up((size_t)input_elems(j), 64);
+            const int cols = j.c_in;
+            const int rows = (int)(input_elems(j) / cols);
+            sj.push_back({j.src, pl, pl + e, rows, cols, cols, cols});
+            j.src = pl;
+            j.src_lo = pl + e;
+            pl += 2 * e;
+        }
+        kfac_status_t st = split_planes(sj.data(), (int)sj.size(), s);
+        if (st != KFAC_OK) return st;
+    }
     if (!tc.empty()) {
         kfac_status_t st = syrk_tc_partial(tc.data(), (int)tc.size(), s);
         if (st != KFAC_OK) return st;

@@ -387,6 +387,107 @@ __global__ void __launch_bounds__(kPT, 2) gemm64_pipe_kernel(const __grid_consta
     epilogue(d, Me, Ne, rows, cols, acc);
 }
 
+// ------------------------------------------------ all-fp64 direct DMMA kernel --
+// Both operands fp64 (divide and conquer, back-transformation): the cp.async stages are laid out
+// so that the DMMA fragments are loaded straight from them -- no conversion pass.  Row strides are
+// padded (K-contiguous rows: 18 doubles; MN-contiguous rows: 64 + 4 / 128 + 8 doubles) so every
+// 8x4 fragment load touches each bank exactly twice (two wavefronts, the minimum for 256 B).
+// Three stages: slab kt is multiplied while kt+1 lands and kt+2 is being issued.
+constexpr int kDS = 3;
+constexpr int kSAk = PBK + 2, kSAm = kPM + 4, kSBk = PBK + 2, kSBn = BN + 8;
+constexpr int kDA = (kPM * kSAk > PBK * kSAm) ? kPM * kSAk : PBK * kSAm;       // doubles per A slab
+constexpr int kDB = (BN * kSBk > PBK * kSBn) ? BN * kSBk : PBK * kSBn;         // doubles per B slab
+constexpr int kDirectSmem = kDS * (kDA + kDB) * 8 + 64;
+
+__device__ __forceinline__ void issue_direct(const double *base, size_t ld, int mn_inner, int ext, int stride,
+                                             int mn0, int mn_lim, int k0, int k_lim, uint32_t dst, int t) {
+    const int inner = mn_inner ? ext : PBK, outer = mn_inner ? PBK : ext;
+    const int cpr = inner / 2;                         // 16-byte chunks (2 doubles) per row
+    for (int c = t; c < outer * cpr; c += kPT) {
+        const int r = c / cpr, i0 = (c - r * cpr) * 2;
+        const int og = mn_inner ? k0 + r : mn0 + r, ig = mn_inner ? mn0 + i0 : k0 + i0;
+        const int olim = mn_inner ? k_lim : mn_lim, ilim = mn_inner ? mn_lim : k_lim;
+        int valid = og < olim ? min(2, ilim - ig) : 0;
+        valid = max(valid, 0);
+        const double *src = valid ? base + (size_t)og * ld + ig : base;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst + (uint32_t)(r * stride + i0) * 8),
+                     "l"(src), "r"((uint32_t)(valid * 8))
+                     : "memory");
+    }
+}
+
+__global__ void __launch_bounds__(kPT, 2) gemm64_direct_kernel(const __grid_constant__ Batch64 batch) {
+    extern __shared__ __align__(16) double smem_d[];
+    const int tile = blockIdx.x;
+    const Gemm64Desc &d = batch.d[find_desc(batch, tile)];
+    const int local = tile - d.tile_begin;
+    const int tiles_n = (d.N + BN - 1) / BN;
+    const int m0 = (local / tiles_n) * kPM, n0 = (local % tiles_n) * BN;
+    const int Me = d.M, Ne = d.dyn ? min(d.N, d.dyn[0]) : d.N, Ke = d.dyn ? min(d.K, d.dyn[1]) : d.K;
+    if (n0 >= Ne) return;
+    if (d.lower && n0 >= m0 + kPM) return;
+    const int t = threadIdx.x, warp = t / 32, lane = t % 32;
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem_d);
+    const double *A = static_cast<const double *>(d.A), *Bm = static_cast<const double *>(d.B);
+    const int a_mn = d.trans_a, b_mn = !d.trans_b;
+    const int sa = a_mn ? kSAm : kSAk, sb = b_mn ? kSBn : kSBk;
+
+    double acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
+    const int wn = warp * 32, g = lane >> 2, q = lane & 3;
+    const int nk = (Ke + PBK - 1) / PBK;
+    auto issue = [&](int kt) {
+        if (kt < nk) {
+            const int st = kt % kDS;
+            const uint32_t da = sbase + (uint32_t)(st * (kDA + kDB)) * 8;
+            issue_direct(A, (size_t)d.lda, a_mn, kPM, sa, m0, Me, kt * PBK, Ke, da, t);
+            issue_direct(Bm, (size_t)d.ldb, b_mn, BN, sb, n0, Ne, kt * PBK, Ke, da + kDA * 8, t);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    issue(0);
+    issue(1);
+    for (int kt = 0; kt < nk; ++kt) {
+        asm volatile("cp.async.wait_group 1;" ::: "memory");      // slab kt (this thread's copies)
+        __syncthreads();                        // slab kt landed everywhere; compute(kt-1) done
+        issue(kt + 2);                          // into the stage of slab kt-1
+        const double *As = smem_d + (kt % kDS) * (kDA + kDB), *Bs = As + kDA;
+#pragma unroll
+        for (int kk = 0; kk < PBK; kk += 4) {
+            double a[8], b[4];
+#pragma unroll
+            for (int mi = 0; mi < 8; ++mi) {
+                const int m = mi * 8 + g, k = kk + q;
+                a[mi] = As[a_mn ? k * kSAm + m : m * kSAk + k];
+            }
+#pragma unroll
+            for (int ni = 0; ni < 4; ++ni) {
+                const int n = wn + ni * 8 + g, k = kk + q;
+                b[ni] = Bs[b_mn ? k * kSBn + n : n * kSBk + k];
+            }
+#pragma unroll
+            for (int mi = 0; mi < 8; ++mi)
+#pragma unroll
+                for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][2 * ni], acc[mi][2 * ni + 1], a[mi], b[ni]);
+        }
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    int rows[8], cols[4];
+#pragma unroll
+    for (int mi = 0; mi < 8; ++mi) rows[mi] = m0 + mi * 8 + g;
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) cols[ni] = n0 + wn + ni * 8 + 2 * q;
+    epilogue(d, Me, Ne, rows, cols, acc);
+}
+
+bool direct_ok(const Gemm64Desc &g) {
+    return g.ta == DT_F64 && g.tb == DT_F64 && (reinterpret_cast<uintptr_t>(g.A) % 16 == 0) &&
+           (reinterpret_cast<uintptr_t>(g.B) % 16 == 0) && (g.lda % 2 == 0) && (g.ldb % 2 == 0);
+}
+
 bool g_pipe_disabled() {
     static int v = -1;
     if (v < 0) {
@@ -409,12 +510,13 @@ kfac_status_t gemm64_grouped(const Gemm64Desc *descs, int count, cudaStream_t s)
         static Batch64 b;       // host staging; parameters are copied at launch
         b.count = 0;
         end = base;
-        bool pipe = !g_pipe_disabled();
+        bool pipe = !g_pipe_disabled(), direct = pipe;
         for (int i = base; i < count && b.count < kGemm64MaxDescs; ++i, ++end) {
             const Gemm64Desc &g = descs[i];
             if (g.M <= 0 || g.N <= 0) continue;
             b.d[b.count++] = g;
             pipe = pipe && pipe_ok(g);
+            direct = direct && direct_ok(g);
         }
         if (b.count == 0) continue;
         const int tm = pipe ? kPM : BM;
@@ -424,7 +526,15 @@ kfac_status_t gemm64_grouped(const Gemm64Desc *descs, int count, cudaStream_t s)
             tiles += cdiv(b.d[i].M, tm) * cdiv(b.d[i].N, BN);
         }
         const int prof = prof_begin(KFAC_PROF_GEMM64, s);
-        if (pipe) {
+        if (direct) {
+            static bool dattr = false;
+            if (!dattr) {
+                KFAC_CUDA_TRY(cudaFuncSetAttribute(gemm64_direct_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   kDirectSmem));
+                dattr = true;
+            }
+            gemm64_direct_kernel<<<tiles, kPT, kDirectSmem, s>>>(b);
+        } else if (pipe) {
             static bool attr = false;
             if (!attr) {
                 KFAC_CUDA_TRY(cudaFuncSetAttribute(gemm64_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -577,42 +577,40 @@ __global__ void __launch_bounds__(NT, 1) gemm_tc_planes_kernel(const __grid_cons
     }
 }
 
-// x -> (rn_tf32(x), rn_tf32(x - hi)), float4 per thread, grid-stride over all jobs' rows.
+// x -> (rn_tf32(x), rn_tf32(x - hi)), one float4 unit per thread and iteration, grid-stride over
+// the units of all jobs (job j: rows x ld_dst/4 units; columns >= cols are written as zeros).
 struct SplitBatch {
     int count;
     SplitJob j[64];
-    long long row_begin[65];
+    long long unit_begin[65];
 };
 
 __global__ void __launch_bounds__(256) split_planes_kernel(const __grid_constant__ SplitBatch b) {
-    const long long total_rows = b.row_begin[b.count];
-    for (long long gr = blockIdx.x; gr < total_rows; gr += gridDim.x) {
-        int ji = 0;
-        while (ji + 1 < b.count && b.row_begin[ji + 1] <= gr) ++ji;
-        const SplitJob &J = b.j[ji];
-        const int r = (int)(gr - b.row_begin[ji]);
-        const float *src = J.src + (size_t)r * J.ld_src;
-        float *hi = J.hi + (size_t)r * J.ld_dst, *lo = J.lo + (size_t)r * J.ld_dst;
-        for (int c = 4 * threadIdx.x; c < J.cols; c += 4 * blockDim.x) {
-            float x[4] = {0.f, 0.f, 0.f, 0.f};
-            if (c + 3 < J.cols) {
-                const float4 v = __ldg(reinterpret_cast<const float4 *>(src + c));
-                x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
-            } else {
-                for (int e = 0; e < 4 && c + e < J.cols; ++e) x[e] = src[c + e];
-            }
-            float h[4], l[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                h[e] = tf32_rn(x[e]);
-                l[e] = tf32_rn(x[e] - h[e]);
-            }
-            *reinterpret_cast<float4 *>(hi + c) = make_float4(h[0], h[1], h[2], h[3]);
-            *reinterpret_cast<float4 *>(lo + c) = make_float4(l[0], l[1], l[2], l[3]);
+    const long long total = b.unit_begin[b.count];
+    for (long long u = (long long)blockIdx.x * blockDim.x + threadIdx.x; u < total;
+         u += (long long)gridDim.x * blockDim.x) {
+        int lo = 0, hi = b.count - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (b.unit_begin[mid] <= u) lo = mid; else hi = mid - 1;
         }
+        const SplitJob &J = b.j[lo];
+        const long long v = u - b.unit_begin[lo];
+        const int w4 = J.ld_dst / 4;
+        const long long r = v / w4;
+        const int c = (int)(v - r * w4) * 4;
+        const float4 x4 = __ldg(reinterpret_cast<const float4 *>(J.src + r * J.ld_src + c));
+        float x[4] = {x4.x, x4.y, x4.z, x4.w}, h[4], l[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const float xe = c + e < J.cols ? x[e] : 0.f;
+            h[e] = tf32_rn(xe);
+            l[e] = tf32_rn(xe - h[e]);
+        }
+        *reinterpret_cast<float4 *>(J.hi + r * J.ld_dst + c) = make_float4(h[0], h[1], h[2], h[3]);
+        *reinterpret_cast<float4 *>(J.lo + r * J.ld_dst + c) = make_float4(l[0], l[1], l[2], l[3]);
     }
 }
-
 // ------------------------------------------------------------ SYRK kernel --
 __device__ __forceinline__ int find_job(const SyrkBatch &b, int item) {
     int lo = 0, hi = b.count - 1;
@@ -659,6 +657,7 @@ __device__ __forceinline__ ChunkInfo chunk_info(const FactorJob &J, int c) {
 struct SyrkGeom {
     const float *src;
     int is_a, c_in, h_in, w_in, h_out, w_out, stride_h, stride_w, pad_h, pad_w;
+    const float *src_lo;
 };
 
 // Producer warps 0-3: cp.async gathers of the 32-row k-block into raw stage s; the stage's
@@ -777,6 +776,165 @@ __global__ void __launch_bounds__(NT, 1) syrk_tc_kernel(const __grid_constant__ 
         for (int j = 0; j < BN / 4; ++j) dst[j] = make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
     }
     teardown(tmem, warp);
+}
+
+
+// ----------------------------------------------------- planes SYRK kernel --
+// The factor's input arrives pre-split as TF32 planes (split_planes), so the producer warps only
+// gather: per k-block each thread issues 16-byte cp.async copies of both planes of its column
+// chunk(s) into [A_hi | B_hi | A_lo | B_lo] of one of kPS 64-KB stages (diagonal tiles: A only),
+// and the MMA thread consumes them directly -- no split pass through shared memory.
+__device__ __forceinline__ void syrk_issue_planes(const SyrkGeom &G, uint32_t st, int2 *tabw, long long r0,
+                                                  long long r_end, const ChunkInfo (&ci)[2], int cc, int t,
+                                                  bool diag) {
+    const int warp = t / 32, lane = t % 32;
+    int org = 0, ihw = 0;
+    {
+        const long long r = r0 + warp + 4 * (lane & 7);
+        const bool rv = r < r_end;
+        if (G.is_a) {
+            const int hw = G.h_out * G.w_out;
+            const int ri = rv ? (int)r : 0;
+            const int img = ri / hw;
+            const int p = ri - img * hw;
+            const int oh = p / G.w_out, ow = p - (p / G.w_out) * G.w_out;
+            const int ih0 = oh * G.stride_h - G.pad_h, iw0 = ow * G.stride_w - G.pad_w;
+            org = ((img * G.h_in + ih0) * G.w_in + iw0) * G.c_in;
+            ihw = rv ? (int)(((unsigned)ih0 << 16) | ((unsigned)iw0 & 0xffffu)) : (int)0x80000000;
+        } else {
+            org = rv ? (int)r * G.c_in : 0;
+            ihw = rv ? 0 : (int)0x80000000;
+        }
+    }
+    __syncwarp();
+    if (lane < 8) tabw[lane] = make_int2(org, ihw);
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const int k = warp + 4 * j;
+        const int2 rd = tabw[j];
+        const int o = rd.x, hv = rd.y;
+        const bool rv = hv != (int)0x80000000;
+        const int ih0 = hv >> 16, iw0 = (int)(short)(hv & 0xffff);
+#pragma unroll
+        for (int op = 0; op < 2; ++op) {
+            if (op == 1 && diag) break;
+            const uint32_t dhi = st + op * kTileBytes + mn_off(k, 4 * cc);
+            const uint32_t dlo = dhi + 2 * kTileBytes;
+            const ChunkInfo &c = ci[op];
+            if (c.kind == 1) {                        // bias chunk: hi {1, 0, 0, 0}, lo 0, on valid rows
+                cp_async16(dhi, kBiasChunk, rv ? 16u : 0u);
+                cp_async16(dlo, kBiasChunk, 0u);
+                continue;
+            }
+            bool ok = rv && c.kind == 0;
+            if (G.is_a)
+                ok = ok && (unsigned)(ih0 + c.kh) < (unsigned)G.h_in && (unsigned)(iw0 + c.kw) < (unsigned)G.w_in;
+            cp_async16(dhi, ok ? G.src + (o + c.off) : G.src, ok ? 16u : 0u);
+            cp_async16(dlo, ok ? G.src_lo + (o + c.off) : G.src_lo, ok ? 16u : 0u);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(NT, 1) syrk_tc_planes_kernel(const __grid_constant__ SyrkBatch batch) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    const uint32_t a0 = smem_u32(smem_raw);
+    uint8_t *base = smem_raw + (((a0 + 1023u) & ~1023u) - a0);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(base + kPS * kPlaneStage);
+    const uint32_t full = smem_u32(bars), empty = smem_u32(bars + kPS);
+    Smem S;
+    S.base = base;
+    S.tfull = smem_u32(bars + 2 * kPS);
+    S.tempty = smem_u32(bars + 2 * kPS + 2);
+    S.tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * kPS + 4);
+    int2 *rowtab = reinterpret_cast<int2 *>(bars + 32);
+
+    const int item = blockIdx.x;
+    const FactorJob &J = batch.j[find_job(batch, item)];
+    const int local = item - J.item_begin;
+    const int tau = local / J.splits, split = local % J.splits;
+    int ti, tj;
+    upper_tile(tau, J.t1d, ti, tj);
+    const bool diag = ti == tj;
+    const long long r_begin = (long long)split * J.chunk;
+    const long long r_end = min(J.n, r_begin + J.chunk);
+    const int nk = (int)((r_end - r_begin + BK - 1) / BK);
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kPS; ++i) {
+            mbar_init(full + 8 * i, 128);
+            mbar_init(empty + 8 * i, 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(S.tfull + 8 * b, 1);
+            mbar_init(S.tempty + 8 * b, 128);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == W_TMA) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(S.tmem_slot)),
+                     "r"(kTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *S.tmem_slot;
+
+    if (warp == W_MMA) {
+        if (lane == 0) {
+            const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | (1u << 16) |
+                                   ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+            const int drain = batch.drain;
+            for (int kb = 0; kb < nk; ++kb) {
+                const int s = kb % kPS;
+                const int seg = kb / drain, pos = kb - seg * drain, b = seg & 1, u = seg >> 1;
+                mbar_wait(full + 8 * s, (kb / kPS) & 1);
+                if (pos == 0 && u >= 1) mbar_wait(S.tempty + 8 * b, (u - 1) & 1);
+                tc_fence_after();
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                const uint32_t st = smem_u32(base + s * kPlaneStage);
+                const uint32_t a_hi = st, a_lo = st + 2 * kTileBytes;
+                const uint32_t b_hi = diag ? a_hi : st + kTileBytes, b_lo = diag ? a_lo : st + 3 * kTileBytes;
+                const uint32_t dt = tmem + b * BN;
+#pragma unroll
+                for (int ks = 0; ks < BK / 8; ++ks) {
+                    mma_tf32(dt, operand_desc(a_lo, ks, 1), operand_desc(b_hi, ks, 1), idesc, (ks > 0 || pos > 0) ? 1u : 0u);
+                    mma_tf32(dt, operand_desc(a_hi, ks, 1), operand_desc(b_lo, ks, 1), idesc, 1u);
+                    mma_tf32(dt, operand_desc(a_hi, ks, 1), operand_desc(b_hi, ks, 1), idesc, 1u);
+                }
+                mma_commit(empty + 8 * s);
+                if (pos == drain - 1 || kb == nk - 1) mma_commit(S.tfull + 8 * b);
+            }
+        }
+    } else if (warp < W_DRAIN0) {
+        const int t = threadIdx.x, cc = t % 32;
+        ChunkInfo ci[2] = {chunk_info(J, ti * BM + 4 * cc), chunk_info(J, tj * BM + 4 * cc)};
+        SyrkGeom G{J.src, J.is_a, J.c_in, J.h_in, J.w_in, J.h_out, J.w_out,
+                   J.stride_h, J.stride_w, J.pad_h, J.pad_w, J.src_lo};
+        int2 *tabw = rowtab + warp * 8;
+        for (int kb = 0; kb < nk; ++kb) {
+            const int s = kb % kPS;
+            if (kb >= kPS) mbar_wait(empty + 8 * s, ((kb / kPS) - 1) & 1);
+            syrk_issue_planes(G, smem_u32(base + s * kPlaneStage), tabw, r_begin + (long long)kb * BK, r_end, ci, cc,
+                              t, diag);
+            cp_async_arrive(full + 8 * s);
+        }
+    } else if (warp < W_TMA) {
+        const int wq = warp - W_DRAIN0;
+        float acc[BN];
+        drain_loop(S, tmem, nk, wq, acc, batch.drain);
+        float4 *dst = reinterpret_cast<float4 *>(J.partial + ((size_t)split * J.tiles + tau) * (BM * BN) +
+                                                 (size_t)(wq * 32 + lane) * BN);
+#pragma unroll
+        for (int j = 0; j < BN / 4; ++j) dst[j] = make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == W_TMA) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+    }
 }
 
 // ------------------------------------------------------------- host side --
@@ -955,16 +1113,21 @@ kfac_status_t split_planes(const SplitJob *jobs, int count, cudaStream_t s) {
     for (int base = 0; base < count; base += 64) {
         SplitBatch b;
         b.count = 0;
-        long long rows = 0;
+        long long units = 0;
         for (int i = base; i < count && b.count < 64; ++i) {
-            b.j[b.count] = jobs[i];
-            b.row_begin[b.count] = rows;
-            rows += jobs[i].rows;
+            const SplitJob &J = jobs[i];
+            KFAC_CHECK_ARG(J.ld_dst % 4 == 0 && J.ld_src % 4 == 0 && J.ld_dst <= J.ld_src && J.cols <= J.ld_dst &&
+                               aligned16(J.src) && aligned16(J.hi) && aligned16(J.lo),
+                           KFAC_ERR_ALIGNMENT, "split_planes: rows must be 16-byte aligned");
+            b.j[b.count] = J;
+            b.unit_begin[b.count] = units;
+            units += (long long)J.rows * (J.ld_dst / 4);
             ++b.count;
         }
-        b.row_begin[b.count] = rows;
-        if (rows == 0) continue;
-        split_planes_kernel<<<(int)std::min<long long>(rows, 4 * 148 * 8), 256, 0, s>>>(b);
+        b.unit_begin[b.count] = units;
+        if (units == 0) continue;
+        const int grid = (int)std::min<long long>((units + 255) / 256, 148 * 16);
+        split_planes_kernel<<<grid, 256, 0, s>>>(b);
         KFAC_LAUNCHED();
     }
     return KFAC_OK;
@@ -999,8 +1162,20 @@ kfac_status_t syrk_tc_partial(const FactorJob *jobs, int count, cudaStream_t s) 
             items += j.tiles * j.splits;
             b.j[b.count++] = j;
         }
+        bool planes = true;
+        for (int i = 0; i < b.count; ++i) planes = planes && b.j[i].src_lo != nullptr;
         const int prof = prof_begin(KFAC_PROF_SYRK_TC, s);
-        syrk_tc_kernel<<<items, NT, kSmemBytes, s>>>(b);
+        if (planes) {
+            static bool pattr = false;
+            if (!pattr) {
+                KFAC_CUDA_TRY(cudaFuncSetAttribute(syrk_tc_planes_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   kSmemBytes));
+                pattr = true;
+            }
+            syrk_tc_planes_kernel<<<items, NT, kSmemBytes, s>>>(b);
+        } else {
+            syrk_tc_kernel<<<items, NT, kSmemBytes, s>>>(b);
+        }
         KFAC_LAUNCHED();
         if (prof >= 0) {
             // algorithmic work of the factors in this launch: n d (d + 1) flops (upper triangle incl.

@@ -93,6 +93,7 @@ kfac_status_t gemm64_grouped(const Gemm64Desc *descs, int count, cudaStream_t s)
 // reduced by syrk_reduce (fixed order, running average, both triangles).
 struct FactorJob {
     const float *src;       // act (NHWC) for A, gout (n x c_in) for G
+    const float *src_lo;    // tensor-core path: src is the TF32 hi plane, src_lo the lo plane
     float *F;
     float *partial;
     long long n;            // rows
