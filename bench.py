@@ -79,6 +79,16 @@ PROF_NAMES = {1: ("trd_panel (Householder tridiagonalisation panel: lower-triang
               4: ("gemm_tc_kernel (preconditioning GEMMs, tcgen05 3xTF32)", "tensor")}
 
 
+TRAFFIC_PATH = os.path.join(ROOT, "profiles", "traffic.json")
+
+
+def traffic_record(kernel_class):
+    try:
+        return json.load(open(TRAFFIC_PATH)).get(str(kernel_class))
+    except Exception:
+        return None
+
+
 # ---------------------------------------------------------------- clocks ------
 class ClockSampler:
     def __init__(self, idx):
@@ -367,6 +377,12 @@ def run_ours(args):
                      "probe_ms_per_step": {PROF_NAMES[k][0]: v for k, v in probe.items()}})
         roof["frac"] = roof["achieved"] / roof["peak"]
         roof["traffic"] = None
+        tr = traffic_record(dom_class)
+        if tr:
+            # dram__bytes_read.sum + dram__bytes_write.sum of one launch of this kernel from the
+            # committed `ncu --set full` capture, with that same launch's algorithmic bytes
+            roof["traffic"] = tr["dram_bytes"]
+            roof["traffic_capture"] = tr
         tensor_tflops = (wm["fac_flops"] + wm["pc_flops"]) / ((stages["factors"] + stages["precond"]) * 1e-3) / 1e12
         line = {"metric": metric_name(args.config), "value": ms, "unit": "ms/iter", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,

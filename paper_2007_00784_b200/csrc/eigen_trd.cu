@@ -67,6 +67,7 @@ struct TrdJob {
     float *Vb;         // n x ldw reflectors: column k = v_k (v_k[k+1] = 1, zero above)
     double *Vd;        // fp64 copy of Vb for the back-transformation GEMMs (all-fp64 DMMA kernel)
     float *VW, *WV;    // n x 64 panel buffers: [V | W] and [W | V] of the current panel
+    double *VWd, *WVd; // fp64 copies of the same (float) values: operands of the trailing update
     double *Z0, *Z1;   // n x ldw eigenvectors of T (D&C ping-pong), fp64
     double *Qnd, *Tmp; // n x ldw D&C scratch (permuted/rotated columns, GEMM output)
     double *Sb;        // n x ldw D&C secular eigenvectors S
@@ -334,6 +335,8 @@ __global__ void __launch_bounds__(kTrdThreads, kTrdCtasPerSm) trd_panel(const __
             J.Vb[(size_t)r * ldw + k] = v;
             VW[(size_t)r * 64 + i] = v;
             WV[(size_t)r * 64 + kNb + i] = v;
+            J.VWd[(size_t)r * 64 + i] = v;
+            J.WVd[(size_t)r * 64 + kNb + i] = v;
         }
         // panel dot partials over the owned rows (lane q -> panel column q)
         double pa = 0.0, pb = 0.0;
@@ -561,6 +564,8 @@ __global__ void __launch_bounds__(kTrdThreads, kTrdCtasPerSm) trd_panel(const __
             const float w = (float)(ldcg(J.y + r) + alpha2 * (double)vsm[r - c0]);
             VW[(size_t)r * 64 + kNb + i] = w;
             WV[(size_t)r * 64 + i] = w;
+            J.VWd[(size_t)r * 64 + kNb + i] = w;
+            J.WVd[(size_t)r * 64 + i] = w;
         }
         w_next = (float)(ldcg(J.y + k + 1) + alpha2);   // row k+1: v = 1
         __syncthreads();
@@ -1169,6 +1174,8 @@ Plan plan(const int32_t *dims, int count) {
         TAKE(Vd, double, sq);
         TAKE(VW, float, (size_t)n * 64);
         TAKE(WV, float, (size_t)n * 64);
+        TAKE(VWd, double, (size_t)n * 64);
+        TAKE(WVd, double, (size_t)n * 64);
         TAKE(Z0, double, sq);
         TAKE(Z1, double, sq);
         TAKE(Qnd, double, sq);
@@ -1304,7 +1311,7 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
         J.F = F[i]; J.Q = Q[i]; J.evals = evals[i];
         J.info = info ? info + i : nullptr;
         J.ldF = ldF[i]; J.ldQ = ldQ[i];
-        J.A = rebase(J.A, base); J.Vb = rebase(J.Vb, base); J.Vd = rebase(J.Vd, base); J.VW = rebase(J.VW, base); J.WV = rebase(J.WV, base);
+        J.A = rebase(J.A, base); J.Vb = rebase(J.Vb, base); J.Vd = rebase(J.Vd, base); J.VWd = rebase(J.VWd, base); J.WVd = rebase(J.WVd, base); J.VW = rebase(J.VW, base); J.WV = rebase(J.WV, base);
         J.Z0 = rebase(J.Z0, base); J.Z1 = rebase(J.Z1, base); J.Qnd = rebase(J.Qnd, base);
         J.Tmp = rebase(J.Tmp, base); J.Sb = rebase(J.Sb, base); J.Yb = rebase(J.Yb, base);
         J.Y2b = rebase(J.Y2b, base); J.Gb = rebase(J.Gb, base); J.Tb = rebase(J.Tb, base);
@@ -1443,8 +1450,8 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
             Gemm64Desc g{};
             g.M = g.N = J.n - q0;
             g.K = 2 * kNb;
-            g.A = J.VW + (size_t)q0 * 64; g.ta = DT_F32; g.lda = 64; g.trans_a = 0;
-            g.B = J.WV + (size_t)q0 * 64; g.tb = DT_F32; g.ldb = 64; g.trans_b = 1;
+            g.A = J.VWd + (size_t)q0 * 64; g.ta = DT_F64; g.lda = 64; g.trans_a = 0;
+            g.B = J.WVd + (size_t)q0 * 64; g.tb = DT_F64; g.ldb = 64; g.trans_b = 1;
             g.C = J.A + (size_t)q0 * J.ldw + q0; g.tc = DT_F32; g.ldc = J.ldw;
             g.epi = EPI_SUB;
             g.lower = 1;                             // the reduction reads only the lower triangle
