@@ -378,7 +378,7 @@ def run_ours(args):
         roof["frac"] = roof["achieved"] / roof["peak"]
         roof["traffic"] = None
         tr = traffic_record(dom_class)
-        if tr:
+        if tr and tr.get("config") == args.config:
             # dram__bytes_read.sum + dram__bytes_write.sum of one launch of this kernel from the
             # committed `ncu --set full` capture, with that same launch's algorithmic bytes
             roof["traffic"] = tr["dram_bytes"]

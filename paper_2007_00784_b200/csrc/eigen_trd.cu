@@ -170,6 +170,7 @@ struct PanelLaunch {
     int p0[kMaxGroupCtas];                 // panel start of each group's factor (staggered)
     int cta_begin[kMaxGroupCtas + 1];
     int ring_off;                          // float offset of the symv prefetch ring in dynamic smem
+    int use_xs;                            // x of the merged column kept in shared memory
 };
 
 // One panel of 32 columns (LAPACK dlatrd, lower) for every active factor.  Column k (i = k - p0):
@@ -205,6 +206,8 @@ __global__ void __launch_bounds__(kTrdThreads, kTrdCtasPerSm) trd_panel(const __
     double *part = J.part;
     const int t = threadIdx.x, warp = t / 32, lane = t % 32;
     const int ring_off = L.ring_off;                 // floats: symv prefetch ring after v
+    // x of the merged column (phase B), after the ring: 16-byte aligned doubles
+    double *xs = reinterpret_cast<double *>(vsm + ring_off + kTrdWarps * 2 * 8 * 32 * 4);
     unsigned target = 0;
     float w_next = 0.f;                              // W[k, i-1], computed redundantly
     // Column k's phase A (its corrected column and diagonal) is folded into column k-1's phase C
@@ -269,6 +272,7 @@ __global__ void __launch_bounds__(kTrdThreads, kTrdCtasPerSm) trd_panel(const __
 #pragma unroll 4
             for (int r = k + 2 + t; r < n; r += kTrdThreads) {
                 const double xr = xval(r);
+                if (L.use_xs) xs[r - (k + 2)] = xr;   // kept for the v fill below (no second load)
                 q2 += xr * xr;
             }
             m_nrm2 = block_sum(q2, sh);
@@ -300,7 +304,7 @@ __global__ void __launch_bounds__(kTrdThreads, kTrdCtasPerSm) trd_panel(const __
             const int col = c0 + j;
             float v = 0.f;
             if (col == k + 1) v = 1.f;
-            else if (col > k + 1 && col < n) v = (float)(xval(col) * scale);
+            else if (col > k + 1 && col < n) v = (float)((merged && L.use_xs ? xs[col - (k + 2)] : xval(col)) * scale);
             vsm[j] = v;
         }
         if (warp == 0) {
@@ -1356,7 +1360,11 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
         attr = true;
     }
     const int ring_off = (int)round_up(round_up(max_n, kSymvC) + kSymvC + 8, 64);
-    const size_t smem = (size_t)ring_off * sizeof(float) + (size_t)kTrdWarps * 2 * 8 * 32 * sizeof(float4);
+    // v (floats) | symv ring | x of the merged column (doubles, phase B; only if it fits)
+    const size_t smem_base = (size_t)ring_off * sizeof(float) + (size_t)kTrdWarps * 2 * 8 * 32 * sizeof(float4);
+    const size_t smem_xs = (size_t)round_up(max_n, 2) * sizeof(double);
+    const int use_xs = smem_base + smem_xs + 12 * 1024 <= 227 * 1024;
+    const size_t smem = smem_base + (use_xs ? smem_xs : 0);
     const int cap = panel_capacity(smem);
     static PanelLaunch PL;
     // Staggered schedule: factor j (P_j panels) starts at launch P_max - P_j, so all factors finish
@@ -1375,18 +1383,28 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
             wsum += m * m;
         }
         if (act.empty()) continue;
-        const int na = (int)act.size();
-        if (na > cap) {
-            set_error("trd: more active factors than co-resident CTAs");
-            return KFAC_ERR_UNSUPPORTED;
+        // More active factors than co-resident CTAs (e.g. ResNet-101's 210 factors): the groups are
+        // independent, so the active set is split into several cooperative launches of <= cap.
+        const std::vector<int> act_all = act, pst_all = pst;
+        for (size_t c0 = 0; c0 < act_all.size(); c0 += (size_t)cap) {
+        act.assign(act_all.begin() + c0, act_all.begin() + std::min(act_all.size(), c0 + (size_t)cap));
+        pst.assign(pst_all.begin() + c0, pst_all.begin() + std::min(pst_all.size(), c0 + (size_t)cap));
+        wsum = 0.0;
+        for (size_t q = 0; q < act.size(); ++q) {
+            const double m = P.jobs[act[q]].n - pst[q];
+            wsum += m * m;
         }
-        // CTAs per factor ~ remaining work, >= 1, <= rows/16, total <= cap
+        const int na = (int)act.size();
+        // CTAs per factor ~ remaining work, >= 1, total <= cap, and no more than one 64 x 128 symv
+        // tile per warp (more CTAs would only add barrier participants and partials)
         std::vector<int> nc(na, 1);
         int spare = cap - na;
         for (int q = 0; q < na; ++q) {
             const double m = P.jobs[act[q]].n - pst[q];
+            const int tiles = cdiv((long long)m, kSymvR) * (cdiv((long long)m, kSymvC) + 1) / 2;
             int want = (int)std::floor((cap - na) * (m * m) / wsum);
             want = std::min(want, std::max(0, (int)(m / 16) - 1));
+            want = std::min(want, std::max(0, cdiv(tiles, kTrdWarps) - 1));
             want = std::min(want, spare);
             nc[q] += want;
             spare -= want;
@@ -1394,6 +1412,7 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
         PL.jobs = djobs;
         PL.count = na;
         PL.ring_off = ring_off;
+        PL.use_xs = use_xs;
         int tot = 0;
         for (int q = 0; q < na; ++q) {
             PL.job[q] = act[q];
@@ -1421,6 +1440,10 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
             }
             prof_end(prof, s, by, fl);
         }
+        }   // chunks of the active set
+        act = act_all;
+        pst = pst_all;
+        const int na = (int)act.size();
         gd.clear();
         if (trail_tc()) {
             // rank-64 trailing update on the tcgen05 3xTF32 engine (fp32-faithful products, fp32

@@ -784,27 +784,42 @@ __global__ void __launch_bounds__(NT, 1) syrk_tc_kernel(const __grid_constant__ 
 // gather: per k-block each thread issues 16-byte cp.async copies of both planes of its column
 // chunk(s) into [A_hi | B_hi | A_lo | B_lo] of one of kPS 64-KB stages (diagonal tiles: A only),
 // and the MMA thread consumes them directly -- no split pass through shared memory.
+template <bool IS_A>
 __device__ __forceinline__ void syrk_issue_planes(const SyrkGeom &G, uint32_t st, int2 *tabw, long long r0,
                                                   long long r_end, const ChunkInfo (&ci)[2], int cc, int t,
                                                   bool diag) {
     const int warp = t / 32, lane = t % 32;
+    if (!IS_A) {
+        // gradient rows: plain row-major gather, no im2col geometry, no bias column
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int k = warp + 4 * j;
+            const long long r = r0 + k;
+            const bool rv = r < r_end;
+            const float *rowh = G.src + (size_t)r * G.c_in, *rowl = G.src_lo + (size_t)r * G.c_in;
+#pragma unroll
+            for (int op = 0; op < 2; ++op) {
+                if (op == 1 && diag) break;
+                const uint32_t dhi = st + op * kTileBytes + mn_off(k, 4 * cc);
+                const bool ok = rv && ci[op].kind == 0;
+                cp_async16(dhi, ok ? rowh + ci[op].off : G.src, ok ? 16u : 0u);
+                cp_async16(dhi + 2 * kTileBytes, ok ? rowl + ci[op].off : G.src_lo, ok ? 16u : 0u);
+            }
+        }
+        return;
+    }
     int org = 0, ihw = 0;
     {
         const long long r = r0 + warp + 4 * (lane & 7);
         const bool rv = r < r_end;
-        if (G.is_a) {
-            const int hw = G.h_out * G.w_out;
-            const int ri = rv ? (int)r : 0;
-            const int img = ri / hw;
-            const int p = ri - img * hw;
-            const int oh = p / G.w_out, ow = p - (p / G.w_out) * G.w_out;
-            const int ih0 = oh * G.stride_h - G.pad_h, iw0 = ow * G.stride_w - G.pad_w;
-            org = ((img * G.h_in + ih0) * G.w_in + iw0) * G.c_in;
-            ihw = rv ? (int)(((unsigned)ih0 << 16) | ((unsigned)iw0 & 0xffffu)) : (int)0x80000000;
-        } else {
-            org = rv ? (int)r * G.c_in : 0;
-            ihw = rv ? 0 : (int)0x80000000;
-        }
+        const int hw = G.h_out * G.w_out;
+        const int ri = rv ? (int)r : 0;
+        const int img = ri / hw;
+        const int p = ri - img * hw;
+        const int oh = p / G.w_out, ow = p - (p / G.w_out) * G.w_out;
+        const int ih0 = oh * G.stride_h - G.pad_h, iw0 = ow * G.stride_w - G.pad_w;
+        org = ((img * G.h_in + ih0) * G.w_in + iw0) * G.c_in;
+        ihw = rv ? (int)(((unsigned)ih0 << 16) | ((unsigned)iw0 & 0xffffu)) : (int)0x80000000;
     }
     __syncwarp();
     if (lane < 8) tabw[lane] = make_int2(org, ihw);
@@ -827,9 +842,8 @@ __device__ __forceinline__ void syrk_issue_planes(const SyrkGeom &G, uint32_t st
                 cp_async16(dlo, kBiasChunk, 0u);
                 continue;
             }
-            bool ok = rv && c.kind == 0;
-            if (G.is_a)
-                ok = ok && (unsigned)(ih0 + c.kh) < (unsigned)G.h_in && (unsigned)(iw0 + c.kw) < (unsigned)G.w_in;
+            const bool ok = rv && c.kind == 0 && (unsigned)(ih0 + c.kh) < (unsigned)G.h_in &&
+                            (unsigned)(iw0 + c.kw) < (unsigned)G.w_in;
             cp_async16(dhi, ok ? G.src + (o + c.off) : G.src, ok ? 16u : 0u);
             cp_async16(dlo, ok ? G.src_lo + (o + c.off) : G.src_lo, ok ? 16u : 0u);
         }
@@ -916,8 +930,12 @@ __global__ void __launch_bounds__(NT, 1) syrk_tc_planes_kernel(const __grid_cons
         for (int kb = 0; kb < nk; ++kb) {
             const int s = kb % kPS;
             if (kb >= kPS) mbar_wait(empty + 8 * s, ((kb / kPS) - 1) & 1);
-            syrk_issue_planes(G, smem_u32(base + s * kPlaneStage), tabw, r_begin + (long long)kb * BK, r_end, ci, cc,
-                              t, diag);
+            if (G.is_a)
+                syrk_issue_planes<true>(G, smem_u32(base + s * kPlaneStage), tabw, r_begin + (long long)kb * BK, r_end,
+                                        ci, cc, t, diag);
+            else
+                syrk_issue_planes<false>(G, smem_u32(base + s * kPlaneStage), tabw, r_begin + (long long)kb * BK, r_end,
+                                         ci, cc, t, diag);
             cp_async_arrive(full + 8 * s);
         }
     } else if (warp < W_TMA) {
@@ -973,11 +991,11 @@ int drain_env(const char *name, int dflt) {
     return v >= 1 ? v : 1;
 }
 int g_drain_gemm() {
-    static int v = drain_env("KFAC_TC_DRAIN_GEMM", 1);
+    static int v = drain_env("KFAC_TC_DRAIN_GEMM", 2);
     return v;
 }
 int g_drain_syrk() {
-    static int v = drain_env("KFAC_TC_DRAIN_SYRK", 1);
+    static int v = drain_env("KFAC_TC_DRAIN_SYRK", 2);
     return v;
 }
 
