@@ -1215,7 +1215,8 @@ kfac_status_t syrk_tc_partial(const FactorJob *jobs, int count, cudaStream_t s) 
 }  // namespace kfac
 
 // Test hook (not part of the public header): run one GEMM through a chosen engine.
-// engine 0 = SIMT, 1 = tcgen05; | 4 selects the C -= AB epilogue.  Returns a kfac_status_t.
+// engine 0 = SIMT, 1 = tcgen05 (in-kernel split), 2 = tcgen05 on pre-split planes; | 4 selects
+// the C -= AB epilogue.  Returns a kfac_status_t.
 extern "C" int kfac_debug_gemm(int engine, const float *A, int lda, int trans_a, const float *B, int ldb,
                                int trans_b, float *C, int ldc, int M, int N, int K, void *stream, float *debug) {
     kfac::GemmDesc d{};
@@ -1228,6 +1229,27 @@ extern "C" int kfac_debug_gemm(int engine, const float *A, int lda, int trans_a,
         if (!kfac::gemm_tc_supported(d)) return KFAC_ERR_UNSUPPORTED;
         (void)debug;
         return kfac::gemm_tc_grouped(&d, 1, 0.f, s);
+    }
+    if (engine == 2) {
+        // pre-split planes engine: A, B split into TF32 planes here; with `debug` non-null the
+        // result is emitted as planes too (hi -> C, lo -> debug, same leading dimension)
+        if (!kfac::gemm_tc_supported(d)) return KFAC_ERR_UNSUPPORTED;
+        const int ar = trans_a ? K : M, ac = trans_a ? M : K, br = trans_b ? N : K, bc = trans_b ? K : N;
+        float *ap = nullptr, *bp = nullptr;
+        if (cudaMalloc(&ap, sizeof(float) * 2 * (size_t)ar * lda) != cudaSuccess) return KFAC_ERR_CUDA;
+        if (cudaMalloc(&bp, sizeof(float) * 2 * (size_t)br * ldb) != cudaSuccess) return KFAC_ERR_CUDA;
+        kfac::SplitJob sj[2] = {{A, ap, ap + (size_t)ar * lda, ar, ac, lda, lda},
+                                {B, bp, bp + (size_t)br * ldb, br, bc, ldb, ldb}};
+        int st = kfac::split_planes(sj, 2, s);
+        kfac::GemmDesc p = d;
+        p.A = ap; p.A_lo = ap + (size_t)ar * lda;
+        p.B = bp; p.B_lo = bp + (size_t)br * ldb;
+        p.C_lo = debug;
+        if (st == KFAC_OK) st = kfac::gemm_tc_planes_grouped(&p, 1, 0.f, s);
+        cudaStreamSynchronize(s);
+        cudaFree(ap);
+        cudaFree(bp);
+        return st;
     }
     return kfac::gemm_simt_grouped(&d, 1, 0.f, s);
 }

@@ -41,8 +41,8 @@ for W in (1, 2, 4, 8):
             per_rank.append(0.0)
             continue
         F = [pc.F[f] for f in fs]
-        Q = [torch.empty_like(x) for x in F]
-        v = [torch.empty(x.shape[0], device="cuda") for x in F]
+        Q = [pc.Q[f] for f in fs]
+        v = [pc.v[f] for f in fs]
         info = torch.zeros(len(fs), dtype=torch.int32, device="cuda")
         _lib.kfac_compute_eigen(F, Q, v, info, 0, ws=ws)          # warm-up (workspace, attributes)
         torch.cuda.synchronize()

@@ -107,3 +107,28 @@ def test_tf32_operand_conversion_probe(lib):
     v = float(out[0, 0])
     print("tf32 conversion of 1+3*2^-12 ->", repr(v), "truncation" if v == 1.0 else "round-to-nearest" if v == 1.0 + 2 ** -10 else "?")
     assert v in (1.0, 1.0 + 2 ** -10)
+
+
+@pytest.mark.parametrize("ta,tb", [(0, 0), (0, 1), (1, 0), (1, 1)])
+@pytest.mark.parametrize("M,N,K", [(128, 128, 32), (200, 72, 45), (512, 385, 1153), (64, 130, 4609)])
+@pytest.mark.parametrize("emit_planes", [False, True])
+def test_tc_planes_gemm_matches_fp64(lib, ta, tb, M, N, K, emit_planes):
+    """The pre-split planes engine (split_planes + gemm_tc_planes_kernel, the preconditioning
+    chain's engine): same bar as the in-kernel split; with emit_planes the product leaves as
+    TF32 planes (hi in C, lo in a second buffer) whose sum is the fp32 result."""
+    rng = np.random.default_rng(M + N + K + 10 * ta + tb + 7)
+    A = rng.standard_normal((K, M) if ta else (M, K)).astype(np.float32).astype(np.float64)
+    B = rng.standard_normal((N, K) if tb else (K, N)).astype(np.float32).astype(np.float64)
+    ref = (A.T if ta else A) @ (B.T if tb else B)
+    lo = torch.zeros((M, (N + 3) // 4 * 4), device="cuda") if emit_planes else None
+    got = _run(lib, 2, A, ta, B, tb, M, N, K, debug=lo)
+    if emit_planes:
+        lo_h = lo[:, :N].double().cpu().numpy()
+        # both planes are exact TF32 values (low 13 mantissa bits zero)
+        for plane in (torch.from_numpy(got).float(), lo[:, :N].cpu()):
+            bits = plane.contiguous().view(torch.int32)
+            assert int((bits & 0x1FFF).abs().sum()) == 0
+        got = got + lo_h
+    assert np.isfinite(got).all()
+    err = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+    assert err <= 2e-6, err
