@@ -34,7 +34,8 @@ def _compile(src, verbose=False):
     dep_t = max(os.path.getmtime(p) for p in _headers() + [src])
     if os.path.exists(obj) and os.path.getmtime(obj) >= dep_t:
         return obj
-    cmd = [NVCC] + ARCH + FLAGS + (["-Xptxas", "-v"] if verbose else []) + ["-c", src, "-o", obj]
+    extra = os.environ.get("KFAC_NVCC_EXTRA", "").split()      # experiments, e.g. -DKFAC_SYMV_ROWS=32
+    cmd = [NVCC] + ARCH + FLAGS + extra + (["-Xptxas", "-v"] if verbose else []) + ["-c", src, "-o", obj]
     if src.endswith(".cpp"):
         cmd = ["g++", "-O2", "-std=c++17", "-fPIC", "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)

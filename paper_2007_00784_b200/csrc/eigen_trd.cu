@@ -51,9 +51,12 @@ constexpr int kTrdWarps = kTrdThreads / 32;
 constexpr int kPart = 2 * kNb + 2;      // per-CTA partials: V^T v, W^T v, ||x||^2, w^T v
 constexpr int kMaxGroupCtas = 512;
 constexpr int kLeaf = 32;               // D&C leaf size
-constexpr int kSymvR = 64;              // symv tile rows (lower triangle only)
+#ifndef KFAC_SYMV_ROWS
+#define KFAC_SYMV_ROWS 64
+#endif
+constexpr int kSymvR = KFAC_SYMV_ROWS;  // symv tile rows (lower triangle only), multiple of 8
 constexpr int kSymvC = 128;             // symv tile columns (one float4 per lane)
-constexpr int kMaxRb = 256;             // symv row blocks: n <= 16384 = 256 x 64
+constexpr int kMaxRb = 16384 / kSymvR;   // symv row blocks for n <= 16384
 constexpr int kBt = 512;                // reflectors per back-transformation block
 constexpr int kTs = 128;                // dlarft sub-block (T built recursively from 128-blocks)
 constexpr double kEps = 1.1102230246251565e-16;   // 2^-53, LAPACK dlamch('E')

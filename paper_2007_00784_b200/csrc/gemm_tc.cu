@@ -790,7 +790,8 @@ __device__ __forceinline__ void syrk_issue_planes(const SyrkGeom &G, uint32_t st
                                                   bool diag) {
     const int warp = t / 32, lane = t % 32;
     if (!IS_A) {
-        // gradient rows: plain row-major gather, no im2col geometry, no bias column
+        // plain rows (gradients; activations of 1x1 stride-1 unpadded convolutions and linear
+        // layers): row r of X is row r of the input, no im2col geometry
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
             const int k = warp + 4 * j;
@@ -801,6 +802,11 @@ __device__ __forceinline__ void syrk_issue_planes(const SyrkGeom &G, uint32_t st
             for (int op = 0; op < 2; ++op) {
                 if (op == 1 && diag) break;
                 const uint32_t dhi = st + op * kTileBytes + mn_off(k, 4 * cc);
+                if (ci[op].kind == 1) {               // bias chunk: hi {1, 0, 0, 0}, lo 0, on valid rows
+                    cp_async16(dhi, kBiasChunk, rv ? 16u : 0u);
+                    cp_async16(dhi + 2 * kTileBytes, kBiasChunk, 0u);
+                    continue;
+                }
                 const bool ok = rv && ci[op].kind == 0;
                 cp_async16(dhi, ok ? rowh + ci[op].off : G.src, ok ? 16u : 0u);
                 cp_async16(dhi + 2 * kTileBytes, ok ? rowl + ci[op].off : G.src_lo, ok ? 16u : 0u);
@@ -930,7 +936,11 @@ __global__ void __launch_bounds__(NT, 1) syrk_tc_planes_kernel(const __grid_cons
         for (int kb = 0; kb < nk; ++kb) {
             const int s = kb % kPS;
             if (kb >= kPS) mbar_wait(empty + 8 * s, ((kb / kPS) - 1) & 1);
-            if (G.is_a)
+            // plain-row gather unless the im2col geometry is needed (A factor of a conv that is not
+            // 1x1, stride 1, unpadded)
+            const bool plain = !G.is_a || (J.k_w == 1 && J.h_in == J.h_out && J.w_in == J.w_out && J.pad_h == 0 &&
+                                           J.pad_w == 0 && J.stride_h == 1 && J.stride_w == 1);
+            if (!plain)
                 syrk_issue_planes<true>(G, smem_u32(base + s * kPlaneStage), tabw, r_begin + (long long)kb * BK, r_end,
                                         ci, cc, t, diag);
             else
