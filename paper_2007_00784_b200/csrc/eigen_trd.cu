@@ -52,7 +52,7 @@ constexpr int kPart = 2 * kNb + 2;      // per-CTA partials: V^T v, W^T v, ||x||
 constexpr int kMaxGroupCtas = 512;
 constexpr int kLeaf = 32;               // D&C leaf size
 #ifndef KFAC_SYMV_ROWS
-#define KFAC_SYMV_ROWS 64
+#define KFAC_SYMV_ROWS 32
 #endif
 constexpr int kSymvR = KFAC_SYMV_ROWS;  // symv tile rows (lower triangle only), multiple of 8
 constexpr int kSymvC = 128;             // symv tile columns (one float4 per lane)
@@ -268,6 +268,7 @@ __global__ void __launch_bounds__(kTrdThreads, kTrdCtasPerSm) trd_panel(const __
             return merged ? ldcg(J.x + r) - m_beta * (double)ldcg(VW + (size_t)r * 64 + (i - 1)) : ldcg(J.x + r);
         };
         double m_nrm2 = 0.0;
+        const double alpha_pre = warp == 0 ? xval(k + 1) : 0.0;      // issued before the q2 pass
         if (merged) {
             // ||x||^2 over rows k+2.. computed by every CTA from the full x (the same loads and the
             // same fixed-order reduction in every CTA, so all CTAs agree bit for bit)
@@ -282,7 +283,7 @@ __global__ void __launch_bounds__(kTrdThreads, kTrdCtasPerSm) trd_panel(const __
         }
         if (warp == 0) {
             const double nrm2 = merged ? m_nrm2 : warp_part_sum(part, 2 * kNb, nc, lane);
-            const double alpha = xval(k + 1);
+            const double alpha = alpha_pre;
             double tau = 0.0, beta = alpha, scale = 0.0;
             if (nrm2 > 0.0) {
                 beta = -copysign(sqrt(alpha * alpha + nrm2), alpha);
@@ -345,15 +346,7 @@ __global__ void __launch_bounds__(kTrdThreads, kTrdCtasPerSm) trd_panel(const __
             J.VWd[(size_t)r * 64 + i] = v;
             J.WVd[(size_t)r * 64 + kNb + i] = v;
         }
-        // panel dot partials over the owned rows (lane q -> panel column q)
-        double pa = 0.0, pb = 0.0;
-        if (lane < i)
-#pragma unroll 4
-            for (int r = lo + warp; r < hi; r += kTrdWarps) {
-                const double vr = vsm[r - c0];
-                pa += (double)ldcg(VW + (size_t)r * 64 + lane) * vr;
-                pb += (double)ldcg(VW + (size_t)r * 64 + kNb + lane) * vr;
-            }
+        double pa, pb;
         // symmetric mat-vec over the lower triangle of A_p[k+1:n, k+1:n] in 64 x 128 tiles (one warp
         // per tile, every tile of the group's factor spread over its warps): each tile adds its
         // row sums to DP[row][chunk] and its column sums (the mirrored upper triangle) to
@@ -400,6 +393,18 @@ __global__ void __launch_bounds__(kTrdThreads, kTrdCtasPerSm) trd_panel(const __
                 locate();
                 issue(0);
             }
+            // panel dot partials over the owned rows (lane q -> panel column q), loads in flight
+            // together with the first symv octet
+            pa = 0.0;
+            pb = 0.0;
+            if (lane < i)
+#pragma unroll 4
+                for (int r = lo + warp; r < hi; r += kTrdWarps) {
+                    const double vr = vsm[r - c0];
+                    pa += (double)ldcg(VW + (size_t)r * 64 + lane) * vr;
+                    pb += (double)ldcg(VW + (size_t)r * 64 + kNb + lane) * vr;
+                }
+
             int stage = 0;
             double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
             while (it < total) {
@@ -557,13 +562,17 @@ __global__ void __launch_bounds__(kTrdThreads, kTrdCtasPerSm) trd_panel(const __
         group_barrier(J.bar, target, nc);
         // ---------------- phase D (+ the merged phase A of column k+1) ----------------
         if (warp == 0) {
+            const double yk1 = ldcg(J.y + k + 1);                     // in flight with the partials
             const double sum = warp_part_sum(part, 2 * kNb + 1, nc, lane);
-            if (lane == 0) scal[2] = -0.5 * tau * sum;
+            if (lane == 0) {
+                scal[2] = -0.5 * tau * sum;
+                scal[3] = yk1;
+            }
         }
         __syncthreads();
-        const double alpha2 = scal[2];
+        const double alpha2 = scal[2], yk1 = scal[3];
         if (mnext) {
-            m_beta = ldcg(J.y + k + 1) + 2.0 * alpha2;                 // w_{k+1} + 2 alpha
+            m_beta = yk1 + 2.0 * alpha2;                               // w_{k+1} + 2 alpha
             if (c == 0 && t == 0) J.d[k + 1] = ldcg(J.x + k + 1) - m_beta;   // f_{k+1} - v_{k+1} beta
         }
         merged = mnext;
@@ -574,7 +583,7 @@ __global__ void __launch_bounds__(kTrdThreads, kTrdCtasPerSm) trd_panel(const __
             J.VWd[(size_t)r * 64 + kNb + i] = w;
             J.WVd[(size_t)r * 64 + i] = w;
         }
-        w_next = (float)(ldcg(J.y + k + 1) + alpha2);   // row k+1: v = 1
+        w_next = (float)(yk1 + alpha2);                 // row k+1: v = 1
         __syncthreads();
     }
 }
