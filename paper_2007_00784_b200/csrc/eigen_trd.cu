@@ -57,6 +57,9 @@ constexpr int kLeaf = 32;               // D&C leaf size
 constexpr int kSymvR = KFAC_SYMV_ROWS;  // symv tile rows (lower triangle only), multiple of 8
 constexpr int kSymvC = 128;             // symv tile columns (one float4 per lane)
 constexpr int kMaxRb = 16384 / kSymvR;   // symv row blocks for n <= 16384
+#ifndef KFAC_SYMV_FP32
+#define KFAC_SYMV_FP32 0                  // 1: fp32 products with 4/8-term fp32 partial sums (experiment)
+#endif
 constexpr int kBt = 512;                // reflectors per back-transformation block
 constexpr int kTs = 128;                // dlarft sub-block (T built recursively from 128-blocks)
 constexpr double kEps = 1.1102230246251565e-16;   // 2^-53, LAPACK dlamch('E')
@@ -431,6 +434,26 @@ __global__ void __launch_bounds__(kTrdThreads, kTrdCtasPerSm) trd_panel(const __
                 for (int u = 0; u < 8; ++u) a[u] = ring[(stage * 8 + u) * 32];
                 stage ^= 1;
                 double p[8];
+#if KFAC_SYMV_FP32
+                // fp32 products and short fp32 partial sums (4 columns / 8 rows), fp64 beyond
+                float tf0 = 0.f, tf1 = 0.f, tf2 = 0.f, tf3 = 0.f;
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int rr = r + u;
+                    const float ax = cc <= rr ? a[u].x : 0.f, ay = cc + 1 <= rr ? a[u].y : 0.f;
+                    const float az = cc + 2 <= rr ? a[u].z : 0.f, aw = cc + 3 <= rr ? a[u].w : 0.f;
+                    p[u] = (double)fmaf(ax, v.x, fmaf(ay, v.y, fmaf(az, v.z, aw * v.w)));
+                    const float vr = rr < r1 ? vsm[rr - c0] : 0.f;
+                    tf0 = fmaf(cc < rr ? ax : 0.f, vr, tf0);
+                    tf1 = fmaf(cc + 1 < rr ? ay : 0.f, vr, tf1);
+                    tf2 = fmaf(cc + 2 < rr ? az : 0.f, vr, tf2);
+                    tf3 = fmaf(cc + 3 < rr ? aw : 0.f, vr, tf3);
+                }
+                t0 += (double)tf0;
+                t1 += (double)tf1;
+                t2 += (double)tf2;
+                t3 += (double)tf3;
+#else
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
                     const int rr = r + u;
@@ -443,6 +466,7 @@ __global__ void __launch_bounds__(kTrdThreads, kTrdCtasPerSm) trd_panel(const __
                     t2 += (cc + 2 < rr ? az : 0.0) * vr;
                     t3 += (cc + 3 < rr ? aw : 0.0) * vr;
                 }
+#endif
                 // butterfly reduce-scatter of the 8 row partials (9 shuffles instead of 40)
                 const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4;
                 double q4[4], q2[2];
