@@ -58,7 +58,7 @@ constexpr int kSymvR = KFAC_SYMV_ROWS;  // symv tile rows (lower triangle only),
 constexpr int kSymvC = 128;             // symv tile columns (one float4 per lane)
 constexpr int kMaxRb = 16384 / kSymvR;   // symv row blocks for n <= 16384
 #ifndef KFAC_SYMV_FP32
-#define KFAC_SYMV_FP32 0                  // 1: fp32 products with 4/8-term fp32 partial sums (experiment)
+#define KFAC_SYMV_FP32 1                  // fp32 products with 4/8-term fp32 partial sums, fp64 beyond (R23)
 #endif
 constexpr int kBt = 512;                // reflectors per back-transformation block
 constexpr int kTs = 128;                // dlarft sub-block (T built recursively from 128-blocks)
