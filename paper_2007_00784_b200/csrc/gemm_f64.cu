@@ -11,7 +11,6 @@
 // memory as fp64 (operands converted once when staged), register prefetch of the next slab.
 #include "internal.cuh"
 
-#include <algorithm>
 #include <cstdlib>
 #include <vector>
 
@@ -417,114 +416,71 @@ __device__ __forceinline__ void issue_direct(const double *base, size_t ld, int 
     }
 }
 
-// One tile of the persistent schedule: its descriptor, origin and slab count (0: nothing to do).
-struct DTile {
-    int di, m0, n0, nk;
-};
-
-__device__ __forceinline__ DTile dtile(const Batch64 &batch, int tile) {
-    DTile r{0, 0, 0, 0};
-    r.di = find_desc(batch, tile);
-    const Gemm64Desc &d = batch.d[r.di];
+__global__ void __launch_bounds__(kPT, 2) gemm64_direct_kernel(const __grid_constant__ Batch64 batch) {
+    extern __shared__ __align__(16) double smem_d[];
+    const int tile = blockIdx.x;
+    const Gemm64Desc &d = batch.d[find_desc(batch, tile)];
     const int local = tile - d.tile_begin;
     const int tiles_n = (d.N + BN - 1) / BN;
-    r.m0 = (local / tiles_n) * kPM;
-    r.n0 = (local % tiles_n) * BN;
-    const int Ne = d.dyn ? min(d.N, d.dyn[0]) : d.N, Ke = d.dyn ? min(d.K, d.dyn[1]) : d.K;
-    if (r.n0 >= Ne || (d.lower && r.n0 >= r.m0 + kPM)) return r;     // empty / above the diagonal
-    r.nk = (Ke + PBK - 1) / PBK;
-    return r;
-}
-
-// Persistent: CTA b takes tiles b, b + G, b + 2G, ... (G = gridDim.x) and runs ONE cp.async
-// pipeline over the concatenation of their slabs, so the next tile's first slabs are in flight
-// while the current tile finishes and writes its epilogue (short-K GEMMs such as the rank-64
-// trailing update are otherwise dominated by per-tile prologue latency).
-__global__ void __launch_bounds__(kPT, 2) gemm64_direct_kernel(const __grid_constant__ Batch64 batch, int total) {
-    extern __shared__ __align__(16) double smem_d[];
+    const int m0 = (local / tiles_n) * kPM, n0 = (local % tiles_n) * BN;
+    const int Me = d.M, Ne = d.dyn ? min(d.N, d.dyn[0]) : d.N, Ke = d.dyn ? min(d.K, d.dyn[1]) : d.K;
+    if (n0 >= Ne) return;
+    if (d.lower && n0 >= m0 + kPM) return;
     const int t = threadIdx.x, warp = t / 32, lane = t % 32;
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem_d);
-    const int wn = warp * 32, g = lane >> 2, q = lane & 3;
+    const double *A = static_cast<const double *>(d.A), *Bm = static_cast<const double *>(d.B);
+    const int a_mn = d.trans_a, b_mn = !d.trans_b;
+    const int sa = a_mn ? kSAm : kSAk, sb = b_mn ? kSBn : kSBk;
 
-    // issue cursor (tile, slab) runs two slabs ahead of the compute cursor
-    int it = blockIdx.x, ik = 0;
-    DTile itl{0, 0, 0, 0};
-    auto next_tile = [&](int &tt, DTile &tl) {      // first tile >= tt with work
-        while (tt < total) {
-            tl = dtile(batch, tt);
-            if (tl.nk > 0) return;
-            tt += gridDim.x;
+    double acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
+    const int wn = warp * 32, g = lane >> 2, q = lane & 3;
+    const int nk = (Ke + PBK - 1) / PBK;
+    auto issue = [&](int kt) {
+        if (kt < nk) {
+            const int st = kt % kDS;
+            const uint32_t da = sbase + (uint32_t)(st * (kDA + kDB)) * 8;
+            issue_direct(A, (size_t)d.lda, a_mn, kPM, sa, m0, Me, kt * PBK, Ke, da, t);
+            issue_direct(Bm, (size_t)d.ldb, b_mn, BN, sb, n0, Ne, kt * PBK, Ke, da + kDA * 8, t);
         }
-    };
-    next_tile(it, itl);
-    int gi = 0;                                      // global slab counter (stage = gi % kDS)
-    auto issue = [&]() {
-        if (it < total) {
-            const Gemm64Desc &d = batch.d[itl.di];
-            const int Me = d.M, Ne = d.dyn ? min(d.N, d.dyn[0]) : d.N, Ke = d.dyn ? min(d.K, d.dyn[1]) : d.K;
-            const int a_mn = d.trans_a, b_mn = !d.trans_b;
-            const uint32_t da = sbase + (uint32_t)((gi % kDS) * (kDA + kDB)) * 8;
-            issue_direct(static_cast<const double *>(d.A), (size_t)d.lda, a_mn, kPM, a_mn ? kSAm : kSAk, itl.m0, Me,
-                         ik * PBK, Ke, da, t);
-            issue_direct(static_cast<const double *>(d.B), (size_t)d.ldb, b_mn, BN, b_mn ? kSBn : kSBk, itl.n0, Ne,
-                         ik * PBK, Ke, da + kDA * 8, t);
-            if (++ik == itl.nk) {
-                ik = 0;
-                it += gridDim.x;
-                next_tile(it, itl);
-            }
-        }
-        ++gi;
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    issue();
-    issue();
-    int ct = blockIdx.x, gc = 0;
-    DTile ctl{0, 0, 0, 0};
-    next_tile(ct, ctl);
-    while (ct < total) {
-        const Gemm64Desc &d = batch.d[ctl.di];
-        const int a_mn = d.trans_a, b_mn = !d.trans_b;
-        double acc[8][8];
+    issue(0);
+    issue(1);
+    for (int kt = 0; kt < nk; ++kt) {
+        asm volatile("cp.async.wait_group 1;" ::: "memory");      // slab kt (this thread's copies)
+        __syncthreads();                        // slab kt landed everywhere; compute(kt-1) done
+        issue(kt + 2);                          // into the stage of slab kt-1
+        const double *As = smem_d + (kt % kDS) * (kDA + kDB), *Bs = As + kDA;
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
+        for (int kk = 0; kk < PBK; kk += 4) {
+            double a[8], b[4];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
-        for (int kt = 0; kt < ctl.nk; ++kt, ++gc) {
-            asm volatile("cp.async.wait_group 1;" ::: "memory");  // slab gc (this thread's copies)
-            __syncthreads();                    // slab gc landed everywhere; compute(gc-1) done
-            issue();                            // slab gc+2 into the stage of slab gc-1
-            const double *As = smem_d + (gc % kDS) * (kDA + kDB), *Bs = As + kDA;
-#pragma unroll
-            for (int kk = 0; kk < PBK; kk += 4) {
-                double a[8], b[4];
-#pragma unroll
-                for (int mi = 0; mi < 8; ++mi) {
-                    const int m = mi * 8 + g, k = kk + q;
-                    a[mi] = As[a_mn ? k * kSAm + m : m * kSAk + k];
-                }
-#pragma unroll
-                for (int ni = 0; ni < 4; ++ni) {
-                    const int n = wn + ni * 8 + g, k = kk + q;
-                    b[ni] = Bs[b_mn ? k * kSBn + n : n * kSBk + k];
-                }
-#pragma unroll
-                for (int mi = 0; mi < 8; ++mi)
-#pragma unroll
-                    for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][2 * ni], acc[mi][2 * ni + 1], a[mi], b[ni]);
+            for (int mi = 0; mi < 8; ++mi) {
+                const int m = mi * 8 + g, k = kk + q;
+                a[mi] = As[a_mn ? k * kSAm + m : m * kSAk + k];
             }
+#pragma unroll
+            for (int ni = 0; ni < 4; ++ni) {
+                const int n = wn + ni * 8 + g, k = kk + q;
+                b[ni] = Bs[b_mn ? k * kSBn + n : n * kSBk + k];
+            }
+#pragma unroll
+            for (int mi = 0; mi < 8; ++mi)
+#pragma unroll
+                for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][2 * ni], acc[mi][2 * ni + 1], a[mi], b[ni]);
         }
-        const int Me = d.M, Ne = d.dyn ? min(d.N, d.dyn[0]) : d.N;
-        int rows[8], cols[4];
-#pragma unroll
-        for (int mi = 0; mi < 8; ++mi) rows[mi] = ctl.m0 + mi * 8 + g;
-#pragma unroll
-        for (int ni = 0; ni < 4; ++ni) cols[ni] = ctl.n0 + wn + ni * 8 + 2 * q;
-        epilogue(d, Me, Ne, rows, cols, acc);
-        ct += gridDim.x;
-        next_tile(ct, ctl);
     }
     asm volatile("cp.async.wait_group 0;" ::: "memory");
+    int rows[8], cols[4];
+#pragma unroll
+    for (int mi = 0; mi < 8; ++mi) rows[mi] = m0 + mi * 8 + g;
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) cols[ni] = n0 + wn + ni * 8 + 2 * q;
+    epilogue(d, Me, Ne, rows, cols, acc);
 }
 
 bool direct_ok(const Gemm64Desc &g) {
@@ -577,8 +533,7 @@ kfac_status_t gemm64_grouped(const Gemm64Desc *descs, int count, cudaStream_t s)
                                                    kDirectSmem));
                 dattr = true;
             }
-            const int grid = std::min(tiles, 2 * num_sms());          // persistent, two CTAs per SM
-            gemm64_direct_kernel<<<grid, kPT, kDirectSmem, s>>>(b, tiles);
+            gemm64_direct_kernel<<<tiles, kPT, kDirectSmem, s>>>(b);
         } else if (pipe) {
             static bool attr = false;
             if (!attr) {
