@@ -965,6 +965,214 @@ __global__ void __launch_bounds__(NT, 1) syrk_tc_planes_kernel(const __grid_cons
     }
 }
 
+
+// ------------------------------------------------- planes SYRK, wide producer --
+// Same pipeline as syrk_tc_planes_kernel with twice the gather throughput: 8 producer warps (warp
+// w fills k-rows w + 8j, j < 4) and 8 drain warps (two per TMEM lane quadrant, 64 columns each,
+// so an accumulator row needs 64 registers), 18 warps in all.
+constexpr int NT2 = 576;
+constexpr int W2_DRAIN0 = 8, W2_ALLOC = 16, W2_MMA = 17;
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n\t"
+        "tcgen05.wait::ld.sync.aligned;"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr)
+        : "memory");
+}
+
+template <bool IS_A>
+__device__ __forceinline__ void syrk_issue_planes8(const SyrkGeom &G, uint32_t st, int2 *tabw, long long r0,
+                                                   long long r_end, const ChunkInfo (&ci)[2], int cc, int warp,
+                                                   int lane, bool diag) {
+    if (!IS_A) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int k = warp + 8 * j;
+            const long long r = r0 + k;
+            const bool rv = r < r_end;
+            const float *rowh = G.src + (size_t)r * G.c_in, *rowl = G.src_lo + (size_t)r * G.c_in;
+#pragma unroll
+            for (int op = 0; op < 2; ++op) {
+                if (op == 1 && diag) break;
+                const uint32_t dhi = st + op * kTileBytes + mn_off(k, 4 * cc);
+                if (ci[op].kind == 1) {
+                    cp_async16(dhi, kBiasChunk, rv ? 16u : 0u);
+                    cp_async16(dhi + 2 * kTileBytes, kBiasChunk, 0u);
+                    continue;
+                }
+                const bool ok = rv && ci[op].kind == 0;
+                cp_async16(dhi, ok ? rowh + ci[op].off : G.src, ok ? 16u : 0u);
+                cp_async16(dhi + 2 * kTileBytes, ok ? rowl + ci[op].off : G.src_lo, ok ? 16u : 0u);
+            }
+        }
+        return;
+    }
+    int org = 0, ihw = 0;
+    {
+        const long long r = r0 + warp + 8 * (lane & 3);
+        const bool rv = r < r_end;
+        const int hw = G.h_out * G.w_out;
+        const int ri = rv ? (int)r : 0;
+        const int img = ri / hw;
+        const int p = ri - img * hw;
+        const int oh = p / G.w_out, ow = p - (p / G.w_out) * G.w_out;
+        const int ih0 = oh * G.stride_h - G.pad_h, iw0 = ow * G.stride_w - G.pad_w;
+        org = ((img * G.h_in + ih0) * G.w_in + iw0) * G.c_in;
+        ihw = rv ? (int)(((unsigned)ih0 << 16) | ((unsigned)iw0 & 0xffffu)) : (int)0x80000000;
+    }
+    __syncwarp();
+    if (lane < 4) tabw[lane] = make_int2(org, ihw);
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int k = warp + 8 * j;
+        const int2 rd = tabw[j];
+        const int o = rd.x, hv = rd.y;
+        const bool rv = hv != (int)0x80000000;
+        const int ih0 = hv >> 16, iw0 = (int)(short)(hv & 0xffff);
+#pragma unroll
+        for (int op = 0; op < 2; ++op) {
+            if (op == 1 && diag) break;
+            const uint32_t dhi = st + op * kTileBytes + mn_off(k, 4 * cc);
+            const uint32_t dlo = dhi + 2 * kTileBytes;
+            const ChunkInfo &c = ci[op];
+            if (c.kind == 1) {
+                cp_async16(dhi, kBiasChunk, rv ? 16u : 0u);
+                cp_async16(dlo, kBiasChunk, 0u);
+                continue;
+            }
+            const bool ok = rv && c.kind == 0 && (unsigned)(ih0 + c.kh) < (unsigned)G.h_in &&
+                            (unsigned)(iw0 + c.kw) < (unsigned)G.w_in;
+            cp_async16(dhi, ok ? G.src + (o + c.off) : G.src, ok ? 16u : 0u);
+            cp_async16(dlo, ok ? G.src_lo + (o + c.off) : G.src_lo, ok ? 16u : 0u);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(NT2, 1) syrk_tc_planes8_kernel(const __grid_constant__ SyrkBatch batch) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    const uint32_t a0 = smem_u32(smem_raw);
+    uint8_t *base = smem_raw + (((a0 + 1023u) & ~1023u) - a0);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(base + kPS * kPlaneStage);
+    const uint32_t full = smem_u32(bars), empty = smem_u32(bars + kPS);
+    const uint32_t tfull = smem_u32(bars + 2 * kPS), tempty = smem_u32(bars + 2 * kPS + 2);
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * kPS + 4);
+    int2 *rowtab = reinterpret_cast<int2 *>(bars + 32);
+
+    const int item = blockIdx.x;
+    const FactorJob &J = batch.j[find_job(batch, item)];
+    const int local = item - J.item_begin;
+    const int tau = local / J.splits, split = local % J.splits;
+    int ti, tj;
+    upper_tile(tau, J.t1d, ti, tj);
+    const bool diag = ti == tj;
+    const long long r_begin = (long long)split * J.chunk;
+    const long long r_end = min(J.n, r_begin + J.chunk);
+    const int nk = (int)((r_end - r_begin + BK - 1) / BK);
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kPS; ++i) {
+            mbar_init(full + 8 * i, 256);
+            mbar_init(empty + 8 * i, 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(tfull + 8 * b, 1);
+            mbar_init(tempty + 8 * b, 256);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == W2_ALLOC) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(kTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const int drain = batch.drain;
+
+    if (warp == W2_MMA) {
+        if (lane == 0) {
+            const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | (1u << 16) |
+                                   ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+            for (int kb = 0; kb < nk; ++kb) {
+                const int s = kb % kPS;
+                const int seg = kb / drain, pos = kb - seg * drain, b = seg & 1, u = seg >> 1;
+                mbar_wait(full + 8 * s, (kb / kPS) & 1);
+                if (pos == 0 && u >= 1) mbar_wait(tempty + 8 * b, (u - 1) & 1);
+                tc_fence_after();
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                const uint32_t st = smem_u32(base + s * kPlaneStage);
+                const uint32_t a_hi = st, a_lo = st + 2 * kTileBytes;
+                const uint32_t b_hi = diag ? a_hi : st + kTileBytes, b_lo = diag ? a_lo : st + 3 * kTileBytes;
+                const uint32_t dt = tmem + b * BN;
+#pragma unroll
+                for (int ks = 0; ks < BK / 8; ++ks) {
+                    mma_tf32(dt, operand_desc(a_lo, ks, 1), operand_desc(b_hi, ks, 1), idesc, (ks > 0 || pos > 0) ? 1u : 0u);
+                    mma_tf32(dt, operand_desc(a_hi, ks, 1), operand_desc(b_lo, ks, 1), idesc, 1u);
+                    mma_tf32(dt, operand_desc(a_hi, ks, 1), operand_desc(b_hi, ks, 1), idesc, 1u);
+                }
+                mma_commit(empty + 8 * s);
+                if (pos == drain - 1 || kb == nk - 1) mma_commit(tfull + 8 * b);
+            }
+        }
+    } else if (warp < W2_DRAIN0) {
+        const int cc = lane;
+        ChunkInfo ci[2] = {chunk_info(J, ti * BM + 4 * cc), chunk_info(J, tj * BM + 4 * cc)};
+        SyrkGeom G{J.src, J.is_a, J.c_in, J.h_in, J.w_in, J.h_out, J.w_out,
+                   J.stride_h, J.stride_w, J.pad_h, J.pad_w, J.src_lo};
+        const bool plain = !G.is_a || (J.k_w == 1 && J.h_in == J.h_out && J.w_in == J.w_out && J.pad_h == 0 &&
+                                       J.pad_w == 0 && J.stride_h == 1 && J.stride_w == 1);
+        int2 *tabw = rowtab + warp * 4;
+        for (int kb = 0; kb < nk; ++kb) {
+            const int s = kb % kPS;
+            if (kb >= kPS) mbar_wait(empty + 8 * s, ((kb / kPS) - 1) & 1);
+            const uint32_t st = smem_u32(base + s * kPlaneStage);
+            if (plain)
+                syrk_issue_planes8<false>(G, st, tabw, r_begin + (long long)kb * BK, r_end, ci, cc, warp, lane, diag);
+            else
+                syrk_issue_planes8<true>(G, st, tabw, r_begin + (long long)kb * BK, r_end, ci, cc, warp, lane, diag);
+            cp_async_arrive(full + 8 * s);
+        }
+    } else if (warp < W2_ALLOC) {
+        // drain warp: TMEM lane quadrant (warp % 4), column half h
+        const int wq = warp % 4, h = (warp - W2_DRAIN0) / 4;
+        float acc[64];
+#pragma unroll
+        for (int j = 0; j < 64; ++j) acc[j] = 0.f;
+        const int nseg = (nk + drain - 1) / drain;
+        for (int sg = 0; sg < nseg; ++sg) {
+            const int b = sg & 1;
+            mbar_wait(tfull + 8 * b, (sg >> 1) & 1);
+            tc_fence_after();
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                uint32_t r[16];
+                tmem_ld16(tmem + b * BN + ((uint32_t)(wq * 32) << 16) + h * 64 + c * 16, r);
+#pragma unroll
+                for (int j = 0; j < 16; ++j) acc[c * 16 + j] += __uint_as_float(r[j]);
+            }
+            tc_fence_before();
+            mbar_arrive(tempty + 8 * b);
+        }
+        float4 *dst = reinterpret_cast<float4 *>(J.partial + ((size_t)split * J.tiles + tau) * (BM * BN) +
+                                                 (size_t)(wq * 32 + lane) * BN + h * 64);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) dst[j] = make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == W2_ALLOC) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+    }
+}
+
 // ------------------------------------------------------------- host side --
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -1007,6 +1215,15 @@ int g_drain_gemm() {
 int g_drain_syrk() {
     static int v = drain_env("KFAC_TC_DRAIN_SYRK", 2);
     return v;
+}
+
+bool g_syrk_narrow() {         // KFAC_SYRK_NARROW=1: the 4-producer-warp planes SYRK
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("KFAC_SYRK_NARROW");
+        v = (e && e[0] == '1') ? 1 : 0;
+    }
+    return v == 1;
 }
 
 bool g_tc_disabled() {
@@ -1193,7 +1410,15 @@ kfac_status_t syrk_tc_partial(const FactorJob *jobs, int count, cudaStream_t s) 
         bool planes = true;
         for (int i = 0; i < b.count; ++i) planes = planes && b.j[i].src_lo != nullptr;
         const int prof = prof_begin(KFAC_PROF_SYRK_TC, s);
-        if (planes) {
+        if (planes && !g_syrk_narrow()) {
+            static bool pattr8 = false;
+            if (!pattr8) {
+                KFAC_CUDA_TRY(cudaFuncSetAttribute(syrk_tc_planes8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   kSmemBytes));
+                pattr8 = true;
+            }
+            syrk_tc_planes8_kernel<<<items, NT2, kSmemBytes, s>>>(b);
+        } else if (planes) {
             static bool pattr = false;
             if (!pattr) {
                 KFAC_CUDA_TRY(cudaFuncSetAttribute(syrk_tc_planes_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
