@@ -716,15 +716,19 @@ struct MergeDesc {
 // Non-deflated entries go to [0, k) of (dval, zval, col) in ascending d; deflated ones fill
 // [k, n) from the back.  Rotations (p, j, c, s) act on original columns: q_p <- c q_p + s q_j,
 // q_j <- c q_j - s q_p.
-__global__ void dc_deflate(const TrdJob *jobs, const MergeDesc *merges, int ping) {
+__global__ void dc_deflate(const TrdJob *jobs, const MergeDesc *merges, int ping, int smem_n) {
+    // With smem_n >= nm the sorted (d, z, col) lists live in shared memory for the serial deflation
+    // scan (dynamic smem: 2 smem_n doubles + smem_n ints); otherwise in the global scratch arrays.
+    extern __shared__ double dsm[];
     const MergeDesc M = merges[blockIdx.x];
     const TrdJob &J = jobs[M.job];
     const int a = M.a, n1 = M.n1, nm = M.n1 + M.n2, ldw = J.ldw;
     const double *Z = ping ? J.Z1 : J.Z0;
     const double rho = J.e[a + n1 - 1];
     const double sgn = rho < 0 ? -1.0 : 1.0;
-    double *dv = J.dval + a, *zv = J.zval + a;
-    int *col = J.col + a;
+    const bool sm = nm <= smem_n;
+    double *dv = sm ? dsm : J.dval + a, *zv = sm ? dsm + smem_n : J.zval + a;
+    int *col = sm ? reinterpret_cast<int *>(dsm + 2 * (size_t)smem_n) : J.col + a;
     const double rs2 = 0.70710678118654752440;
     double dmax = 0.0, zmax = 0.0;
     for (int c = threadIdx.x; c < nm; c += blockDim.x) {
@@ -762,85 +766,97 @@ __global__ void dc_deflate(const TrdJob *jobs, const MergeDesc *merges, int ping
         zmax = fmax(zmax, __shfl_xor_sync(0xffffffffu, zmax, o));
     }
     __shared__ double shd[32], shz[32];
+    __shared__ int s_k, s_ndef, s_all;
     if (threadIdx.x % 32 == 0) {
         shd[threadIdx.x / 32] = dmax;
         shz[threadIdx.x / 32] = zmax;
     }
     __syncthreads();
-    if (threadIdx.x != 0) return;
-    for (int w = 0; w < (int)(blockDim.x / 32); ++w) {
-        dmax = fmax(dmax, shd[w]);
-        zmax = fmax(zmax, shz[w]);
-    }
-    const double rho2 = 2.0 * fabs(rho);
-    const double tol = 8.0 * kEps * fmax(dmax, zmax);
-    int *posof = J.posof + a, *rp = J.rot_p + a, *rj = J.rot_j + a;
-    double *rc = J.rot_c + a, *rsn = J.rot_s + a;
-    int k = 0, nrot = 0;
-    if (rho2 * zmax <= tol) {
-        // everything deflates: keep order
-        for (int j = 0; j < nm; ++j) posof[col[j]] = j;
-        J.mstate[4 * a + 0] = 0;
-        J.mstate[4 * a + 1] = 0;
-        J.mstate[4 * a + 2] = 0;
-        J.mstate[4 * a + 3] = 0;
-        J.mscal[2 * a + 0] = rho2;
-        J.mscal[2 * a + 1] = tol;
-        return;
-    }
-    // Deflated list is accumulated in rtau/rorg scratch (value, col) and appended at the end.
     double *defv = J.rtau + a;
     int *defc = J.rorg + a;
-    int ndef = 0;
-    int pj = -1;
-    double dp = 0.0, zp = 0.0;
-    int cp = 0;
-    for (int j = 0; j < nm; ++j) {
-        double dj = dv[j], zj = zv[j];
+    if (threadIdx.x == 0) {
+        for (int w = 0; w < (int)(blockDim.x / 32); ++w) {
+            dmax = fmax(dmax, shd[w]);
+            zmax = fmax(zmax, shz[w]);
+        }
+        const double rho2 = 2.0 * fabs(rho);
+        const double tol = 8.0 * kEps * fmax(dmax, zmax);
+        int *rp = J.rot_p + a, *rj = J.rot_j + a;
+        double *rc = J.rot_c + a, *rsn = J.rot_s + a;
+        int k = 0, nrot = 0, ndef = 0;
+        s_all = rho2 * zmax <= tol;
+        if (!s_all) {
+            // Deflated entries are accumulated in rtau/rorg scratch (value, col) and appended.
+            int pj = -1;
+            double dp = 0.0, zp = 0.0;
+            int cp = 0;
+            for (int j = 0; j < nm; ++j) {
+                double dj = dv[j], zj = zv[j];
+                const int cj = col[j];
+                if (rho2 * fabs(zj) <= tol) {
+                    defv[ndef] = dj;
+                    defc[ndef++] = cj;
+                    continue;
+                }
+                if (pj < 0) {
+                    pj = j; dp = dj; zp = zj; cp = cj;
+                    continue;
+                }
+                double sv = zp, cv = zj;
+                const double tt = hypot(cv, sv);
+                const double t = dj - dp;
+                cv /= tt;
+                sv = -sv / tt;
+                if (fabs(t * cv * sv) <= tol) {
+                    // deflate p after rotating (p, j)
+                    zj = tt;
+                    rp[nrot] = cp; rj[nrot] = cj; rc[nrot] = cv; rsn[nrot] = sv; ++nrot;
+                    const double t2 = dp * cv * cv + dj * sv * sv;
+                    dj = dp * sv * sv + dj * cv * cv;
+                    defv[ndef] = t2;
+                    defc[ndef++] = cp;
+                    pj = j; dp = dj; zp = zj; cp = cj;
+                } else {
+                    dv[k] = dp; zv[k] = zp; col[k] = cp; ++k;
+                    pj = j; dp = dj; zp = zj; cp = cj;
+                }
+            }
+            if (pj >= 0) {
+                dv[k] = dp; zv[k] = zp; col[k] = cp; ++k;
+            }
+        }
+        s_k = k;
+        s_ndef = ndef;
+        J.mstate[4 * a + 0] = k;
+        J.mstate[4 * a + 1] = nrot;
+        J.mstate[4 * a + 2] = k;
+        J.mstate[4 * a + 3] = k;
+        J.mscal[2 * a + 0] = rho2;
+        J.mscal[2 * a + 1] = tol;
+    }
+    __syncthreads();
+    // everything deflated: keep the sorted order; otherwise append the deflated list after k
+    const int k = s_k, ndef = s_ndef;
+    if (!s_all) {
+        for (int q = threadIdx.x; q < ndef; q += blockDim.x) {
+            dv[k + q] = defv[q];
+            col[k + q] = defc[q];
+            zv[k + q] = 0.0;
+        }
+        __syncthreads();
+    }
+    int *posof = J.posof + a;
+    double *gdv = J.dval + a, *gzv = J.zval + a;
+    int *gcol = J.col + a;
+    for (int j = threadIdx.x; j < nm; j += blockDim.x) {
         const int cj = col[j];
-        if (rho2 * fabs(zj) <= tol) {
-            defv[ndef] = dj;
-            defc[ndef++] = cj;
-            continue;
-        }
-        if (pj < 0) {
-            pj = j; dp = dj; zp = zj; cp = cj;
-            continue;
-        }
-        double s = zp, c = zj;
-        const double tt = hypot(c, s);
-        const double t = dj - dp;
-        c /= tt;
-        s = -s / tt;
-        if (fabs(t * c * s) <= tol) {
-            // deflate p after rotating (p, j)
-            zj = tt;
-            rp[nrot] = cp; rj[nrot] = cj; rc[nrot] = c; rsn[nrot] = s; ++nrot;
-            const double t2 = dp * c * c + dj * s * s;
-            dj = dp * s * s + dj * c * c;
-            defv[ndef] = t2;
-            defc[ndef++] = cp;
-            pj = j; dp = dj; zp = zj; cp = cj;
-        } else {
-            dv[k] = dp; zv[k] = zp; col[k] = cp; ++k;
-            pj = j; dp = dj; zp = zj; cp = cj;
+        posof[cj] = j;
+        if (sm) {
+            gdv[j] = dv[j];
+            gzv[j] = zv[j];
+            gcol[j] = cj;
         }
     }
-    if (pj >= 0) {
-        dv[k] = dp; zv[k] = zp; col[k] = cp; ++k;
-    }
-    for (int q = 0; q < ndef; ++q) {
-        dv[k + q] = defv[q];
-        col[k + q] = defc[q];
-        zv[k + q] = 0.0;
-    }
-    for (int j = 0; j < nm; ++j) posof[col[j]] = j;
-    J.mstate[4 * a + 0] = k;
-    J.mstate[4 * a + 1] = nrot;
-    J.mstate[4 * a + 2] = k;
-    J.mstate[4 * a + 3] = k;
-    J.mscal[2 * a + 0] = rho2;
-    J.mscal[2 * a + 1] = tol;
 }
 
 // Qnd[a + r][posof[c]] = (block-diagonal child eigenvectors)[r][c]  (one warp per row).
@@ -1545,7 +1561,16 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
         moff += nmg;
         int nmax = 0;
         for (auto &m : lv) nmax = std::max(nmax, m.n1 + m.n2);
-        dc_deflate<<<nmg, 256, 0, s>>>(djobs, dm, ping);
+        // sorted lists in shared memory when they fit (2 doubles + 1 int per entry)
+        const int smem_n = (nmax * 20 <= 200 * 1024) ? nmax : 0;
+        if (smem_n) {
+            static bool dattr = false;
+            if (!dattr) {
+                KFAC_CUDA_TRY(cudaFuncSetAttribute(dc_deflate, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024 + 64));
+                dattr = true;
+            }
+        }
+        dc_deflate<<<nmg, 256, smem_n ? (size_t)smem_n * 20 + 16 : 0, s>>>(djobs, dm, ping, smem_n);
         KFAC_LAUNCHED();
         dc_permute<<<dim3(cdiv(nmax, 8), nmg), 256, 0, s>>>(djobs, dm, ping);
         KFAC_LAUNCHED();
