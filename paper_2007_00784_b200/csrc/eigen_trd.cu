@@ -1064,19 +1064,26 @@ __global__ void dc_build_s(const TrdJob *jobs, const MergeDesc *merges) {
 
 // Final order of the merged eigenvalues: lambda_j (j < k, from the GEMM output Tmp) and the
 // deflated d's (Qnd columns k..n-1); rank by counting (ties by index).
-__global__ void dc_rank(const TrdJob *jobs, const MergeDesc *merges) {
+__global__ void dc_rank(const TrdJob *jobs, const MergeDesc *merges, int smem_n) {
     const MergeDesc M = merges[blockIdx.y];
     const TrdJob &J = jobs[M.job];
     const int a = M.a, nm = M.n1 + M.n2, k = J.mstate[4 * a + 0];
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= nm) return;
     const double *dv = J.dval + a, *rt = J.rtau + a;
     const int *ro = J.rorg + a;
     auto val = [&](int q) { return q < k ? dv[ro[q]] + rt[q] : dv[q]; };
-    const double ve = val(e);
+    // all nm values staged in shared memory once per block (when they fit), then counted from there
+    extern __shared__ double vals[];
+    const bool sm = nm <= smem_n;
+    if (sm) {
+        for (int q = threadIdx.x; q < nm; q += blockDim.x) vals[q] = val(q);
+        __syncthreads();
+    }
+    if (e >= nm) return;
+    const double ve = sm ? vals[e] : val(e);
     int rk = 0;
     for (int f = 0; f < nm; ++f) {
-        const double vf = val(f);
+        const double vf = sm ? vals[f] : val(f);
         rk += (vf < ve) || (vf == ve && f < e);
     }
     J.D[a + rk] = ve;
@@ -1597,7 +1604,17 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
             gd.push_back(g);
         }
         RET_OK(gemm64_grouped(gd.data(), (int)gd.size(), s));
-        dc_rank<<<dim3(cdiv(nmax, 128), nmg), 128, 0, s>>>(djobs, dm);
+        {
+            const int rank_n = (nmax * 8 <= 96 * 1024) ? nmax : 0;
+            if (rank_n) {
+                static bool rattr = false;
+                if (!rattr) {
+                    KFAC_CUDA_TRY(cudaFuncSetAttribute(dc_rank, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+                    rattr = true;
+                }
+            }
+            dc_rank<<<dim3(cdiv(nmax, 128), nmg), 128, (size_t)rank_n * 8, s>>>(djobs, dm, rank_n);
+        }
         KFAC_LAUNCHED();
         dc_assemble<<<dim3(cdiv(nmax, 128), nmax, nmg), 128, 0, s>>>(djobs, dm, ping);
         KFAC_LAUNCHED();
