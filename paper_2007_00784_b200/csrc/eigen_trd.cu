@@ -177,6 +177,7 @@ struct PanelLaunch {
     int cta_begin[kMaxGroupCtas + 1];
     int ring_off;                          // float offset of the symv prefetch ring in dynamic smem
     int use_xs;                            // x of the merged column kept in shared memory
+    int fused;                             // trailing update fused into the panel kernel
 };
 
 // One panel of 32 columns (LAPACK dlatrd, lower) for every active factor.  Column k (i = k - p0):
@@ -609,6 +610,80 @@ __global__ void __launch_bounds__(kTrdThreads, kTrdCtasPerSm) trd_panel(const __
         }
         w_next = (float)(yk1 + alpha2);                 // row k+1: v = 1
         __syncthreads();
+    }
+    if (L.fused && p0 + kNb < n) {
+        // Fused rank-64 trailing update A[q0:n, q0:n] -= V W^T + W V^T (lower 64 x 64 tiles) on the
+        // fp64 tensor cores, by the same group once every CTA has written its rows of the panel:
+        // two teams of 8 warps per CTA, each tile's whole K = 64 of [V|W] and [W|V] (fp64 copies)
+        // staged at once in shared memory (row stride 68 doubles), 16 DMMA k-steps, fp32 RMW.
+        group_barrier(J.bar, target, nc);
+        const int q0 = p0 + kNb, m = n - q0, nt = (m + 63) / 64, ntiles = nt * (nt + 1) / 2;
+        const int team = warp / 8, tw = warp % 8, tt = t % 256;
+        double *Ts = reinterpret_cast<double *>(vsm + ring_off) + (size_t)team * (2 * 64 * 68);
+        double *As = Ts, *Bs = Ts + 64 * 68;
+        const uint32_t as_s = (uint32_t)__cvta_generic_to_shared(As), bs_s = (uint32_t)__cvta_generic_to_shared(Bs);
+        const int wr = (tw / 2) * 16, wc = (tw % 2) * 32, g = lane >> 2, q = lane & 3;
+        for (int tile = c * 2 + team; tile < ntiles; tile += nc * 2) {
+            int ti = 0, rem = tile;                       // lower tiles row-major: row ti has ti + 1
+            while (rem > ti) { rem -= ti + 1; ++ti; }
+            const int tj = rem;
+            const int r0 = q0 + ti * 64, c0t = q0 + tj * 64;
+            // stage A = VWd[r0 .. r0+63, 0:64), B = WVd[c0t .. c0t+63, 0:64) (16-B chunks, zero fill)
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int ch = tt + 256 * u, row = ch / 32, k2 = (ch % 32) * 2;
+                const bool oka = r0 + row < n, okb = c0t + row < n;
+                const double *sa = oka ? J.VWd + (size_t)(r0 + row) * 64 + k2 : J.VWd;
+                const double *sb = okb ? J.WVd + (size_t)(c0t + row) * 64 + k2 : J.WVd;
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(as_s + (uint32_t)(row * 68 + k2) * 8),
+                             "l"(sa), "r"(oka ? 16u : 0u) : "memory");
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(bs_s + (uint32_t)(row * 68 + k2) * 8),
+                             "l"(sb), "r"(okb ? 16u : 0u) : "memory");
+            }
+            asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+            asm volatile("bar.sync %0, 256;" ::"r"(team + 1) : "memory");
+            double acc[2][4][2];
+#pragma unroll
+            for (int a = 0; a < 2; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+#pragma unroll 4
+            for (int kk = 0; kk < 64; kk += 4) {
+                double fa[2], fb[4];
+#pragma unroll
+                for (int a = 0; a < 2; ++a) fa[a] = As[(wr + a * 8 + g) * 68 + kk + q];
+#pragma unroll
+                for (int b = 0; b < 4; ++b) fb[b] = Bs[(wc + b * 8 + g) * 68 + kk + q];
+#pragma unroll
+                for (int a = 0; a < 2; ++a)
+#pragma unroll
+                    for (int b = 0; b < 4; ++b)
+                        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                                     : "+d"(acc[a][b][0]), "+d"(acc[a][b][1])
+                                     : "d"(fa[a]), "d"(fb[b]));
+            }
+            // C (fp32 working matrix) -= acc: element (r0 + wr + 8a + g, c0t + wc + 8b + 2q + e)
+            float *Aw = const_cast<float *>(A);
+#pragma unroll
+            for (int a = 0; a < 2; ++a) {
+                const int rr = r0 + wr + a * 8 + g;
+                if (rr >= n) continue;
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    const int cc2 = c0t + wc + b * 8 + 2 * q;
+                    float *cp = Aw + (size_t)rr * ldw + cc2;
+                    if (cc2 + 1 < n) {
+                        float2 cv = *reinterpret_cast<float2 *>(cp);
+                        cv.x = (float)((double)cv.x - acc[a][b][0]);
+                        cv.y = (float)((double)cv.y - acc[a][b][1]);
+                        *reinterpret_cast<float2 *>(cp) = cv;
+                    } else if (cc2 < n) {
+                        cp[0] = (float)((double)cp[0] - acc[a][b][0]);
+                    }
+                }
+            }
+            asm volatile("bar.sync %0, 256;" ::"r"(team + 1) : "memory");   // smem reused by the next tile
+        }
     }
 }
 
@@ -1320,6 +1395,15 @@ T *rebase(T *p, char *base) {
     return reinterpret_cast<T *>(base + reinterpret_cast<uintptr_t>(p));
 }
 
+bool trail_fused() {       // KFAC_TRD_FUSED_TRAIL=1: trailing update inside trd_panel
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("KFAC_TRD_FUSED_TRAIL");
+        v = (e && e[0] == '1') ? 1 : 0;
+    }
+    return v == 1;
+}
+
 bool trail_tc() {
     static int v = -1;
     if (v < 0) {
@@ -1424,6 +1508,7 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
     const size_t smem_xs = (size_t)round_up(max_n, 2) * sizeof(double);
     const int use_xs = smem_base + smem_xs + 12 * 1024 <= 227 * 1024;
     const size_t smem = smem_base + (use_xs ? smem_xs : 0);
+    const int fused_trail = trail_fused() && smem - (size_t)ring_off * sizeof(float) >= 2 * 2 * 64 * 68 * sizeof(double);
     const int cap = panel_capacity(smem);
     static PanelLaunch PL;
     // Staggered schedule: factor j (P_j panels) starts at launch P_max - P_j, so all factors finish
@@ -1472,6 +1557,7 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
         PL.count = na;
         PL.ring_off = ring_off;
         PL.use_xs = use_xs;
+        PL.fused = fused_trail;
         int tot = 0;
         for (int q = 0; q < na; ++q) {
             PL.job[q] = act[q];
@@ -1504,6 +1590,7 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
         pst = pst_all;
         const int na = (int)act.size();
         gd.clear();
+        if (fused_trail) continue;                  // done inside trd_panel
         if (trail_tc()) {
             // rank-64 trailing update on the tcgen05 3xTF32 engine (fp32-faithful products, fp32
             // accumulation with IEEE drains; experiment switch KFAC_TRD_TRAIL_TC=1)
