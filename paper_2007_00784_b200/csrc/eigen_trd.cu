@@ -1395,11 +1395,11 @@ T *rebase(T *p, char *base) {
     return reinterpret_cast<T *>(base + reinterpret_cast<uintptr_t>(p));
 }
 
-bool trail_fused() {       // KFAC_TRD_FUSED_TRAIL=1: trailing update inside trd_panel
+bool trail_fused() {       // trailing update inside trd_panel (KFAC_TRD_FUSED_TRAIL=0: separate GEMM)
     static int v = -1;
     if (v < 0) {
         const char *e = getenv("KFAC_TRD_FUSED_TRAIL");
-        v = (e && e[0] == '1') ? 1 : 0;
+        v = (e && e[0] == '0') ? 0 : 1;
     }
     return v == 1;
 }
