@@ -72,8 +72,9 @@ def peaks():
 
 
 PROF_CLASSES = (1, 2, 3, 4)     # KFAC_PROF_* in include/kfac.h
-PROF_NAMES = {1: ("trd_panel (Householder tridiagonalisation panel: lower-triangle symv, "
-                  "4 B per trailing-matrix element per column)", "hbm"),
+PROF_NAMES = {1: ("trd_panel (Householder tridiagonalisation panel: lower-triangle symv, 4 B per "
+                  "trailing-matrix element per column, + the fused rank-64 trailing update: 8 B per "
+                  "lower element per panel)", "hbm"),
               2: ("gemm64 (fp64-accumulating eigensolver GEMMs)", "alu"),
               3: ("syrk_tc_kernel (factor SYRK, tcgen05 3xTF32)", "tensor"),
               4: ("gemm_tc_kernel (preconditioning GEMMs, tcgen05 3xTF32)", "tensor")}

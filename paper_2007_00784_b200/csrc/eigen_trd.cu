@@ -1582,6 +1582,11 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
                     by += 4.0 * m * (m + 1) / 2;
                     fl += 2.0 * m * m;
                 }
+                const double mt = n - pst[q] - kNb;          // fused trailing update of the panel
+                if (fused_trail && mt > 0) {
+                    by += 8.0 * mt * (mt + 1) / 2 + 2.0 * 8 * 64 * mt;   // C lower RMW + [V|W], [W|V]
+                    fl += 2.0 * 64 * mt * (mt + 1);
+                }
             }
             prof_end(prof, s, by, fl);
         }
