@@ -155,16 +155,29 @@ __device__ __forceinline__ void part_range(int r0, int n, int c, int nc, int &lo
 // ------------------------------------------------------------ init --
 // A = (F + F^T)/2 in fp32 (pads zero), Vb = 0.
 __global__ void trd_init(const TrdJob *jobs) {
+    // 32 x 32 tiles (grid-stride over the tile grid of the factor): F's tile and its transposed
+    // partner are both read row-wise (coalesced) through shared memory.
+    __shared__ float tr[32][33];
     const TrdJob &J = jobs[blockIdx.y];
     const int n = J.n, ldw = J.ldw;
-    const long long total = (long long)n * ldw;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-         i += (long long)gridDim.x * blockDim.x) {
-        const int r = (int)(i / ldw), c = (int)(i % ldw);
-        float a = 0.f;
-        if (c < n) a = 0.5f * (J.F[(size_t)r * J.ldF + c] + J.F[(size_t)c * J.ldF + r]);
-        J.A[i] = a;
-        J.Vb[i] = 0.f;
+    const int tn = (ldw + 31) / 32, tiles = tn * tn;
+    const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;      // 32 x 8 threads
+    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        const int r0 = (tile / tn) * 32, c0 = (tile % tn) * 32;
+        __syncthreads();
+        for (int y = ty; y < 32; y += 8) {          // F[c0 + y][r0 + tx] -> tr[y][tx]
+            const int rr = c0 + y, cc = r0 + tx;
+            tr[y][tx] = (rr < n && cc < n) ? J.F[(size_t)rr * J.ldF + cc] : 0.f;
+        }
+        __syncthreads();
+        for (int y = ty; y < 32; y += 8) {
+            const int r = r0 + y, c = c0 + tx;
+            if (r >= n || c >= ldw) continue;
+            float a = 0.f;
+            if (c < n) a = 0.5f * (J.F[(size_t)r * J.ldF + c] + tr[tx][y]);
+            J.A[(size_t)r * ldw + c] = a;
+            J.Vb[(size_t)r * ldw + c] = 0.f;
+        }
     }
 }
 
@@ -1493,7 +1506,8 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
     KFAC_LAUNCHED();
     std::vector<Gemm64Desc> gd;
     if (mode != TRD_DEBUG_STEDC) {
-    trd_init<<<dim3(std::min(2048, cdiv((long long)max_n * ldw_for(max_n), 256)), count), 256, 0, s>>>(djobs);
+    trd_init<<<dim3(std::min(2048, cdiv((long long)ldw_for(max_n), 32) * cdiv((long long)ldw_for(max_n), 32)), count), 256,
+               0, s>>>(djobs);
     KFAC_LAUNCHED();
 
     // ---- (1) tridiagonalisation: one persistent launch + one trailing GEMM per panel ----
