@@ -99,7 +99,9 @@ kfac_status_t kfac_layer_dims(const kfac_layer_t *layer, int32_t *d_a, int32_t *
  * A[l]: device d_A x ld_A[l]; G[l]: device d_G x ld_G[l]; both triangles are written
  * (symmetric).  When first == 0 the previous A/G are read (must be symmetric).
  * out_scale = 1/W before an allreduce-SUM averages the factors.
- * Rows per layer must be < 2^31; decay in [0, 1]. */
+ * Rows per layer must be < 2^31; decay in [0, 1].
+ * Workspace: the per-(tile, row chunk) partial sums and, for the tensor-core factors, the TF32
+ * hi/lo planes of their inputs (two copies of each activation / gradient tensor). */
 size_t kfac_update_factors_workspace_size(const kfac_layer_t *layers, int32_t num_layers);
 kfac_status_t kfac_update_factors(const kfac_layer_t *layers, int32_t num_layers,
                                   const float *const *act, const float *const *gout,
@@ -141,7 +143,9 @@ kfac_status_t kfac_compute_inverse(const float *const *F, const int32_t *dims, c
  *   out = Q_G ((Q_G^T grad Q_A) / D) Q_A^T,  D = v_G v_A^T + damping  (or factored).
  * INVERSE: Q_G = (G + damping I)^{-1}, Q_A = (A + damping I)^{-1}, v_* ignored (may be NULL):
  *   out = Q_G grad Q_A.
- * out may alias grad.  damping >= 0 (denominators are floored at 1e-12). */
+ * out may alias grad.  damping >= 0 (denominators are floored at 1e-12).
+ * Workspace: the intermediates T, V2, U and, for layers whose dimensions are all >= 64, the TF32
+ * hi/lo planes of Q_G, Q_A and grad (pre-split once per call for the tensor-core engine). */
 size_t kfac_precondition_workspace_size(const int32_t *d_g, const int32_t *d_a, int32_t num_layers,
                                         int32_t mode);
 kfac_status_t kfac_precondition(const int32_t *d_g, const int32_t *d_a, int32_t num_layers,
