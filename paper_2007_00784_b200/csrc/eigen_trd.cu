@@ -56,7 +56,8 @@ constexpr int kLeaf = 32;               // D&C leaf size
 #endif
 constexpr int kSymvR = KFAC_SYMV_ROWS;  // symv tile rows (lower triangle only), multiple of 8
 constexpr int kSymvC = 128;             // symv tile columns (one float4 per lane)
-constexpr int kMaxRb = 16384 / kSymvR;   // symv row blocks for n <= 16384
+constexpr int kPairR = 2 * kSymvR;       // rows per column partial (a warp pair's two half tiles)
+constexpr int kMaxRb = 16384 / kPairR;   // super blocks for n <= 16384
 #ifndef KFAC_SYMV_FP32
 #define KFAC_SYMV_FP32 1                  // fp32 products with 4/8-term fp32 partial sums, fp64 beyond (R23)
 #endif
@@ -207,7 +208,8 @@ __global__ void __launch_bounds__(kTrdThreads, kTrdCtasPerSm) trd_panel(const __
     __shared__ double ab[2 * kNb];                   // (V^T v, W^T v)
     __shared__ float rowV[kNb], rowW[kNb];           // V[k, <i], W[k, <i]
     __shared__ double scal[8];
-    __shared__ int tpre[kMaxRb + 1];                 // symv tile prefix per row block
+    __shared__ int tpre[kMaxRb + 1];                 // symv unit prefix per 64-row super block
+    __shared__ __align__(16) double pairbuf[(kTrdWarps / 2) * 2 * 2 * 32 * 2];   // pair column sums
 
     int g = 0;
     {
@@ -331,12 +333,13 @@ __global__ void __launch_bounds__(kTrdThreads, kTrdCtasPerSm) trd_panel(const __
         if (warp == 0) {
             // tile prefix of the symv: tpre[b] = number of 64 x 128 lower-triangle tiles in row
             // blocks < b (block b spans chunks c0 .. its last row), for the warps' tile cursors
-            const int r00 = k + 1, nrb = (n - r00 + kSymvR - 1) / kSymvR;
+            // (units: 64-row super blocks x 128-column chunks, each shared by a warp pair)
+            const int r00 = k + 1, nrb = (n - r00 + kPairR - 1) / kPairR;
             int loc[kMaxRb / 32], run = 0;
 #pragma unroll
             for (int u = 0; u < kMaxRb / 32; ++u) {
                 const int b = lane * (kMaxRb / 32) + u;
-                run += b < nrb ? (min(n, r00 + kSymvR * (b + 1)) - 1 - c0) / kSymvC + 1 : 0;
+                run += b < nrb ? (min(n, r00 + kPairR * (b + 1)) - 1 - c0) / kSymvC + 1 : 0;
                 loc[u] = run;
             }
             int incl = run;
@@ -373,14 +376,17 @@ __global__ void __launch_bounds__(kTrdThreads, kTrdCtasPerSm) trd_panel(const __
         // above the diagonal and past the last row), so the loads of octet q+1 are in flight while
         // octet q is reduced.
         {
-            const int r00 = k + 1, nrb = (n - r00 + kSymvR - 1) / kSymvR;
+            const int r00 = k + 1, nrb = (n - r00 + kPairR - 1) / kPairR;
             const int total = tpre[nrb];
-            const int W = nc * kTrdWarps;
+            const int W = nc * (kTrdWarps / 2);      // warp pairs of the group
+            const int half = warp & 1, pair = warp >> 1;
             const float4 *v4 = reinterpret_cast<const float4 *>(vsm);
             float4 *ring = reinterpret_cast<float4 *>(vsm + ring_off) + (size_t)warp * (2 * 8 * 32) + lane;
-            // octet cursor: tile it (row block bq, chunk jq), first row rq
-            int it = c * kTrdWarps + warp, bq = 0, base = 0, jq = 0, rq = 0;
-            auto locate = [&]() {                    // last row block with tpre[bq] <= it
+            // octet cursor: unit it (64-row super block bq, chunk jq); this warp's 32-row half starts
+            // at hs and every unit yields at least one (possibly fully masked) octet, so both warps of
+            // a pair meet at the same per-unit combine
+            int it = c * (kTrdWarps / 2) + pair, bq = 0, base = 0, jq = 0, rq = 0;
+            auto locate = [&]() {                    // last super block with tpre[bq] <= it
                 int lo2 = bq, hi2 = nrb - 1;
                 while (lo2 < hi2) {
                     const int mid = (lo2 + hi2 + 1) >> 1;
@@ -389,10 +395,10 @@ __global__ void __launch_bounds__(kTrdThreads, kTrdCtasPerSm) trd_panel(const __
                 bq = lo2;
                 base = tpre[bq];
                 jq = it - base;
-                rq = r00 + kSymvR * bq;
+                rq = r00 + kPairR * bq + kSymvR * half;
             };
             auto issue = [&](int stage) {
-                const int rend = min(n, r00 + kSymvR * (bq + 1));
+                const int rend = min(n, r00 + kPairR * bq + kSymvR * (half + 1));
                 const int ccq = c0 + kSymvC * jq + 4 * lane;
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
@@ -424,14 +430,18 @@ __global__ void __launch_bounds__(kTrdThreads, kTrdCtasPerSm) trd_panel(const __
 
             int stage = 0;
             double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
+            double2 *pslot = reinterpret_cast<double2 *>(pairbuf) + (size_t)pair * (2 * 2 * 32);
+            int unit_parity = 0;
             while (it < total) {
                 // current octet
                 const int b = bq, j = jq, r = rq;
-                const int r0 = r00 + kSymvR * b, r1 = min(n, r0 + kSymvR);
+                const int r0 = r00 + kPairR * b + kSymvR * half, r1 = min(n, r0 + kSymvR);
                 const int cc = c0 + kSymvC * j + 4 * lane;
-                // advance the cursor and prefetch the next octet into the other stage
+                // advance the cursor (a unit ends after the half's last octet, or after its single
+                // masked octet when the half is empty) and prefetch the next octet
                 rq += 8;
-                if (rq >= r1) {
+                const bool unit_end = rq >= r1;
+                if (unit_end) {
                     it += W;
                     if (it < total) locate();
                 }
@@ -499,12 +509,22 @@ __global__ void __launch_bounds__(kTrdThreads, kTrdCtasPerSm) trd_panel(const __
                 sd += __shfl_xor_sync(0xffffffffu, sd, 1);
                 const int rs = r + (h16 ? 4 : 0) + (h8 ? 2 : 0) + (h4 ? 1 : 0);
                 if ((lane & 3) == 0 && rs < r1) __stcg(J.DP + (size_t)rs * J.ldp + j, sd);
-                if (r + 8 >= r1) {                   // tile done: its column sums
-                    if (cc < n) __stcg(J.TP + (size_t)cc * J.ldtp + b, t0);
-                    if (cc + 1 < n) __stcg(J.TP + (size_t)(cc + 1) * J.ldtp + b, t1);
-                    if (cc + 2 < n) __stcg(J.TP + (size_t)(cc + 2) * J.ldtp + b, t2);
-                    if (cc + 3 < n) __stcg(J.TP + (size_t)(cc + 3) * J.ldtp + b, t3);
-                    t0 = t1 = t2 = t3 = 0.0;
+                if (unit_end) {                      // unit done: the pair's column sums
+                    double2 *sl = pslot + unit_parity * (2 * 32);
+                    if (half == 1) {
+                        sl[lane] = make_double2(t0, t1);
+                        sl[32 + lane] = make_double2(t2, t3);
+                    }
+                    asm volatile("bar.sync %0, 64;" ::"r"(1 + pair) : "memory");
+                    if (half == 0) {
+                        const double2 u01 = sl[lane], u23 = sl[32 + lane];
+                        if (cc < n) __stcg(J.TP + (size_t)cc * J.ldtp + b, t0 + u01.x);
+                        if (cc + 1 < n) __stcg(J.TP + (size_t)(cc + 1) * J.ldtp + b, t1 + u01.y);
+                        if (cc + 2 < n) __stcg(J.TP + (size_t)(cc + 2) * J.ldtp + b, t2 + u23.x);
+                        if (cc + 3 < n) __stcg(J.TP + (size_t)(cc + 3) * J.ldtp + b, t3 + u23.y);
+                    }
+                    unit_parity ^= 1;                // the other slot is free: its reader passed
+                    t0 = t1 = t2 = t3 = 0.0;         // the barrier of the previous unit already
                 }
             }
         }
@@ -537,14 +557,14 @@ __global__ void __launch_bounds__(kTrdThreads, kTrdCtasPerSm) trd_panel(const __
         __syncthreads();
         double wv = 0.0;
         {
-            const int nrb = (n - (k + 1) + kSymvR - 1) / kSymvR;
+            const int nrb = (n - (k + 1) + kPairR - 1) / kPairR;
             const int sub = lane >> 3, sl = lane & 7;      // 8 lanes per row, 4 rows per warp
             for (int r0 = lo + 4 * warp; r0 < hi; r0 += 4 * kTrdWarps) {
                 const int r = r0 + sub;
                 double yr = 0.0, corr = 0.0;
                 if (r < hi) {
-                    const int b = (r - (k + 1)) / kSymvR;
-                    const int nj = (min(n, k + 1 + kSymvR * (b + 1)) - 1 - c0) / kSymvC + 1;
+                    const int b = (r - (k + 1)) / kPairR;          // TP: 64-row super blocks
+                    const int nj = (min(n, k + 1 + kSymvR * ((r - (k + 1)) / kSymvR + 1)) - 1 - c0) / kSymvC + 1;
                     // independent loads in flight: 4-way unrolled with separate partial sums
                     double y0 = 0.0, y1 = 0.0, y2 = 0.0, y3 = 0.0;
                     const double *dp = J.DP + (size_t)r * J.ldp, *tp = J.TP + (size_t)r * J.ldtp;
@@ -1361,7 +1381,7 @@ Plan plan(const int32_t *dims, int count) {
         TAKE(part, double, (size_t)kMaxGroupCtas * kPart);
         J.ldp = cdiv(n + 3, kSymvC) + 1;
         TAKE(DP, double, (size_t)n * J.ldp);
-        J.ldtp = cdiv(n, kSymvR) + 1;
+        J.ldtp = cdiv(n, kPairR) + 1;
         TAKE(TP, double, (size_t)n * J.ldtp);
 #undef TAKE
         // leaves and merges
