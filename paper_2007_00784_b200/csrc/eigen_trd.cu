@@ -1549,6 +1549,11 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
     // together and the small ones share the GPU with the big ones' small trailing matrices.
     int pmax = 0;
     for (int i = 0; i < count; ++i) pmax = std::max(pmax, cdiv(P.jobs[i].n, kNb));
+    // CTAs per active factor ~ (remaining trailing size)^wexp (default 2: the mat-vec bytes)
+    static const double wexp = [] {
+        const char *e = getenv("KFAC_TRD_WEXP");
+        return e ? atof(e) : 2.0;
+    }();
     for (int t = 0; t < pmax; ++t) {
         std::vector<int> act, pst;
         double wsum = 0.0;
@@ -1558,7 +1563,7 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
             act.push_back(i);
             pst.push_back(pidx * kNb);
             const double m = P.jobs[i].n - pidx * kNb;
-            wsum += m * m;
+            wsum += std::pow(m, wexp);
         }
         if (act.empty()) continue;
         // More active factors than co-resident CTAs (e.g. ResNet-101's 210 factors): the groups are
@@ -1570,7 +1575,7 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
         wsum = 0.0;
         for (size_t q = 0; q < act.size(); ++q) {
             const double m = P.jobs[act[q]].n - pst[q];
-            wsum += m * m;
+            wsum += std::pow(m, wexp);
         }
         const int na = (int)act.size();
         // CTAs per factor ~ remaining work, >= 1, total <= cap, and no more than one 64 x 128 symv
@@ -1580,7 +1585,7 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
         for (int q = 0; q < na; ++q) {
             const double m = P.jobs[act[q]].n - pst[q];
             const int tiles = cdiv((long long)m, kSymvR) * (cdiv((long long)m, kSymvC) + 1) / 2;
-            int want = (int)std::floor((cap - na) * (m * m) / wsum);
+            int want = (int)std::floor((cap - na) * std::pow(m, wexp) / wsum);
             want = std::min(want, std::max(0, (int)(m / 16) - 1));
             want = std::min(want, std::max(0, cdiv(tiles, kTrdWarps) - 1));
             want = std::min(want, spare);
