@@ -183,6 +183,24 @@ __global__ void trd_init(const TrdJob *jobs) {
 }
 
 // ----------------------------------------------------- panel kernel --
+#ifndef KFAC_TRD_TIMING
+#define KFAC_TRD_TIMING 0
+#endif
+#if KFAC_TRD_TIMING
+// Diagnostic build only (-DKFAC_TRD_TIMING=1): clock64 stamps of the phases of every column, taken
+// by thread 0 of three CTAs (first, middle, last) of group 0; read with kfac_debug_trd_timing.
+constexpr int kTimCols = 8192, kTimPts = 10;
+__device__ unsigned long long g_trd_tim[3][kTimCols][kTimPts];
+#define TRD_TS(col, pt)                                                              \
+    do {                                                                             \
+        if (tim_slot >= 0 && (col) < kTimCols) g_trd_tim[tim_slot][col][pt] = clock64(); \
+    } while (0)
+#else
+#define TRD_TS(col, pt) \
+    do {                \
+    } while (0)
+#endif
+
 struct PanelLaunch {
     const TrdJob *jobs;
     int count;
@@ -231,6 +249,9 @@ __global__ void __launch_bounds__(kTrdThreads, kTrdCtasPerSm) trd_panel(const __
     // x of the merged column (phase B), after the ring: 16-byte aligned doubles
     double *xs = reinterpret_cast<double *>(vsm + ring_off + kTrdWarps * 2 * 8 * 32 * 4);
     unsigned target = 0;
+#if KFAC_TRD_TIMING
+    const int tim_slot = (g != 0 || t != 0) ? -1 : c == 0 ? 0 : c == nc / 2 ? 1 : c == nc - 1 ? 2 : -1;
+#endif
     float w_next = 0.f;                              // W[k, i-1], computed redundantly
     // Column k's phase A (its corrected column and diagonal) is folded into column k-1's phase C
     // whenever both lie in the same panel: there every row's c_r = f_r - v_r beta with f_r known
@@ -244,6 +265,7 @@ __global__ void __launch_bounds__(kTrdThreads, kTrdCtasPerSm) trd_panel(const __
         const int k = p0 + i;
         if (k >= n) break;
         int lo, hi;
+        TRD_TS(k, 0);
         // ---------------- phase A (rows [k, n)) ----------------
         if (!merged) {
         if (t < i) {
@@ -280,23 +302,38 @@ __global__ void __launch_bounds__(kTrdThreads, kTrdCtasPerSm) trd_panel(const __
         if (t == 0) __stcg(part + (size_t)c * kPart + 2 * kNb, s2);
         group_barrier(J.bar, target, nc);
         }   // !merged
+        TRD_TS(k, 1);
         if (k == n - 1) break;
         // ---------------- phase B (rows [k+1, n)) ----------------
         // x_r = J.x[r] (phase A), or f_r - v'_r beta with v' = V[:, i-1] (merged)
+        // (with xs in shared memory, v' is still the previous column's v in vsm: no strided load)
+        const int c0p = k & ~3;                      // previous column's v offset
         auto xval = [&](int r) -> double {
-            return merged ? ldcg(J.x + r) - m_beta * (double)ldcg(VW + (size_t)r * 64 + (i - 1)) : ldcg(J.x + r);
+            if (!merged) return ldcg(J.x + r);
+            const double vp = L.use_xs ? (double)vsm[r - c0p] : (double)ldcg(VW + (size_t)r * 64 + (i - 1));
+            return ldcg(J.x + r) - m_beta * vp;
         };
         double m_nrm2 = 0.0;
         const double alpha_pre = warp == 0 ? xval(k + 1) : 0.0;      // issued before the q2 pass
         if (merged) {
             // ||x||^2 over rows k+2.. computed by every CTA from the full x (the same loads and the
-            // same fixed-order reduction in every CTA, so all CTAs agree bit for bit)
+            // same fixed-order reduction in every CTA, so all CTAs agree bit for bit); 8 loads in
+            // flight per thread
             double q2 = 0.0;
-#pragma unroll 4
-            for (int r = k + 2 + t; r < n; r += kTrdThreads) {
-                const double xr = xval(r);
-                if (L.use_xs) xs[r - (k + 2)] = xr;   // kept for the v fill below (no second load)
-                q2 += xr * xr;
+            for (int r0 = k + 2 + t; r0 < n; r0 += 8 * kTrdThreads) {
+                double fx[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) fx[u] = r0 + u * kTrdThreads < n ? ldcg(J.x + r0 + u * kTrdThreads) : 0.0;
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int r = r0 + u * kTrdThreads;
+                    if (r < n) {
+                        const double vp = L.use_xs ? (double)vsm[r - c0p] : (double)ldcg(VW + (size_t)r * 64 + (i - 1));
+                        const double xr = fx[u] - m_beta * vp;
+                        if (L.use_xs) xs[r - (k + 2)] = xr;   // kept for the v fill below (no second load)
+                        q2 += xr * xr;
+                    }
+                }
             }
             m_nrm2 = block_sum(q2, sh);
         }
@@ -319,6 +356,7 @@ __global__ void __launch_bounds__(kTrdThreads, kTrdCtasPerSm) trd_panel(const __
             }
         }
         __syncthreads();
+        TRD_TS(k, 2);
         const double tau = scal[0], scale = scal[1];
         const int c0 = (k + 1) & ~3;
         const int nvp = (n - c0 + kSymvC - 1) / kSymvC * kSymvC;   // v padded to whole column chunks
@@ -367,6 +405,7 @@ __global__ void __launch_bounds__(kTrdThreads, kTrdCtasPerSm) trd_panel(const __
             J.WVd[(size_t)r * 64 + kNb + i] = v;
         }
         double pa, pb;
+        TRD_TS(k, 3);
         // symmetric mat-vec over the lower triangle of A_p[k+1:n, k+1:n] in 64 x 128 tiles (one warp
         // per tile, every tile of the group's factor spread over its warps): each tile adds its
         // row sums to DP[row][chunk] and its column sums (the mirrored upper triangle) to
@@ -528,6 +567,7 @@ __global__ void __launch_bounds__(kTrdThreads, kTrdCtasPerSm) trd_panel(const __
                 }
             }
         }
+        TRD_TS(k, 4);
         red[warp][lane] = pa;
         red[warp][kNb + lane] = pb;
         __syncthreads();
@@ -536,14 +576,23 @@ __global__ void __launch_bounds__(kTrdThreads, kTrdCtasPerSm) trd_panel(const __
             for (int w = 0; w < kTrdWarps; ++w) s += red[w][t];
             __stcg(part + (size_t)c * kPart + t, s);
         }
+        TRD_TS(k, 5);
         group_barrier(J.bar, target, nc);
+        TRD_TS(k, 6);
         // ---------------- phase C ----------------
         {   // (V^T v, W^T v): kTpc consecutive threads per panel column sum the group's CTA partials
             constexpr int kTpc = kTrdThreads / (2 * kNb);
             const int col = t / kTpc, sub = t % kTpc;
             double sum = 0.0;
             if ((col % kNb) < i)
-                for (int q = sub; q < nc; q += kTpc) sum += ldcg(part + (size_t)q * kPart + col);
+                for (int q0 = sub; q0 < nc; q0 += 8 * kTpc) {     // 8 loads in flight, same order
+                    double pv[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+                        pv[u] = q0 + kTpc * u < nc ? ldcg(part + (size_t)(q0 + kTpc * u) * kPart + col) : 0.0;
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) sum += pv[u];
+                }
 #pragma unroll
             for (int o = kTpc / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
             if (sub == 0) ab[col] = sum;
@@ -617,7 +666,9 @@ __global__ void __launch_bounds__(kTrdThreads, kTrdCtasPerSm) trd_panel(const __
         }
         wv = block_sum(wv, sh);
         if (t == 0) __stcg(part + (size_t)c * kPart + 2 * kNb + 1, wv);
+        TRD_TS(k, 7);
         group_barrier(J.bar, target, nc);
+        TRD_TS(k, 8);
         // ---------------- phase D (+ the merged phase A of column k+1) ----------------
         if (warp == 0) {
             const double yk1 = ldcg(J.y + k + 1);                     // in flight with the partials
@@ -643,6 +694,7 @@ __global__ void __launch_bounds__(kTrdThreads, kTrdCtasPerSm) trd_panel(const __
         }
         w_next = (float)(yk1 + alpha2);                 // row k+1: v = 1
         __syncthreads();
+        TRD_TS(k, 9);
     }
     if (L.fused && p0 + kNb < n) {
         // Fused rank-64 trailing update A[q0:n, q0:n] -= V W^T + W V^T (lower 64 x 64 tiles) on the
@@ -1856,6 +1908,14 @@ extern "C" int kfac_debug_tridiag(const float *F, int n, int ldF, double *d, dou
     cudaFree(ws);
     return st;
 }
+
+#if KFAC_TRD_TIMING
+extern "C" int kfac_debug_trd_timing(unsigned long long *out, int count) {
+    const size_t want = sizeof(unsigned long long) * 3 * kfac::kTimCols * kfac::kTimPts;
+    if ((size_t)count * sizeof(unsigned long long) < want) return KFAC_ERR_INVALID_VALUE;
+    return cudaMemcpyFromSymbol(out, kfac::g_trd_tim, want) == cudaSuccess ? KFAC_OK : KFAC_ERR_CUDA;
+}
+#endif
 
 extern "C" int kfac_debug_stedc(const double *d, const double *e, int n, float *Z, int ldZ, double *w,
                                 void *stream) {
