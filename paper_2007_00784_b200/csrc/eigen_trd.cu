@@ -611,26 +611,36 @@ __global__ void __launch_bounds__(kTrdThreads, kTrdCtasPerSm) trd_panel(const __
             for (int r0 = lo + 4 * warp; r0 < hi; r0 += 4 * kTrdWarps) {
                 const int r = r0 + sub;
                 double yr = 0.0, corr = 0.0;
+                float a_next = 0.f;                        // A_p[r, k+1] for the merged column
                 if (r < hi) {
                     const int b = (r - (k + 1)) / kPairR;          // TP: 64-row super blocks
                     const int nj = (min(n, k + 1 + kSymvR * ((r - (k + 1)) / kSymvR + 1)) - 1 - c0) / kSymvC + 1;
-                    // independent loads in flight: 4-way unrolled with separate partial sums
-                    double y0 = 0.0, y1 = 0.0, y2 = 0.0, y3 = 0.0;
-                    const double *dp = J.DP + (size_t)r * J.ldp, *tp = J.TP + (size_t)r * J.ldtp;
-                    int jj = sl;
-                    for (; jj + 24 < nj; jj += 32) {
-                        y0 += ldcg(dp + jj); y1 += ldcg(dp + jj + 8); y2 += ldcg(dp + jj + 16); y3 += ldcg(dp + jj + 24);
-                    }
-                    for (; jj < nj; jj += 8) y0 += ldcg(dp + jj);
-                    int bb = b + sl;
-                    for (; bb + 24 < nrb; bb += 32) {
-                        y0 += ldcg(tp + bb); y1 += ldcg(tp + bb + 8); y2 += ldcg(tp + bb + 16); y3 += ldcg(tp + bb + 24);
-                    }
-                    for (; bb < nrb; bb += 8) y1 += ldcg(tp + bb);
-                    yr = (y0 + y1) + (y2 + y3);
+                    const int nt = nrb - b;
+                    // every load of the row issued before any is used: V/W row, A_p[r, k+1], then
+                    // DP and TP partials in batches of 8 + 8 per lane (one batch for n <= 8192)
+                    float4 vv = make_float4(0.f, 0.f, 0.f, 0.f), ww = vv;
                     if (4 * sl < i) {
-                        const float4 vv = __ldcg(reinterpret_cast<const float4 *>(VW + (size_t)r * 64) + sl);
-                        const float4 ww = __ldcg(reinterpret_cast<const float4 *>(VW + (size_t)r * 64 + kNb) + sl);
+                        vv = __ldcg(reinterpret_cast<const float4 *>(VW + (size_t)r * 64) + sl);
+                        ww = __ldcg(reinterpret_cast<const float4 *>(VW + (size_t)r * 64 + kNb) + sl);
+                    }
+                    if (mnext && sl == 0) a_next = A[(size_t)r * ldw + k + 1];
+                    const double *dp = J.DP + (size_t)r * J.ldp, *tp = J.TP + (size_t)r * J.ldtp + b;
+                    double y0 = 0.0, y1 = 0.0;
+                    const int ntot = max(nj, nt);
+                    for (int base = sl; base < ntot; base += 64) {
+                        double pd[8], pt[8];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) pd[u] = base + 8 * u < nj ? ldcg(dp + base + 8 * u) : 0.0;
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) pt[u] = base + 8 * u < nt ? ldcg(tp + base + 8 * u) : 0.0;
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            y0 += pd[u];
+                            y1 += pt[u];
+                        }
+                    }
+                    yr = y0 + y1;
+                    if (4 * sl < i) {
                         const float v4[4] = {vv.x, vv.y, vv.z, vv.w}, w4[4] = {ww.x, ww.y, ww.z, ww.w};
 #pragma unroll
                         for (int u = 0; u < 4; ++u)
@@ -652,6 +662,7 @@ __global__ void __launch_bounds__(kTrdThreads, kTrdCtasPerSm) trd_panel(const __
                     const double w = tau * yr;
                     const double vr = (double)vsm[r - c0];
                     __stcg(J.y + r, w);
+                    if (L.use_xs) xs[r - lo] = w;           // own rows, reused in phase D
                     wv += w * vr;
                     if (mnext) {
                         // column k+1 before its last correction term:
@@ -659,7 +670,7 @@ __global__ void __launch_bounds__(kTrdThreads, kTrdCtasPerSm) trd_panel(const __
                         //         - (V[r,i] W[k+1,i] + W[r,i] V[k+1,i])
                         // with V[:, i] = v (v_{k+1} = 1) and W[:, i] = w + alpha v, the last term is
                         // w_r + v_r (w_{k+1} + 2 alpha), so c_r = f_r - v_r beta:
-                        __stcg(J.x + r, (double)A[(size_t)r * ldw + k + 1] - corr - w);
+                        __stcg(J.x + r, (double)a_next - corr - w);
                     }
                 }
             }
@@ -686,7 +697,7 @@ __global__ void __launch_bounds__(kTrdThreads, kTrdCtasPerSm) trd_panel(const __
         }
         merged = mnext;
         for (int r = lo + t; r < hi; r += kTrdThreads) {
-            const float w = (float)(ldcg(J.y + r) + alpha2 * (double)vsm[r - c0]);
+            const float w = (float)((L.use_xs ? xs[r - lo] : ldcg(J.y + r)) + alpha2 * (double)vsm[r - c0]);
             VW[(size_t)r * 64 + kNb + i] = w;
             WV[(size_t)r * 64 + i] = w;
             J.VWd[(size_t)r * 64 + kNb + i] = w;
