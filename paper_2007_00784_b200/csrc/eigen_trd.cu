@@ -681,16 +681,12 @@ __global__ void __launch_bounds__(kTrdThreads, kTrdCtasPerSm) trd_panel(const __
         group_barrier(J.bar, target, nc);
         TRD_TS(k, 8);
         // ---------------- phase D (+ the merged phase A of column k+1) ----------------
-        if (warp == 0) {
-            const double yk1 = ldcg(J.y + k + 1);                     // in flight with the partials
-            const double sum = warp_part_sum(part, 2 * kNb + 1, nc, lane);
-            if (lane == 0) {
-                scal[2] = -0.5 * tau * sum;
-                scal[3] = yk1;
-            }
-        }
-        __syncthreads();
-        const double alpha2 = scal[2], yk1 = scal[3];
+        // w^T v: one partial per thread (a single round trip), fixed-order block reduction, so
+        // every CTA of the group gets the same alpha bit for bit
+        double ps = 0.0;
+        for (int q = t; q < nc; q += kTrdThreads) ps += ldcg(part + (size_t)q * kPart + 2 * kNb + 1);
+        const double yk1 = ldcg(J.y + k + 1);                         // in flight with the partials
+        const double alpha2 = -0.5 * tau * block_sum(ps, sh);
         if (mnext) {
             m_beta = yk1 + 2.0 * alpha2;                               // w_{k+1} + 2 alpha
             if (c == 0 && t == 0) J.d[k + 1] = ldcg(J.x + k + 1) - m_beta;   // f_{k+1} - v_{k+1} beta
