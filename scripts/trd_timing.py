@@ -43,6 +43,9 @@ def main():
         torch.cuda.synchronize()
         assert st == 0, st
         print(f"rep {rep}: tridiagonalisation {t0.elapsed_time(t1):.2f} ms (n={n})")
+    if not hasattr(_lib.lib, "kfac_debug_trd_timing"):
+        print("(library built without -DKFAC_TRD_TIMING=1: no phase stamps)")
+        return
     tim = np.zeros(3 * 8192 * 10, dtype=np.uint64)
     fn2 = _lib.lib.kfac_debug_trd_timing
     fn2.argtypes = [C.c_void_p, C.c_int]
