@@ -31,18 +31,27 @@ def _headers():
 
 def _compile(src, verbose=False):
     obj = os.path.join(OBJ, os.path.basename(src) + ".o")
-    dep_t = max(os.path.getmtime(p) for p in _headers() + [src])
-    if os.path.exists(obj) and os.path.getmtime(obj) >= dep_t:
-        return obj
     extra = os.environ.get("KFAC_NVCC_EXTRA", "").split()      # experiments, e.g. -DKFAC_SYMV_ROWS=32
-    cmd = [NVCC] + ARCH + FLAGS + extra + (["-Xptxas", "-v"] if verbose else []) + ["-c", src, "-o", obj]
+    cmd = [NVCC] + ARCH + FLAGS + extra + ["-c", src, "-o", obj]
     if src.endswith(".cpp"):
         cmd = ["g++", "-O2", "-std=c++17", "-fPIC", "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
-    r = subprocess.run(cmd, capture_output=True, text=True)
+    # an object is reused only if it is newer than its sources AND was built with the same command
+    # (a diagnostic -D flag must never leak into a later default build)
+    stamp = obj + ".cmd"
+    dep_t = max(os.path.getmtime(p) for p in _headers() + [src])
+    if os.path.exists(obj) and os.path.getmtime(obj) >= dep_t and os.path.exists(stamp) \
+            and open(stamp).read() == " ".join(cmd):
+        return obj
+    if os.path.exists(stamp):
+        os.remove(stamp)
+    run = cmd[:-4] + (["-Xptxas", "-v"] if verbose and not src.endswith(".cpp") else []) + cmd[-4:]
+    r = subprocess.run(run, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
     if verbose and r.stderr:
         sys.stderr.write(r.stderr)
+    with open(stamp, "w") as f:
+        f.write(" ".join(cmd))
     return obj
 
 
