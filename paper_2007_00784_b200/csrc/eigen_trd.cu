@@ -89,7 +89,9 @@ struct TrdJob {
     double *vnorm;             // merge: eigenvector column norms
     double *rot_c, *rot_s;     // merge: Givens rotations
     int *col, *posof, *rorg, *rot_p, *rot_j, *srcpos;
-    int *mstate;               // per merge: {k, nrot, k, k} (k twice: GEMM dynamic N, K)
+    int *ctyp;                 // merge: column type (1 upper, 2 mixed, 3 lower), then GEMM position
+    int *mstate;               // per merge at slot a: {k, nrot, k, k1 + k2, 0, k, k, k1}
+                               // (two GEMM dynamic {N, K, K start} triples: upper and lower rows)
     double *mscal;             // per merge: {rho2, tol}
     double *part;              // kMaxGroupCtas x kPart
     double *DP;                // symv direct partials  [n][ldp]  (row, 128-column chunk)
@@ -951,12 +953,16 @@ __global__ void dc_deflate(const TrdJob *jobs, const MergeDesc *merges, int ping
         int *rp = J.rot_p + a, *rj = J.rot_j + a;
         double *rc = J.rot_c + a, *rsn = J.rot_s + a;
         int k = 0, nrot = 0, ndef = 0;
+        int kt[4] = {0, 0, 0, 0};                    // non-deflated columns per type
+        int *ctyp = J.ctyp + a;
         s_all = rho2 * zmax <= tol;
         if (!s_all) {
             // Deflated entries are accumulated in rtau/rorg scratch (value, col) and appended.
+            // Column types (LAPACK dlaed2): 1 = nonzero only in the upper n1 rows, 3 = only in the
+            // lower rows, 2 = mixed by a rotation; the eigenvector GEMM skips the zero blocks.
             int pj = -1;
             double dp = 0.0, zp = 0.0;
-            int cp = 0;
+            int cp = 0, tp = 0;
             for (int j = 0; j < nm; ++j) {
                 double dj = dv[j], zj = zv[j];
                 const int cj = col[j];
@@ -965,8 +971,9 @@ __global__ void dc_deflate(const TrdJob *jobs, const MergeDesc *merges, int ping
                     defc[ndef++] = cj;
                     continue;
                 }
+                const int tj = cj < n1 ? 1 : 3;
                 if (pj < 0) {
-                    pj = j; dp = dj; zp = zj; cp = cj;
+                    pj = j; dp = dj; zp = zj; cp = cj; tp = tj;
                     continue;
                 }
                 double sv = zp, cv = zj;
@@ -982,22 +989,33 @@ __global__ void dc_deflate(const TrdJob *jobs, const MergeDesc *merges, int ping
                     dj = dp * sv * sv + dj * cv * cv;
                     defv[ndef] = t2;
                     defc[ndef++] = cp;
+                    tp = tp == tj ? tj : 2;          // q_j now mixes q_p in
                     pj = j; dp = dj; zp = zj; cp = cj;
                 } else {
-                    dv[k] = dp; zv[k] = zp; col[k] = cp; ++k;
-                    pj = j; dp = dj; zp = zj; cp = cj;
+                    dv[k] = dp; zv[k] = zp; col[k] = cp; ctyp[k] = tp; ++kt[tp]; ++k;
+                    pj = j; dp = dj; zp = zj; cp = cj; tp = tj;
                 }
             }
             if (pj >= 0) {
-                dv[k] = dp; zv[k] = zp; col[k] = cp; ++k;
+                dv[k] = dp; zv[k] = zp; col[k] = cp; ctyp[k] = tp; ++kt[tp]; ++k;
+            }
+            // GEMM position of each non-deflated column: types grouped 1 | 2 | 3, stable
+            int g1 = 0, g2 = kt[1], g3 = kt[1] + kt[2];
+            for (int q = 0; q < k; ++q) {
+                const int ty = ctyp[q];
+                ctyp[q] = ty == 1 ? g1++ : ty == 2 ? g2++ : g3++;
             }
         }
         s_k = k;
         s_ndef = ndef;
         J.mstate[4 * a + 0] = k;
         J.mstate[4 * a + 1] = nrot;
-        J.mstate[4 * a + 2] = k;
-        J.mstate[4 * a + 3] = k;
+        J.mstate[4 * a + 2] = k;                     // upper rows: N = k, K = [0, k1 + k2)
+        J.mstate[4 * a + 3] = kt[1] + kt[2];
+        J.mstate[4 * a + 4] = 0;
+        J.mstate[4 * a + 5] = k;                     // lower rows: N = k, K = [k1, k)
+        J.mstate[4 * a + 6] = k;
+        J.mstate[4 * a + 7] = kt[1];
         J.mscal[2 * a + 0] = rho2;
         J.mscal[2 * a + 1] = tol;
     }
@@ -1015,9 +1033,10 @@ __global__ void dc_deflate(const TrdJob *jobs, const MergeDesc *merges, int ping
     int *posof = J.posof + a;
     double *gdv = J.dval + a, *gzv = J.zval + a;
     int *gcol = J.col + a;
+    const int *gpos = J.ctyp + a;
     for (int j = threadIdx.x; j < nm; j += blockDim.x) {
         const int cj = col[j];
-        posof[cj] = j;
+        posof[cj] = j < k ? gpos[j] : j;
         if (sm) {
             gdv[j] = dv[j];
             gzv[j] = zv[j];
@@ -1221,12 +1240,14 @@ __global__ void dc_build_s(const TrdJob *jobs, const MergeDesc *merges) {
     const int rows = min(nm, (k + 31) & ~31);
     if (i >= rows || j >= k) return;
     double v = 0.0;
+    int row = i;                                     // S row of sorted entry i: its GEMM position
     if (i < k) {
         const double *dv = J.dval + a, *rt = J.rtau + a;
         const int *ro = J.rorg + a;
         v = J.wz[a + i] / delta(dv, rt, ro, i, j) * J.vnorm[a + j];
+        row = J.ctyp[a + i];
     }
-    J.Sb[(size_t)(a + i) * J.ldw + j] = v;
+    J.Sb[(size_t)(a + row) * J.ldw + j] = v;
 }
 
 // Final order of the merged eigenvalues: lambda_j (j < k, from the GEMM output Tmp) and the
@@ -1435,6 +1456,7 @@ Plan plan(const int32_t *dims, int count) {
         TAKE(rot_p, int, n);
         TAKE(rot_j, int, n);
         TAKE(srcpos, int, n);
+        TAKE(ctyp, int, n);
         TAKE(mstate, int, 4 * (size_t)n);
         TAKE(mscal, double, 2 * (size_t)n);
         TAKE(part, double, (size_t)kMaxGroupCtas * kPart);
@@ -1560,7 +1582,7 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
         J.wz = rebase(J.wz, base); J.vnorm = rebase(J.vnorm, base); J.rot_c = rebase(J.rot_c, base);
         J.rot_s = rebase(J.rot_s, base); J.col = rebase(J.col, base); J.posof = rebase(J.posof, base);
         J.rorg = rebase(J.rorg, base); J.rot_p = rebase(J.rot_p, base); J.rot_j = rebase(J.rot_j, base);
-        J.srcpos = rebase(J.srcpos, base); J.mstate = rebase(J.mstate, base); J.mscal = rebase(J.mscal, base);
+        J.srcpos = rebase(J.srcpos, base); J.ctyp = rebase(J.ctyp, base); J.mstate = rebase(J.mstate, base); J.mscal = rebase(J.mscal, base);
         J.part = rebase(J.part, base); J.bar = rebase(J.bar, base);
         J.DP = rebase(J.DP, base); J.TP = rebase(J.TP, base); J.Wt = rebase(J.Wt, base);
         max_n = std::max(max_n, J.n);
@@ -1783,15 +1805,22 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
         KFAC_LAUNCHED();
         gd.clear();
         for (auto &m : lv) {
+            // Tmp = Qnd S split by rows: the upper n1 rows only meet columns of types 1-2 (GEMM
+            // positions [0, k1 + k2)), the lower n2 rows only types 2-3 ([k1, k)); both bounds
+            // are device-side (mstate), so the zero blocks of diag(Q1, Q2) are skipped
             const TrdJob &J = P.jobs[m.job];
-            Gemm64Desc g{};
             const int nm = m.n1 + m.n2;
-            g.M = nm; g.N = nm; g.K = nm;
-            g.A = J.Qnd + (size_t)m.a * J.ldw; g.ta = DT_F64; g.lda = J.ldw;
-            g.B = J.Sb + (size_t)m.a * J.ldw; g.tb = DT_F64; g.ldb = J.ldw;
-            g.C = J.Tmp + (size_t)m.a * J.ldw; g.tc = DT_F64; g.ldc = J.ldw;
-            g.dyn = J.mstate + 4 * m.a + 2;
-            gd.push_back(g);
+            for (int h = 0; h < 2; ++h) {
+                Gemm64Desc g{};
+                const int r0 = h ? m.n1 : 0;
+                g.M = h ? m.n2 : m.n1; g.N = nm; g.K = nm;
+                g.A = J.Qnd + (size_t)(m.a + r0) * J.ldw; g.ta = DT_F64; g.lda = J.ldw;
+                g.B = J.Sb + (size_t)m.a * J.ldw; g.tb = DT_F64; g.ldb = J.ldw;
+                g.C = J.Tmp + (size_t)(m.a + r0) * J.ldw; g.tc = DT_F64; g.ldc = J.ldw;
+                g.dyn = J.mstate + 4 * m.a + (h ? 5 : 2);
+                g.dyn_koff = 1;
+                gd.push_back(g);
+            }
         }
         RET_OK(gemm64_grouped(gd.data(), (int)gd.size(), s));
         {

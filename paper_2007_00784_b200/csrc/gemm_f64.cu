@@ -448,9 +448,11 @@ __global__ void __launch_bounds__(kPT, 2) gemm64_direct_kernel(const __grid_cons
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    issue(0);
-    issue(1);
-    for (int kt = 0; kt < nk; ++kt) {
+    // K slabs below dyn[2] multiply known zeros (divide-and-conquer column types): skipped
+    const int kt0 = (d.dyn && d.dyn_koff) ? min(max(d.dyn[2], 0), Ke) / PBK : 0;
+    issue(kt0);
+    issue(kt0 + 1);
+    for (int kt = kt0; kt < nk; ++kt) {
         asm volatile("cp.async.wait_group 1;" ::: "memory");      // slab kt (this thread's copies)
         __syncthreads();                        // slab kt landed everywhere; compute(kt-1) done
         issue(kt + 2);                          // into the stage of slab kt-1

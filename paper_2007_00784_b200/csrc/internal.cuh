@@ -75,7 +75,8 @@ struct Gemm64Desc {
     const void *A;
     const void *B;
     void *C;
-    const int *dyn;          // optional device {N_eff, K_eff}
+    const int *dyn;          // optional device {N_eff, K_eff} (+ K start with dyn_koff)
+    int dyn_koff;            // dyn[2]: first K index with nonzero products (kernels may ignore it)
     int ta, tb, tc;          // DType of A, B, C
     int M, N, K;
     int lda, ldb, ldc;
