@@ -1232,22 +1232,28 @@ __global__ void dc_vnorm(const TrdJob *jobs, const MergeDesc *merges) {
 
 // S[a + i][j] (k x k, row-major at rows a..a+k) = z-hat_i / (d_i - lambda_j) / ||.||; rows k..k+31
 // (inside the merge's row range) zeroed so the GEMM's last K block reads zeros.
+constexpr int kBuildRows = 16;                   // S rows per dc_build_s thread
 __global__ void dc_build_s(const TrdJob *jobs, const MergeDesc *merges) {
+    // one thread per column j and kBuildRows rows: the column's pole d_{org(j)}, offset and norm
+    // are loaded once, each row adds only its d_i and z-hat_i (warp-uniform broadcasts)
     const MergeDesc M = merges[blockIdx.z];
     const TrdJob &J = jobs[M.job];
     const int a = M.a, nm = M.n1 + M.n2, k = J.mstate[4 * a + 0];
-    const int i = blockIdx.y, j = blockIdx.x * blockDim.x + threadIdx.x;
+    const int i0 = blockIdx.y * kBuildRows, j = blockIdx.x * blockDim.x + threadIdx.x;
     const int rows = min(nm, (k + 31) & ~31);
-    if (i >= rows || j >= k) return;
-    double v = 0.0;
-    int row = i;                                     // S row of sorted entry i: its GEMM position
-    if (i < k) {
-        const double *dv = J.dval + a, *rt = J.rtau + a;
-        const int *ro = J.rorg + a;
-        v = J.wz[a + i] / delta(dv, rt, ro, i, j) * J.vnorm[a + j];
-        row = J.ctyp[a + i];
+    if (i0 >= rows || j >= k) return;
+    const double *dv = J.dval + a, *rt = J.rtau + a;
+    const int *ro = J.rorg + a;
+    const double dj = dv[ro[j]], rj = rt[j], nj = J.vnorm[a + j];
+    for (int i = i0; i < min(rows, i0 + kBuildRows); ++i) {
+        double v = 0.0;
+        int row = i;                                 // S row of sorted entry i: its GEMM position
+        if (i < k) {
+            v = J.wz[a + i] / ((dv[i] - dj) - rj) * nj;
+            row = J.ctyp[a + i];
+        }
+        J.Sb[(size_t)(a + row) * J.ldw + j] = v;
     }
-    J.Sb[(size_t)(a + row) * J.ldw + j] = v;
 }
 
 // Final order of the merged eigenvalues: lambda_j (j < k, from the GEMM output Tmp) and the
@@ -1282,12 +1288,13 @@ __global__ void dc_assemble(const TrdJob *jobs, const MergeDesc *merges, int pin
     const MergeDesc M = merges[blockIdx.z];
     const TrdJob &J = jobs[M.job];
     const int a = M.a, nm = M.n1 + M.n2, k = J.mstate[4 * a + 0], ldw = J.ldw;
-    const int r = blockIdx.y, p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= nm || p >= nm) return;
+    const int r0 = blockIdx.y * kBuildRows, p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r0 >= nm || p >= nm) return;
     double *Zd = ping ? J.Z0 : J.Z1;                // destination = the other buffer
-    const int src = J.srcpos[a + p];
-    const double v = src < k ? J.Tmp[(size_t)(a + r) * ldw + src] : J.Qnd[(size_t)(a + r) * ldw + src];
-    Zd[(size_t)(a + r) * ldw + a + p] = v;
+    const int src = J.srcpos[a + p];                 // once per thread, kBuildRows rows each
+    const double *from = src < k ? J.Tmp : J.Qnd;
+    for (int r = r0; r < min(nm, r0 + kBuildRows); ++r)
+        Zd[(size_t)(a + r) * ldw + a + p] = from[(size_t)(a + r) * ldw + src];
 }
 
 // ------------------------------------------------- back-transformation --
@@ -1801,7 +1808,7 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
         KFAC_LAUNCHED();
         dc_vnorm<<<dim3(cdiv(nmax, 8), nmg), 256, 0, s>>>(djobs, dm);
         KFAC_LAUNCHED();
-        dc_build_s<<<dim3(cdiv(nmax, 128), nmax, nmg), 128, 0, s>>>(djobs, dm);
+        dc_build_s<<<dim3(cdiv(nmax, 128), cdiv(nmax, kBuildRows), nmg), 128, 0, s>>>(djobs, dm);
         KFAC_LAUNCHED();
         gd.clear();
         for (auto &m : lv) {
@@ -1835,7 +1842,7 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
             dc_rank<<<dim3(cdiv(nmax, 128), nmg), 128, (size_t)rank_n * 8, s>>>(djobs, dm, rank_n);
         }
         KFAC_LAUNCHED();
-        dc_assemble<<<dim3(cdiv(nmax, 128), nmax, nmg), 128, 0, s>>>(djobs, dm, ping);
+        dc_assemble<<<dim3(cdiv(nmax, 128), cdiv(nmax, kBuildRows), nmg), 128, 0, s>>>(djobs, dm, ping);
         KFAC_LAUNCHED();
         ping ^= 1;
     }
