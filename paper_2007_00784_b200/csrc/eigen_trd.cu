@@ -1199,16 +1199,20 @@ __device__ __forceinline__ double delta(const double *dv, const double *rt, cons
 __global__ void dc_zhat(const TrdJob *jobs, const MergeDesc *merges) {
     const MergeDesc M = merges[blockIdx.y];
     const TrdJob &J = jobs[M.job];
+    // one warp per i: lane-strided partial products (each factor is O(1) by interlacing, so the
+    // partial products neither overflow nor underflow), then a fixed-order butterfly product
     const int a = M.a, k = J.mstate[4 * a + 0];
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x % 32;
     if (i >= k) return;
     const double *dv = J.dval + a, *rt = J.rtau + a;
     const int *ro = J.rorg + a;
-    double w = delta(dv, rt, ro, i, i);
     const double di = dv[i];
-    for (int j = 0; j < k; ++j)
+    double w = lane == 0 ? delta(dv, rt, ro, i, i) : 1.0;
+    for (int j = lane; j < k; j += 32)
         if (j != i) w *= delta(dv, rt, ro, i, j) / (di - dv[j]);
-    J.wz[a + i] = copysign(sqrt(fmax(-w, 0.0)), J.zval[a + i]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) w *= __shfl_xor_sync(0xffffffffu, w, o);
+    if (lane == 0) J.wz[a + i] = copysign(sqrt(fmax(-w, 0.0)), J.zval[a + i]);
 }
 
 // Column norms of S[:, j] = z-hat / (d - lambda_j) (one warp per column).
@@ -1804,7 +1808,7 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
         KFAC_LAUNCHED();
         dc_secular<<<dim3(cdiv(nmax, 8), nmg), 256, 0, s>>>(djobs, dm);
         KFAC_LAUNCHED();
-        dc_zhat<<<dim3(cdiv(nmax, 128), nmg), 128, 0, s>>>(djobs, dm);
+        dc_zhat<<<dim3(cdiv(nmax, 8), nmg), 256, 0, s>>>(djobs, dm);
         KFAC_LAUNCHED();
         dc_vnorm<<<dim3(cdiv(nmax, 8), nmg), 256, 0, s>>>(djobs, dm);
         KFAC_LAUNCHED();
