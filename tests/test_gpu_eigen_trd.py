@@ -163,6 +163,14 @@ def _tcases():
     n = 130                                               # Clement (Kac) matrix, symmetric form
     cases["clement130"] = (np.zeros(n), np.sqrt(np.arange(1, n) * np.arange(n - 1, 0, -1)))
     cases["diag96"] = (rng.standard_normal(96), np.zeros(95))
+    # D&C column types: identical halves glued by a tiny coupling make almost every non-deflated
+    # column of the top merges a rotation mix of an upper and a lower column (type 2), while an
+    # unbalanced glue of different blocks keeps most columns pure (types 1 and 3)
+    d1, e1 = rng.standard_normal(250), rng.standard_normal(249)
+    cases["glued_halves1000"] = (np.concatenate([d1] * 4), np.concatenate([e1, [1e-12], e1, [1e-12], e1, [1e-12], e1]))
+    d2, e2 = rng.standard_normal(700), rng.standard_normal(699)
+    d3, e3 = 3.0 + rng.standard_normal(301), rng.standard_normal(300)
+    cases["unbalanced1001"] = (np.concatenate([d2, d3]), np.concatenate([e2, [0.5], e3]))
     return cases
 
 
