@@ -935,7 +935,7 @@ __global__ void dc_deflate(const TrdJob *jobs, const MergeDesc *merges, int ping
         zmax = fmax(zmax, __shfl_xor_sync(0xffffffffu, zmax, o));
     }
     __shared__ double shd[32], shz[32];
-    __shared__ int s_k, s_ndef, s_all;
+    __shared__ int s_k, s_ndef, s_all, s_kt1, s_kt2;
     if (threadIdx.x % 32 == 0) {
         shd[threadIdx.x / 32] = dmax;
         shz[threadIdx.x / 32] = zmax;
@@ -999,13 +999,9 @@ __global__ void dc_deflate(const TrdJob *jobs, const MergeDesc *merges, int ping
             if (pj >= 0) {
                 dv[k] = dp; zv[k] = zp; col[k] = cp; ctyp[k] = tp; ++kt[tp]; ++k;
             }
-            // GEMM position of each non-deflated column: types grouped 1 | 2 | 3, stable
-            int g1 = 0, g2 = kt[1], g3 = kt[1] + kt[2];
-            for (int q = 0; q < k; ++q) {
-                const int ty = ctyp[q];
-                ctyp[q] = ty == 1 ? g1++ : ty == 2 ? g2++ : g3++;
-            }
         }
+        s_kt1 = kt[1];
+        s_kt2 = kt[2];
         s_k = k;
         s_ndef = ndef;
         J.mstate[4 * a + 0] = k;
@@ -1033,6 +1029,42 @@ __global__ void dc_deflate(const TrdJob *jobs, const MergeDesc *merges, int ping
     int *posof = J.posof + a;
     double *gdv = J.dval + a, *gzv = J.zval + a;
     int *gcol = J.col + a;
+    // GEMM position of each non-deflated column: types grouped 1 | 2 | 3, stable (block-wide
+    // ballot scan over chunks of blockDim entries; ctyp is overwritten in place by its reader)
+    {
+        __shared__ int wcnt[32][3], run[3];
+        int *gpos = J.ctyp + a;
+        const int lane = threadIdx.x % 32, w = threadIdx.x / 32, nw = blockDim.x / 32;
+        const int base[4] = {0, 0, s_kt1, s_kt1 + s_kt2};
+        if (threadIdx.x < 3) run[threadIdx.x] = 0;
+        for (int c0 = 0; c0 < k; c0 += blockDim.x) {
+            __syncthreads();
+            const int p = c0 + threadIdx.x;
+            const int ty = p < k ? gpos[p] : 0;
+            const unsigned m1 = __ballot_sync(0xffffffffu, ty == 1), m2 = __ballot_sync(0xffffffffu, ty == 2),
+                           m3 = __ballot_sync(0xffffffffu, ty == 3);
+            if (lane == 0) {
+                wcnt[w][0] = __popc(m1);
+                wcnt[w][1] = __popc(m2);
+                wcnt[w][2] = __popc(m3);
+            }
+            __syncthreads();
+            int g = 0;
+            if (ty > 0) {
+                const unsigned mt = ty == 1 ? m1 : ty == 2 ? m2 : m3;
+                g = base[ty] + run[ty - 1] + __popc(mt & ((1u << lane) - 1u));
+                for (int q = 0; q < w; ++q) g += wcnt[q][ty - 1];
+            }
+            __syncthreads();
+            if (threadIdx.x < 3) {
+                int add = 0;
+                for (int q = 0; q < nw; ++q) add += wcnt[q][threadIdx.x];
+                run[threadIdx.x] += add;
+            }
+            if (ty > 0) gpos[p] = g;
+        }
+        __syncthreads();
+    }
     const int *gpos = J.ctyp + a;
     for (int j = threadIdx.x; j < nm; j += blockDim.x) {
         const int cj = col[j];
