@@ -1353,7 +1353,7 @@ __global__ void bt_larft(const TrdJob *jobs, const BtStep *steps) {
     if (nr <= 0) return;
     for (int j = 0; j < nr; ++j) {
         const double tj = J.tau[S.b0 + o + j];
-        if (t < j) gcol[t] = J.Gb[(size_t)(o + t) * kBt + o + j];
+        if (t < j) gcol[t] = J.Gb[(size_t)(o + j) * kBt + o + t];   // G[t][j] = G[j][t] (lower half stored)
         __syncthreads();
         double acc = 0.0;
         if (t < j)
@@ -1899,10 +1899,11 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
             const double *V = J.Vd + (size_t)(b.b0 + 1) * J.ldw + b.b0;
             double *X = final_z(J) + (size_t)(b.b0 + 1) * J.ldw;
             Gemm64Desc g{};
-            g.M = b.nr; g.N = b.nr; g.K = m;                     // G = V^T V
+            g.M = b.nr; g.N = b.nr; g.K = m;                     // G = V^T V, lower half only
             g.A = V; g.ta = DT_F64; g.lda = J.ldw; g.trans_a = 1;
             g.B = V; g.tb = DT_F64; g.ldb = J.ldw;
             g.C = J.Gb; g.tc = DT_F64; g.ldc = kBt;
+            g.lower = 1;                                         // (G is symmetric)
             g1.push_back(g);
             Gemm64Desc h{};
             h.M = b.nr; h.N = J.n; h.K = m;                      // Y = V^T X
@@ -1935,10 +1936,10 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
                 const TrdJob &J = P.jobs[b.job];
                 for (int o = 0; o + h < b.nr; o += 2 * h) {
                     const int n1 = h, n2 = std::min(h, b.nr - o - h);
-                    Gemm64Desc x{};                      // Wt = T1 G12
+                    Gemm64Desc x{};                      // Wt = T1 G12, G12 = G21^T (lower half stored)
                     x.M = n1; x.N = n2; x.K = n1;
                     x.A = J.Tb + (size_t)o * kBt + o; x.ta = DT_F64; x.lda = kBt;
-                    x.B = J.Gb + (size_t)o * kBt + o + h; x.tb = DT_F64; x.ldb = kBt;
+                    x.B = J.Gb + (size_t)(o + h) * kBt + o; x.tb = DT_F64; x.ldb = kBt; x.trans_b = 1;
                     x.C = J.Wt + (size_t)o * kBt; x.tc = DT_F64; x.ldc = kBt;
                     ga.push_back(x);
                     Gemm64Desc y{};                      // T12 = 0 - Wt T2
