@@ -1911,12 +1911,14 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
             h.B = X; h.tb = DT_F64; h.ldb = J.ldw;
             h.C = J.Yb; h.tc = DT_F64; h.ldc = J.ldw;
             g1.push_back(h);
-            Gemm64Desc u{};
-            u.M = b.nr; u.N = J.n; u.K = b.nr;                   // Y2 = T Y
-            u.A = J.Tb; u.ta = DT_F64; u.lda = kBt;
-            u.B = J.Yb; u.tb = DT_F64; u.ldb = J.ldw;
-            u.C = J.Y2b; u.tc = DT_F64; u.ldc = J.ldw;
-            g2.push_back(u);
+            for (int m0 = 0; m0 < b.nr; m0 += 64) {              // Y2 = T Y, T upper triangular:
+                Gemm64Desc u{};                                  // row slab m0 only meets K >= m0
+                u.M = std::min(64, b.nr - m0); u.N = J.n; u.K = b.nr - m0;
+                u.A = J.Tb + (size_t)m0 * kBt + m0; u.ta = DT_F64; u.lda = kBt;
+                u.B = J.Yb + (size_t)m0 * J.ldw; u.tb = DT_F64; u.ldb = J.ldw;
+                u.C = J.Y2b + (size_t)m0 * J.ldw; u.tc = DT_F64; u.ldc = J.ldw;
+                g2.push_back(u);
+            }
             Gemm64Desc v{};
             v.M = m; v.N = J.n; v.K = b.nr;                      // X -= V Y2
             v.A = V; v.ta = DT_F64; v.lda = J.ldw;
