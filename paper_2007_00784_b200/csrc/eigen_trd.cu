@@ -1905,12 +1905,14 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
             g.C = J.Gb; g.tc = DT_F64; g.ldc = kBt;
             g.lower = 1;                                         // (G is symmetric)
             g1.push_back(g);
-            Gemm64Desc h{};
-            h.M = b.nr; h.N = J.n; h.K = m;                      // Y = V^T X
-            h.A = V; h.ta = DT_F64; h.lda = J.ldw; h.trans_a = 1;
-            h.B = X; h.tb = DT_F64; h.ldb = J.ldw;
-            h.C = J.Yb; h.tc = DT_F64; h.ldc = J.ldw;
-            g1.push_back(h);
+            for (int i0 = 0; i0 < b.nr; i0 += 64) {              // Y = V^T X; V[r][i] = 0 for r < i,
+                Gemm64Desc h{};                                  // so row slab i0 only meets r >= i0
+                h.M = std::min(64, b.nr - i0); h.N = J.n; h.K = m - i0;
+                h.A = V + (size_t)i0 * J.ldw + i0; h.ta = DT_F64; h.lda = J.ldw; h.trans_a = 1;
+                h.B = X + (size_t)i0 * J.ldw; h.tb = DT_F64; h.ldb = J.ldw;
+                h.C = J.Yb + (size_t)i0 * J.ldw; h.tc = DT_F64; h.ldc = J.ldw;
+                g1.push_back(h);
+            }
             for (int m0 = 0; m0 < b.nr; m0 += 64) {              // Y2 = T Y, T upper triangular:
                 Gemm64Desc u{};                                  // row slab m0 only meets K >= m0
                 u.M = std::min(64, b.nr - m0); u.N = J.n; u.K = b.nr - m0;
@@ -1919,13 +1921,26 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
                 u.C = J.Y2b + (size_t)m0 * J.ldw; u.tc = DT_F64; u.ldc = J.ldw;
                 g2.push_back(u);
             }
-            Gemm64Desc v{};
-            v.M = m; v.N = J.n; v.K = b.nr;                      // X -= V Y2
-            v.A = V; v.ta = DT_F64; v.lda = J.ldw;
-            v.B = J.Y2b; v.tb = DT_F64; v.ldb = J.ldw;
-            v.C = X; v.tc = DT_F64; v.ldc = J.ldw;
-            v.epi = EPI_SUB;
-            g3.push_back(v);
+            // X -= V Y2: rows r < nr of V are zero beyond column r (unit lower triangle on top)
+            for (int r0 = 0; r0 < m; r0 += 64) {
+                if (r0 >= b.nr) {                                // the rectangular rest in one desc
+                    Gemm64Desc v{};
+                    v.M = m - r0; v.N = J.n; v.K = b.nr;
+                    v.A = V + (size_t)r0 * J.ldw; v.ta = DT_F64; v.lda = J.ldw;
+                    v.B = J.Y2b; v.tb = DT_F64; v.ldb = J.ldw;
+                    v.C = X + (size_t)r0 * J.ldw; v.tc = DT_F64; v.ldc = J.ldw;
+                    v.epi = EPI_SUB;
+                    g3.push_back(v);
+                    break;
+                }
+                Gemm64Desc v{};
+                v.M = std::min(64, m - r0); v.N = J.n; v.K = std::min(b.nr, r0 + 64);
+                v.A = V + (size_t)r0 * J.ldw; v.ta = DT_F64; v.lda = J.ldw;
+                v.B = J.Y2b; v.tb = DT_F64; v.ldb = J.ldw;
+                v.C = X + (size_t)r0 * J.ldw; v.tc = DT_F64; v.ldc = J.ldw;
+                v.epi = EPI_SUB;
+                g3.push_back(v);
+            }
         }
         RET_OK(gemm64_grouped(g1.data(), (int)g1.size(), s));
         bt_larft<<<ns * (kBt / kTs), kTs, kLarftSmem, s>>>(djobs, dbt + boff);
