@@ -43,6 +43,7 @@ def parse():
     p.add_argument("--exchange", default="bcast-eig", choices=["bcast-eig", "allgather-grad"])
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-graph", action="store_true")
     p.add_argument("--seed", type=int, default=0)
     return p.parse_args()
 
@@ -187,9 +188,21 @@ def run_reference(args):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": config_block(args, layers),
-            "cpu_baseline": {"value": ms, "unit": "ms/iter", "cores": cores, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": ms, "unit": "ms/iter", "cores": cores, "kind": "oracle", "sample": sample,
+                             "full_workload_measured": oracle_full_record(args.config)},
             "e2e": {"value": ms, "unit": "ms/iter", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def oracle_full_record(cfg):
+    """The oracle timed once on the whole workload (scripts/time_oracle_full.py): the measured
+    cross-check of the sample extrapolation (its host and core count are in the record)."""
+    try:
+        r = json.load(open(os.path.join(ROOT, "profiles", f"oracle_full_{cfg}.json")))
+        return {"total_ms": 1e3 * r["total_s"], "stages_s": r["stages_s"], "cores": r["cores"], "cpu": r["cpu"],
+                "source": f"profiles/oracle_full_{cfg}.json"}
+    except Exception:
+        return None
 
 
 def metric_name(cfg):
@@ -244,7 +257,7 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
     ev = lambda: torch.cuda.Event(enable_timing=True)
 
-    def one_step(i, first, warm, log=None):
+    def one_step(i, first, warm=False, log=None):
         acts, gouts = dev_sets[i % 2]
         e = [ev() for _ in range(4)]
         e[0].record(stream)
@@ -266,7 +279,7 @@ def run_ours(args):
     cold = []
     one_step(0, first=True, warm=False, log=cold)
     for i in range(1, args.warmup):
-        one_step(i, first=False, warm=True)
+        one_step(i, first=False)
     barrier()
     cold_ms = cold[0][0].elapsed_time(cold[0][3])
     cold_eig_ms = cold[0][1].elapsed_time(cold[0][2])
@@ -276,7 +289,7 @@ def run_ours(args):
     probe = {}
     for j, kc in enumerate(PROF_CLASSES):
         _lib.kfac_profile_start(kc)
-        one_step(args.warmup + j, first=False, warm=True)
+        one_step(args.warmup + j, first=False)
         probe[kc] = _lib.kfac_profile_stop()[0]
     if world > 1:       # same class on every rank: max over ranks of each probe
         pv = torch.tensor([probe[k] for k in PROF_CLASSES], dtype=torch.float64, device="cuda")
@@ -292,7 +305,7 @@ def run_ours(args):
         barrier()
         t0.record(stream)
         for i in range(args.steps):
-            one_step(args.warmup + i, first=False, warm=True, log=log)
+            one_step(args.warmup + i, first=False, log=log)
         t1.record(stream)
         barrier()
     launches = _lib.kfac_launch_count() - n0
@@ -301,7 +314,46 @@ def run_ours(args):
     stages = {"factors": float(np.mean([e[0].elapsed_time(e[1]) for e in log])),
               "eigen": float(np.mean([e[1].elapsed_time(e[2]) for e in log])),
               "precond": float(np.mean([e[2].elapsed_time(e[3]) for e in log]))}
-    info = pc.info.cpu().tolist()
+    info = pc.info[:max(1, len(pc.owned))].cpu().tolist()
+    # accuracy of the timed step's output (outside the timed region): the largest owned factor's
+    # eigendecomposition checked in fp64 (torch, test-side arithmetic)
+    check = None
+    if pc.owned and args.variant != "inverse":
+        f = max(pc.owned, key=lambda q: pc.dims[q])
+        Fm = pc.F[f].double()
+        Fm = 0.5 * (Fm + Fm.T)
+        Qm, vm = pc.Q[f].double(), pc.v[f].double()
+        eye = torch.eye(Fm.shape[0], dtype=torch.float64, device=Fm.device)
+        check = {"factor": int(f), "d": int(pc.dims[f]),
+                 "rel_reconstruction": float(torch.linalg.norm((Qm * vm) @ Qm.T - Fm) / torch.linalg.norm(Fm)),
+                 "orthogonality_max": float((Qm.T @ Qm - eye).abs().max())}
+        del Fm, Qm, vm, eye
+    # the same full step captured once in a CUDA graph and replayed (W = 1; launch overhead removed)
+    graph_ms = None
+    if world == 1 and not args.no_graph:
+        try:
+            g = torch.cuda.CUDAGraph()
+            side = torch.cuda.Stream()
+            side.wait_stream(stream)
+            with torch.cuda.stream(side):
+                with torch.cuda.graph(g, stream=side):
+                    acts, gouts = dev_sets[0]
+                    pc.update_factors(acts, gouts, False)
+                    pc.compute_eigen(check=False)
+                    pc.precondition(grad_bufs[0])
+            stream.wait_stream(side)
+            g.replay()
+            barrier()
+            r0, r1 = ev(), ev()
+            r0.record(stream)
+            for _ in range(args.steps):
+                g.replay()
+            r1.record(stream)
+            barrier()
+            graph_ms = r0.elapsed_time(r1) / args.steps
+            del g
+        except Exception as e:   # report, never fail the bench line
+            graph_ms = f"capture failed: {type(e).__name__}: {str(e)[:120]}"
 
     # end-to-end through the public API with host buffers: every step copies that step's inputs
     # (activations, output gradients, averaged weight gradient) from pinned host memory and reads
@@ -341,7 +393,7 @@ def run_ours(args):
                 issue_h2d(i + 1)
             stream.wait_event(h2d_done[i % 2])
             pc.update_factors(acts, gouts, False)
-            pc.compute_eigen(warm=True)
+            pc.compute_eigen()
             pc.precondition(grad_bufs[i % 2])
             buf_free[i % 2].record(stream)
             nu_h.copy_(pc.nu, non_blocking=True)
@@ -409,8 +461,8 @@ def run_ours(args):
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
                 "config": dict(config_block(args, layers), parallelism=f"dp{world}",
-                               protocol="steady state: EMA factors of alternating batches, eigen refresh "
-                                        "warm-started from the previous eigenbasis, every step"),
+                               protocol="full update every step: EMA factors of alternating batches, every "
+                                        "factor re-decomposed from scratch (no warm start), preconditioning, KL-clip"),
                 "stages_ms": stages, "cold_update_ms": cold_ms, "cold_eigen_ms": cold_eig_ms,
                 # the paper's training schedule refreshes the eigenbases every 10 K-FAC updates
                 # while factors and preconditioning run every iteration
@@ -418,7 +470,9 @@ def run_ours(args):
                 "steady_state_precondition_ms": stages["precond"],
                 "factor_precond_tflops": tensor_tflops,
                 "factor_precond_frac_of_3xtf32_peak": tensor_tflops / (tf32_peak / 3),
-                "eigen_info": info[:8],
+                "eigen_info": {"factors": len(info), "max": int(max(info)), "nonzero": int(sum(1 for c in info if c))},
+                "eigen_check_largest_factor": check,
+                "graph_replay_ms_per_step": graph_ms,
                 "roofline": roof, "gpu_launches": int(launches),
                 "clocks": clk.summary(), "e2e": e2e}
         if not args.no_cpu_baseline and world == 1:
@@ -426,6 +480,7 @@ def run_ours(args):
             oracle.build()
             est, det = oracle_sample(layers, hp, args.seed, SAMPLE[args.config])
             line["cpu_baseline"] = {"value": est * 1e3, "unit": "ms/iter", "cores": len(os.sched_getaffinity(0)),
+                                    "full_workload_measured": oracle_full_record(args.config),
                                     "kind": "oracle",
                                     "sample": f"oracle on layers {det['names']}, per-stage times scaled by "
                                               f"algorithmic work to all {len(layers)} layers; measured "

@@ -20,10 +20,16 @@
  *  - Matrices are fp32, row-major, with a leading dimension `ld` (elements)
  *    that is >= the column count and a multiple of 4 (16-byte rows, TMA rule);
  *    every matrix base address must be 16-byte aligned.
- *  - Errors: arguments are validated on the host before anything is launched;
- *    on a non-OK status nothing was launched and outputs are untouched.
+ *  - Errors: arguments are validated on the host before anything is launched.
+ *    A validation status (INVALID_VALUE, SHAPE, ALIGNMENT, WORKSPACE, UNSUPPORTED)
+ *    means nothing was launched and outputs are untouched.  KFAC_ERR_CUDA (a CUDA
+ *    runtime call or kernel launch failed) can occur after earlier kernels of the
+ *    same call were queued, so outputs may be partly written.
  *    kfac_last_error() returns a thread-local message for the last failure.
  *    Numerical failures are device-side `info` codes, not statuses.
+ *  - Concurrency: host state is thread-local (staging) or mutex-guarded (per-device
+ *    kernel attributes), so calls from several host threads, on several devices, or
+ *    on different streams with disjoint buffers and workspaces may overlap.
  *  - Determinism: identical inputs on the same GPU model give bitwise
  *    identical outputs (fixed reduction orders; no float atomics).
  *  - Workspace: each stage has a *_workspace_size twin taking the same shape
@@ -158,8 +164,11 @@ kfac_status_t kfac_precondition(const int32_t *d_g, const int32_t *d_a, int32_t 
 /* ---- Eq. 18 (R12): KL-clip.
  *   s = sum_l |<precond_l, grad_l>_F|,  nu = s > 0 ? min(1, sqrt(kappa / (lr^2 s))) : 1,
  *   precond_l *= nu  (in place).
- * precond[l], grad[l]: device rows[l] x ld[l].  nu_out: device float (nullable);
- * s_out: device double (nullable).  Fixed reduction order (fp64 partial sums). */
+ * precond[l], grad[l]: device rows[l] x ld[l] (columns >= cols[l] are padding: never read into
+ * the sum, scaled along with the row).  Any number of layers.  nu_out: device float (nullable);
+ * s_out: device double (nullable).  Fixed reduction order (fp64 partial sums, per-layer sums in
+ * layer order), so identical inputs give bitwise identical nu and outputs.
+ * Workspace: per-CTA fp64 partials, per-layer dot products, nu. */
 size_t kfac_kl_clip_workspace_size(const int32_t *rows, const int32_t *cols, int32_t num_layers);
 kfac_status_t kfac_kl_clip(float *const *precond, const float *const *grad,
                            const int32_t *rows, const int32_t *cols, const int32_t *ld,

@@ -1,6 +1,10 @@
 // api.cu -- the C-ABI of libkfac: host-side validation, workspace sizing and dispatch.
 // See include/kfac.h for the contract of every entry point.
+#include <map>
+#include <mutex>
+#include <set>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "internal.cuh"
@@ -27,7 +31,7 @@ kfac_status_t precond_run(const int32_t *d_g, const int32_t *d_a, int nl, const 
                           const float *const *vG, const float *const *QA, const int32_t *ldQA,
                           const float *const *vA, float damping, int mode, float *const *out,
                           void *ws, cudaStream_t s);
-size_t klclip_workspace_bytes(const int32_t *rows, int nl);
+size_t klclip_workspace_bytes(const int32_t *rows, const int32_t *cols, int nl);
 kfac_status_t klclip_run(float *const *P, const float *const *W, const int32_t *rows,
                          const int32_t *cols, const int32_t *ld, int nl, float lr, float kappa,
                          float *nu_out, double *s_out, void *ws, cudaStream_t s);
@@ -42,14 +46,32 @@ std::atomic<uint64_t> &launch_counter() {
 }
 
 int num_sms() {
-    static int n = 0;
-    if (!n) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        if (n <= 0) n = 148;
-    }
+    static std::mutex mu;
+    static std::map<int, int> cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(dev);
+    if (it != cache.end()) return it->second;
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+    cache[dev] = n;
     return n;
+}
+
+cudaError_t set_smem_attr(const void *kernel, int bytes) {
+    static std::mutex mu;
+    static std::set<std::tuple<const void *, int, int>> done;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lk(mu);
+    const auto key = std::make_tuple(kernel, dev, bytes);
+    if (done.count(key)) return cudaSuccess;
+    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) done.insert(key);
+    return e;
 }
 
 namespace {
@@ -276,9 +298,10 @@ kfac_status_t kfac_precondition(const int32_t *d_g, const int32_t *d_a, int32_t 
 }
 
 size_t kfac_kl_clip_workspace_size(const int32_t *rows, const int32_t *cols, int32_t num_layers) {
-    (void)cols;
-    if (!rows || num_layers <= 0) return 0;
-    return klclip_workspace_bytes(rows, num_layers);
+    if (!rows || !cols || num_layers <= 0) return 0;
+    for (int l = 0; l < num_layers; ++l)
+        if (rows[l] <= 0 || cols[l] <= 0) return 0;
+    return klclip_workspace_bytes(rows, cols, num_layers);
 }
 
 kfac_status_t kfac_kl_clip(float *const *precond, const float *const *grad, const int32_t *rows,
@@ -292,7 +315,7 @@ kfac_status_t kfac_kl_clip(float *const *precond, const float *const *grad, cons
         RET_IF(check_matrix(precond[l], rows[l], cols[l], ld[l], "precond", l));
         RET_IF(check_matrix(grad[l], rows[l], cols[l], ld[l], "grad", l));
     }
-    RET_IF(check_ws(ws, ws_bytes, klclip_workspace_bytes(rows, num_layers), "kfac_kl_clip"));
+    RET_IF(check_ws(ws, ws_bytes, klclip_workspace_bytes(rows, cols, num_layers), "kfac_kl_clip"));
     RET_IF(check_device());
     return klclip_run(precond, grad, rows, cols, ld, num_layers, lr, kappa, nu_out, s_out, ws,
                       reinterpret_cast<cudaStream_t>(stream));

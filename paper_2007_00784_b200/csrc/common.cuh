@@ -69,7 +69,11 @@ struct WsArena {
     bool ok() const { return off <= cap; }
 };
 
-int num_sms();   // cached multiprocessor count of the current device
+int num_sms();   // multiprocessor count of the current device (cached per device)
+
+// cudaFuncSetAttribute(kernel, MaxDynamicSharedMemorySize, bytes) on the current device, done once
+// per (kernel, device, bytes); thread-safe.
+cudaError_t set_smem_attr(const void *kernel, int bytes);
 
 // Per-launch instrumentation (kfac_profile_start/stop).  prof_begin returns a slot (< 0 when the
 // class is not armed); prof_end records the closing event and the launch's algorithmic work.

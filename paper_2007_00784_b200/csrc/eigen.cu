@@ -482,11 +482,7 @@ kfac_status_t jacobi_run(const float *const *F, const int32_t *dims, const int32
         eig_table_init<<<1, 64, 0, s>>>(ti);
         KFAC_LAUNCHED();
     }
-    static bool attr = false;
-    if (!attr) {
-        KFAC_CUDA_TRY(cudaFuncSetAttribute(eig_round, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRoundSmem));
-        attr = true;
-    }
+    KFAC_CUDA_TRY(set_smem_attr((const void *)eig_round, (int)kRoundSmem));
     const bool warm = flags & KFAC_EIG_WARM_START;
     int max_n = 0;
     for (auto &J : sorted) max_n = std::max(max_n, J.n);
@@ -521,19 +517,14 @@ kfac_status_t jacobi_run(const float *const *F, const int32_t *dims, const int32
     return KFAC_OK;
 }
 
-int trd_min_dim() {
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("KFAC_EIG_TRD_MIN");
-        v = e ? atoi(e) : 64;
-    }
-    return v;
-}
+// Factors of order >= kTrdMinDim go to the tridiagonal solver (Jacobi for d = 300/600/1200 measured
+// +6/+29/+122 ms on ResNet-50).
+constexpr int kTrdMinDim = 64;
 
 bool use_trd(int n, uint32_t flags) {
     if (flags & KFAC_EIG_JACOBI) return false;
     if (flags & KFAC_EIG_TRIDIAG) return true;
-    return n >= trd_min_dim();
+    return n >= kTrdMinDim;
 }
 
 }  // namespace

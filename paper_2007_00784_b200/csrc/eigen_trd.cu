@@ -211,7 +211,6 @@ struct PanelLaunch {
     int cta_begin[kMaxGroupCtas + 1];
     int ring_off;                          // float offset of the symv prefetch ring in dynamic smem
     int use_xs;                            // x of the merged column kept in shared memory
-    int fused;                             // trailing update fused into the panel kernel
 };
 
 // One panel of 32 columns (LAPACK dlatrd, lower) for every active factor.  Column k (i = k - p0):
@@ -705,7 +704,7 @@ __global__ void __launch_bounds__(kTrdThreads, kTrdCtasPerSm) trd_panel(const __
         __syncthreads();
         TRD_TS(k, 9);
     }
-    if (L.fused && p0 + kNb < n) {
+    if (p0 + kNb < n) {
         // Fused rank-64 trailing update A[q0:n, q0:n] -= V W^T + W V^T (lower 64 x 64 tiles) on the
         // fp64 tensor cores, by the same group once every CTA has written its rows of the panel:
         // two teams of 8 warps per CTA, each tile's whole K = 64 of [V|W] and [W|V] (fp64 copies)
@@ -1413,7 +1412,7 @@ __global__ void upload_kernel(const __grid_constant__ Upload u) {
 }
 
 kfac_status_t upload(void *dst, const void *src, size_t bytes, cudaStream_t s) {
-    static Upload u;     // host staging (kernel params are copied at launch)
+    thread_local Upload u;     // host staging (kernel params are copied at launch)
     const unsigned char *p = static_cast<const unsigned char *>(src);
     for (size_t off = 0; off < bytes; off += sizeof(u.data)) {
         const size_t nb = std::min(sizeof(u.data), bytes - off);
@@ -1552,35 +1551,11 @@ T *rebase(T *p, char *base) {
     return reinterpret_cast<T *>(base + reinterpret_cast<uintptr_t>(p));
 }
 
-bool trail_fused() {       // trailing update inside trd_panel (KFAC_TRD_FUSED_TRAIL=0: separate GEMM)
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("KFAC_TRD_FUSED_TRAIL");
-        v = (e && e[0] == '0') ? 0 : 1;
-    }
-    return v == 1;
-}
-
-bool trail_tc() {
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("KFAC_TRD_TRAIL_TC");
-        v = (e && e[0] == '1') ? 1 : 0;
-    }
-    return v == 1;
-}
-
 int panel_capacity(size_t smem) {
-    static int cap = -1;
-    static size_t cap_smem = 0;
-    if (cap < 0 || cap_smem != smem) {
-        int per_sm = 0;
-        cudaFuncSetAttribute(trd_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, trd_panel, kTrdThreads, smem);
-        cap = std::max(1, per_sm) * num_sms();
-        cap_smem = smem;
-    }
-    return std::min(cap, kMaxGroupCtas);
+    int per_sm = 0;
+    set_smem_attr((const void *)trd_panel, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, trd_panel, kTrdThreads, smem);
+    return std::min(std::max(1, per_sm) * num_sms(), kMaxGroupCtas);
 }
 
 // Test modes (single factor): TRD_DEBUG_TRIDIAG stops after the reduction and copies (d, e) out;
@@ -1655,29 +1630,24 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
     KFAC_LAUNCHED();
 
     // ---- (1) tridiagonalisation: one persistent launch + one trailing GEMM per panel ----
-    static bool attr = false;
-    if (!attr) {
-        KFAC_CUDA_TRY(cudaFuncSetAttribute(bt_larft, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLarftSmem));
-        attr = true;
-    }
+    KFAC_CUDA_TRY(set_smem_attr((const void *)bt_larft, (int)kLarftSmem));
     const int ring_off = (int)round_up(round_up(max_n, kSymvC) + kSymvC + 8, 64);
     // v (floats) | symv ring | x of the merged column (doubles, phase B; only if it fits)
     const size_t smem_base = (size_t)ring_off * sizeof(float) + (size_t)kTrdWarps * 2 * 8 * 32 * sizeof(float4);
     const size_t smem_xs = (size_t)round_up(max_n, 2) * sizeof(double);
     const int use_xs = smem_base + smem_xs + 12 * 1024 <= 227 * 1024;
-    const size_t smem = smem_base + (use_xs ? smem_xs : 0);
-    const int fused_trail = trail_fused() && smem - (size_t)ring_off * sizeof(float) >= 2 * 2 * 64 * 68 * sizeof(double);
+    // the fused trailing update reuses the ring as two teams' 64 x 68 fp64 operand tiles
+    const size_t smem = std::max(smem_base + (use_xs ? smem_xs : 0),
+                                 (size_t)ring_off * sizeof(float) + 2 * 2 * 64 * 68 * sizeof(double));
     const int cap = panel_capacity(smem);
-    static PanelLaunch PL;
+    thread_local PanelLaunch PL;       // host staging (kernel parameters are copied at launch)
     // Staggered schedule: factor j (P_j panels) starts at launch P_max - P_j, so all factors finish
     // together and the small ones share the GPU with the big ones' small trailing matrices.
     int pmax = 0;
     for (int i = 0; i < count; ++i) pmax = std::max(pmax, cdiv(P.jobs[i].n, kNb));
-    // CTAs per active factor ~ (remaining trailing size)^wexp (default 2: the mat-vec bytes)
-    static const double wexp = [] {
-        const char *e = getenv("KFAC_TRD_WEXP");
-        return e ? atof(e) : 2.0;
-    }();
+    // CTAs per active factor ~ (remaining trailing size)^2 (the mat-vec bytes; exponents 1.5-3
+    // measured equal within noise)
+    constexpr double wexp = 2.0;
     for (int t = 0; t < pmax; ++t) {
         std::vector<int> act, pst;
         double wsum = 0.0;
@@ -1720,7 +1690,6 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
         PL.count = na;
         PL.ring_off = ring_off;
         PL.use_xs = use_xs;
-        PL.fused = fused_trail;
         int tot = 0;
         for (int q = 0; q < na; ++q) {
             PL.job[q] = act[q];
@@ -1746,7 +1715,7 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
                     fl += 2.0 * m * m;
                 }
                 const double mt = n - pst[q] - kNb;          // fused trailing update of the panel
-                if (fused_trail && mt > 0) {
+                if (mt > 0) {
                     by += 8.0 * mt * (mt + 1) / 2 + 2.0 * 8 * 64 * mt;   // C lower RMW + [V|W], [W|V]
                     fl += 2.0 * 64 * mt * (mt + 1);
                 }
@@ -1754,47 +1723,6 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
             prof_end(prof, s, by, fl);
         }
         }   // chunks of the active set
-        act = act_all;
-        pst = pst_all;
-        const int na = (int)act.size();
-        gd.clear();
-        if (fused_trail) continue;                  // done inside trd_panel
-        if (trail_tc()) {
-            // rank-64 trailing update on the tcgen05 3xTF32 engine (fp32-faithful products, fp32
-            // accumulation with IEEE drains; experiment switch KFAC_TRD_TRAIL_TC=1)
-            std::vector<GemmDesc> td;
-            for (int q = 0; q < na; ++q) {
-                const TrdJob &J = P.jobs[act[q]];
-                const int q0 = pst[q] + kNb;
-                if (J.n <= q0) continue;
-                GemmDesc g{};
-                g.M = g.N = J.n - q0;
-                g.K = 2 * kNb;
-                g.A = J.VW + (size_t)q0 * 64; g.lda = 64; g.trans_a = 0;
-                g.B = J.WV + (size_t)q0 * 64; g.ldb = 64; g.trans_b = 1;
-                g.C = J.A + (size_t)q0 * J.ldw + q0; g.ldc = J.ldw;
-                g.epi = EPI_SUB;
-                g.lower = 1;
-                td.push_back(g);
-            }
-            if (!td.empty()) RET_OK(gemm_grouped(td.data(), (int)td.size(), 0.f, s));
-            continue;
-        }
-        for (int q = 0; q < na; ++q) {
-            const TrdJob &J = P.jobs[act[q]];
-            const int q0 = pst[q] + kNb;
-            if (J.n <= q0) continue;
-            Gemm64Desc g{};
-            g.M = g.N = J.n - q0;
-            g.K = 2 * kNb;
-            g.A = J.VWd + (size_t)q0 * 64; g.ta = DT_F64; g.lda = 64; g.trans_a = 0;
-            g.B = J.WVd + (size_t)q0 * 64; g.tb = DT_F64; g.ldb = 64; g.trans_b = 1;
-            g.C = J.A + (size_t)q0 * J.ldw + q0; g.tc = DT_F32; g.ldc = J.ldw;
-            g.epi = EPI_SUB;
-            g.lower = 1;                             // the reduction reads only the lower triangle
-            gd.push_back(g);
-        }
-        if (!gd.empty()) RET_OK(gemm64_grouped(gd.data(), (int)gd.size(), s));
     }
 
     }   // mode != TRD_DEBUG_STEDC
@@ -1826,11 +1754,7 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
         // sorted lists in shared memory when they fit (2 doubles + 1 int per entry)
         const int smem_n = (nmax * 20 <= 200 * 1024) ? nmax : 0;
         if (smem_n) {
-            static bool dattr = false;
-            if (!dattr) {
-                KFAC_CUDA_TRY(cudaFuncSetAttribute(dc_deflate, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024 + 64));
-                dattr = true;
-            }
+            KFAC_CUDA_TRY(set_smem_attr((const void *)dc_deflate, 200 * 1024 + 64));
         }
         dc_deflate<<<nmg, 256, smem_n ? (size_t)smem_n * 20 + 16 : 0, s>>>(djobs, dm, ping, smem_n);
         KFAC_LAUNCHED();
@@ -1869,11 +1793,7 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
         {
             const int rank_n = (nmax * 8 <= 96 * 1024) ? nmax : 0;
             if (rank_n) {
-                static bool rattr = false;
-                if (!rattr) {
-                    KFAC_CUDA_TRY(cudaFuncSetAttribute(dc_rank, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
-                    rattr = true;
-                }
+                KFAC_CUDA_TRY(set_smem_attr((const void *)dc_rank, 96 * 1024));
             }
             dc_rank<<<dim3(cdiv(nmax, 128), nmg), 128, (size_t)rank_n * 8, s>>>(djobs, dm, rank_n);
         }

@@ -265,15 +265,6 @@ Plan make_plan(const kfac_layer_t *layers, int nl, float *const *A, const int32_
     return p;
 }
 
-bool planes_disabled() {
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("KFAC_SYRK_NO_PLANES");
-        v = (e && e[0] == '1') ? 1 : 0;
-    }
-    return v == 1;
-}
-
 }  // namespace
 
 size_t factors_workspace_bytes(const kfac_layer_t *layers, int nl) {
@@ -293,7 +284,7 @@ kfac_status_t factors_run(const kfac_layer_t *layers, int nl, const float *const
     // so the SYRK kernel gathers both planes and never splits in shared memory.
     std::vector<FactorJob> tc, simt;
     for (auto &j : p.jobs) (syrk_tc_supported(j) ? tc : simt).push_back(j);
-    if (!tc.empty() && !planes_disabled()) {
+    if (!tc.empty()) {
         float *pl = base + round_up(p.partial_floats, 64);
         std::vector<SplitJob> sj;
         for (auto &j : tc) {

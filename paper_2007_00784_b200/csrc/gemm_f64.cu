@@ -490,15 +490,6 @@ bool direct_ok(const Gemm64Desc &g) {
            (reinterpret_cast<uintptr_t>(g.B) % 16 == 0) && (g.lda % 2 == 0) && (g.ldb % 2 == 0);
 }
 
-bool g_pipe_disabled() {
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("KFAC_GEMM64_NOPIPE");
-        v = (e && e[0] == '1') ? 1 : 0;
-    }
-    return v == 1;
-}
-
 bool pipe_ok(const Gemm64Desc &g) {
     const int ea = g.ta == DT_F64 ? 8 : 4, eb = g.tb == DT_F64 ? 8 : 4;
     return (reinterpret_cast<uintptr_t>(g.A) % 16 == 0) && (reinterpret_cast<uintptr_t>(g.B) % 16 == 0) &&
@@ -509,10 +500,10 @@ bool pipe_ok(const Gemm64Desc &g) {
 
 kfac_status_t gemm64_grouped(const Gemm64Desc *descs, int count, cudaStream_t s) {
     for (int base = 0, end = 0; base < count; base = end) {
-        static Batch64 b;       // host staging; parameters are copied at launch
+        thread_local Batch64 b;   // host staging; parameters are copied at launch
         b.count = 0;
         end = base;
-        bool pipe = !g_pipe_disabled(), direct = pipe;
+        bool pipe = true, direct = true;
         for (int i = base; i < count && b.count < kGemm64MaxDescs; ++i, ++end) {
             const Gemm64Desc &g = descs[i];
             if (g.M <= 0 || g.N <= 0) continue;
@@ -529,20 +520,10 @@ kfac_status_t gemm64_grouped(const Gemm64Desc *descs, int count, cudaStream_t s)
         }
         const int prof = prof_begin(KFAC_PROF_GEMM64, s);
         if (direct) {
-            static bool dattr = false;
-            if (!dattr) {
-                KFAC_CUDA_TRY(cudaFuncSetAttribute(gemm64_direct_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   kDirectSmem));
-                dattr = true;
-            }
+            KFAC_CUDA_TRY(set_smem_attr((const void *)gemm64_direct_kernel, kDirectSmem));
             gemm64_direct_kernel<<<tiles, kPT, kDirectSmem, s>>>(b);
         } else if (pipe) {
-            static bool attr = false;
-            if (!attr) {
-                KFAC_CUDA_TRY(cudaFuncSetAttribute(gemm64_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   kPipeSmem));
-                attr = true;
-            }
+            KFAC_CUDA_TRY(set_smem_attr((const void *)gemm64_pipe_kernel, kPipeSmem));
             gemm64_pipe_kernel<<<tiles, kPT, kPipeSmem, s>>>(b);
         } else {
             gemm64_kernel<<<tiles, NT, 0, s>>>(b);

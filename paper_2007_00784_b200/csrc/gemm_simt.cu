@@ -153,15 +153,8 @@ kfac_status_t gemm_simt_grouped(const GemmDesc *descs, int count, float damping,
 }
 
 kfac_status_t gemm_grouped(const GemmDesc *descs, int count, float damping, cudaStream_t s) {
-    // Tensor-core path for the descriptors it supports, SIMT for the rest.
-    std::vector<GemmDesc> tc, simt;
-    for (int i = 0; i < count; ++i) (gemm_tc_supported(descs[i]) ? tc : simt).push_back(descs[i]);
-    if (!tc.empty()) {
-        kfac_status_t st = gemm_tc_grouped(tc.data(), (int)tc.size(), damping, s);
-        if (st != KFAC_OK) return st;
-    }
-    if (!simt.empty()) return gemm_simt_grouped(simt.data(), (int)simt.size(), damping, s);
-    return KFAC_OK;
+    // Layers below the tensor-core engine's tile (a dimension < 64) run the SIMT fp32 chain.
+    return gemm_simt_grouped(descs, count, damping, s);
 }
 
 }  // namespace kfac

@@ -59,13 +59,6 @@ struct TcDesc {
     int tile_begin, tiles_n;
 };
 
-struct __align__(64) TcBatch {
-    TcDesc d[kMaxTc];
-    int count;
-    float damping;
-    int drain;            // k-blocks accumulated in TMEM per drain (>= 1)
-};
-
 struct SyrkBatch {
     int count;
     int drain;
@@ -167,80 +160,9 @@ struct Smem {
     __device__ __forceinline__ uint8_t *lo(int l) const { return base + (kRaw + l) * kStageBytes; }
 };
 
-__device__ __forceinline__ Smem carve(uint8_t *smem_raw) {
-    Smem s;
-    // align by an integer offset on the __shared__ array itself (a uintptr round trip would turn
-    // every later access into a generic LD/ST instead of LDS/STS)
-    const uint32_t a0 = smem_u32(smem_raw);
-    s.base = smem_raw + (((a0 + 1023u) & ~1023u) - a0);
-    uint64_t *bars = reinterpret_cast<uint64_t *>(s.base + (kRaw + kLo) * kStageBytes);
-    s.raw_full = smem_u32(bars);
-    s.ready = smem_u32(bars + kRaw);
-    s.raw_empty = smem_u32(bars + 2 * kRaw);
-    s.lo_empty = smem_u32(bars + 3 * kRaw);
-    s.tfull = smem_u32(bars + 3 * kRaw + kLo);
-    s.tempty = smem_u32(bars + 3 * kRaw + kLo + 2);
-    s.tmem_slot = reinterpret_cast<uint32_t *>(bars + 3 * kRaw + kLo + 4);
-    s.rowtab = reinterpret_cast<int2 *>(bars + 32);      // bytes 256..511 of the barrier area
-    return s;
-}
-
-__device__ __forceinline__ void setup(const Smem &S, int warp, uint32_t raw_full_count) {
-    if (threadIdx.x == 0) {
-        for (int i = 0; i < kRaw; ++i) {
-            mbar_init(S.raw_full + 8 * i, raw_full_count);
-            mbar_init(S.ready + 8 * i, 128);
-            mbar_init(S.raw_empty + 8 * i, 1);
-        }
-        for (int i = 0; i < kLo; ++i) mbar_init(S.lo_empty + 8 * i, 1);
-        for (int b = 0; b < 2; ++b) {
-            mbar_init(S.tfull + 8 * b, 1);
-            mbar_init(S.tempty + 8 * b, 128);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    if (warp == W_TMA) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(S.tmem_slot)),
-                     "r"(kTmemCols));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-}
-
-__device__ __forceinline__ void teardown(uint32_t tmem, int warp) {
-    tc_fence_before();
-    __syncthreads();
-    if (warp == W_TMA) {
-        tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
-    }
-}
-
 // Round an fp32 value to the nearest TF32 (10-bit mantissa), ties away from zero; exact in fp32.
 __device__ __forceinline__ float tf32_rn(float x) {
     return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
-}
-
-// hi = rn_tf32(x) in place, lo = rn_tf32(x - hi): 3xTF32 operands, both exact TF32 values, so the
-// dropped terms (lo*lo and the rounding of lo) are < 2^-22 relative per product.  (Feeding the raw
-// tile as hi and writing only lo = x - trunc(x) would save the in-place write, but the hardware
-// truncation makes |lo| up to 2^-10|x| and the product error 4x larger -- too much for the
-// 1/damping amplification on rank-deficient layers.)
-__device__ __forceinline__ void split_region(uint8_t *raw, uint8_t *lo_base, int n_f4, int t) {
-    float4 *hi = reinterpret_cast<float4 *>(raw);
-    float4 *lo = reinterpret_cast<float4 *>(lo_base);
-#pragma unroll 4
-    for (int i = t; i < n_f4; i += 128) {
-        float4 x = hi[i], h, l;
-        h.x = tf32_rn(x.x); h.y = tf32_rn(x.y); h.z = tf32_rn(x.z); h.w = tf32_rn(x.w);
-        l.x = tf32_rn(x.x - h.x); l.y = tf32_rn(x.y - h.y);
-        l.z = tf32_rn(x.z - h.z); l.w = tf32_rn(x.w - h.w);
-        hi[i] = h;
-        lo[i] = l;
-    }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
 __device__ __forceinline__ uint64_t operand_desc(uint32_t base, int kstep, int mn_major) {
@@ -249,33 +171,6 @@ __device__ __forceinline__ uint64_t operand_desc(uint32_t base, int kstep, int m
     // LBO 4096 = 32-element mn groups).
     if (!mn_major) return smem_desc(base + kstep * 32, 16, 1024, 2);
     return smem_desc(base + kstep * 1024, 4096, 512, 1);
-}
-
-// MMA issuer: for each k-block, the three 3xTF32 products into TMEM buffer (segment & 1), where a
-// segment is `drain` consecutive k-blocks accumulated in TMEM before the drain warps take it.
-__device__ __forceinline__ void mma_loop(const Smem &S, uint32_t tmem, int nk, int a_mn, int b_mn, bool same_ab,
-                                         int drain) {
-    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
-                           ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
-    for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % kRaw, l = kb % kLo;
-        const int seg = kb / drain, pos = kb - seg * drain, b = seg & 1, u = seg >> 1;
-        mbar_wait(S.ready + 8 * s, (kb / kRaw) & 1);
-        if (pos == 0 && u >= 1) mbar_wait(S.tempty + 8 * b, (u - 1) & 1);
-        tc_fence_after();
-        const uint32_t a_hi = smem_u32(S.raw(s)), a_lo = smem_u32(S.lo(l));
-        const uint32_t b_hi = same_ab ? a_hi : a_hi + kTileBytes, b_lo = same_ab ? a_lo : a_lo + kTileBytes;
-        const uint32_t d = tmem + b * BN;
-#pragma unroll
-        for (int ks = 0; ks < BK / 8; ++ks) {
-            mma_tf32(d, operand_desc(a_lo, ks, a_mn), operand_desc(b_hi, ks, b_mn), idesc, (ks > 0 || pos > 0) ? 1u : 0u);
-            mma_tf32(d, operand_desc(a_hi, ks, a_mn), operand_desc(b_lo, ks, b_mn), idesc, 1u);
-            mma_tf32(d, operand_desc(a_hi, ks, a_mn), operand_desc(b_hi, ks, b_mn), idesc, 1u);
-        }
-        mma_commit(S.raw_empty + 8 * s);
-        mma_commit(S.lo_empty + 8 * l);
-        if (pos == drain - 1 || kb == nk - 1) mma_commit(S.tfull + 8 * b);
-    }
 }
 
 // Drain warps: every segment's 128x128 partial product is added into fp32 registers with IEEE
@@ -303,15 +198,6 @@ __device__ __forceinline__ void drain_loop(const Smem &S, uint32_t tmem, int nk,
 }
 
 // ------------------------------------------------------------ GEMM kernel --
-__device__ __forceinline__ int find_desc(const TcBatch &b, int tile) {
-    int lo = 0, hi = b.count - 1;
-    while (lo < hi) {
-        int mid = (lo + hi + 1) >> 1;
-        if (b.d[mid].tile_begin <= tile) lo = mid; else hi = mid - 1;
-    }
-    return lo;
-}
-
 //   K-major: one box {32 (k), 128 (mn)}, 128B swizzle -> 128 rows x 128 B
 //   MN-major: four boxes {32 (mn), 32 (k)}, 128B swizzle with 32-B atoms -> 32 k-rows x 128 B each
 __device__ __forceinline__ void load_tile(uint32_t dst, const CUtensorMap *map, uint32_t bar, int mn0, int k0, int mn_major) {
@@ -322,73 +208,6 @@ __device__ __forceinline__ void load_tile(uint32_t dst, const CUtensorMap *map, 
         for (int g = 0; g < 4; ++g) tma_load_2d(dst + g * 4096, map, bar, mn0 + 32 * g, k0);
     }
 }
-
-__global__ void __launch_bounds__(NT, 1) gemm_tc_kernel(const __grid_constant__ TcBatch batch) {
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
-    const Smem S = carve(smem_raw);
-    const int tile = blockIdx.x;
-    const TcDesc &d = batch.d[find_desc(batch, tile)];
-    const int local = tile - d.tile_begin;
-    const int m0 = (local / d.tiles_n) * BM, n0 = (local % d.tiles_n) * BN;
-    const int Ne = d.dyn ? min(d.N, d.dyn[0]) : d.N, Ke = d.dyn ? min(d.K, d.dyn[1]) : d.K;
-    const int nk = (Ke + BK - 1) / BK;
-    if (n0 >= Ne || nk <= 0) return;          // whole CTA exits before any barrier / TMEM setup
-    if (d.lower && n0 >= m0 + BM) return;     // strictly above the diagonal (symmetric update)
-    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    if (warp == W_TMA && lane == 0) {
-        prefetch_map(&d.ta);
-        prefetch_map(&d.tb);
-    }
-    setup(S, warp, 1);
-    const uint32_t tmem = *S.tmem_slot;
-
-    if (warp == W_TMA) {
-        if (lane == 0) {
-            for (int kb = 0; kb < nk; ++kb) {
-                const int s = kb % kRaw;
-                if (kb >= kRaw) mbar_wait(S.raw_empty + 8 * s, ((kb / kRaw) - 1) & 1);
-                const uint32_t st = smem_u32(S.raw(s));
-                mbar_expect_tx(S.raw_full + 8 * s, 2 * kTileBytes);
-                load_tile(st, &d.ta, S.raw_full + 8 * s, m0, kb * BK, d.a_mn);
-                load_tile(st + kTileBytes, &d.tb, S.raw_full + 8 * s, n0, kb * BK, d.b_mn);
-            }
-        }
-    } else if (warp == W_MMA) {
-        if (lane == 0) mma_loop(S, tmem, nk, d.a_mn, d.b_mn, false, batch.drain);
-    } else if (warp < W_DRAIN0) {
-        const int t = threadIdx.x;
-        for (int kb = 0; kb < nk; ++kb) {
-            const int s = kb % kRaw, l = kb % kLo;
-            mbar_wait(S.raw_full + 8 * s, (kb / kRaw) & 1);
-            if (kb >= kLo) mbar_wait(S.lo_empty + 8 * l, ((kb / kLo) - 1) & 1);
-            split_region(S.raw(s), S.lo(l), 2 * kTileBytes / 16, t);
-            mbar_arrive(S.ready + 8 * s);
-        }
-    } else {
-        const int wq = warp - W_DRAIN0;
-        float acc[BN];
-        drain_loop(S, tmem, nk, wq, acc, batch.drain);
-        const int m = m0 + wq * 32 + lane;
-        if (m < d.M) {
-            const float vr = epi_uses_vectors(d.epi) ? d.vr[m] : 0.f;
-            float *crow = d.C + (size_t)m * d.ldc;
-#pragma unroll
-            for (int j = 0; j < BN; ++j) {
-                const int n = n0 + j;
-                if (n < Ne) {
-                    float v = acc[j];
-                    if (d.epi == EPI_DIV_EIGEN) v = v / fmaxf(fmaf(vr, d.vc[n], batch.damping), 1e-12f);
-                    else if (d.epi == EPI_DIV_FACTORED)
-                        v = v / fmaxf((vr + batch.damping) * (d.vc[n] + batch.damping), 1e-12f);
-                    else if (d.epi == EPI_SUB) v = crow[n] - v;
-                    crow[n] = v;
-                }
-            }
-        }
-    }
-    teardown(tmem, warp);
-}
-
 
 // --------------------------------------------------- planes GEMM kernel --
 // Operands arrive pre-split as TF32 planes (hi, lo), so there is no split pass: per k-block the
@@ -660,312 +479,6 @@ struct SyrkGeom {
     const float *src_lo;
 };
 
-// Producer warps 0-3: cp.async gathers of the 32-row k-block into raw stage s; the stage's
-// mbarrier completes when every producer thread's copies have landed.  Warp w fills rows
-// w + 4j (j < 8).  The row -> (image, output pixel) decomposition is done once per row by lanes
-// 0-7 in parallel and broadcast through a per-warp shared-memory table (the integer divisions
-// were the producer's instruction-issue bottleneck); per (row, operand) only a bounds test and
-// an add remain.
-__device__ __forceinline__ void syrk_issue(const SyrkGeom &G, const Smem &S, int s, long long r0, long long r_end,
-                                           const ChunkInfo (&ci)[2], int cc, int t, bool diag) {
-    const uint32_t st = smem_u32(S.raw(s));
-    const int warp = t / 32, lane = t % 32;
-    // lane j < 8 describes row r0 + warp + 4 j: element offset of its receptive-field origin and
-    // the origin's (ih0, iw0); invalid rows (past r_end) get ih0 = -32768 so every tap fails
-    int org = 0, ihw = 0;
-    {
-        const long long r = r0 + warp + 4 * (lane & 7);
-        const bool rv = r < r_end;
-        if (G.is_a) {
-            const int hw = G.h_out * G.w_out;
-            const int ri = rv ? (int)r : 0;
-            const int img = ri / hw;
-            const int p = ri - img * hw;
-            const int oh = p / G.w_out, ow = p - (p / G.w_out) * G.w_out;
-            const int ih0 = oh * G.stride_h - G.pad_h, iw0 = ow * G.stride_w - G.pad_w;
-            org = ((img * G.h_in + ih0) * G.w_in + iw0) * G.c_in;
-            ihw = rv ? (int)(((unsigned)ih0 << 16) | ((unsigned)iw0 & 0xffffu)) : (int)0x80000000;
-        } else {
-            org = rv ? (int)r * G.c_in : 0;
-            ihw = rv ? 0 : (int)0x80000000;
-        }
-    }
-    int2 *tab = S.rowtab + warp * 8;
-    __syncwarp();                                     // previous k-block's reads are done
-    if (lane < 8) tab[lane] = make_int2(org, ihw);
-    __syncwarp();
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        const int k = warp + 4 * j;
-        const int2 rd = tab[j];
-        const int o = rd.x, hv = rd.y;
-        const bool rv = hv != (int)0x80000000;
-        const int ih0 = hv >> 16, iw0 = (int)(short)(hv & 0xffff);
-#pragma unroll
-        for (int op = 0; op < 2; ++op) {
-            if (op == 1 && diag) break;
-            const uint32_t dst = st + op * kTileBytes + mn_off(k, 4 * cc);
-            const ChunkInfo &c = ci[op];
-            if (c.kind == 1) {                        // bias chunk {1, 0, 0, 0} on valid rows
-                cp_async16(dst, kBiasChunk, rv ? 16u : 0u);
-                continue;
-            }
-            bool ok = rv && c.kind == 0;
-            if (G.is_a) {
-                // c.off holds (kh * w_in + kw) * c_in + channel (offset inside the receptive field)
-                ok = ok && (unsigned)(ih0 + c.kh) < (unsigned)G.h_in && (unsigned)(iw0 + c.kw) < (unsigned)G.w_in;
-            }
-            cp_async16(dst, ok ? G.src + (o + c.off) : G.src, ok ? 16u : 0u);
-        }
-    }
-}
-
-__global__ void __launch_bounds__(NT, 1) syrk_tc_kernel(const __grid_constant__ SyrkBatch batch) {
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
-    const Smem S = carve(smem_raw);
-    const int item = blockIdx.x;
-    const FactorJob &J = batch.j[find_job(batch, item)];
-    const int local = item - J.item_begin;
-    const int tau = local / J.splits, split = local % J.splits;
-    int ti, tj;
-    upper_tile(tau, J.t1d, ti, tj);
-    const bool diag = ti == tj;
-    const long long r_begin = (long long)split * J.chunk;
-    const long long r_end = min(J.n, r_begin + J.chunk);
-    const int nk = (int)((r_end - r_begin + BK - 1) / BK);
-    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    setup(S, warp, 128);
-    const uint32_t tmem = *S.tmem_slot;
-
-    if (warp == W_MMA) {
-        if (lane == 0) mma_loop(S, tmem, nk, 1, 1, diag, batch.drain);
-    } else if (warp < W_DRAIN0) {
-        const int t = threadIdx.x, cc = t % 32;
-        ChunkInfo ci[2] = {chunk_info(J, ti * BM + 4 * cc), chunk_info(J, tj * BM + 4 * cc)};
-        const SyrkGeom G{J.src, J.is_a, J.c_in, J.h_in, J.w_in, J.h_out, J.w_out,
-                         J.stride_h, J.stride_w, J.pad_h, J.pad_w};
-        const int n_f4 = (diag ? 1 : 2) * kTileBytes / 16;
-        // prologue: k-blocks 0 .. kRaw-2 in flight before the first split
-        for (int p = 0; p < kRaw - 1 && p < nk; ++p) {
-            syrk_issue(G, S, p, r_begin + (long long)p * BK, r_end, ci, cc, t, diag);
-            cp_async_arrive(S.raw_full + 8 * p);
-        }
-        for (int kb = 0; kb < nk; ++kb) {
-            // split k-block kb first (overlaps the MMA of kb-1), then refill the stage that
-            // MMA kb-1 releases with k-block kb + kRaw - 1
-            const int s = kb % kRaw, l = kb % kLo;
-            mbar_wait(S.raw_full + 8 * s, (kb / kRaw) & 1);
-            if (kb >= kLo) mbar_wait(S.lo_empty + 8 * l, ((kb / kLo) - 1) & 1);
-            split_region(S.raw(s), S.lo(l), n_f4, t);
-            mbar_arrive(S.ready + 8 * s);
-            const int nxt = kb + kRaw - 1;
-            if (nxt < nk) {
-                const int s2 = nxt % kRaw;
-                if (nxt >= kRaw) mbar_wait(S.raw_empty + 8 * s2, ((nxt / kRaw) - 1) & 1);
-                syrk_issue(G, S, s2, r_begin + (long long)nxt * BK, r_end, ci, cc, t, diag);
-                cp_async_arrive(S.raw_full + 8 * s2);
-            }
-        }
-    } else if (warp < W_TMA) {
-        const int wq = warp - W_DRAIN0;
-        float acc[BN];
-        drain_loop(S, tmem, nk, wq, acc, batch.drain);
-        float4 *dst = reinterpret_cast<float4 *>(J.partial + ((size_t)split * J.tiles + tau) * (BM * BN) +
-                                                 (size_t)(wq * 32 + lane) * BN);
-#pragma unroll
-        for (int j = 0; j < BN / 4; ++j) dst[j] = make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
-    }
-    teardown(tmem, warp);
-}
-
-
-// ----------------------------------------------------- planes SYRK kernel --
-// The factor's input arrives pre-split as TF32 planes (split_planes), so the producer warps only
-// gather: per k-block each thread issues 16-byte cp.async copies of both planes of its column
-// chunk(s) into [A_hi | B_hi | A_lo | B_lo] of one of kPS 64-KB stages (diagonal tiles: A only),
-// and the MMA thread consumes them directly -- no split pass through shared memory.
-template <bool IS_A>
-__device__ __forceinline__ void syrk_issue_planes(const SyrkGeom &G, uint32_t st, int2 *tabw, long long r0,
-                                                  long long r_end, const ChunkInfo (&ci)[2], int cc, int t,
-                                                  bool diag) {
-    const int warp = t / 32, lane = t % 32;
-    if (!IS_A) {
-        // plain rows (gradients; activations of 1x1 stride-1 unpadded convolutions and linear
-        // layers): row r of X is row r of the input, no im2col geometry
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const int k = warp + 4 * j;
-            const long long r = r0 + k;
-            const bool rv = r < r_end;
-            const float *rowh = G.src + (size_t)r * G.c_in, *rowl = G.src_lo + (size_t)r * G.c_in;
-#pragma unroll
-            for (int op = 0; op < 2; ++op) {
-                if (op == 1 && diag) break;
-                const uint32_t dhi = st + op * kTileBytes + mn_off(k, 4 * cc);
-                if (ci[op].kind == 1) {               // bias chunk: hi {1, 0, 0, 0}, lo 0, on valid rows
-                    cp_async16(dhi, kBiasChunk, rv ? 16u : 0u);
-                    cp_async16(dhi + 2 * kTileBytes, kBiasChunk, 0u);
-                    continue;
-                }
-                const bool ok = rv && ci[op].kind == 0;
-                cp_async16(dhi, ok ? rowh + ci[op].off : G.src, ok ? 16u : 0u);
-                cp_async16(dhi + 2 * kTileBytes, ok ? rowl + ci[op].off : G.src_lo, ok ? 16u : 0u);
-            }
-        }
-        return;
-    }
-    int org = 0, ihw = 0;
-    {
-        const long long r = r0 + warp + 4 * (lane & 7);
-        const bool rv = r < r_end;
-        const int hw = G.h_out * G.w_out;
-        const int ri = rv ? (int)r : 0;
-        const int img = ri / hw;
-        const int p = ri - img * hw;
-        const int oh = p / G.w_out, ow = p - (p / G.w_out) * G.w_out;
-        const int ih0 = oh * G.stride_h - G.pad_h, iw0 = ow * G.stride_w - G.pad_w;
-        org = ((img * G.h_in + ih0) * G.w_in + iw0) * G.c_in;
-        ihw = rv ? (int)(((unsigned)ih0 << 16) | ((unsigned)iw0 & 0xffffu)) : (int)0x80000000;
-    }
-    __syncwarp();
-    if (lane < 8) tabw[lane] = make_int2(org, ihw);
-    __syncwarp();
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        const int k = warp + 4 * j;
-        const int2 rd = tabw[j];
-        const int o = rd.x, hv = rd.y;
-        const bool rv = hv != (int)0x80000000;
-        const int ih0 = hv >> 16, iw0 = (int)(short)(hv & 0xffff);
-#pragma unroll
-        for (int op = 0; op < 2; ++op) {
-            if (op == 1 && diag) break;
-            const uint32_t dhi = st + op * kTileBytes + mn_off(k, 4 * cc);
-            const uint32_t dlo = dhi + 2 * kTileBytes;
-            const ChunkInfo &c = ci[op];
-            if (c.kind == 1) {                        // bias chunk: hi {1, 0, 0, 0}, lo 0, on valid rows
-                cp_async16(dhi, kBiasChunk, rv ? 16u : 0u);
-                cp_async16(dlo, kBiasChunk, 0u);
-                continue;
-            }
-            const bool ok = rv && c.kind == 0 && (unsigned)(ih0 + c.kh) < (unsigned)G.h_in &&
-                            (unsigned)(iw0 + c.kw) < (unsigned)G.w_in;
-            cp_async16(dhi, ok ? G.src + (o + c.off) : G.src, ok ? 16u : 0u);
-            cp_async16(dlo, ok ? G.src_lo + (o + c.off) : G.src_lo, ok ? 16u : 0u);
-        }
-    }
-}
-
-__global__ void __launch_bounds__(NT, 1) syrk_tc_planes_kernel(const __grid_constant__ SyrkBatch batch) {
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
-    const uint32_t a0 = smem_u32(smem_raw);
-    uint8_t *base = smem_raw + (((a0 + 1023u) & ~1023u) - a0);
-    uint64_t *bars = reinterpret_cast<uint64_t *>(base + kPS * kPlaneStage);
-    const uint32_t full = smem_u32(bars), empty = smem_u32(bars + kPS);
-    Smem S;
-    S.base = base;
-    S.tfull = smem_u32(bars + 2 * kPS);
-    S.tempty = smem_u32(bars + 2 * kPS + 2);
-    S.tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * kPS + 4);
-    int2 *rowtab = reinterpret_cast<int2 *>(bars + 32);
-
-    const int item = blockIdx.x;
-    const FactorJob &J = batch.j[find_job(batch, item)];
-    const int local = item - J.item_begin;
-    const int tau = local / J.splits, split = local % J.splits;
-    int ti, tj;
-    upper_tile(tau, J.t1d, ti, tj);
-    const bool diag = ti == tj;
-    const long long r_begin = (long long)split * J.chunk;
-    const long long r_end = min(J.n, r_begin + J.chunk);
-    const int nk = (int)((r_end - r_begin + BK - 1) / BK);
-    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    if (threadIdx.x == 0) {
-        for (int i = 0; i < kPS; ++i) {
-            mbar_init(full + 8 * i, 128);
-            mbar_init(empty + 8 * i, 1);
-        }
-        for (int b = 0; b < 2; ++b) {
-            mbar_init(S.tfull + 8 * b, 1);
-            mbar_init(S.tempty + 8 * b, 128);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    if (warp == W_TMA) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(S.tmem_slot)),
-                     "r"(kTmemCols));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem = *S.tmem_slot;
-
-    if (warp == W_MMA) {
-        if (lane == 0) {
-            const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | (1u << 16) |
-                                   ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
-            const int drain = batch.drain;
-            for (int kb = 0; kb < nk; ++kb) {
-                const int s = kb % kPS;
-                const int seg = kb / drain, pos = kb - seg * drain, b = seg & 1, u = seg >> 1;
-                mbar_wait(full + 8 * s, (kb / kPS) & 1);
-                if (pos == 0 && u >= 1) mbar_wait(S.tempty + 8 * b, (u - 1) & 1);
-                tc_fence_after();
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                const uint32_t st = smem_u32(base + s * kPlaneStage);
-                const uint32_t a_hi = st, a_lo = st + 2 * kTileBytes;
-                const uint32_t b_hi = diag ? a_hi : st + kTileBytes, b_lo = diag ? a_lo : st + 3 * kTileBytes;
-                const uint32_t dt = tmem + b * BN;
-#pragma unroll
-                for (int ks = 0; ks < BK / 8; ++ks) {
-                    mma_tf32(dt, operand_desc(a_lo, ks, 1), operand_desc(b_hi, ks, 1), idesc, (ks > 0 || pos > 0) ? 1u : 0u);
-                    mma_tf32(dt, operand_desc(a_hi, ks, 1), operand_desc(b_lo, ks, 1), idesc, 1u);
-                    mma_tf32(dt, operand_desc(a_hi, ks, 1), operand_desc(b_hi, ks, 1), idesc, 1u);
-                }
-                mma_commit(empty + 8 * s);
-                if (pos == drain - 1 || kb == nk - 1) mma_commit(S.tfull + 8 * b);
-            }
-        }
-    } else if (warp < W_DRAIN0) {
-        const int t = threadIdx.x, cc = t % 32;
-        ChunkInfo ci[2] = {chunk_info(J, ti * BM + 4 * cc), chunk_info(J, tj * BM + 4 * cc)};
-        SyrkGeom G{J.src, J.is_a, J.c_in, J.h_in, J.w_in, J.h_out, J.w_out,
-                   J.stride_h, J.stride_w, J.pad_h, J.pad_w, J.src_lo};
-        int2 *tabw = rowtab + warp * 8;
-        for (int kb = 0; kb < nk; ++kb) {
-            const int s = kb % kPS;
-            if (kb >= kPS) mbar_wait(empty + 8 * s, ((kb / kPS) - 1) & 1);
-            // plain-row gather unless the im2col geometry is needed (A factor of a conv that is not
-            // 1x1, stride 1, unpadded)
-            const bool plain = !G.is_a || (J.k_w == 1 && J.h_in == J.h_out && J.w_in == J.w_out && J.pad_h == 0 &&
-                                           J.pad_w == 0 && J.stride_h == 1 && J.stride_w == 1);
-            if (!plain)
-                syrk_issue_planes<true>(G, smem_u32(base + s * kPlaneStage), tabw, r_begin + (long long)kb * BK, r_end,
-                                        ci, cc, t, diag);
-            else
-                syrk_issue_planes<false>(G, smem_u32(base + s * kPlaneStage), tabw, r_begin + (long long)kb * BK, r_end,
-                                         ci, cc, t, diag);
-            cp_async_arrive(full + 8 * s);
-        }
-    } else if (warp < W_TMA) {
-        const int wq = warp - W_DRAIN0;
-        float acc[BN];
-        drain_loop(S, tmem, nk, wq, acc, batch.drain);
-        float4 *dst = reinterpret_cast<float4 *>(J.partial + ((size_t)split * J.tiles + tau) * (BM * BN) +
-                                                 (size_t)(wq * 32 + lane) * BN);
-#pragma unroll
-        for (int j = 0; j < BN / 4; ++j) dst[j] = make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
-    }
-    tc_fence_before();
-    __syncthreads();
-    if (warp == W_TMA) {
-        tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
-    }
-}
-
-
 // ------------------------------------------------- planes SYRK, wide producer --
 // Same pipeline as syrk_tc_planes_kernel with twice the gather throughput: 8 producer warps (warp
 // w fills k-rows w + 8j, j < 4) and 8 drain warps (two per TMEM lane quadrant, 64 columns each,
@@ -1202,115 +715,28 @@ bool make_map(CUtensorMap *map, const float *ptr, int rows, int cols, int ld, in
     return r == CUDA_SUCCESS;
 }
 
-// k-blocks per TMEM accumulation segment: KFAC_TC_DRAIN_GEMM / KFAC_TC_DRAIN_SYRK.
-int drain_env(const char *name, int dflt) {
-    const char *e = getenv(name);
-    const int v = e ? atoi(e) : dflt;
-    return v >= 1 ? v : 1;
-}
-int g_drain_gemm() {
-    static int v = drain_env("KFAC_TC_DRAIN_GEMM", 2);
-    return v;
-}
-int g_drain_syrk() {
-    static int v = drain_env("KFAC_TC_DRAIN_SYRK", 2);
-    return v;
-}
-
-bool g_syrk_narrow() {         // KFAC_SYRK_NARROW=1: the 4-producer-warp planes SYRK
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("KFAC_SYRK_NARROW");
-        v = (e && e[0] == '1') ? 1 : 0;
-    }
-    return v == 1;
-}
-
-bool g_tc_disabled() {
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("KFAC_DISABLE_TC");
-        v = (e && e[0] == '1') ? 1 : 0;
-    }
-    return v == 1;
-}
+// k-blocks per TMEM accumulation segment: the tensor core's fp32 accumulation
+// truncates, so a segment stays in TMEM for 2 k-blocks (24 MMAs) before the IEEE drain.
+constexpr int kDrainGemm = 2;
+constexpr int kDrainSyrk = 2;
 
 }  // namespace
 
 bool gemm_tc_supported(const GemmDesc &d) {
-    if (g_tc_disabled()) return false;
     if (d.M < 64 || d.N < 64 || d.K < 32) return false;         // small problems: SIMT
     if ((d.lda & 3) || (d.ldb & 3) || (d.ldc & 3)) return false;
     if (!aligned16(d.A) || !aligned16(d.B)) return false;
     return encode_fn() != nullptr;
 }
 
-kfac_status_t gemm_tc_grouped(const GemmDesc *descs, int count, float damping, cudaStream_t s) {
-    static bool attr = false;
-    if (!attr) {
-        KFAC_CUDA_TRY(cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
-        attr = true;
-    }
-    for (int base = 0; base < count; base += kMaxTc) {
-        TcBatch b;
-        memset(&b, 0, sizeof(b));
-        b.damping = damping;
-        b.drain = g_drain_gemm();
-        b.count = 0;
-        int tiles = 0;
-        for (int i = base; i < count && b.count < kMaxTc; ++i) {
-            const GemmDesc &g = descs[i];
-            TcDesc &t = b.d[b.count];
-            // op(A) (M x K): K-major if A[m*lda + k] (trans_a = 0), MN-major if A[k*lda + m]
-            t.a_mn = g.trans_a ? 1 : 0;
-            t.b_mn = g.trans_b ? 0 : 1;      // op(B)[k][n] = B[k*ldb + n] is N-contiguous -> MN-major
-            const CUtensorMapSwizzle kmaj = CU_TENSOR_MAP_SWIZZLE_128B, mnmaj = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
-            bool ok = t.a_mn ? make_map(&t.ta, g.A, g.K, g.M, g.lda, 32, 32, mnmaj)
-                             : make_map(&t.ta, g.A, g.M, g.K, g.lda, 32, 128, kmaj);
-            ok = ok && (t.b_mn ? make_map(&t.tb, g.B, g.K, g.N, g.ldb, 32, 32, mnmaj)
-                               : make_map(&t.tb, g.B, g.N, g.K, g.ldb, 32, 128, kmaj));
-            if (!ok) {
-                set_error("cuTensorMapEncodeTiled failed");
-                return KFAC_ERR_CUDA;
-            }
-            t.C = g.C; t.vr = g.vr; t.vc = g.vc; t.dyn = g.dyn; t.lower = g.lower;
-            t.M = g.M; t.N = g.N; t.K = g.K; t.ldc = g.ldc; t.epi = g.epi;
-            t.tiles_n = cdiv(g.N, BN);
-            t.tile_begin = tiles;
-            tiles += cdiv(g.M, BM) * t.tiles_n;
-            ++b.count;
-        }
-        if (!b.count) continue;
-        const int prof = prof_begin(KFAC_PROF_GEMM_TC, s);
-        gemm_tc_kernel<<<tiles, NT, kSmemBytes, s>>>(b);
-        KFAC_LAUNCHED();
-        if (prof >= 0) {
-            double by = 0.0, fl = 0.0;
-            for (int i = 0; i < b.count; ++i) {
-                const TcDesc &g = b.d[i];
-                fl += 2.0 * g.M * g.N * g.K;
-                by += 4.0 * ((double)g.M * g.K + (double)g.K * g.N + (double)g.M * g.N);
-            }
-            prof_end(prof, s, by, fl);
-        }
-    }
-    return KFAC_OK;
-}
-
-
 kfac_status_t gemm_tc_planes_grouped(const GemmDesc *descs, int count, float damping, cudaStream_t s) {
-    static bool attr = false;
-    if (!attr) {
-        KFAC_CUDA_TRY(cudaFuncSetAttribute(gemm_tc_planes_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           kSmemBytes));
-        attr = true;
-    }
+    KFAC_CUDA_TRY(set_smem_attr((const void *)gemm_tc_planes_kernel, kSmemBytes));
     static_assert(kPS * kPlaneStage + 1024 + 2 * kPS * 8 + 64 <= kSmemBytes, "planes smem");
     for (int base = 0; base < count; base += kMaxTc) {
-        static TcPlanesBatch b;
+        thread_local TcPlanesBatch b;    // host staging (kernel parameters are copied at launch)
         memset(&b, 0, sizeof(b));
         b.damping = damping;
-        b.drain = g_drain_gemm();
+        b.drain = kDrainGemm;
         int tiles = 0;
         for (int i = base; i < count && b.count < kMaxTc; ++i) {
             const GemmDesc &g = descs[i];
@@ -1379,7 +805,6 @@ kfac_status_t split_planes(const SplitJob *jobs, int count, cudaStream_t s) {
 }
 
 bool syrk_tc_supported(const FactorJob &j) {
-    if (g_tc_disabled()) return false;
     if (j.d < 64 || j.n < 32) return false;               // small factors: SIMT tile
     if (j.c_in % 4 != 0) return false;                    // 16-byte gathers
     if (j.is_a && j.bias_col && j.patch_cols % 4 != 0) return false;
@@ -1391,15 +816,11 @@ bool syrk_tc_supported(const FactorJob &j) {
 }
 
 kfac_status_t syrk_tc_partial(const FactorJob *jobs, int count, cudaStream_t s) {
-    static bool attr = false;
-    if (!attr) {
-        KFAC_CUDA_TRY(cudaFuncSetAttribute(syrk_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
-        attr = true;
-    }
+    KFAC_CUDA_TRY(set_smem_attr((const void *)syrk_tc_planes8_kernel, kSmemBytes));
     for (int base = 0; base < count; base += kMaxSyrk) {
         SyrkBatch b;
         b.count = 0;
-        b.drain = g_drain_syrk();
+        b.drain = kDrainSyrk;
         int items = 0;
         for (int i = base; i < count && b.count < kMaxSyrk; ++i) {
             FactorJob j = jobs[i];
@@ -1407,28 +828,8 @@ kfac_status_t syrk_tc_partial(const FactorJob *jobs, int count, cudaStream_t s) 
             items += j.tiles * j.splits;
             b.j[b.count++] = j;
         }
-        bool planes = true;
-        for (int i = 0; i < b.count; ++i) planes = planes && b.j[i].src_lo != nullptr;
         const int prof = prof_begin(KFAC_PROF_SYRK_TC, s);
-        if (planes && !g_syrk_narrow()) {
-            static bool pattr8 = false;
-            if (!pattr8) {
-                KFAC_CUDA_TRY(cudaFuncSetAttribute(syrk_tc_planes8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   kSmemBytes));
-                pattr8 = true;
-            }
-            syrk_tc_planes8_kernel<<<items, NT2, kSmemBytes, s>>>(b);
-        } else if (planes) {
-            static bool pattr = false;
-            if (!pattr) {
-                KFAC_CUDA_TRY(cudaFuncSetAttribute(syrk_tc_planes_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   kSmemBytes));
-                pattr = true;
-            }
-            syrk_tc_planes_kernel<<<items, NT, kSmemBytes, s>>>(b);
-        } else {
-            syrk_tc_kernel<<<items, NT, kSmemBytes, s>>>(b);
-        }
+        syrk_tc_planes8_kernel<<<items, NT2, kSmemBytes, s>>>(b);
         KFAC_LAUNCHED();
         if (prof >= 0) {
             // algorithmic work of the factors in this launch: n d (d + 1) flops (upper triangle incl.
@@ -1460,11 +861,7 @@ extern "C" int kfac_debug_gemm(int engine, const float *A, int lda, int trans_a,
     if (engine & 4) d.epi = kfac::EPI_SUB;      // C -= op(A) op(B)
     engine &= 3;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    if (engine == 1) {
-        if (!kfac::gemm_tc_supported(d)) return KFAC_ERR_UNSUPPORTED;
-        (void)debug;
-        return kfac::gemm_tc_grouped(&d, 1, 0.f, s);
-    }
+    if (engine == 1) return KFAC_ERR_UNSUPPORTED;     // the in-kernel-split engine was retired
     if (engine == 2) {
         // pre-split planes engine: A, B split into TF32 planes here; with `debug` non-null the
         // result is emitted as planes too (hi -> C, lo -> debug, same leading dimension)

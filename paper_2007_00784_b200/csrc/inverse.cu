@@ -271,12 +271,8 @@ size_t inverse_workspace_bytes(const int32_t *dims, int count) { return plan(dim
 kfac_status_t inverse_run(const float *const *F, const int32_t *dims, const int32_t *ldF, int count,
                           float damping, float *const *Finv, const int32_t *ldFinv, int32_t *info,
                           void *ws, cudaStream_t s) {
-    static bool attrs = false;
-    if (!attrs) {
-        KFAC_CUDA_TRY(cudaFuncSetAttribute(inv_potrf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPotrfSmem));
-        KFAC_CUDA_TRY(cudaFuncSetAttribute(inv_trtri, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTrtriSmem));
-        attrs = true;
-    }
+    KFAC_CUDA_TRY(set_smem_attr((const void *)inv_potrf, (int)kPotrfSmem));
+    KFAC_CUDA_TRY(set_smem_attr((const void *)inv_trtri, (int)kTrtriSmem));
     Plan p = plan(dims, count);
     char *base = reinterpret_cast<char *>(round_up(reinterpret_cast<uintptr_t>(ws), 256));
     for (int i = 0; i < count; ++i) {

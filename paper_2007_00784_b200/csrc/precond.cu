@@ -12,22 +12,19 @@
 // by the last CTA (deterministic), nu computed on the device, then P *= nu (float4).
 #include "internal.cuh"
 
+#include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 namespace kfac {
-
-static bool getenv_flag(const char *name) {
-    const char *e = getenv(name);
-    return e && e[0] == '1';
-}
 
 // Layers whose four GEMMs all run on the tensor cores (every dimension >= 64, 16-byte rows) use
 // the pre-split "planes" engine: Q_G, Q_A and the gradient are split once into TF32 hi/lo planes
 // and every intermediate (T, V2, U) leaves its GEMM's epilogue as planes, so no GEMM re-splits
 // an operand.  The others run the fp32 SIMT chain.
 static bool planes_layer(int dg, int da, int ldW, int ldQG, int ldQA) {
-    return !getenv_flag("KFAC_PRECOND_NO_PLANES") && dg >= 64 && da >= 64 && (ldW % 4) == 0 &&
+    return dg >= 64 && da >= 64 && (ldW % 4) == 0 &&
            (ldQG % 4) == 0 && (ldQA % 4) == 0;
 }
 
@@ -150,26 +147,34 @@ kfac_status_t precond_run(const int32_t *d_g, const int32_t *d_a, int nl, const 
 }
 
 // ------------------------------------------------------------------ KL-clip --
+// Eq. 18 (R12) in three passes, every one a float4 stream over the layers' rows:
+//   kl_dot   per CTA, a contiguous run of rows of one layer (about kKlUnits float4 of P and of
+//            grad, masked at the row tail: d_A is odd with the bias column), fp32 products summed
+//            in fp64; the last CTA of the launch reduces its layers' CTA partials, one warp per
+//            layer in a fixed order, into layer_dot[l];
+//   kl_nu    one warp: s = sum_l |layer_dot[l]| in layer order, nu = min(1, sqrt(kappa/(lr^2 s)));
+//   kl_scale P *= nu over the same runs of rows.
+// Layers are launched in chunks of kKlMax descriptors (kernel parameters), so any layer count
+// works; the reduction order depends only on the shapes (bitwise reproducible).
 namespace {
 
-constexpr int kKlMax = 128;
+constexpr int kKlMax = 256;
 constexpr int kKlThreads = 256;
-constexpr int kKlRowsPerCta = 8;     // rows of one layer per CTA in the dot pass
+constexpr int kKlUnits = 8192;       // float4 of P per CTA (128 KB of P + grad in flight per CTA)
 
 struct KlLayer {
     float *P;
     const float *W;
-    int rows, cols, ld, cta_begin;
+    int rows, cols, ld, nch;         // nch = ceil(cols / 4) float4 chunks per row
+    int rows_per_cta, cta_begin;
 };
 
 struct KlBatch {
-    int count, ctas_total;
-    float lr, kappa;
-    double *partial;        // [ctas_total]
-    unsigned int *counter;  // last-CTA ticket
-    float *nu_ws;           // nu for the scale pass
-    float *nu_out;
-    double *s_out;
+    int count, ctas_total, layer_base;
+    double *partial;        // [ctas_total] of this chunk
+    double *layer_dot;      // [all layers]
+    unsigned int *counter;  // last-CTA ticket of this chunk
+    const float *nu;        // scale pass
     KlLayer l[kKlMax];
 };
 
@@ -182,47 +187,55 @@ __device__ __forceinline__ int find_layer(const KlBatch &b, int cta) {
     return lo;
 }
 
-__device__ __forceinline__ double block_sum(double v) {
-    __shared__ double red[kKlThreads / 32];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
-    __syncthreads();
-    if (lane == 0) red[w] = v;
-    __syncthreads();
-    double s = 0.0;
-    if (threadIdx.x < 32) {
-        s = threadIdx.x < kKlThreads / 32 ? red[threadIdx.x] : 0.0;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+__device__ __forceinline__ float4 masked(float4 v, int c, int cols) {
+    if (c + 3 >= cols) {             // row tail: elements at or past `cols` are padding
+        if (c + 1 >= cols) v.y = 0.f;
+        if (c + 2 >= cols) v.z = 0.f;
+        if (c + 3 >= cols) v.w = 0.f;
     }
-    return s;   // valid in thread 0
+    return v;
 }
 
 __global__ void __launch_bounds__(kKlThreads) kl_dot_kernel(const __grid_constant__ KlBatch b) {
+    __shared__ double red[kKlThreads / 32];
+    __shared__ bool last;
     const int cta = blockIdx.x;
-    const int li = find_layer(b, cta);
-    const KlLayer &L = b.l[li];
-    const int r0 = (cta - L.cta_begin) * kKlRowsPerCta;
-    const int r1 = min(L.rows, r0 + kKlRowsPerCta);
+    const KlLayer &L = b.l[find_layer(b, cta)];
+    const int r0 = (cta - L.cta_begin) * L.rows_per_cta;
+    const int r1 = min(L.rows, r0 + L.rows_per_cta);
+    const int units = (r1 - r0) * L.nch;
     double acc = 0.0;
-    if ((L.cols & 3) == 0) {
-        const int c4 = L.cols / 4;
-        for (int e = threadIdx.x; e < (r1 - r0) * c4; e += kKlThreads) {
-            const int r = r0 + e / c4, c = (e % c4) * 4;
-            const float4 p = *reinterpret_cast<const float4 *>(L.P + (size_t)r * L.ld + c);
-            const float4 w = __ldg(reinterpret_cast<const float4 *>(L.W + (size_t)r * L.ld + c));
-            acc += (double)(p.x * w.x) + (double)(p.y * w.y) + (double)(p.z * w.z) + (double)(p.w * w.w);
+    for (int e0 = threadIdx.x; e0 < units; e0 += 4 * kKlThreads) {
+        float4 p[4], w[4];
+        int cc[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {           // all loads of the round before any use
+            const int e = e0 + u * kKlThreads;
+            const int r = r0 + e / L.nch, c = (e % L.nch) * 4;
+            cc[u] = c;
+            if (e < units) {
+                p[u] = __ldcs(reinterpret_cast<const float4 *>(L.P + (size_t)r * L.ld + c));
+                w[u] = __ldcs(reinterpret_cast<const float4 *>(L.W + (size_t)r * L.ld + c));
+            } else {
+                p[u] = w[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
         }
-    } else {
-        for (int e = threadIdx.x; e < (r1 - r0) * L.cols; e += kKlThreads) {
-            const int r = r0 + e / L.cols, c = e % L.cols;
-            acc += (double)(L.P[(size_t)r * L.ld + c] * __ldg(L.W + (size_t)r * L.ld + c));
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const float4 q = masked(p[u], cc[u], L.cols);
+            acc += (double)(q.x * w[u].x) + (double)(q.y * w[u].y) + (double)(q.z * w[u].z) +
+                   (double)(q.w * w[u].w);
         }
     }
-    const double s = block_sum(acc);
-    __shared__ bool last;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    if (lane == 0) red[warp] = acc;
+    __syncthreads();
     if (threadIdx.x == 0) {
+        double s = 0.0;
+#pragma unroll
+        for (int i = 0; i < kKlThreads / 32; ++i) s += red[i];
         b.partial[cta] = s;
         __threadfence();
         last = atomicAdd(b.counter, 1u) == (unsigned)(b.ctas_total - 1);
@@ -230,85 +243,128 @@ __global__ void __launch_bounds__(kKlThreads) kl_dot_kernel(const __grid_constan
     __syncthreads();
     if (!last) return;
     __threadfence();
-    // Last CTA: per-layer sums in a fixed order (strided per thread + fixed tree), then
-    // s = sum_l |dot_l| (R12) and nu (Eq. 18).
-    double total = 0.0;
-    for (int l = 0; l < b.count; ++l) {
+    // last CTA of the chunk: one warp per layer, lane-strided partial sums, fixed butterfly
+    for (int l = warp; l < b.count; l += kKlThreads / 32) {
         const int beg = b.l[l].cta_begin;
         const int end = l + 1 < b.count ? b.l[l + 1].cta_begin : b.ctas_total;
-        double part = 0.0;
-        for (int c = beg + threadIdx.x; c < end; c += kKlThreads) part += ((volatile double *)b.partial)[c];
-        const double dot = block_sum(part);
-        total += fabs(dot);                 // meaningful in thread 0 only
+        double s = 0.0;
+        for (int c = beg + lane; c < end; c += 32) s += __ldcg(b.partial + c);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) b.layer_dot[b.layer_base + l] = s;
     }
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0) *b.counter = 0u;    // re-arm for the next chunk / call / graph replay
+}
+
+__global__ void kl_nu_kernel(const double *layer_dot, int nl, float lr, float kappa, float *nu_ws,
+                             float *nu_out, double *s_out) {
+    const int lane = threadIdx.x;
+    double s = 0.0;
+    for (int l = lane; l < nl; l += 32) s += fabs(__ldcg(layer_dot + l));      // R12: |.| per layer
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) {
         double nu = 1.0;
-        if (total > 0.0) nu = fmin(1.0, sqrt((double)b.kappa / ((double)b.lr * (double)b.lr * total)));
-        *b.nu_ws = (float)nu;
-        if (b.nu_out) *b.nu_out = (float)nu;
-        if (b.s_out) *b.s_out = total;
-        *b.counter = 0u;        // re-arm for the next call / graph replay
+        if (s > 0.0) nu = fmin(1.0, sqrt((double)kappa / ((double)lr * (double)lr * s)));
+        *nu_ws = (float)nu;
+        if (nu_out) *nu_out = (float)nu;
+        if (s_out) *s_out = s;
     }
 }
 
 __global__ void __launch_bounds__(kKlThreads) kl_scale_kernel(const __grid_constant__ KlBatch b) {
     const int cta = blockIdx.x;
     const KlLayer &L = b.l[find_layer(b, cta)];
-    const float nu = *b.nu_ws;
+    const float nu = *b.nu;
     if (nu == 1.0f) return;
-    const int r0 = (cta - L.cta_begin) * kKlRowsPerCta;
-    const int r1 = min(L.rows, r0 + kKlRowsPerCta);
-    if ((L.cols & 3) == 0) {
-        const int c4 = L.cols / 4;
-        for (int e = threadIdx.x; e < (r1 - r0) * c4; e += kKlThreads) {
-            const int r = r0 + e / c4, c = (e % c4) * 4;
-            float4 *p = reinterpret_cast<float4 *>(L.P + (size_t)r * L.ld + c);
-            float4 v = *p;
-            v.x *= nu; v.y *= nu; v.z *= nu; v.w *= nu;
-            *p = v;
+    const int r0 = (cta - L.cta_begin) * L.rows_per_cta;
+    const int r1 = min(L.rows, r0 + L.rows_per_cta);
+    const int units = (r1 - r0) * L.nch;
+    for (int e0 = threadIdx.x; e0 < units; e0 += 4 * kKlThreads) {
+        float4 p[4];
+        float4 *ptr[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int e = e0 + u * kKlThreads;
+            const int r = r0 + e / L.nch, c = (e % L.nch) * 4;
+            ptr[u] = e < units ? reinterpret_cast<float4 *>(L.P + (size_t)r * L.ld + c) : nullptr;
+            if (ptr[u]) p[u] = __ldcs(ptr[u]);
         }
-    } else {
-        for (int e = threadIdx.x; e < (r1 - r0) * L.cols; e += kKlThreads) {
-            const int r = r0 + e / L.cols, c = e % L.cols;
-            L.P[(size_t)r * L.ld + c] *= nu;
-        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (ptr[u]) __stcs(ptr[u], make_float4(p[u].x * nu, p[u].y * nu, p[u].z * nu, p[u].w * nu));
     }
+}
+
+struct KlPlan {
+    std::vector<KlBatch> chunks;
+    size_t partial_off, dot_off, tail_off, bytes;
+};
+
+KlPlan kl_plan(const int32_t *rows, const int32_t *cols, int nl) {
+    KlPlan p;
+    size_t ctas_max = 0;
+    for (int base = 0; base < nl; base += kKlMax) {
+        KlBatch b;
+        memset(&b, 0, sizeof(b));
+        b.layer_base = base;
+        int ctas = 0;
+        for (int l = base; l < nl && b.count < kKlMax; ++l) {
+            KlLayer &L = b.l[b.count++];
+            L.rows = rows[l];
+            L.cols = cols[l];
+            L.nch = (cols[l] + 3) / 4;
+            L.rows_per_cta = std::max(1, kKlUnits / L.nch);
+            L.cta_begin = ctas;
+            ctas += cdiv(L.rows, L.rows_per_cta);
+        }
+        b.ctas_total = ctas;
+        ctas_max = std::max(ctas_max, (size_t)ctas);
+        p.chunks.push_back(b);
+    }
+    p.partial_off = 0;
+    p.dot_off = round_up(ctas_max * sizeof(double), 256);
+    p.tail_off = p.dot_off + round_up((size_t)nl * sizeof(double), 256);
+    p.bytes = p.tail_off + 256 * 2 + 256;
+    return p;
 }
 
 }  // namespace
 
-size_t klclip_workspace_bytes(const int32_t *rows, int nl) {
-    size_t ctas = 0;
-    for (int l = 0; l < nl; ++l) ctas += cdiv(rows[l], kKlRowsPerCta);
-    return round_up(ctas * sizeof(double), 256) + 256 * 2 + 256;
+size_t klclip_workspace_bytes(const int32_t *rows, const int32_t *cols, int nl) {
+    return kl_plan(rows, cols, nl).bytes;
 }
 
 kfac_status_t klclip_run(float *const *P, const float *const *W, const int32_t *rows,
                          const int32_t *cols, const int32_t *ld, int nl, float lr, float kappa,
                          float *nu_out, double *s_out, void *ws, cudaStream_t s) {
     char *base = reinterpret_cast<char *>(round_up(reinterpret_cast<uintptr_t>(ws), 256));
-    KFAC_CHECK_ARG(nl <= kKlMax, KFAC_ERR_SHAPE, "kfac_kl_clip: at most %d layers per call", kKlMax);
-    KlBatch b;
-    b.count = nl;
-    b.lr = lr;
-    b.kappa = kappa;
-    int ctas = 0;
-    for (int l = 0; l < nl; ++l) {
-        b.l[l] = KlLayer{P[l], W[l], rows[l], cols[l], ld[l], ctas};
-        ctas += cdiv(rows[l], kKlRowsPerCta);
+    KlPlan plan = kl_plan(rows, cols, nl);
+    double *partial = reinterpret_cast<double *>(base + plan.partial_off);
+    double *layer_dot = reinterpret_cast<double *>(base + plan.dot_off);
+    unsigned int *counter = reinterpret_cast<unsigned int *>(base + plan.tail_off);
+    float *nu_ws = reinterpret_cast<float *>(base + plan.tail_off + 256);
+    KFAC_CUDA_TRY(cudaMemsetAsync(counter, 0, sizeof(unsigned int), s));
+    for (auto &b : plan.chunks) {
+        for (int q = 0; q < b.count; ++q) {
+            const int l = b.layer_base + q;
+            b.l[q].P = P[l];
+            b.l[q].W = W[l];
+            b.l[q].ld = ld[l];
+        }
+        b.partial = partial;
+        b.layer_dot = layer_dot;
+        b.counter = counter;
+        b.nu = nu_ws;
+        kl_dot_kernel<<<b.ctas_total, kKlThreads, 0, s>>>(b);
+        KFAC_LAUNCHED();
     }
-    b.ctas_total = ctas;
-    b.partial = reinterpret_cast<double *>(base);
-    char *tail = base + round_up(ctas * sizeof(double), 256);
-    b.counter = reinterpret_cast<unsigned int *>(tail);
-    b.nu_ws = reinterpret_cast<float *>(tail + 256);
-    b.nu_out = nu_out;
-    b.s_out = s_out;
-    KFAC_CUDA_TRY(cudaMemsetAsync(b.counter, 0, sizeof(unsigned int), s));
-    kl_dot_kernel<<<ctas, kKlThreads, 0, s>>>(b);
+    kl_nu_kernel<<<1, 32, 0, s>>>(layer_dot, nl, lr, kappa, nu_ws, nu_out, s_out);
     KFAC_LAUNCHED();
-    kl_scale_kernel<<<ctas, kKlThreads, 0, s>>>(b);
-    KFAC_LAUNCHED();
+    for (auto &b : plan.chunks) {
+        kl_scale_kernel<<<b.ctas_total, kKlThreads, 0, s>>>(b);
+        KFAC_LAUNCHED();
+    }
     return KFAC_OK;
 }
 

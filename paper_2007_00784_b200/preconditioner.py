@@ -147,8 +147,14 @@ class KFACPreconditioner:
         if self.world > 1:
             dist.all_reduce(self.factor_flat, op=dist.ReduceOp.SUM, group=self.pg)
 
-    def compute_eigen(self, warm: bool = False):
-        """Alg. 1 step 2 on the owned factors, then the exchange of the results."""
+    def compute_eigen(self, warm: bool = False, check: Optional[bool] = None):
+        """Alg. 1 step 2 on the owned factors, then the exchange of the results.
+
+        check: read back the device `info` codes and raise if a decomposition failed (an
+        unconverged eigensolver or a non-SPD damped factor would otherwise reach P and the
+        KL-clip silently).  Default: on the first decomposition only (one host sync)."""
+        if check is None:
+            check = not self.have_eigen
         if self.owned:
             F = [self.F[f] for f in self.owned]
             Q = [self.Q[f] for f in self.owned]
@@ -158,6 +164,12 @@ class KFACPreconditioner:
                 flags = _lib.EIG_WARM_START if (warm and self.have_eigen) else 0
                 _lib.kfac_compute_eigen(F, Q, [self.v[f] for f in self.owned], self.info, flags,
                                         ws=self.ws["eigen"])
+        if check and self.owned:
+            bad = [(self.owned[i], int(c)) for i, c in enumerate(self.info[:len(self.owned)].tolist()) if c != 0]
+            if bad:
+                what = "not SPD at leading minor" if self.variant == "inverse" else "not converged after sweeps"
+                raise FloatingPointError(f"kfac_compute_{'inverse' if self.variant == 'inverse' else 'eigen'}: "
+                                         f"factor(s) {what}: {bad[:8]}")
         self.have_eigen = True
         if self.world > 1 and self.exchange == "bcast-eig":
             all_gather_inplace(self.q_flat, self.q_slice, self.pg)

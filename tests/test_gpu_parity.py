@@ -80,6 +80,34 @@ def test_kl_clip_deterministic_and_repeatable(L):
         assert all(np.array_equal(a, b) for a, b in zip(o[1], outs[0][1]))
 
 
+def test_kl_clip_many_layers_r152(L, orc):
+    """ResNet-152's 156 layers in one call (more than one kernel-parameter chunk of layers),
+    odd d_A (bias column) so every row ends in a masked float4 tail, padded ld with NaN pads."""
+    layers = shapes.resnet152()
+    assert len(layers) > 128
+    g = np.random.Generator(np.random.Philox(key=[152, 7]))
+    Ps, Ws, P, W = [], [], [], []
+    for i, l in enumerate(layers):
+        r, c = min(l.d_g, 96), min(l.d_a, 301)        # shapes of the real layers, trimmed for the oracle
+        Ps.append(g.standard_normal((r, c)).astype(np.float32))
+        Ws.append(g.standard_normal((r, c)).astype(np.float32))
+        ld = (c + 3) // 4 * 4 + 4
+        for src, dst in ((Ps[-1], P), (Ws[-1], W)):
+            t = torch.full((r, ld), float("nan"), dtype=torch.float32, device="cuda")
+            t[:, :c] = torch.from_numpy(src)
+            dst.append(t[:, :c])
+    ref, nu_ref, s_ref = orc.kl_clip(Ps, Ws, 0.0125, 1e-3)
+    nu = torch.zeros(1, device="cuda")
+    s = torch.zeros(1, dtype=torch.float64, device="cuda")
+    L.kfac_kl_clip(P, W, 0.0125, 1e-3, nu, s)
+    torch.cuda.synchronize()
+    assert nu_ref < 1.0
+    assert abs(s.item() - s_ref) <= 1e-6 * s_ref
+    assert abs(nu.item() - nu_ref) <= 1e-6 * nu_ref
+    for p, r in zip(P, ref):
+        assert relF(host(p), r) <= 2e-6
+
+
 # ---------------------------------------------------------- preconditioning --
 def _eig_inputs(orc, dg, da, seed, deficit=0):
     G = random_spd(dg, seed, rank_deficit=min(deficit, dg - 1))
