@@ -61,16 +61,19 @@ int num_sms() {
 }
 
 cudaError_t set_smem_attr(const void *kernel, int bytes) {
+    // the attribute is an upper bound: keep the largest value requested per (kernel, device), so
+    // a launch with less dynamic shared memory never lowers it under a later, larger one
     static std::mutex mu;
-    static std::set<std::tuple<const void *, int, int>> done;
+    static std::map<std::pair<const void *, int>, int> done;
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
     std::lock_guard<std::mutex> lk(mu);
-    const auto key = std::make_tuple(kernel, dev, bytes);
-    if (done.count(key)) return cudaSuccess;
+    const auto key = std::make_pair(kernel, dev);
+    auto it = done.find(key);
+    if (it != done.end() && it->second >= bytes) return cudaSuccess;
     e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    if (e == cudaSuccess) done.insert(key);
+    if (e == cudaSuccess) done[key] = bytes;
     return e;
 }
 

@@ -1435,6 +1435,7 @@ int ldw_for(int n) { return (int)round_up((size_t)n, 32); }
 struct Plan {
     std::vector<TrdJob> jobs;
     size_t bytes = 0, table_off = 0, leaf_off = 0, merge_off = 0, bt_off = 0;
+    size_t oz_off = 0, oz_bytes = 0;                  // Ozaki GEMM scratch (digit planes)
     size_t bar_off = 0;                               // all factors' group-barrier counters (64 B apart)
     std::vector<LeafDesc> leaves;
     std::vector<std::vector<MergeDesc>> merges;       // per level (1..maxL)
@@ -1542,6 +1543,14 @@ Plan plan(const int32_t *dims, int count) {
     size_t nbt = 0;
     for (auto &v : P.bt) nbt += v.size();
     P.bt_off = take(nbt * sizeof(BtStep));
+    // Ozaki scratch: the largest grouped GEMM of one step slices at most ~18 n^2 int8 digits per
+    // factor (a merge level: both halves' Q rows plus S twice) or 6 n (n + 1536) (a back-transform
+    // block: V^T, X, T), plus per-row exponents and maxima
+    for (int i = 0; i < count; ++i) {
+        const size_t n = (size_t)dims[i];
+        P.oz_bytes += std::max(18 * n * (n + 64), 6 * (n + 64) * (n + 1600)) + (1 << 20);
+    }
+    P.oz_off = take(P.oz_bytes);
     P.bytes = cur + 256;
     return P;
 }
@@ -1621,6 +1630,11 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
         for (auto &v : P.bt) flat.insert(flat.end(), v.begin(), v.end());
         if (!flat.empty()) RET_OK(upload(dbt, flat.data(), sizeof(BtStep) * flat.size(), s));
     }
+    // the eigensolver's large fp64 GEMMs go to the int8 tensor cores (Ozaki) while this arena is set
+    struct ArenaGuard {
+        ArenaGuard(void *p, size_t b) { oz_set_arena(p, b); }
+        ~ArenaGuard() { oz_set_arena(nullptr, 0); }
+    } arena_guard(base + P.oz_off, P.oz_bytes);
     trd_zero_info<<<count, 32, 0, s>>>(djobs);
     KFAC_LAUNCHED();
     std::vector<Gemm64Desc> gd;
@@ -1825,23 +1839,55 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
             g.C = J.Gb; g.tc = DT_F64; g.ldc = kBt;
             g.lower = 1;                                         // (G is symmetric)
             g1.push_back(g);
-            for (int i0 = 0; i0 < b.nr; i0 += 64) {              // Y = V^T X; V[r][i] = 0 for r < i,
-                Gemm64Desc h{};                                  // so row slab i0 only meets r >= i0
-                h.M = std::min(64, b.nr - i0); h.N = J.n; h.K = m - i0;
-                h.A = V + (size_t)i0 * J.ldw + i0; h.ta = DT_F64; h.lda = J.ldw; h.trans_a = 1;
-                h.B = X + (size_t)i0 * J.ldw; h.tb = DT_F64; h.ldb = J.ldw;
-                h.C = J.Yb + (size_t)i0 * J.ldw; h.tc = DT_F64; h.ldc = J.ldw;
-                g1.push_back(h);
+            // Each product runs either whole on the int8 tensor cores (Ozaki, when gemm64_grouped
+            // routes it there; the zero triangles of V and T are then multiplied, ~6% of the block)
+            // or on DMMA as 64-row slabs that skip those triangles.
+            const bool oz = oz_arena_active();
+            Gemm64Desc yw{};                                     // Y = V^T X
+            yw.M = b.nr; yw.N = J.n; yw.K = m;
+            yw.A = V; yw.ta = DT_F64; yw.lda = J.ldw; yw.trans_a = 1;
+            yw.B = X; yw.tb = DT_F64; yw.ldb = J.ldw;
+            yw.C = J.Yb; yw.tc = DT_F64; yw.ldc = J.ldw;
+            if (oz && oz_eligible(yw)) {
+                g1.push_back(yw);
+            } else {
+                for (int i0 = 0; i0 < b.nr; i0 += 64) {          // V[r][i] = 0 for r < i, so row
+                    Gemm64Desc h{};                              // slab i0 only meets r >= i0
+                    h.M = std::min(64, b.nr - i0); h.N = J.n; h.K = m - i0;
+                    h.A = V + (size_t)i0 * J.ldw + i0; h.ta = DT_F64; h.lda = J.ldw; h.trans_a = 1;
+                    h.B = X + (size_t)i0 * J.ldw; h.tb = DT_F64; h.ldb = J.ldw;
+                    h.C = J.Yb + (size_t)i0 * J.ldw; h.tc = DT_F64; h.ldc = J.ldw;
+                    g1.push_back(h);
+                }
             }
-            for (int m0 = 0; m0 < b.nr; m0 += 64) {              // Y2 = T Y, T upper triangular:
-                Gemm64Desc u{};                                  // row slab m0 only meets K >= m0
-                u.M = std::min(64, b.nr - m0); u.N = J.n; u.K = b.nr - m0;
-                u.A = J.Tb + (size_t)m0 * kBt + m0; u.ta = DT_F64; u.lda = kBt;
-                u.B = J.Yb + (size_t)m0 * J.ldw; u.tb = DT_F64; u.ldb = J.ldw;
-                u.C = J.Y2b + (size_t)m0 * J.ldw; u.tc = DT_F64; u.ldc = J.ldw;
-                g2.push_back(u);
+            Gemm64Desc uw{};                                     // Y2 = T Y
+            uw.M = b.nr; uw.N = J.n; uw.K = b.nr;
+            uw.A = J.Tb; uw.ta = DT_F64; uw.lda = kBt;
+            uw.B = J.Yb; uw.tb = DT_F64; uw.ldb = J.ldw;
+            uw.C = J.Y2b; uw.tc = DT_F64; uw.ldc = J.ldw;
+            if (oz && oz_eligible(uw)) {
+                g2.push_back(uw);
+            } else {
+                for (int m0 = 0; m0 < b.nr; m0 += 64) {          // T upper triangular: row slab
+                    Gemm64Desc u{};                              // m0 only meets K >= m0
+                    u.M = std::min(64, b.nr - m0); u.N = J.n; u.K = b.nr - m0;
+                    u.A = J.Tb + (size_t)m0 * kBt + m0; u.ta = DT_F64; u.lda = kBt;
+                    u.B = J.Yb + (size_t)m0 * J.ldw; u.tb = DT_F64; u.ldb = J.ldw;
+                    u.C = J.Y2b + (size_t)m0 * J.ldw; u.tc = DT_F64; u.ldc = J.ldw;
+                    g2.push_back(u);
+                }
             }
-            // X -= V Y2: rows r < nr of V are zero beyond column r (unit lower triangle on top)
+            Gemm64Desc vw{};                                     // X -= V Y2
+            vw.M = m; vw.N = J.n; vw.K = b.nr;
+            vw.A = V; vw.ta = DT_F64; vw.lda = J.ldw;
+            vw.B = J.Y2b; vw.tb = DT_F64; vw.ldb = J.ldw;
+            vw.C = X; vw.tc = DT_F64; vw.ldc = J.ldw;
+            vw.epi = EPI_SUB;
+            if (oz && oz_eligible(vw)) {
+                g3.push_back(vw);
+                continue;
+            }
+            // rows r < nr of V are zero beyond column r (unit lower triangle on top)
             for (int r0 = 0; r0 < m; r0 += 64) {
                 if (r0 >= b.nr) {                                // the rectangular rest in one desc
                     Gemm64Desc v{};

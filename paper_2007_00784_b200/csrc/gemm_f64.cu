@@ -498,7 +498,8 @@ bool pipe_ok(const Gemm64Desc &g) {
 
 }  // namespace
 
-kfac_status_t gemm64_grouped(const Gemm64Desc *descs, int count, cudaStream_t s) {
+namespace {
+kfac_status_t gemm64_dmma_grouped(const Gemm64Desc *descs, int count, cudaStream_t s) {
     for (int base = 0, end = 0; base < count; base = end) {
         thread_local Batch64 b;   // host staging; parameters are copied at launch
         b.count = 0;
@@ -542,6 +543,20 @@ kfac_status_t gemm64_grouped(const Gemm64Desc *descs, int count, cudaStream_t s)
         }
     }
     return KFAC_OK;
+}
+}  // namespace
+
+kfac_status_t gemm64_grouped(const Gemm64Desc *descs, int count, cudaStream_t s) {
+    if (!oz_arena_active()) return gemm64_dmma_grouped(descs, count, s);
+    // Ozaki (int8 tensor cores) for the large fp64 products, DMMA for the rest
+    std::vector<Gemm64Desc> oz, dm;
+    for (int i = 0; i < count; ++i)
+        if (descs[i].M > 0 && descs[i].N > 0) (oz_eligible(descs[i]) ? oz : dm).push_back(descs[i]);
+    if (!oz.empty()) {
+        kfac_status_t st = oz_gemm_grouped(oz.data(), (int)oz.size(), s);
+        if (st != KFAC_OK) return st;
+    }
+    return dm.empty() ? KFAC_OK : gemm64_dmma_grouped(dm.data(), (int)dm.size(), s);
 }
 
 }  // namespace kfac

@@ -87,6 +87,15 @@ struct Gemm64Desc {
 constexpr int kGemm64MaxDescs = 256;
 kfac_status_t gemm64_grouped(const Gemm64Desc *descs, int count, cudaStream_t s);
 
+// fp64-accurate GEMM on the int8 tensor cores (Ozaki scheme, gemm_ozaki.cu).  gemm64_grouped routes
+// the eligible descriptors (fp64 operands, M >= 128, N >= 64, K >= 256) there while a scratch arena
+// is set on the calling thread (oz_set_arena; the eigensolver carves it from its workspace).
+bool oz_eligible(const Gemm64Desc &g);
+size_t oz_scratch_bytes(const Gemm64Desc &g);
+void oz_set_arena(void *base, size_t bytes);
+bool oz_arena_active();
+kfac_status_t oz_gemm_grouped(const Gemm64Desc *descs, int count, cudaStream_t s);
+
 // ------------------------------------------------------------ factor SYRK --
 // One Kronecker factor of one layer: F_batch = X^T X / n over the n rows of X, where X is
 // [im2col(act) | 1] (A factor, Eq. 5) or the output gradients (G factor).  The upper 128x128

@@ -222,9 +222,9 @@ __global__ void __launch_bounds__(kKlThreads) kl_dot_kernel(const __grid_constan
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-            const float4 q = masked(p[u], cc[u], L.cols);
-            acc += (double)(q.x * w[u].x) + (double)(q.y * w[u].y) + (double)(q.z * w[u].z) +
-                   (double)(q.w * w[u].w);
+            // padding columns of either operand may hold anything (NaN included): mask both
+            const float4 q = masked(p[u], cc[u], L.cols), v = masked(w[u], cc[u], L.cols);
+            acc += (double)(q.x * v.x) + (double)(q.y * v.y) + (double)(q.z * v.z) + (double)(q.w * v.w);
         }
     }
 #pragma unroll
