@@ -104,6 +104,10 @@ kfac_status_t kfac_layer_dims(const kfac_layer_t *layer, int32_t *d_a, int32_t *
  * act[l]: device, NHWC (conv) or (n, c_in) (linear) fp32, contiguous.
  * A[l]: device d_A x ld_A[l]; G[l]: device d_G x ld_G[l]; both triangles are written
  * (symmetric).  When first == 0 the previous A/G are read (must be symmetric).
+ * packed_A / packed_G (nullable host arrays of device pointers): also write each factor's upper
+ * triangle row-major, d(d+1)/2 floats (row i starts at i d - i (i-1)/2), the same values as F --
+ * the factor allreduce buffer at half the full-matrix bytes (kfac_unpack_factors restores
+ * both triangles after the collective).
  * out_scale = 1/W before an allreduce-SUM averages the factors.
  * Rows per layer must be < 2^31; decay in [0, 1].
  * Workspace: the per-(tile, row chunk) partial sums and, for the tensor-core factors, the TF32
@@ -113,8 +117,14 @@ kfac_status_t kfac_update_factors(const kfac_layer_t *layers, int32_t num_layers
                                   const float *const *act, const float *const *gout,
                                   float *const *A, const int32_t *ld_A,
                                   float *const *G, const int32_t *ld_G,
+                                  float *const *packed_A, float *const *packed_G,
                                   float decay, int32_t first, float out_scale,
                                   void *ws, size_t ws_bytes, kfac_stream_t stream);
+
+/* Packed upper triangles (layout of kfac_update_factors' packed outputs) -> both triangles of F[i]
+ * (device dims[i] x ld_F[i]).  No workspace. */
+kfac_status_t kfac_unpack_factors(const float *const *packed, const int32_t *dims, float *const *F,
+                                  const int32_t *ld_F, int32_t count, kfac_stream_t stream);
 
 /* ---- Stage 2: symmetric eigendecomposition of each factor (Alg. 1).
  * F[i]: device dims[i] x ld_F[i] (read only; (F + F^T)/2 is decomposed).

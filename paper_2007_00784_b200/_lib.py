@@ -43,8 +43,9 @@ def _load():
     L.kfac_layer_dims.argtypes = [C.POINTER(kfac_layer_t), I32P, I32P, C.POINTER(C.c_int64)]
     L.kfac_update_factors_workspace_size.argtypes = [C.POINTER(kfac_layer_t), C.c_int32]
     L.kfac_update_factors_workspace_size.restype = SZ
-    L.kfac_update_factors.argtypes = [C.POINTER(kfac_layer_t), C.c_int32, PP, PP, PP, I32P, PP, I32P,
+    L.kfac_update_factors.argtypes = [C.POINTER(kfac_layer_t), C.c_int32, PP, PP, PP, I32P, PP, I32P, PP, PP,
                                       C.c_float, C.c_int32, C.c_float, P, SZ, P]
+    L.kfac_unpack_factors.argtypes = [PP, I32P, PP, I32P, C.c_int32, P]
     L.kfac_compute_eigen_workspace_size.argtypes = [I32P, C.c_int32]
     L.kfac_compute_eigen_workspace_size.restype = SZ
     L.kfac_compute_eigen.argtypes = [PP, I32P, I32P, C.c_int32, PP, I32P, PP, P, C.c_uint32, P, SZ, P]
@@ -67,7 +68,7 @@ def _load():
     L.kfac_profile_start.argtypes = [C.c_int32]
     L.kfac_profile_stop.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_int64), C.POINTER(C.c_double),
                                     C.POINTER(C.c_double)]
-    for f in ("kfac_layer_dims", "kfac_update_factors", "kfac_compute_eigen", "kfac_compute_inverse",
+    for f in ("kfac_layer_dims", "kfac_update_factors", "kfac_unpack_factors", "kfac_compute_eigen", "kfac_compute_inverse",
               "kfac_precondition", "kfac_kl_clip", "kfac_assign", "kfac_profile_start", "kfac_profile_stop"):
         getattr(L, f).restype = C.c_int
     return L
@@ -75,7 +76,7 @@ def _load():
 
 lib = _load()
 
-EXPORTED = ("kfac_layer_dims", "kfac_update_factors_workspace_size", "kfac_update_factors",
+EXPORTED = ("kfac_layer_dims", "kfac_update_factors_workspace_size", "kfac_update_factors", "kfac_unpack_factors",
             "kfac_compute_eigen_workspace_size", "kfac_compute_eigen",
             "kfac_compute_inverse_workspace_size", "kfac_compute_inverse",
             "kfac_precondition_workspace_size", "kfac_precondition",
@@ -146,15 +147,25 @@ def kfac_layer_dims(layer):
 
 def kfac_update_factors(layers, acts: List[torch.Tensor], gouts: List[torch.Tensor],
                         A: List[torch.Tensor], G: List[torch.Tensor], decay: float, first: bool,
-                        out_scale: float = 1.0, ws: Optional[Workspace] = None, stream=None):
+                        out_scale: float = 1.0, ws: Optional[Workspace] = None, stream=None,
+                        packed_A: Optional[List[torch.Tensor]] = None, packed_G: Optional[List[torch.Tensor]] = None):
     n = len(layers)
     arr = (kfac_layer_t * n)(*[layer_struct(l) for l in layers])
     need = lib.kfac_update_factors_workspace_size(arr, n)
     buf = _ws(ws, "factors").get(need)
     _check(lib.kfac_update_factors(arr, n, _ptrs(acts), _ptrs(gouts), _ptrs(A), _i32([_ld(a) for a in A]),
-                                   _ptrs(G), _i32([_ld(g) for g in G]), float(decay), int(bool(first)),
+                                   _ptrs(G), _i32([_ld(g) for g in G]),
+                                   _ptrs(packed_A) if packed_A is not None else None,
+                                   _ptrs(packed_G) if packed_G is not None else None,
+                                   float(decay), int(bool(first)),
                                    float(out_scale), C.c_void_p(buf.data_ptr()), buf.numel(),
                                    _stream(stream)), "kfac_update_factors")
+
+
+def kfac_unpack_factors(packed: List[torch.Tensor], F: List[torch.Tensor], stream=None):
+    n = len(F)
+    _check(lib.kfac_unpack_factors(_ptrs(packed), _i32([f.shape[0] for f in F]), _ptrs(F),
+                                   _i32([_ld(f) for f in F]), n, _stream(stream)), "kfac_unpack_factors")
 
 
 def kfac_compute_eigen(F: List[torch.Tensor], Q: List[torch.Tensor], evals: List[torch.Tensor],

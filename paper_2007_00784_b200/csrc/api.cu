@@ -15,8 +15,10 @@ namespace kfac {
 size_t factors_workspace_bytes(const kfac_layer_t *layers, int nl);
 kfac_status_t factors_run(const kfac_layer_t *layers, int nl, const float *const *act,
                           const float *const *gout, float *const *A, const int32_t *ldA,
-                          float *const *G, const int32_t *ldG, float decay, int first,
-                          float out_scale, void *ws, cudaStream_t s);
+                          float *const *G, const int32_t *ldG, float *const *pA, float *const *pG,
+                          float decay, int first, float out_scale, void *ws, cudaStream_t s);
+kfac_status_t unpack_run(const float *const *packed, const int32_t *dims, float *const *F, const int32_t *ldF,
+                         int count, cudaStream_t s);
 size_t eigen_workspace_bytes(const int32_t *dims, int count);
 kfac_status_t eigen_run(const float *const *F, const int32_t *dims, const int32_t *ldF, int count,
                         float *const *Q, const int32_t *ldQ, float *const *evals, int32_t *info,
@@ -189,7 +191,8 @@ size_t kfac_update_factors_workspace_size(const kfac_layer_t *layers, int32_t nu
 kfac_status_t kfac_update_factors(const kfac_layer_t *layers, int32_t num_layers,
                                   const float *const *act, const float *const *gout,
                                   float *const *A, const int32_t *ld_A, float *const *G,
-                                  const int32_t *ld_G, float decay, int32_t first, float out_scale,
+                                  const int32_t *ld_G, float *const *packed_A, float *const *packed_G,
+                                  float decay, int32_t first, float out_scale,
                                   void *ws, size_t ws_bytes, kfac_stream_t stream) {
     KFAC_CHECK_ARG(layers && act && gout && A && ld_A && G && ld_G, KFAC_ERR_INVALID_VALUE,
                    "kfac_update_factors: NULL argument");
@@ -205,11 +208,26 @@ kfac_status_t kfac_update_factors(const kfac_layer_t *layers, int32_t num_layers
         const int da = L.c_in * L.k_h * L.k_w + L.bias_col;
         RET_IF(check_matrix(A[l], da, da, ld_A[l], "A", l));
         RET_IF(check_matrix(G[l], L.c_out, L.c_out, ld_G[l], "G", l));
+        if (packed_A) KFAC_CHECK_ARG(packed_A[l] != nullptr, KFAC_ERR_INVALID_VALUE, "packed_A[%d] is NULL", l);
+        if (packed_G) KFAC_CHECK_ARG(packed_G[l] != nullptr, KFAC_ERR_INVALID_VALUE, "packed_G[%d] is NULL", l);
     }
     RET_IF(check_ws(ws, ws_bytes, factors_workspace_bytes(layers, num_layers), "kfac_update_factors"));
     RET_IF(check_device());
-    return factors_run(layers, num_layers, act, gout, A, ld_A, G, ld_G, decay, first ? 1 : 0, out_scale,
-                       ws, reinterpret_cast<cudaStream_t>(stream));
+    return factors_run(layers, num_layers, act, gout, A, ld_A, G, ld_G, packed_A, packed_G, decay,
+                       first ? 1 : 0, out_scale, ws, reinterpret_cast<cudaStream_t>(stream));
+}
+
+kfac_status_t kfac_unpack_factors(const float *const *packed, const int32_t *dims, float *const *F,
+                                  const int32_t *ld_F, int32_t count, kfac_stream_t stream) {
+    KFAC_CHECK_ARG(packed && dims && F && ld_F, KFAC_ERR_INVALID_VALUE, "kfac_unpack_factors: NULL argument");
+    KFAC_CHECK_ARG(count > 0, KFAC_ERR_INVALID_VALUE, "kfac_unpack_factors: count <= 0");
+    for (int i = 0; i < count; ++i) {
+        KFAC_CHECK_ARG(dims[i] > 0 && dims[i] <= 16384, KFAC_ERR_SHAPE, "dims[%d] = %d out of range", i, dims[i]);
+        KFAC_CHECK_ARG(packed[i] != nullptr, KFAC_ERR_INVALID_VALUE, "packed[%d] is NULL", i);
+        RET_IF(check_matrix(F[i], dims[i], dims[i], ld_F[i], "F", i));
+    }
+    RET_IF(check_device());
+    return unpack_run(packed, dims, F, ld_F, count, reinterpret_cast<cudaStream_t>(stream));
 }
 
 size_t kfac_compute_eigen_workspace_size(const int32_t *dims, int32_t count) {

@@ -209,6 +209,8 @@ __global__ void __launch_bounds__(256) syrk_reduce_kernel(const __grid_constant_
             if (!batch.first) v = batch.decay * (*dst) + (1.f - batch.decay) * v;
             v *= batch.out_scale;
             *dst = v;
+            if (J.packed && gi <= gj)            // each upper entry once: row gi starts at gi d - gi (gi - 1) / 2
+                J.packed[(long long)gi * J.d - (long long)gi * (gi - 1) / 2 + (gj - gi)] = v;
         }
         tr[rr][tx] = v;
     }
@@ -234,7 +236,7 @@ inline long long input_elems(const FactorJob &j) {
 
 Plan make_plan(const kfac_layer_t *layers, int nl, float *const *A, const int32_t *ldA,
                float *const *G, const int32_t *ldG, const float *const *act,
-               const float *const *gout) {
+               const float *const *gout, float *const *pA = nullptr, float *const *pG = nullptr) {
     Plan p;
     for (int l = 0; l < nl; ++l) {
         const kfac_layer_t &L = layers[l];
@@ -245,6 +247,7 @@ Plan make_plan(const kfac_layer_t *layers, int nl, float *const *A, const int32_
             j.d = j.is_a ? L.c_in * L.k_h * L.k_w + L.bias_col : L.c_out;
             j.src = act ? (j.is_a ? act[l] : gout[l]) : nullptr;
             j.F = A ? (j.is_a ? A[l] : G[l]) : nullptr;
+            j.packed = j.is_a ? (pA ? pA[l] : nullptr) : (pG ? pG[l] : nullptr);
             j.ldF = ldA ? (j.is_a ? ldA[l] : ldG[l]) : 0;
             j.c_in = j.is_a ? L.c_in : L.c_out;
             j.h_in = L.h_in; j.w_in = L.w_in; j.h_out = L.h_out; j.w_out = L.w_out;
@@ -274,9 +277,9 @@ size_t factors_workspace_bytes(const kfac_layer_t *layers, int nl) {
 
 kfac_status_t factors_run(const kfac_layer_t *layers, int nl, const float *const *act,
                           const float *const *gout, float *const *A, const int32_t *ldA,
-                          float *const *G, const int32_t *ldG, float decay, int first,
-                          float out_scale, void *ws, cudaStream_t s) {
-    Plan p = make_plan(layers, nl, A, ldA, G, ldG, act, gout);
+                          float *const *G, const int32_t *ldG, float *const *pA, float *const *pG,
+                          float decay, int first, float out_scale, void *ws, cudaStream_t s) {
+    Plan p = make_plan(layers, nl, A, ldA, G, ldG, act, gout, pA, pG);
     float *base = reinterpret_cast<float *>(round_up(reinterpret_cast<uintptr_t>(ws), 256));
     for (auto &j : p.jobs) j.partial = base + reinterpret_cast<uintptr_t>(j.partial);
     // Partial SYRKs: tcgen05 3xTF32 for the factors it supports, the SIMT tile for the rest.  The
@@ -331,6 +334,71 @@ kfac_status_t factors_run(const kfac_layer_t *layers, int nl, const float *const
             fb.j[fb.count++] = j;
         }
         syrk_reduce_kernel<<<subtiles, 256, 0, s>>>(fb);
+        KFAC_LAUNCHED();
+    }
+    return KFAC_OK;
+}
+
+// Packed upper triangles (row-major, d(d+1)/2 floats) -> full symmetric factors (both triangles):
+// the receive side of the halved factor allreduce.  One 32 x 32 tile per CTA (lower tiles are the
+// mirrored writes of the upper ones).
+struct UnpackJob {
+    const float *packed;
+    float *F;
+    int d, ldF, t1d, tile_begin;
+};
+struct UnpackBatch {
+    int count;
+    UnpackJob j[64];
+};
+
+__global__ void __launch_bounds__(256) unpack_kernel(const __grid_constant__ UnpackBatch b) {
+    __shared__ float tr[32][33];
+    int lo = 0, hi = b.count - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (b.j[mid].tile_begin <= (int)blockIdx.x) lo = mid; else hi = mid - 1;
+    }
+    const UnpackJob &J = b.j[lo];
+    int t = blockIdx.x - J.tile_begin, ti = 0;
+    while (t >= J.t1d - ti) { t -= J.t1d - ti; ++ti; }         // upper tiles, row-major
+    const int tj = ti + t;
+    const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;
+    for (int rr = ty; rr < 32; rr += 8) {
+        const int gi = ti * 32 + rr, gj = tj * 32 + tx;
+        float v = 0.f;
+        if (gi < J.d && gj < J.d) {
+            const int a = min(gi, gj), c = max(gi, gj);
+            v = J.packed[(long long)a * J.d - (long long)a * (a - 1) / 2 + (c - a)];
+            J.F[(size_t)gi * J.ldF + gj] = v;
+        }
+        tr[rr][tx] = v;
+    }
+    if (ti == tj) return;
+    __syncthreads();
+    for (int rr = ty; rr < 32; rr += 8) {
+        const int gi = tj * 32 + rr, gj = ti * 32 + tx;
+        if (gi < J.d && gj < J.d) J.F[(size_t)gi * J.ldF + gj] = tr[tx][rr];
+    }
+}
+
+kfac_status_t unpack_run(const float *const *packed, const int32_t *dims, float *const *F, const int32_t *ldF,
+                         int count, cudaStream_t s) {
+    for (int b0 = 0; b0 < count; b0 += 64) {
+        UnpackBatch b;
+        b.count = 0;
+        int tiles = 0;
+        for (int i = b0; i < count && b.count < 64; ++i) {
+            UnpackJob &j = b.j[b.count++];
+            j.packed = packed[i];
+            j.F = F[i];
+            j.d = dims[i];
+            j.ldF = ldF[i];
+            j.t1d = cdiv(dims[i], 32);
+            j.tile_begin = tiles;
+            tiles += j.t1d * (j.t1d + 1) / 2;
+        }
+        unpack_kernel<<<tiles, 256, 0, s>>>(b);
         KFAC_LAUNCHED();
     }
     return KFAC_OK;

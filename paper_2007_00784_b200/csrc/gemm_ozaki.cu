@@ -21,8 +21,9 @@
 // pattern), ozk_slice (exponent + digits, int8 planes [s][R][Kp], K-major), ozk_gemm:
 //   128 x 64 output tile per CTA, K staged 64 bytes at a time (SWIZZLE_64B, 3 stages of 72 KB:
 //   all six A digit planes and six B digit planes of the k-block, one 3-D TMA box each);
-//   warp 0 TMA producer, warp 1 MMA issuer (21 pairs x 2 k-steps per stage into six int32 TMEM
-//   accumulators of 64 columns, one per level L), warps 4-7 the epilogue (TMEM -> fp64 sum of the
+//   warp 0 TMA producer, warp 1 MMA issuer (per k-step, digit plane i of A times the stacked B
+//   planes 0..s-1-i in one MMA that starts at TMEM column 64 i, so product (i, j) accumulates into
+//   level i + j's 64 columns; 8 MMAs of N <= 256), warps 4-7 the epilogue (TMEM -> fp64 sum of the
 //   levels -> 2^(e_r + f_c) -> store / C -= through shared memory in coalesced rows).
 #include "internal.cuh"
 #include "tc_ptx.cuh"
@@ -292,8 +293,12 @@ __global__ void __launch_bounds__(kOzThreads, 1) ozk_gemm(const __grid_constant_
         }
     } else if (warp == 1) {
         if (lane == 0) {
-            const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(OBN >> 3) << 17) |
-                                   ((uint32_t)(OBM >> 4) << 24);
+            // A digit plane i times the stacked B planes 0 .. s-1-i in ONE instruction: product
+            // (i, j) lands in TMEM columns 64 (i + j) -- level i + j -- because the MMA starts at
+            // column 64 i and the B planes are consecutive 64-row blocks in shared memory; N is split
+            // at 256 (the instruction's maximum).  8 MMAs per k-step instead of 21, so each reads
+            // the A tile once per plane and B in up to 256-row blocks (half the smem operand traffic).
+            const uint32_t idesc0 = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(OBM >> 4) << 24);
             for (int q = 0; q < nk; ++q) {
                 const int s = q % kOzStages;
                 mbar_wait(full + 8 * s, (q / kOzStages) & 1);
@@ -302,11 +307,15 @@ __global__ void __launch_bounds__(kOzThreads, 1) ozk_gemm(const __grid_constant_
 #pragma unroll
                 for (int ks = 0; ks < OBK / 32; ++ks) {
 #pragma unroll
-                    for (int i = 0; i < kOzS; ++i)
+                    for (int i = 0; i < kOzS; ++i) {
 #pragma unroll
-                        for (int j = 0; j + i < kOzS; ++j)
-                            mma_i8(tmem + (uint32_t)((i + j) * OBN), oz_desc(sa + i * kOzATile + ks * 32),
-                                   oz_desc(sb + j * kOzBTile + ks * 32), idesc, (q > 0 || ks > 0 || i > 0) ? 1u : 0u);
+                        for (int j0 = 0; j0 + i < kOzS; j0 += 4) {
+                            const int nb = min(4, kOzS - i - j0);          // B planes in this MMA
+                            const uint32_t idesc = idesc0 | ((uint32_t)((nb * OBN) >> 3) << 17);
+                            mma_i8(tmem + (uint32_t)((i + j0) * OBN), oz_desc(sa + i * kOzATile + ks * 32),
+                                   oz_desc(sb + j0 * kOzBTile + ks * 32), idesc, (q > 0 || ks > 0 || i > 0) ? 1u : 0u);
+                        }
+                    }
                 }
                 mma_commit(empty + 8 * s);
             }

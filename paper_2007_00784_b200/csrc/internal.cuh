@@ -105,6 +105,7 @@ struct FactorJob {
     const float *src;       // act (NHWC) for A, gout (n x c_in) for G
     const float *src_lo;    // tensor-core path: src is the TF32 hi plane, src_lo the lo plane
     float *F;
+    float *packed;          // nullable: upper triangle, row-major, d(d+1)/2 floats
     float *partial;
     long long n;            // rows
     int ldF, d, is_a;

@@ -115,7 +115,8 @@ class KFAC:
             self._acts[id(module)] = inputs[0].detach()
 
     def _save_grad_output(self, module, grad_input, grad_output):
-        if self._capturing() and id(module) in self._acts:
+        # autograd runs backward hooks with grad mode off: capture whenever the forward did
+        if id(module) in self._acts:
             self._gouts[id(module)] = grad_output[0].detach()
 
     # ------------------------------------------------------------- marshalling --

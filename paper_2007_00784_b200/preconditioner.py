@@ -4,13 +4,15 @@ One process per GPU.  Every arithmetic step runs in libkfac's CUDA kernels
 (`_lib`); this module owns the buffers (torch CUDA tensors), decides which
 calls to make, and issues the collectives through torch.distributed:
 
-  step 1  kfac_update_factors (all layers, local mini-batch), then ONE allreduce
-          of the flat factor buffer (out_scale = 1/W fused into the kernel,
-          SUM on the wire) -- Alg. 1
+  step 1  kfac_update_factors (local mini-batch; out_scale = 1/W fused into the kernel), the
+          factors' packed upper triangles (half the bytes of the full matrices) all-reduced with
+          SUM in buckets of layers on a communication stream, each bucket's allreduce overlapping
+          the next bucket's factor kernels, then kfac_unpack_factors -- Alg. 1 P:343-345, P:387,
+          P:426-428 (asynchronous, batched communication)
   step 2  kfac_assign (host, identical on all ranks) -> kfac_compute_eigen on the
           owned factors -> exchange:
-            K-FAC-opt ("bcast-eig"): all-gather of the eigenbases, laid out
-              owner-major so each rank's slice is contiguous (no packing);
+            K-FAC-opt ("bcast-eig"): every owner broadcasts its contiguous, owner-major slice
+              of eigenbases (exactly its bytes, no padding to the largest slice);
             K-FAC-lw ("allgather-grad"): layer owners keep their
               eigenbases and the preconditioned gradients are all-gathered.
   step 3  kfac_precondition (Eqs. 13-15) and kfac_kl_clip (Eq. 18).
@@ -87,16 +89,27 @@ class KFACPreconditioner:
         self.F = _views(self.factor_flat, self.fseg)
         self.A = self.F[0::2]
         self.G = self.F[1::2]
-        # eigenbases / inverses: owner-major, one equal-size slice per rank (all-gather in place)
+        # packed upper triangles of the factors (the allreduce buffer, W > 1), same factor order
+        self.packed_seg, off = [], 0
+        for d in self.dims:
+            self.packed_seg.append((off, d * (d + 1) // 2))
+            off += _aligned(d * (d + 1) // 2)
+        self.packed_flat = torch.zeros(off if self.world > 1 else 64, **f32)
+        self.packed = [self.packed_flat[o:o + n] for o, n in self.packed_seg] if self.world > 1 else None
+        self.bucket_bytes = 64 << 20
+        self.comm_stream = torch.cuda.Stream(self.device) if (self.world > 1 and self.device.type == "cuda") else None
+        # eigenbases / inverses: owner-major, each rank's factors contiguous; slices have their real
+        # sizes (the exchange broadcasts exactly each owner's bytes)
         per_rank = [[f for f in range(len(self.dims)) if self.owner[f] == r] for r in range(self.world)]
-        q_sizes = [sum(_aligned(self.dims[f] * _ld(self.dims[f])) for f in fs) for fs in per_rank]
-        v_sizes = [sum(_aligned(self.dims[f]) for f in fs) for fs in per_rank]
-        self.q_slice, self.v_slice = max(q_sizes + [64]), max(v_sizes + [64])
-        self.q_flat = torch.zeros(self.q_slice * self.world, **f32)
-        self.v_flat = torch.zeros(self.v_slice * self.world, **f32)
+        self.q_size = [sum(_aligned(self.dims[f] * _ld(self.dims[f])) for f in fs) for fs in per_rank]
+        self.v_size = [sum(_aligned(self.dims[f]) for f in fs) for fs in per_rank]
+        self.q_off = [sum(self.q_size[:r]) for r in range(self.world)]
+        self.v_off = [sum(self.v_size[:r]) for r in range(self.world)]
+        self.q_flat = torch.zeros(max(64, sum(self.q_size)), **f32)
+        self.v_flat = torch.zeros(max(64, sum(self.v_size)), **f32)
         self.qseg, self.vseg = [None] * len(self.dims), [None] * len(self.dims)
         for r, fs in enumerate(per_rank):
-            qo, vo = r * self.q_slice, r * self.v_slice
+            qo, vo = self.q_off[r], self.v_off[r]
             for f in fs:
                 d = self.dims[f]
                 self.qseg[f] = Segment(qo, d, d, _ld(d))
@@ -109,12 +122,12 @@ class KFACPreconditioner:
         self.info = torch.zeros(max(1, len(self.owned)), dtype=torch.int32, device=self.device)
         # preconditioned gradients: owner-major by layer (K-FAC-lw all-gathers them in place)
         per_rank_l = [[i for i in range(L) if self.layer_owner[i] == r] for r in range(self.world)]
-        p_sizes = [sum(_aligned(self.d_g[i] * _ld(self.d_a[i])) for i in ls) for ls in per_rank_l]
-        self.p_slice = max(p_sizes + [64])
-        self.p_flat = torch.zeros(self.p_slice * self.world, **f32)
+        self.p_size = [sum(_aligned(self.d_g[i] * _ld(self.d_a[i])) for i in ls) for ls in per_rank_l]
+        self.p_off = [sum(self.p_size[:r]) for r in range(self.world)]
+        self.p_flat = torch.zeros(max(64, sum(self.p_size)), **f32)
         self.pseg = [None] * L
         for r, ls in enumerate(per_rank_l):
-            o = r * self.p_slice
+            o = self.p_off[r]
             for i in ls:
                 self.pseg[i] = Segment(o, self.d_g[i], self.d_a[i], _ld(self.d_a[i]))
                 o += self.pseg[i].numel
@@ -140,12 +153,47 @@ class KFACPreconditioner:
         return (views, flat) if return_flat else views
 
     # -------------------------------------------------------------- steps --
+    def buckets(self):
+        """Contiguous layer ranges whose packed factors hold about bucket_bytes each."""
+        out, start, acc = [], 0, 0
+        for i in range(len(self.layers)):
+            acc += 4 * sum(self.packed_seg[2 * i + k][1] for k in (0, 1))
+            if acc >= self.bucket_bytes or i == len(self.layers) - 1:
+                out.append((start, i + 1))
+                start, acc = i + 1, 0
+        return out
+
     def update_factors(self, acts, gouts, first: bool):
-        """Alg. 1 step 1: local factors + running average, then the factor allreduce."""
-        _lib.kfac_update_factors(self.layers, acts, gouts, self.A, self.G, self.decay, first,
-                                 1.0 / self.world, ws=self.ws["factors"])
-        if self.world > 1:
-            dist.all_reduce(self.factor_flat, op=dist.ReduceOp.SUM, group=self.pg)
+        """Alg. 1 step 1: local factors + running average, then the factor allreduce.
+
+        W > 1: the factors' packed upper triangles are all-reduced (SUM of the out_scale = 1/W
+        factors = their average) bucket by bucket; with NCCL each bucket's allreduce runs on the
+        communication stream as soon as its factor kernels are done, overlapping the next bucket's
+        kernels.  Then both triangles are restored from the reduced packed buffer."""
+        if self.world == 1:
+            _lib.kfac_update_factors(self.layers, acts, gouts, self.A, self.G, self.decay, first,
+                                     1.0, ws=self.ws["factors"])
+            return
+        compute = torch.cuda.current_stream(self.device) if self.comm_stream is not None else None
+        works = []
+        for b0, b1 in self.buckets():
+            _lib.kfac_update_factors(self.layers[b0:b1], acts[b0:b1], gouts[b0:b1], self.A[b0:b1], self.G[b0:b1],
+                                     self.decay, first, 1.0 / self.world, ws=self.ws["factors"],
+                                     packed_A=self.packed[2 * b0:2 * b1:2], packed_G=self.packed[2 * b0 + 1:2 * b1:2])
+            lo = self.packed_seg[2 * b0][0]
+            hi = self.packed_seg[2 * b1 - 1][0] + self.packed_seg[2 * b1 - 1][1]
+            if self.comm_stream is not None:
+                self.comm_stream.wait_stream(compute)
+                with torch.cuda.stream(self.comm_stream):
+                    works.append(dist.all_reduce(self.packed_flat[lo:hi], op=dist.ReduceOp.SUM, group=self.pg,
+                                                 async_op=True))
+            else:
+                dist.all_reduce(self.packed_flat[lo:hi], op=dist.ReduceOp.SUM, group=self.pg)
+        for w in works:
+            w.wait()                                   # the compute stream waits for the collectives
+        if self.comm_stream is not None:
+            compute.wait_stream(self.comm_stream)
+        _lib.kfac_unpack_factors(self.packed, self.F)
 
     def compute_eigen(self, warm: bool = False, check: Optional[bool] = None):
         """Alg. 1 step 2 on the owned factors, then the exchange of the results.
@@ -172,9 +220,9 @@ class KFACPreconditioner:
                                          f"factor(s) {what}: {bad[:8]}")
         self.have_eigen = True
         if self.world > 1 and self.exchange == "bcast-eig":
-            all_gather_inplace(self.q_flat, self.q_slice, self.pg)
+            exchange_from_owners(self.q_flat, self.q_off, self.q_size, self.pg)
             if self.variant != "inverse":
-                all_gather_inplace(self.v_flat, self.v_slice, self.pg)
+                exchange_from_owners(self.v_flat, self.v_off, self.v_size, self.pg)
 
     def precondition(self, grads: List[torch.Tensor]) -> List[torch.Tensor]:
         """Alg. 1 step 3 (Eqs. 13-15 / Eq. 12) followed by the KL-clip (Eq. 18)."""
@@ -193,7 +241,7 @@ class KFACPreconditioner:
             _lib.kfac_precondition(g, QG, vG, QA, vA, self.damping, mode, [self.P[i] for i in layers],
                                    ws=self.ws["precond"])
         if self.world > 1 and self.exchange == "allgather-grad":
-            all_gather_inplace(self.p_flat, self.p_slice, self.pg)
+            exchange_from_owners(self.p_flat, self.p_off, self.p_size, self.pg)
         _lib.kfac_kl_clip(self.P, grads, self.lr, self.kappa, self.nu, self.s, ws=self.ws["klclip"])
         return self.P
 
@@ -205,12 +253,13 @@ class KFACPreconditioner:
         return self.precondition(grads)
 
 
-def all_gather_inplace(flat: torch.Tensor, slice_numel: int, group=None):
-    """Every rank contributes flat[rank*slice:(rank+1)*slice]; afterwards all ranks hold all slices."""
+def exchange_from_owners(flat: torch.Tensor, offs, sizes, group=None):
+    """Rank r owns flat[offs[r]:offs[r]+sizes[r]]; afterwards every rank holds every slice.  One
+    broadcast per owner of exactly its bytes (an all-gather would pad every slice to the largest);
+    all are issued before any is waited on, so NCCL pipelines them."""
     world = dist.get_world_size(group)
-    rank = dist.get_rank(group)
-    mine = flat[rank * slice_numel:(rank + 1) * slice_numel]
-    if dist.get_backend(group) == "nccl":
-        dist.all_gather_into_tensor(flat, mine, group=group)
-    else:
-        dist.all_gather(list(flat.split(slice_numel)), mine.clone(), group=group)
+    works = [dist.broadcast(flat[offs[r]:offs[r] + sizes[r]], src=dist.get_global_rank(group, r) if group else r,
+                            group=group, async_op=True)
+             for r in range(world) if sizes[r] > 0]
+    for w in works:
+        w.wait()

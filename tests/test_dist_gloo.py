@@ -1,7 +1,7 @@
 """Multi-process (world_size 2, gloo, CPU) tests of the distributed orchestration:
 the same assignment on every rank, the owner-major buffer layout that lets the eigenbasis
-(K-FAC-opt) and preconditioned-gradient (K-FAC-lw) exchanges run as one in-place
-all-gather, and the factor average through allreduce-SUM of out_scale = 1/W factors
+(K-FAC-opt) and preconditioned-gradient (K-FAC-lw) exchanges run as one broadcast per owner
+of exactly its bytes, the packed-triangle factor allreduce in layer buckets, and the factor average through allreduce-SUM of out_scale = 1/W factors
 (Alg. 1).  The CUDA kernels are not exercised here."""
 import os
 import socket
@@ -27,7 +27,7 @@ def _worker(rank, world, port, cfg, exchange, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        from paper_2007_00784_b200.preconditioner import KFACPreconditioner, all_gather_inplace
+        from paper_2007_00784_b200.preconditioner import KFACPreconditioner, exchange_from_owners
         layers = shapes.layers_for(cfg)
         pc = KFACPreconditioner(layers, device="cpu", exchange=exchange)
         # 1) identical assignment everywhere
@@ -40,18 +40,33 @@ def _worker(rank, world, port, cfg, exchange, q):
         dist.all_reduce(pc.factor_flat, op=dist.ReduceOp.SUM)
         expect = (vals * world + 1000 * sum(range(world))) / world
         assert torch.allclose(pc.factor_flat, expect)
-        # 3) eigenbasis exchange (K-FAC-opt): owners write their factors, one in-place all-gather
+        # 2b) packed factor allreduce: the upper triangles are half the full-matrix bytes, the layer
+        # buckets tile all layers in order, and SUM of 1/W-scaled packed buffers is their average
+        full = sum(d * ((d + 3) // 4 * 4) for d in pc.dims)
+        packed = sum(d * (d + 1) // 2 for d in pc.dims)
+        assert packed <= 0.5 * full + sum(pc.dims)
+        bks = pc.buckets()
+        assert bks[0][0] == 0 and bks[-1][1] == len(layers) and all(a[1] == b[0] for a, b in zip(bks, bks[1:]))
+        pv = torch.arange(pc.packed_flat.numel(), dtype=torch.float32) % 89
+        for b0, b1 in bks:
+            lo = pc.packed_seg[2 * b0][0]
+            hi = pc.packed_seg[2 * b1 - 1][0] + pc.packed_seg[2 * b1 - 1][1]
+            seg = pc.packed_flat[lo:hi]
+            seg.copy_((pv[lo:hi] + 10 * rank) / world)
+            dist.all_reduce(seg, op=dist.ReduceOp.SUM)
+            assert torch.allclose(seg, pv[lo:hi] + 10 * sum(range(world)) / world)
+        # 3) eigenbasis exchange (K-FAC-opt): owners write their factors, one broadcast per owner
         for f in pc.owned:
             pc.Q[f].fill_(float(f + 1))
             pc.v[f].fill_(float(-(f + 1)))
-        all_gather_inplace(pc.q_flat, pc.q_slice)
-        all_gather_inplace(pc.v_flat, pc.v_slice)
+        exchange_from_owners(pc.q_flat, pc.q_off, pc.q_size)
+        exchange_from_owners(pc.v_flat, pc.v_off, pc.v_size)
         for f in range(len(pc.dims)):
             assert torch.all(pc.Q[f] == f + 1) and torch.all(pc.v[f] == -(f + 1))
         # 4) preconditioned-gradient exchange (K-FAC-lw): layer owners write P
         for i in pc.owned_layers:
             pc.P[i].fill_(float(i + 7))
-        all_gather_inplace(pc.p_flat, pc.p_slice)
+        exchange_from_owners(pc.p_flat, pc.p_off, pc.p_size)
         for i in range(len(layers)):
             assert torch.all(pc.P[i] == i + 7)
         if exchange == "allgather-grad":

@@ -346,3 +346,23 @@ def test_full_size_r50_sampled_layers(L, orc):
     floors = _noise_floor(orc, sub, ref["A"], ref["G"], grads, dict(hp, kappa=1e12), 0)
     print("R50 sampled relF(P):", errs, "fp32-storage floors:", floors)
     assert max(errs) <= 1e-3, (errs, floors)
+
+
+def test_packed_factor_outputs_roundtrip_bitwise(L):
+    """packed_A/packed_G (the halved allreduce buffer) carry exactly the values written
+    to the full factors: unpacking them reproduces both triangles bit for bit."""
+    layers = FACTOR_LAYERS
+    a1, g1, _ = layer_inputs(layers, seed=3, with_grad=False)
+    A = [empty(l.d_a, l.d_a) for l in layers]
+    G = [empty(l.d_g, l.d_g) for l in layers]
+    pA = [torch.full((l.d_a * (l.d_a + 1) // 2,), float("nan"), device="cuda") for l in layers]
+    pG = [torch.full((l.d_g * (l.d_g + 1) // 2,), float("nan"), device="cuda") for l in layers]
+    L.kfac_update_factors(layers, [torch.from_numpy(a).cuda() for a in a1], [torch.from_numpy(g).cuda() for g in g1],
+                          A, G, 0.95, True, 0.5, packed_A=pA, packed_G=pG)
+    A2 = [empty(l.d_a, l.d_a) for l in layers]
+    G2 = [empty(l.d_g, l.d_g) for l in layers]
+    L.kfac_unpack_factors(pA + pG, A2 + G2)
+    torch.cuda.synchronize()
+    for x, y, p in zip(A + G, A2 + G2, pA + pG):
+        assert torch.isfinite(p).all()
+        assert torch.equal(x, y)
