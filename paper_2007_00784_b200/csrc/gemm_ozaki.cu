@@ -54,7 +54,7 @@ constexpr int kOzMaxOps = 128;
 constexpr int kOzEpiStride = OBN + 1;                 // fp64 staging row stride
 // smallest K routed here: below it the two slicing passes and the per-tile prologue/epilogue cost
 // more than DMMA saves (scripts/micro_ozaki.py)
-constexpr int kOzMinK = 1024;
+constexpr int kOzMinK = 512;
 
 static_assert(kOzSmem <= 227 * 1024, "ozaki smem");
 static_assert(kOzS * OBN <= kOzTmemCols, "ozaki tmem");

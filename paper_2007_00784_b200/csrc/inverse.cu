@@ -2,7 +2,9 @@
 //   (F + damping I)^{-1} = L^{-T} L^{-1},  F + damping I = L L^T  (R15),
 // blocked right-looking Cholesky in FP64 (64x64 tiles), blocked triangular inversion and the
 // product X = Y^T Y with Y = L^{-1}; every launch covers the same step of all factors of the
-// batch.  FP64 because the explicit inverse amplifies rounding by cond(F + damping I)
+// batch.  The 64x64 diagonal factorisations and panel solves are SIMT kernels; the O(n^3) parts --
+// the trailing rank-64 updates, the triangular-inverse row products and the Gram product -- are
+// grouped fp64 GEMMs (gemm64_grouped: DMMA, or the int8 Ozaki engine for the large ones).  FP64 because the explicit inverse amplifies rounding by cond(F + damping I)
 // (SURVEY 8(c) numerics: fp32 inversion adds up to 4.8e-3 error on ResNet-50 layer4).
 #include "internal.cuh"
 
@@ -11,6 +13,12 @@
 
 namespace kfac {
 namespace {
+
+#define RET_OK_INV(x)                       \
+    do {                                    \
+        kfac_status_t _st = (x);            \
+        if (_st != KFAC_OK) return _st;     \
+    } while (0)
 
 constexpr int TB = 64;          // tile
 constexpr int KS = 16;          // k-slice staged in shared memory
@@ -22,6 +30,7 @@ struct InvJob {
     float *Finv;
     double *M;        // nP x nP working matrix (lower triangle becomes L)
     double *Y;        // nP x nP, lower triangle becomes L^{-1}
+    double *W;        // 64 x nP scratch of the triangular inverse
     int *info;
     int n, ldF, ldFinv, nP, nbk;
 };
@@ -73,7 +82,7 @@ __device__ void tile_gemm(double (&acc)[4][4], const double *A, int lda, int ta,
     }
 }
 
-__device__ __forceinline__ double *tile(double *M, int nP, int bi, int bj) {
+__host__ __device__ __forceinline__ double *tile(double *M, int nP, int bi, int bj) {
     return M + (size_t)bi * TB * nP + (size_t)bj * TB;
 }
 
@@ -96,7 +105,6 @@ __global__ void inv_init(const __grid_constant__ InvBatch b) {
 
 // Step k (a): factor the diagonal tile in shared memory; write L_kk and Y_kk = L_kk^{-1}.
 constexpr size_t kPotrfSmem = 2 * sizeof(double) * TB * (TB + 1);
-constexpr size_t kTrtriSmem = sizeof(double) * TB * (TB + 1);
 
 __global__ void __launch_bounds__(NT) inv_potrf(const __grid_constant__ InvBatch b) {
     extern __shared__ double dyn[];
@@ -169,79 +177,31 @@ __global__ void __launch_bounds__(NT) inv_trsm(const __grid_constant__ InvBatch 
         for (int c = 0; c < 4; ++c) Aik[(size_t)(ty + 16 * a) * J.nP + tx + 16 * c] = acc[a][c];
 }
 
-// Step k (c): A_ij -= L_ik L_jk^T for i >= j > k (lower tiles).
-__global__ void __launch_bounds__(NT) inv_update(const __grid_constant__ InvBatch b) {
-    const int ji = find(b, blockIdx.x);
-    const InvJob &J = b.j[ji];
-    const int k = b.step;
-    int e = blockIdx.x - b.begin[ji];
-    int i = k + 1, j;
-    while (e >= i - k) { e -= i - k; ++i; }      // tile rows i = k+1.., cols j = k+1..i
-    j = k + 1 + e;
-    double acc[4][4] = {};
-    tile_gemm(acc, tile(J.M, J.nP, i, k), J.nP, 0, tile(J.M, J.nP, j, k), J.nP, 1, TB);
-    double *Aij = tile(J.M, J.nP, i, j);
-    const int ty = threadIdx.x / 16, tx = threadIdx.x % 16;
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) Aij[(size_t)(ty + 16 * a) * J.nP + tx + 16 * c] -= acc[a][c];
-}
-
-// Triangular inverse, row tile i: Y_ij = -Y_ii sum_{m=j}^{i-1} L_im Y_mj for j < i.
-__global__ void __launch_bounds__(NT) inv_trtri(const __grid_constant__ InvBatch b) {
-    extern __shared__ double dyn[];
-    double(*Sacc)[TB + 1] = reinterpret_cast<double(*)[TB + 1]>(dyn);
-    const int ji = find(b, blockIdx.x);
-    const InvJob &J = b.j[ji];
-    const int i = b.step;
-    const int j = blockIdx.x - b.begin[ji];
-    double acc[4][4] = {};
-    for (int m = j; m < i; ++m)
-        tile_gemm(acc, tile(J.M, J.nP, i, m), J.nP, 0, tile(J.Y, J.nP, m, j), J.nP, 0, TB);
-    const int ty = threadIdx.x / 16, tx = threadIdx.x % 16;
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) Sacc[ty + 16 * a][tx + 16 * c] = acc[a][c];
-    __syncthreads();
-    const double *Yii = tile(J.Y, J.nP, i, i);
-    double *Yij = tile(J.Y, J.nP, i, j);
-    for (int e = threadIdx.x; e < TB * TB; e += NT) {
-        const int r = e / TB, c = e % TB;
-        double v = 0.0;
-        for (int m = 0; m <= r; ++m) v -= Yii[(size_t)r * J.nP + m] * Sacc[m][c];
-        Yij[(size_t)r * J.nP + c] = v;
+// Finv[j][i] = Finv[i][j] for j < i (the Gram GEMM writes the lower triangle; mirrored so the
+// output is exactly symmetric).  32 x 32 tiles through shared memory.
+__global__ void __launch_bounds__(256) inv_mirror(const __grid_constant__ InvBatch b) {
+    __shared__ float tr[32][33];
+    const InvJob &J = b.j[find(b, blockIdx.x)];
+    int t = blockIdx.x - b.begin[find(b, blockIdx.x)], ti = 0;
+    const int nt = (J.n + 31) / 32;
+    while (t >= ti + 1) { t -= ti + 1; ++ti; }           // lower tiles (ti >= tj), row-major
+    const int tj = t;
+    const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;
+    (void)nt;
+    for (int rr = ty; rr < 32; rr += 8) {
+        const int gi = ti * 32 + rr, gj = tj * 32 + tx;
+        tr[rr][tx] = (gi < J.n && gj < J.n && gj <= gi) ? J.Finv[(size_t)gi * J.ldFinv + gj] : 0.f;
     }
-}
-
-// X_ij = sum_{m >= max(i,j)} Y_mi^T Y_mj  for i >= j; writes X_ij and X_ji (fp32 output).
-__global__ void __launch_bounds__(NT) inv_gram(const __grid_constant__ InvBatch b) {
-    const int ji = find(b, blockIdx.x);
-    const InvJob &J = b.j[ji];
-    int e = blockIdx.x - b.begin[ji];
-    int i = 0;
-    while (e >= i + 1) { e -= i + 1; ++i; }
-    const int j = e;
-    double acc[4][4] = {};
-    for (int m = i; m < J.nbk; ++m)
-        tile_gemm(acc, tile(J.Y, J.nP, m, i), J.nP, 1, tile(J.Y, J.nP, m, j), J.nP, 0, TB);
-    const int ty = threadIdx.x / 16, tx = threadIdx.x % 16;
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            const int r = i * TB + ty + 16 * a, col = j * TB + tx + 16 * c;
-            if (r < J.n && col < J.n) {
-                J.Finv[(size_t)r * J.ldFinv + col] = (float)acc[a][c];
-                J.Finv[(size_t)col * J.ldFinv + r] = (float)acc[a][c];
-            }
-        }
+    __syncthreads();
+    for (int rr = ty; rr < 32; rr += 8) {
+        const int gi = tj * 32 + rr, gj = ti * 32 + tx;    // upper element (gi < gj) <- lower (gj, gi)
+        if (gi < J.n && gj < J.n && gi < gj) J.Finv[(size_t)gi * J.ldFinv + gj] = tr[tx][rr];
+    }
 }
 
 struct Plan {
     std::vector<InvJob> jobs;
-    size_t bytes = 0;
+    size_t bytes = 0, oz_off = 0, oz_bytes = 0;
 };
 
 Plan plan(const int32_t *dims, int count) {
@@ -258,8 +218,16 @@ Plan plan(const int32_t *dims, int count) {
         off = round_up(off, 256);
         J.Y = reinterpret_cast<double *>(off);
         off += sizeof(double) * (size_t)J.nP * J.nP;
+        off = round_up(off, 256);
+        J.W = reinterpret_cast<double *>(off);
+        off += sizeof(double) * (size_t)TB * J.nP;
         p.jobs.push_back(J);
+        // Ozaki scratch of the largest grouped GEMM (the Gram product Y^T Y, n x n x n)
+        p.oz_bytes += 12 * (size_t)(J.nP + 64) * J.nP + (1 << 20);
     }
+    off = round_up(off, 256);
+    p.oz_off = off;
+    off += p.oz_bytes;
     p.bytes = off + 256;
     return p;
 }
@@ -272,7 +240,6 @@ kfac_status_t inverse_run(const float *const *F, const int32_t *dims, const int3
                           float damping, float *const *Finv, const int32_t *ldFinv, int32_t *info,
                           void *ws, cudaStream_t s) {
     KFAC_CUDA_TRY(set_smem_attr((const void *)inv_potrf, (int)kPotrfSmem));
-    KFAC_CUDA_TRY(set_smem_attr((const void *)inv_trtri, (int)kTrtriSmem));
     Plan p = plan(dims, count);
     char *base = reinterpret_cast<char *>(round_up(reinterpret_cast<uintptr_t>(ws), 256));
     for (int i = 0; i < count; ++i) {
@@ -281,7 +248,12 @@ kfac_status_t inverse_run(const float *const *F, const int32_t *dims, const int3
         J.info = info ? info + i : nullptr;
         J.M = reinterpret_cast<double *>(base + reinterpret_cast<uintptr_t>(J.M));
         J.Y = reinterpret_cast<double *>(base + reinterpret_cast<uintptr_t>(J.Y));
+        J.W = reinterpret_cast<double *>(base + reinterpret_cast<uintptr_t>(J.W));
     }
+    struct ArenaGuard {
+        ArenaGuard(void *q, size_t b) { oz_set_arena(q, b); }
+        ~ArenaGuard() { oz_set_arena(nullptr, 0); }
+    } arena_guard(base + p.oz_off, p.oz_bytes);
     for (int b0 = 0; b0 < count; b0 += kMaxJobs) {
         InvBatch B;
         B.count = std::min(kMaxJobs, count - b0);
@@ -315,18 +287,64 @@ kfac_status_t inverse_run(const float *const *F, const int32_t *dims, const int3
             kfac_status_t st;
             if ((st = launch(inv_potrf, kPotrfSmem, [&](const InvJob &J) { return k < J.nbk ? 1 : 0; })) != KFAC_OK) return st;
             if ((st = launch(inv_trsm, 0, [&](const InvJob &J) { return k < J.nbk ? J.nbk - k - 1 : 0; })) != KFAC_OK) return st;
-            if ((st = launch(inv_update, 0, [&](const InvJob &J) {
-                     const int r = k < J.nbk ? J.nbk - k - 1 : 0;
-                     return r * (r + 1) / 2;
-                 })) != KFAC_OK)
-                return st;
+            // trailing update A22 -= L21 L21^T (lower tiles; K = 64)
+            std::vector<Gemm64Desc> gd;
+            for (int i = 0; i < B.count; ++i) {
+                const InvJob &J = B.j[i];
+                const int r = J.nbk - k - 1;
+                if (r <= 0) continue;
+                Gemm64Desc g{};
+                g.M = g.N = r * TB; g.K = TB;
+                g.A = tile(J.M, J.nP, k + 1, k); g.ta = DT_F64; g.lda = J.nP;
+                g.B = tile(J.M, J.nP, k + 1, k); g.tb = DT_F64; g.ldb = J.nP; g.trans_b = 1;
+                g.C = tile(J.M, J.nP, k + 1, k + 1); g.tc = DT_F64; g.ldc = J.nP;
+                g.epi = EPI_SUB;
+                g.lower = 1;
+                gd.push_back(g);
+            }
+            if (!gd.empty()) RET_OK_INV(gemm64_grouped(gd.data(), (int)gd.size(), s));
         }
+        // triangular inverse Y = L^{-1}, row tile i: W = L[i, 0:i) Y[0:i, 0:i);  Y[i, 0:i) = -Y_ii W
         for (int i = 1; i < max_nbk; ++i) {
-            B.step = i;
-            kfac_status_t st = launch(inv_trtri, kTrtriSmem, [&](const InvJob &J) { return i < J.nbk ? i : 0; });
-            if (st != KFAC_OK) return st;
+            std::vector<Gemm64Desc> g1, g2;
+            for (int q = 0; q < B.count; ++q) {
+                const InvJob &J = B.j[q];
+                if (i >= J.nbk) continue;
+                Gemm64Desc a{};
+                a.M = TB; a.N = i * TB; a.K = i * TB;
+                a.A = tile(J.M, J.nP, i, 0); a.ta = DT_F64; a.lda = J.nP;
+                a.B = J.Y; a.tb = DT_F64; a.ldb = J.nP;
+                a.C = J.W; a.tc = DT_F64; a.ldc = J.nP;
+                g1.push_back(a);
+                Gemm64Desc c{};
+                c.M = TB; c.N = i * TB; c.K = TB;
+                c.A = tile(J.Y, J.nP, i, i); c.ta = DT_F64; c.lda = J.nP;
+                c.B = J.W; c.tb = DT_F64; c.ldb = J.nP;
+                c.C = tile(J.Y, J.nP, i, 0); c.tc = DT_F64; c.ldc = J.nP;
+                c.epi = EPI_SUB;                    // Y[i, 0:i) is zero: 0 - Y_ii W
+                g2.push_back(c);
+            }
+            if (g1.empty()) continue;
+            RET_OK_INV(gemm64_grouped(g1.data(), (int)g1.size(), s));
+            RET_OK_INV(gemm64_grouped(g2.data(), (int)g2.size(), s));
         }
-        kfac_status_t st = launch(inv_gram, 0, [&](const InvJob &J) { return J.nbk * (J.nbk + 1) / 2; });
+        // Gram product X = Y^T Y (lower triangle, fp32 out), then mirrored
+        std::vector<Gemm64Desc> gg;
+        for (int q = 0; q < B.count; ++q) {
+            const InvJob &J = B.j[q];
+            Gemm64Desc g{};
+            g.M = g.N = J.n; g.K = J.n;
+            g.A = J.Y; g.ta = DT_F64; g.lda = J.nP; g.trans_a = 1;
+            g.B = J.Y; g.tb = DT_F64; g.ldb = J.nP;
+            g.C = J.Finv; g.tc = DT_F32; g.ldc = J.ldFinv;
+            g.lower = 1;
+            gg.push_back(g);
+        }
+        RET_OK_INV(gemm64_grouped(gg.data(), (int)gg.size(), s));
+        kfac_status_t st = launch(inv_mirror, 0, [&](const InvJob &J) {
+            const int nt = (J.n + 31) / 32;
+            return nt * (nt + 1) / 2;
+        });
         if (st != KFAC_OK) return st;
     }
     return KFAC_OK;
