@@ -92,6 +92,8 @@ typedef enum {
 #define KFAC_EIG_WARM_START 1u   /* Jacobi factors start from the Q passed in (stale basis) */
 #define KFAC_EIG_JACOBI 2u       /* every factor by one-sided block Jacobi */
 #define KFAC_EIG_TRIDIAG 4u      /* every factor by tridiagonalisation + divide and conquer */
+#define KFAC_EIG_TWO_STAGE 8u    /* tridiagonal factors with 1024 <= dims <= 5632: two-stage reduction */
+#define KFAC_EIG_ONE_STAGE 16u   /* tridiagonal factors: one-stage reduction only */
 
 /* Derived dimensions of one layer.  Host only; any output pointer may be NULL. */
 kfac_status_t kfac_layer_dims(const kfac_layer_t *layer, int32_t *d_a, int32_t *d_g, int64_t *rows);
@@ -133,7 +135,11 @@ kfac_status_t kfac_unpack_factors(const float *const *packed, const int32_t *dim
  * info: device int32[count]; 0 = converged, k > 0 = not converged after k sweeps
  * (outputs still written).  Method: factors with dims >= 64 by
  * Householder tridiagonalisation + divide and conquer + blocked back-transformation, smaller
- * ones by one-sided block Jacobi; KFAC_EIG_JACOBI / KFAC_EIG_TRIDIAG force one method.
+ * ones by one-sided block Jacobi; KFAC_EIG_JACOBI / KFAC_EIG_TRIDIAG force one method.  The
+ * tridiagonalisation is one-stage (Householder panels) or two-stage (dense -> band 16 -> tridiagonal,
+ * DESIGN.md §8) for 1024 <= dims <= 5632; by default the two-stage reduction takes a factor that
+ * carries most of the call's d^3 (a latency-bound lone factor, e.g. one rank's share at W >= 4) and
+ * is measured faster at its size; KFAC_EIG_TWO_STAGE / KFAC_EIG_ONE_STAGE force either reduction.
  * KFAC_EIG_WARM_START: Q[i] holds the previous orthonormal eigenbasis on entry and the Jacobi
  * factors start from it.  Eigenvector sign/order within equal eigenvalues is free (R11).
  * 1 <= dims[i] <= 16384. */

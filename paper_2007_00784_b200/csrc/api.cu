@@ -244,8 +244,10 @@ kfac_status_t kfac_compute_eigen(const float *const *F, const int32_t *dims, con
     KFAC_CHECK_ARG(F && dims && ld_F && Q && ld_Q && evals, KFAC_ERR_INVALID_VALUE,
                    "kfac_compute_eigen: NULL argument");
     KFAC_CHECK_ARG(count > 0, KFAC_ERR_INVALID_VALUE, "kfac_compute_eigen: count <= 0");
-    KFAC_CHECK_ARG((flags & ~(KFAC_EIG_WARM_START | KFAC_EIG_JACOBI | KFAC_EIG_TRIDIAG)) == 0 &&
-                       (flags & (KFAC_EIG_JACOBI | KFAC_EIG_TRIDIAG)) != (KFAC_EIG_JACOBI | KFAC_EIG_TRIDIAG),
+    KFAC_CHECK_ARG((flags & ~(KFAC_EIG_WARM_START | KFAC_EIG_JACOBI | KFAC_EIG_TRIDIAG | KFAC_EIG_TWO_STAGE |
+                              KFAC_EIG_ONE_STAGE)) == 0 &&
+                       (flags & (KFAC_EIG_JACOBI | KFAC_EIG_TRIDIAG)) != (KFAC_EIG_JACOBI | KFAC_EIG_TRIDIAG) &&
+                       (flags & (KFAC_EIG_TWO_STAGE | KFAC_EIG_ONE_STAGE)) != (KFAC_EIG_TWO_STAGE | KFAC_EIG_ONE_STAGE),
                    KFAC_ERR_INVALID_VALUE, "unknown or conflicting flags 0x%x", flags);
     for (int i = 0; i < count; ++i) {
         KFAC_CHECK_ARG(dims[i] > 0 && dims[i] <= 16384, KFAC_ERR_SHAPE, "dims[%d] = %d out of range", i, dims[i]);

@@ -24,8 +24,8 @@ namespace kfac {
 size_t eigen_workspace_bytes(const int32_t *dims, int count);
 size_t trd_workspace_bytes(const int32_t *dims, int count);
 kfac_status_t trd_run(const float *const *F, const int32_t *dims, const int32_t *ldF, int count,
-                      float *const *Q, const int32_t *ldQ, float *const *evals, int32_t *info, void *ws,
-                      cudaStream_t s);
+                      float *const *Q, const int32_t *ldQ, float *const *evals, int32_t *info, uint32_t flags,
+                      void *ws, cudaStream_t s);
 kfac_status_t eigen_run(const float *const *F, const int32_t *dims, const int32_t *ldF, int count,
                         float *const *Q, const int32_t *ldQ, float *const *evals, int32_t *info,
                         uint32_t flags, void *ws, cudaStream_t s);
@@ -588,7 +588,7 @@ kfac_status_t eigen_run(const float *const *F, const int32_t *dims, const int32_
     }
     if (!td.empty()) {
         kfac_status_t st = trd_run(tF.data(), td.data(), tl.data(), (int)td.size(), tQ.data(), tlq.data(),
-                                   te.data(), local + jd.size(), base + joff, s);
+                                   te.data(), local + jd.size(), flags, base + joff, s);
         if (st != KFAC_OK) return st;
         if (info) {
             st = scatter_info(local + jd.size(), tidx, info, s);

@@ -1,26 +1,27 @@
 // eigen_trd.cu -- eigendecomposition of the large Kronecker factors (Alg. 1, Eqs. 13-15)
-// by the classical three-phase dense symmetric eigensolver, re-designed for B200:
+// by the classical three-phase dense symmetric eigensolver, re-designed for B200 (DESIGN.md §8):
 //
 //   (1) Householder tridiagonalisation F = H T H^T, H = H_0 H_1 ... H_{n-2}
 //       (Golub & Van Loan Alg. 8.3.1; blocked as in LAPACK dsytrd/dlatrd with panels of 32):
-//       a persistent kernel per panel in which every factor of the batch owns a group of CTAs
-//       (sized by its remaining work) synchronised by its own global-memory barrier -- three
-//       barriers per column (norm, symmetric mat-vec + panel dots, w^T v); the rank-64 trailing
-//       update A -= V W^T + W V^T between panels is a tcgen05 3xTF32 GEMM.  Working matrix fp32,
-//       every reduction in fp64, (d, e, tau) in fp64.
-//   (2) Cuppen's divide and conquer on T (fp64 arithmetic, fp32 eigenvector storage):
+//       a persistent cooperative kernel per panel in which every factor of the batch owns a group
+//       of CTAs (sized by its remaining work) synchronised by its own global-memory barrier -- two
+//       barriers per column; the rank-64 trailing update A -= V W^T + W V^T runs inside the same
+//       kernel on the fp64 tensor cores (DMMA).  Working matrix fp32, every reduction in fp64,
+//       (d, e, tau) in fp64.  Factors the router sends to the two-stage reduction (eigen_sbr.cu:
+//       dense -> band 16 -> tridiagonal) skip these panels.
+//   (2) Cuppen's divide and conquer on T (fp64 arithmetic and fp64 eigenvector storage):
 //       leaves of <= 32 rows by implicit QL (one warp each); each merge solves
 //       D + rho z z^T with LAPACK-style deflation (small z_i, and close d_i by a Givens rotation),
 //       a bracketed rational-Newton secular solver (one warp per root), the Gu-Eisenstat
 //       recomputed z-hat (orthogonal eigenvectors without extra precision), and the
-//       eigenvector update Q_nd S as a grouped tensor-core GEMM whose N and K are the
-//       device-side count of non-deflated roots.
-//   (3) back-transformation X = H Z in blocks of 128 reflectors with the compact WY form
-//       H_b...H_{b+127} = I - V T V^T (LAPACK dlarft), three grouped GEMMs per block.
+//       eigenvector update Q_nd S as grouped fp64 GEMMs (DMMA, or the Ozaki int8 engine for the
+//       large ones) whose N and K are the device-side count of non-deflated roots.
+//   (3) back-transformation X = H Z in blocks of 512 reflectors with the compact WY form
+//       H_b...H_{b+511} = I - V T V^T (LAPACK dlarft by 128-blocks joined recursively), three
+//       grouped fp64 GEMMs per block (for two-stage factors after Q2, with reflector offset 16).
 //
-// Work ~ (4/3 + 4/3 + 2) n^3 flops, most of it on the tensor pipe, against ~12 n^3 per sweep of the
-// one-sided Jacobi (eigen.cu), which remains the solver for small factors and warm starts.
-#include "internal.cuh"
+// One-sided block Jacobi (eigen.cu) remains the solver for factors below 64 and warm starts.
+#include "eigen_trd.cuh"
 
 #include <algorithm>
 #include <cmath>
@@ -36,8 +37,8 @@ namespace kfac {
 
 size_t trd_workspace_bytes(const int32_t *dims, int count);
 kfac_status_t trd_run(const float *const *F, const int32_t *dims, const int32_t *ldF, int count,
-                      float *const *Q, const int32_t *ldQ, float *const *evals, int32_t *info, void *ws,
-                      cudaStream_t s);
+                      float *const *Q, const int32_t *ldQ, float *const *evals, int32_t *info, uint32_t flags,
+                      void *ws, cudaStream_t s);
 
 namespace {
 
@@ -65,42 +66,6 @@ constexpr int kBt = 512;                // reflectors per back-transformation bl
 constexpr int kTs = 128;                // dlarft sub-block (T built recursively from 128-blocks)
 constexpr double kEps = 1.1102230246251565e-16;   // 2^-53, LAPACK dlamch('E')
 
-// ----------------------------------------------------------------- job --
-struct TrdJob {
-    const float *F;
-    float *Q, *evals;
-    int *info;
-    float *A;          // n x ldw working matrix (full symmetric storage, pads zero)
-    float *Vb;         // n x ldw reflectors: column k = v_k (v_k[k+1] = 1, zero above)
-    double *Vd;        // fp64 copy of Vb for the back-transformation GEMMs (all-fp64 DMMA kernel)
-    float *VW, *WV;    // n x 64 panel buffers: [V | W] and [W | V] of the current panel
-    double *VWd, *WVd; // fp64 copies of the same (float) values: operands of the trailing update
-    double *Z0, *Z1;   // n x ldw eigenvectors of T (D&C ping-pong), fp64
-    double *Qnd, *Tmp; // n x ldw D&C scratch (permuted/rotated columns, GEMM output)
-    double *Sb;        // n x ldw D&C secular eigenvectors S
-    double *Yb, *Y2b;  // kBt x ldw back-transformation scratch
-    double *Gb, *Tb;   // kBt x kBt Gram matrix V^T V and WY factor T
-    double *Wt;        // kBt x kBt scratch for the recursive T
-    double *d, *e, *tau;       // tridiagonal T and reflector scalars
-    double *x, *y;             // corrected column / mat-vec result (sytrd)
-    double *D;                 // current eigenvalues of the D&C subproblems
-    double *dval, *zval;       // merge: sorted (d, z) -- non-deflated first, deflated last
-    double *rtau, *wz;         // merge: root offsets, z-hat
-    double *vnorm;             // merge: eigenvector column norms
-    double *rot_c, *rot_s;     // merge: Givens rotations
-    int *col, *posof, *rorg, *rot_p, *rot_j, *srcpos;
-    int *ctyp;                 // merge: column type (1 upper, 2 mixed, 3 lower), then GEMM position
-    int *mstate;               // per merge at slot a: {k, nrot, k, k1 + k2, 0, k, k, k1}
-                               // (two GEMM dynamic {N, K, K start} triples: upper and lower rows)
-    double *mscal;             // per merge: {rho2, tol}
-    double *part;              // kMaxGroupCtas x kPart
-    double *DP;                // symv direct partials  [n][ldp]  (row, 128-column chunk)
-    double *TP;                // symv transposed partials [n][ldtp] (column, 64-row block)
-    int ldp, ldtp;
-    unsigned *bar;
-    int n, ldF, ldQ, ldw;
-    int levels;                // D&C merge levels (n <= kLeaf -> 0)
-};
 
 template <class T>
 __device__ __forceinline__ T ldcg(const T *p) { return __ldcg(p); }
@@ -176,6 +141,13 @@ __global__ void trd_init(const TrdJob *jobs) {
         for (int y = ty; y < 32; y += 8) {
             const int r = r0 + y, c = c0 + tx;
             if (r >= n || c >= ldw) continue;
+            if (J.off != 1) {                       // two-stage: fp64 working matrix, Vd = 0
+                double a = 0.0;
+                if (c < n) a = 0.5 * ((double)J.F[(size_t)r * J.ldF + c] + (double)tr[tx][y]);
+                J.Ad[(size_t)r * ldw + c] = a;
+                J.Vd[(size_t)r * ldw + c] = 0.0;
+                continue;
+            }
             float a = 0.f;
             if (c < n) a = 0.5f * (J.F[(size_t)r * J.ldF + c] + tr[tx][y]);
             J.A[(size_t)r * ldw + c] = a;
@@ -1371,8 +1343,6 @@ __global__ void bt_larft(const TrdJob *jobs, const BtStep *steps) {
     }
 }
 
-// Eigenvectors of T after the last merge level: level l writes Z0 (l even) / Z1 (l odd).
-__host__ __device__ inline double *final_z(const TrdJob &J) { return (J.levels & 1) ? J.Z1 : J.Z0; }
 
 __global__ void trd_output(const TrdJob *jobs) {
     const TrdJob &J = jobs[blockIdx.y];
@@ -1386,9 +1356,11 @@ __global__ void trd_output(const TrdJob *jobs) {
     }
 }
 
-// Vd = (double) Vb (exact), so every back-transformation GEMM has fp64 operands.
+// Vd = (double) Vb (exact), so every back-transformation GEMM has fp64 operands (one-stage factors;
+// the two-stage reduction writes Vd itself).
 __global__ void trd_vb_to_f64(const TrdJob *jobs) {
     const TrdJob &J = jobs[blockIdx.y];
+    if (J.off != 1) return;
     const long long total = (long long)J.n * J.ldw;
     for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
          e += (long long)gridDim.x * blockDim.x)
@@ -1461,8 +1433,13 @@ Plan plan(const int32_t *dims, int count) {
         J.n = n;
         J.ldw = ldw;
         J.levels = levels_for(n);
+        J.off = 1;                                       // set per call by sbr::route
         const size_t sq = (size_t)n * ldw;
 #define TAKE(field, T, cnt) J.field = reinterpret_cast<T *>(take(sizeof(T) * (size_t)(cnt)))
+        if (sbr::eligible(n)) {                          // either reduction may take the factor
+            cur = round_up(cur, 256);
+            sbr::plan_fields(J, cur);
+        }
         TAKE(A, float, sq);
         TAKE(Vb, float, sq);
         TAKE(Vd, double, sq);
@@ -1526,7 +1503,7 @@ Plan plan(const int32_t *dims, int count) {
             }
         }
         // back-transformation blocks (reflectors 0..n-2), processed last block first
-        const int nref = std::max(0, n - 1);
+        const int nref = std::max(0, n - J.off);
         const int nblk = (nref + kBt - 1) / kBt;
         if ((int)P.bt.size() < nblk) P.bt.resize(nblk);
         for (int s = 0; s < nblk; ++s) {
@@ -1556,8 +1533,8 @@ Plan plan(const int32_t *dims, int count) {
 }
 
 template <class T>
-T *rebase(T *p, char *base) {
-    return reinterpret_cast<T *>(base + reinterpret_cast<uintptr_t>(p));
+T *rebase(T *p, char *base) {           // offsets from plan(); fields a factor does not use stay null
+    return p ? reinterpret_cast<T *>(base + reinterpret_cast<uintptr_t>(p)) : nullptr;
 }
 
 int panel_capacity(size_t smem) {
@@ -1573,25 +1550,29 @@ int panel_capacity(size_t smem) {
 enum { TRD_FULL = 0, TRD_DEBUG_TRIDIAG = 1, TRD_DEBUG_STEDC = 2 };
 
 kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t *ldF, int count,
-                       float *const *Q, const int32_t *ldQ, float *const *evals, int32_t *info, void *ws,
-                       cudaStream_t s, int mode, double *dbg_d, double *dbg_e);
+                       float *const *Q, const int32_t *ldQ, float *const *evals, int32_t *info, uint32_t flags,
+                       void *ws, cudaStream_t s, int mode, double *dbg_d, double *dbg_e);
 
 }  // namespace
 
 size_t trd_workspace_bytes(const int32_t *dims, int count) { return plan(dims, count).bytes; }
 
 kfac_status_t trd_run(const float *const *F, const int32_t *dims, const int32_t *ldF, int count,
-                      float *const *Q, const int32_t *ldQ, float *const *evals, int32_t *info, void *ws,
-                      cudaStream_t s) {
-    return trd_exec(F, dims, ldF, count, Q, ldQ, evals, info, ws, s, TRD_FULL, nullptr, nullptr);
+                      float *const *Q, const int32_t *ldQ, float *const *evals, int32_t *info, uint32_t flags,
+                      void *ws, cudaStream_t s) {
+    return trd_exec(F, dims, ldF, count, Q, ldQ, evals, info, flags, ws, s, TRD_FULL, nullptr, nullptr);
 }
 
 namespace {
 
 kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t *ldF, int count,
-                       float *const *Q, const int32_t *ldQ, float *const *evals, int32_t *info, void *ws,
-                       cudaStream_t s, int mode, double *dbg_d, double *dbg_e) {
+                       float *const *Q, const int32_t *ldQ, float *const *evals, int32_t *info, uint32_t flags,
+                       void *ws, cudaStream_t s, int mode, double *dbg_d, double *dbg_e) {
     Plan P = plan(dims, count);
+    {   // reduction per factor (the workspace holds both): reflector offset 1 (one-stage) or 16
+        const std::vector<char> two = sbr::route(dims, count, flags);
+        for (int i = 0; i < count; ++i) P.jobs[i].off = two[i] ? sbr::kSbrBw : 1;
+    }
     char *base = reinterpret_cast<char *>(round_up(reinterpret_cast<uintptr_t>(ws), 256));
     int max_n = 0;
     for (int i = 0; i < count; ++i) {
@@ -1612,6 +1593,7 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
         J.srcpos = rebase(J.srcpos, base); J.ctyp = rebase(J.ctyp, base); J.mstate = rebase(J.mstate, base); J.mscal = rebase(J.mscal, base);
         J.part = rebase(J.part, base); J.bar = rebase(J.bar, base);
         J.DP = rebase(J.DP, base); J.TP = rebase(J.TP, base); J.Wt = rebase(J.Wt, base);
+        sbr::rebase_fields(J, base);
         max_n = std::max(max_n, J.n);
     }
     TrdJob *djobs = reinterpret_cast<TrdJob *>(base + P.table_off);
@@ -1657,8 +1639,12 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
     thread_local PanelLaunch PL;       // host staging (kernel parameters are copied at launch)
     // Staggered schedule: factor j (P_j panels) starts at launch P_max - P_j, so all factors finish
     // together and the small ones share the GPU with the big ones' small trailing matrices.
+    std::vector<int> sbr_ids;           // factors on the two-stage reduction (eigen_sbr.cu)
+    for (int i = 0; i < count; ++i)
+        if (P.jobs[i].off != 1) sbr_ids.push_back(i);
     int pmax = 0;
-    for (int i = 0; i < count; ++i) pmax = std::max(pmax, cdiv(P.jobs[i].n, kNb));
+    for (int i = 0; i < count; ++i)
+        if (P.jobs[i].off == 1) pmax = std::max(pmax, cdiv(P.jobs[i].n, kNb));
     // CTAs per active factor ~ (remaining trailing size)^2 (the mat-vec bytes; exponents 1.5-3
     // measured equal within noise)
     constexpr double wexp = 2.0;
@@ -1667,7 +1653,7 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
         double wsum = 0.0;
         for (int i = 0; i < count; ++i) {
             const int pidx = t - (pmax - cdiv(P.jobs[i].n, kNb));
-            if (pidx < 0) continue;
+            if (pidx < 0 || P.jobs[i].off != 1) continue;
             act.push_back(i);
             pst.push_back(pidx * kNb);
             const double m = P.jobs[i].n - pidx * kNb;
@@ -1739,6 +1725,7 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
         }   // chunks of the active set
     }
 
+    if (!sbr_ids.empty()) RET_OK(sbr::reduce(djobs, P.jobs, sbr_ids, s));
     }   // mode != TRD_DEBUG_STEDC
     if (mode == TRD_DEBUG_TRIDIAG) {
         KFAC_CUDA_TRY(cudaMemcpyAsync(dbg_d, P.jobs[0].d, sizeof(double) * P.jobs[0].n, cudaMemcpyDeviceToDevice, s));
@@ -1819,6 +1806,10 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
 
     // ---- (3) back-transformation X = H Z, last block of reflectors first ----
     if (mode != TRD_DEBUG_STEDC) {
+        std::vector<int> sbr_ids;
+        for (int i = 0; i < count; ++i)
+            if (P.jobs[i].off != 1) sbr_ids.push_back(i);
+        if (!sbr_ids.empty()) RET_OK(sbr::apply_q2(djobs, P.jobs, sbr_ids, s));
         trd_vb_to_f64<<<dim3(std::min(1024, cdiv((long long)max_n * ldw_for(max_n), 256)), count), 256, 0, s>>>(djobs);
         KFAC_LAUNCHED();
     }
@@ -1829,9 +1820,9 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
         std::vector<Gemm64Desc> g1, g2, g3;
         for (auto &b : stp) {
             const TrdJob &J = P.jobs[b.job];
-            const int m = J.n - b.b0 - 1;
-            const double *V = J.Vd + (size_t)(b.b0 + 1) * J.ldw + b.b0;
-            double *X = final_z(J) + (size_t)(b.b0 + 1) * J.ldw;
+            const int m = J.n - b.b0 - J.off;                    // reflector b0 + i: rows b0 + off + i ..
+            const double *V = J.Vd + (size_t)(b.b0 + J.off) * J.ldw + b.b0;
+            double *X = final_z(J) + (size_t)(b.b0 + J.off) * J.ldw;
             Gemm64Desc g{};
             g.M = b.nr; g.N = b.nr; g.K = m;                     // G = V^T V, lower half only
             g.A = V; g.ta = DT_F64; g.lda = J.ldw; g.trans_a = 1;
@@ -1957,7 +1948,8 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
 //   kfac_debug_tridiag: F (n x ldF, device) -> d (n), e (n-1) of H^T F H (device fp64).
 //   kfac_debug_stedc:   tridiagonal (d, e) (device fp64) -> Z (n x ldZ fp32, columns =
 //                       eigenvectors), w (n fp64, ascending).
-extern "C" int kfac_debug_tridiag(const float *F, int n, int ldF, double *d, double *e, void *stream) {
+extern "C" int kfac_debug_tridiag_ex(const float *F, int n, int ldF, double *d, double *e, unsigned flags,
+                                    void *stream) {
     const int32_t dims[1] = {n}, ld[1] = {ldF};
     const size_t bytes = kfac::trd_workspace_bytes(dims, 1);
     void *ws = nullptr;
@@ -1966,10 +1958,13 @@ extern "C" int kfac_debug_tridiag(const float *F, int n, int ldF, double *d, dou
     const float *Fp[1] = {F};
     float *Qp[1] = {Qd}, *Ep[1] = {ev};
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    int st = kfac::trd_exec(Fp, dims, ld, 1, Qp, ld, Ep, nullptr, ws, s, kfac::TRD_DEBUG_TRIDIAG, d, e);
+    int st = kfac::trd_exec(Fp, dims, ld, 1, Qp, ld, Ep, nullptr, flags, ws, s, kfac::TRD_DEBUG_TRIDIAG, d, e);
     cudaStreamSynchronize(s);
     cudaFree(ws);
     return st;
+}
+extern "C" int kfac_debug_tridiag(const float *F, int n, int ldF, double *d, double *e, void *stream) {
+    return kfac_debug_tridiag_ex(F, n, ldF, d, e, 0u, stream);
 }
 
 #if KFAC_TRD_TIMING
@@ -1995,7 +1990,7 @@ extern "C" int kfac_debug_stedc(const double *d, const double *e, int n, float *
     if (n > 1) cudaMemcpyAsync(e_copy, e, sizeof(double) * (n - 1), cudaMemcpyDeviceToDevice, s);
     const float *Fp[1] = {nullptr};
     float *Qp[1] = {Z}, *Ep[1] = {static_cast<float *>(ev)};
-    int st = kfac::trd_exec(Fp, dims, ld, 1, Qp, ld, Ep, nullptr, ws, s, kfac::TRD_DEBUG_STEDC, w, e_copy);
+    int st = kfac::trd_exec(Fp, dims, ld, 1, Qp, ld, Ep, nullptr, 0u, ws, s, kfac::TRD_DEBUG_STEDC, w, e_copy);
     cudaStreamSynchronize(s);
     cudaFree(ws);
     cudaFree(ev);

@@ -1,14 +1,16 @@
-// gemm_f64.cu -- grouped SIMT GEMM with fp64 accumulation for the eigensolver's internal
-// products (trailing rank-2k update, divide-and-conquer eigenvector updates, back-transformation).
+// gemm_f64.cu -- grouped GEMM with fp64 accumulation for the eigensolver's internal products
+// (trailing rank-2k updates, divide-and-conquer eigenvector updates, back-transformation, the
+// two-stage reduction's rank-32 update), and the explicit inverse's blocked updates.
 //
-// Why not the tensor cores there: the preconditioner divides by v_G v_A^T + damping, so an
-// eigenvector error e along a direction of eigenvalue L is amplified by ~L/damping (5e5 for the
-// ResNet-50 fc A factor); the eigenvectors must be accurate to the fp32 rounding level, while a
-// 3xTF32 product carries ~2^-22 relative error per term and accumulates across ~10 chained GEMMs.
-// fp64 products of fp32/fp64 operands with fp64 accumulation leave one rounding per output.
+// Why fp64 there: the preconditioner divides by v_G v_A^T + damping, so an eigenvector error e along
+// a direction of eigenvalue L is amplified by ~L/damping (5e5 for the ResNet-50 fc A factor); the
+// eigenvectors must be accurate to the fp32 rounding level, while a 3xTF32 product carries ~2^-22
+// relative error per term and accumulates across ~10 chained GEMMs.
 //
-// 128x128 tile per CTA, 256 threads, 8x8 outputs per thread, K staged 8 at a time through shared
-// memory as fp64 (operands converted once when staged), register prefetch of the next slab.
+// Engines (gemm64_grouped picks per batch): fp64 tensor cores (DMMA, mma.sync m8n8k4) fed by a
+// cp.async pipeline -- straight from the fp64 stages when both operands are fp64 ("direct"), through
+// an fp32->fp64 conversion pass otherwise ("pipe"); a SIMT fallback for unaligned operands; and,
+// while an Ozaki arena is set, the int8 tensor-core Ozaki scheme (gemm_ozaki.cu) for large products.
 #include "internal.cuh"
 
 #include <cstdlib>
