@@ -147,7 +147,7 @@ def oracle_sample(layers, hp, seed, sample_idx):
     sub = [layers[i] for i in sample_idx]
     acts, gouts, grads = layer_inputs(sub, seed=seed)
     t0 = time.perf_counter()
-    A, G = oracle.update_factors(sub, acts, gouts, decay=hp["decay"], first=True)
+    A, G = oracle.update_factors(sub, acts, gouts, xi=hp["xi"], first=True)
     t1 = time.perf_counter()
     Qs, vs = oracle.symeig_batch(A + G)
     t2 = time.perf_counter()
@@ -243,7 +243,7 @@ def run_ours(args):
         acts_h, gouts_h, grads_h = layer_inputs(layers, seed=args.seed + 1000 * b, rank=rank, device="cuda")
         host_sets.append((acts_h, gouts_h, grads_h))
         dev_sets.append(([torch.from_numpy(a).cuda() for a in acts_h], [torch.from_numpy(g).cuda() for g in gouts_h]))
-    pc = KFACPreconditioner(layers, damping=hp["damping"], decay=hp["decay"], kappa=hp["kappa"], lr=lr,
+    pc = KFACPreconditioner(layers, damping=hp["damping"], xi=hp["xi"], kappa=hp["kappa"], lr=lr,
                             variant=args.variant, exchange=args.exchange)
     grad_bufs = []
     for b in range(2):

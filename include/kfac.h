@@ -102,7 +102,8 @@ kfac_status_t kfac_layer_dims(const kfac_layer_t *layer, int32_t *d_a, int32_t *
  * (Eqs. 16-17; R5).  For every layer l (host arrays of length num_layers):
  *   A_batch = X^T X / n with X = [im2col(act[l]) | 1]   (n x d_A),
  *   G_batch = gout[l]^T gout[l] / n                     (gout: n x c_out, row-major, device),
- *   F = first ? F_batch : decay*F + (1-decay)*F_batch;  F *= out_scale   (F in {A, G}).
+ *   F = first ? F_batch : xi*F_batch + (1-xi)*F;  F *= out_scale   (F in {A, G}; Eqs. 16-17 P:383-386:
+ *   xi weights the new batch estimate, xi = 1 keeps only the batch).
  * act[l]: device, NHWC (conv) or (n, c_in) (linear) fp32, contiguous.
  * A[l]: device d_A x ld_A[l]; G[l]: device d_G x ld_G[l]; both triangles are written
  * (symmetric).  When first == 0 the previous A/G are read (must be symmetric).
@@ -111,7 +112,7 @@ kfac_status_t kfac_layer_dims(const kfac_layer_t *layer, int32_t *d_a, int32_t *
  * the factor allreduce buffer at half the full-matrix bytes (kfac_unpack_factors restores
  * both triangles after the collective).
  * out_scale = 1/W before an allreduce-SUM averages the factors.
- * Rows per layer must be < 2^31; decay in [0, 1].
+ * Rows per layer must be < 2^31; xi in [0, 1].
  * Workspace: the per-(tile, row chunk) partial sums and, for the tensor-core factors, the TF32
  * hi/lo planes of their inputs (two copies of each activation / gradient tensor). */
 size_t kfac_update_factors_workspace_size(const kfac_layer_t *layers, int32_t num_layers);
@@ -120,7 +121,7 @@ kfac_status_t kfac_update_factors(const kfac_layer_t *layers, int32_t num_layers
                                   float *const *A, const int32_t *ld_A,
                                   float *const *G, const int32_t *ld_G,
                                   float *const *packed_A, float *const *packed_G,
-                                  float decay, int32_t first, float out_scale,
+                                  float xi, int32_t first, float out_scale,
                                   void *ws, size_t ws_bytes, kfac_stream_t stream);
 
 /* Packed upper triangles (layout of kfac_update_factors' packed outputs) -> both triangles of F[i]

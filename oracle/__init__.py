@@ -112,14 +112,14 @@ def covariance(X) -> np.ndarray:
     return F
 
 
-def running_average(F, Fb, decay, first) -> np.ndarray:
+def running_average(F, Fb, xi, first) -> np.ndarray:
     F = _f64(F).copy()
     Fb = _f64(Fb)
-    lib().orc_running_average(_d(F), _d(Fb), F.shape[0], float(decay), int(bool(first)))
+    lib().orc_running_average(_d(F), _d(Fb), F.shape[0], float(xi), int(bool(first)))
     return F
 
 
-def update_factors(layers, acts, gouts, A=None, G=None, decay=0.95, first=True):
+def update_factors(layers, acts, gouts, A=None, G=None, xi=0.95, first=True):
     """Returns (A list, G list) in fp64 after one running-average update."""
     nl = len(layers)
     acts = [_f32(a) for a in acts]
@@ -128,7 +128,7 @@ def update_factors(layers, acts, gouts, A=None, G=None, decay=0.95, first=True):
     G = [np.zeros((l.d_g, l.d_g)) if G is None else _f64(G[i]).copy() for i, l in enumerate(layers)]
     arr = (_Layer * nl)(*[_layer(l) for l in layers])
     lib().orc_update_factors(arr, nl, _ptrs(acts, _fp), _ptrs(gouts, _fp), _ptrs(A, _dp),
-                             _ptrs(G, _dp), float(decay), int(bool(first)))
+                             _ptrs(G, _dp), float(xi), int(bool(first)))
     return A, G
 
 
@@ -234,9 +234,9 @@ def assign(dims, layer_of, num_layers, world, policy):
     return owner
 
 
-def full_step(layers, acts, gouts, grads, damping, lr, kappa, mode=EIGEN, decay=0.95):
+def full_step(layers, acts, gouts, grads, damping, lr, kappa, mode=EIGEN, xi=0.95):
     """One full K-FAC update from a cold state (Alg. 1 steps 1-3 + Eq. 18)."""
-    A, G = update_factors(layers, acts, gouts, decay=decay, first=True)
+    A, G = update_factors(layers, acts, gouts, xi=xi, first=True)
     if mode == INVERSE:
         QA = [damped_inverse(a, damping) for a in A]
         QG = [damped_inverse(g, damping) for g in G]

@@ -77,17 +77,17 @@ void orc_covariance(const double *X, int64_t n, int32_t d, double *F) {
     finish_covariance(F, d, n);
 }
 
-/* Eqs. 16-17 with `decay` the weight on the previous value (R5);
+/* Eqs. 16-17: xi weights the new batch estimate, 1 - xi the previous value (R5);
  * the first observation seeds the average. */
-void orc_running_average(double *F, const double *Fb, int32_t d, double decay, int32_t first) {
+void orc_running_average(double *F, const double *Fb, int32_t d, double xi, int32_t first) {
     int64_t m = (int64_t)d * d;
     for (int64_t i = 0; i < m; ++i)
-        F[i] = first ? Fb[i] : decay * F[i] + (1.0 - decay) * Fb[i];
+        F[i] = first ? Fb[i] : xi * Fb[i] + (1.0 - xi) * F[i];
 }
 
 void orc_update_factors(const orc_layer_t *layers, int32_t nl, const float *const *act,
                         const float *const *gout, double *const *A, double *const *G,
-                        double decay, int32_t first) {
+                        double xi, int32_t first) {
 #pragma omp parallel for schedule(dynamic, 1)
     for (int32_t l = 0; l < 2 * nl; ++l) {
         const orc_layer_t *L = &layers[l / 2];
@@ -105,7 +105,7 @@ void orc_update_factors(const orc_layer_t *layers, int32_t nl, const float *cons
             accumulate_outer(x, d, S);
         }
         finish_covariance(S, d, n);
-        orc_running_average(l % 2 == 0 ? A[l / 2] : G[l / 2], S, d, decay, first);
+        orc_running_average(l % 2 == 0 ? A[l / 2] : G[l / 2], S, d, xi, first);
         free(S);
         free(x);
     }

@@ -41,14 +41,14 @@ void orc_im2col(const orc_layer_t *L, const float *act, double *X);
 void orc_covariance(const double *X, int64_t n, int32_t d, double *F);
 
 /* Running average, Eqs. 16-17 read as R5:
- * F = first ? F_batch : decay*F + (1-decay)*F_batch. */
-void orc_running_average(double *F, const double *Fbatch, int32_t d, double decay, int32_t first);
+ * F = first ? F_batch : xi*F_batch + (1-xi)*F  (xi: weight on the new batch estimate). */
+void orc_running_average(double *F, const double *Fbatch, int32_t d, double xi, int32_t first);
 
 /* Stage 1 for a set of layers (act NHWC fp32, gout rows x C_out fp32).
  * A[l] (d_A x d_A), G[l] (d_G x d_G) row-major doubles updated in place. */
 void orc_update_factors(const orc_layer_t *layers, int32_t nl, const float *const *act,
                         const float *const *gout, double *const *A, double *const *G,
-                        double decay, int32_t first);
+                        double xi, int32_t first);
 
 /* Symmetric eigendecomposition of (F+F^T)/2 (Alg. 1):
  * Householder tridiagonalisation (Golub & Van Loan Alg. 8.3.1) then implicit

@@ -146,7 +146,7 @@ def kfac_layer_dims(layer):
 
 
 def kfac_update_factors(layers, acts: List[torch.Tensor], gouts: List[torch.Tensor],
-                        A: List[torch.Tensor], G: List[torch.Tensor], decay: float, first: bool,
+                        A: List[torch.Tensor], G: List[torch.Tensor], xi: float, first: bool,
                         out_scale: float = 1.0, ws: Optional[Workspace] = None, stream=None,
                         packed_A: Optional[List[torch.Tensor]] = None, packed_G: Optional[List[torch.Tensor]] = None):
     n = len(layers)
@@ -157,7 +157,7 @@ def kfac_update_factors(layers, acts: List[torch.Tensor], gouts: List[torch.Tens
                                    _ptrs(G), _i32([_ld(g) for g in G]),
                                    _ptrs(packed_A) if packed_A is not None else None,
                                    _ptrs(packed_G) if packed_G is not None else None,
-                                   float(decay), int(bool(first)),
+                                   float(xi), int(bool(first)),
                                    float(out_scale), C.c_void_p(buf.data_ptr()), buf.numel(),
                                    _stream(stream)), "kfac_update_factors")
 

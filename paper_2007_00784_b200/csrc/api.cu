@@ -16,7 +16,7 @@ size_t factors_workspace_bytes(const kfac_layer_t *layers, int nl);
 kfac_status_t factors_run(const kfac_layer_t *layers, int nl, const float *const *act,
                           const float *const *gout, float *const *A, const int32_t *ldA,
                           float *const *G, const int32_t *ldG, float *const *pA, float *const *pG,
-                          float decay, int first, float out_scale, void *ws, cudaStream_t s);
+                          float xi, int first, float out_scale, void *ws, cudaStream_t s);
 kfac_status_t unpack_run(const float *const *packed, const int32_t *dims, float *const *F, const int32_t *ldF,
                          int count, cudaStream_t s);
 size_t eigen_workspace_bytes(const int32_t *dims, int count);
@@ -192,12 +192,12 @@ kfac_status_t kfac_update_factors(const kfac_layer_t *layers, int32_t num_layers
                                   const float *const *act, const float *const *gout,
                                   float *const *A, const int32_t *ld_A, float *const *G,
                                   const int32_t *ld_G, float *const *packed_A, float *const *packed_G,
-                                  float decay, int32_t first, float out_scale,
+                                  float xi, int32_t first, float out_scale,
                                   void *ws, size_t ws_bytes, kfac_stream_t stream) {
     KFAC_CHECK_ARG(layers && act && gout && A && ld_A && G && ld_G, KFAC_ERR_INVALID_VALUE,
                    "kfac_update_factors: NULL argument");
     KFAC_CHECK_ARG(num_layers > 0, KFAC_ERR_INVALID_VALUE, "kfac_update_factors: num_layers <= 0");
-    KFAC_CHECK_ARG(decay >= 0.f && decay <= 1.f, KFAC_ERR_INVALID_VALUE, "decay %g not in [0,1]", decay);
+    KFAC_CHECK_ARG(xi >= 0.f && xi <= 1.f, KFAC_ERR_INVALID_VALUE, "xi %g not in [0,1]", xi);
     KFAC_CHECK_ARG(out_scale == out_scale, KFAC_ERR_INVALID_VALUE, "out_scale is NaN");
     for (int l = 0; l < num_layers; ++l) {
         const kfac_layer_t &L = layers[l];
@@ -213,7 +213,7 @@ kfac_status_t kfac_update_factors(const kfac_layer_t *layers, int32_t num_layers
     }
     RET_IF(check_ws(ws, ws_bytes, factors_workspace_bytes(layers, num_layers), "kfac_update_factors"));
     RET_IF(check_device());
-    return factors_run(layers, num_layers, act, gout, A, ld_A, G, ld_G, packed_A, packed_G, decay,
+    return factors_run(layers, num_layers, act, gout, A, ld_A, G, ld_G, packed_A, packed_G, xi,
                        first ? 1 : 0, out_scale, ws, reinterpret_cast<cudaStream_t>(stream));
 }
 

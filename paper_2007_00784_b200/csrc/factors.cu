@@ -2,7 +2,7 @@
 //
 //   A_batch = X^T X / n, X = [im2col(a_{i-1}) | 1]   (Eq. 5; im2col fused into the loads)
 //   G_batch = g^T g / n                                (Eq. 5)
-//   F = first ? F_batch : decay F + (1 - decay) F_batch;  F *= out_scale   (Eqs. 16-17, R5)
+//   F = first ? F_batch : xi F_batch + (1 - xi) F;  F *= out_scale   (Eqs. 16-17, R5)
 //
 // Two launches per group of factors:
 //   syrk_partial : one CTA per (upper-triangle 128x128 tile, row chunk); im2col patches are
@@ -26,7 +26,7 @@ constexpr int kMaxJobs = 64;
 
 struct FactorBatch {
     int count;
-    float decay, out_scale;
+    float xi, out_scale;  // xi: weight on the new batch estimate
     int first;
     FactorJob j[kMaxJobs];
 };
@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(256) syrk_reduce_kernel(const __grid_constant_
         float v = s * inv_n;
         if (gi < J.d && gj < J.d) {
             float *dst = J.F + (size_t)gi * J.ldF + gj;
-            if (!batch.first) v = batch.decay * (*dst) + (1.f - batch.decay) * v;
+            if (!batch.first) v = batch.xi * v + (1.f - batch.xi) * (*dst);
             v *= batch.out_scale;
             *dst = v;
             if (J.packed && gi <= gj)            // each upper entry once: row gi starts at gi d - gi (gi - 1) / 2
@@ -278,7 +278,7 @@ size_t factors_workspace_bytes(const kfac_layer_t *layers, int nl) {
 kfac_status_t factors_run(const kfac_layer_t *layers, int nl, const float *const *act,
                           const float *const *gout, float *const *A, const int32_t *ldA,
                           float *const *G, const int32_t *ldG, float *const *pA, float *const *pG,
-                          float decay, int first, float out_scale, void *ws, cudaStream_t s) {
+                          float xi, int first, float out_scale, void *ws, cudaStream_t s) {
     Plan p = make_plan(layers, nl, A, ldA, G, ldG, act, gout, pA, pG);
     float *base = reinterpret_cast<float *>(round_up(reinterpret_cast<uintptr_t>(ws), 256));
     for (auto &j : p.jobs) j.partial = base + reinterpret_cast<uintptr_t>(j.partial);
@@ -323,7 +323,7 @@ kfac_status_t factors_run(const kfac_layer_t *layers, int nl, const float *const
     for (size_t b0 = 0; b0 < p.jobs.size(); b0 += kMaxJobs) {
         FactorBatch fb;
         fb.count = 0;
-        fb.decay = decay;
+        fb.xi = xi;
         fb.out_scale = out_scale;
         fb.first = first;
         int subtiles = 0;

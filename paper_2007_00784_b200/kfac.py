@@ -77,14 +77,14 @@ def supported(m: nn.Module) -> bool:
 
 
 class KFAC:
-    def __init__(self, model: nn.Module, lr: float = 0.1, damping: float = 1e-3, decay: float = 0.95,
+    def __init__(self, model: nn.Module, lr: float = 0.1, damping: float = 1e-3, xi: float = 0.95,
                  kappa: float = 1e-3, kfac_update_freq: int = 10, factor_update_freq: int = 1,
                  damping_decay_steps: Sequence[int] = (), damping_decay_rate: float = 0.5,
                  update_freq_decay_steps: Sequence[int] = (), update_freq_decay_rate: float = 1.0,
                  variant: str = "eigen", exchange: str = "bcast-eig", grad_scale: str = "batch",
                  process_group=None, skip_modules: Sequence[nn.Module] = ()):
         self.model = model
-        self.lr, self.damping, self.decay, self.kappa = lr, damping, decay, kappa
+        self.lr, self.damping, self.xi, self.kappa = lr, damping, xi, kappa
         self.kfac_update_freq, self.factor_update_freq = int(kfac_update_freq), int(factor_update_freq)
         self.damping_decay_steps = set(int(s) for s in damping_decay_steps)
         self.damping_decay_rate = damping_decay_rate
@@ -158,7 +158,7 @@ class KFAC:
 
     # -------------------------------------------------------------------- step --
     def _build(self, descs):
-        self.pc = KFACPreconditioner(descs, damping=self.damping, decay=self.decay, kappa=self.kappa, lr=self.lr,
+        self.pc = KFACPreconditioner(descs, damping=self.damping, xi=self.xi, kappa=self.kappa, lr=self.lr,
                                      variant=self.variant, exchange=self.exchange, process_group=self.process_group)
         self._grads, self._grad_flat = KFACPreconditioner.grad_buffer(descs, self.pc.device, return_flat=True)
 

@@ -56,13 +56,13 @@ def _views(flat: torch.Tensor, segs: List[Segment]) -> List[torch.Tensor]:
 
 
 class KFACPreconditioner:
-    def __init__(self, layers, device=None, damping: float = 1e-3, decay: float = 0.95,
+    def __init__(self, layers, device=None, damping: float = 1e-3, xi: float = 0.95,
                  kappa: float = 1e-3, lr: float = 0.1, variant: str = "eigen",
                  exchange: str = "bcast-eig", assign_policy: int = _lib.LPT_D3,
                  process_group=None):
         self.layers = list(layers)
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-        self.damping, self.decay, self.kappa, self.lr = damping, decay, kappa, lr
+        self.damping, self.xi, self.kappa, self.lr = damping, xi, kappa, lr
         assert variant in ("eigen", "factored", "inverse")
         assert exchange in ("bcast-eig", "allgather-grad")
         self.variant, self.exchange = variant, exchange
@@ -171,14 +171,14 @@ class KFACPreconditioner:
         communication stream as soon as its factor kernels are done, overlapping the next bucket's
         kernels.  Then both triangles are restored from the reduced packed buffer."""
         if self.world == 1:
-            _lib.kfac_update_factors(self.layers, acts, gouts, self.A, self.G, self.decay, first,
+            _lib.kfac_update_factors(self.layers, acts, gouts, self.A, self.G, self.xi, first,
                                      1.0, ws=self.ws["factors"])
             return
         compute = torch.cuda.current_stream(self.device) if self.comm_stream is not None else None
         works = []
         for b0, b1 in self.buckets():
             _lib.kfac_update_factors(self.layers[b0:b1], acts[b0:b1], gouts[b0:b1], self.A[b0:b1], self.G[b0:b1],
-                                     self.decay, first, 1.0 / self.world, ws=self.ws["factors"],
+                                     self.xi, first, 1.0 / self.world, ws=self.ws["factors"],
                                      packed_A=self.packed[2 * b0:2 * b1:2], packed_G=self.packed[2 * b0 + 1:2 * b1:2])
             lo = self.packed_seg[2 * b0][0]
             hi = self.packed_seg[2 * b1 - 1][0] + self.packed_seg[2 * b1 - 1][1]

@@ -27,7 +27,7 @@ a = ap.parse_args()
 layers = shapes.layers_for(a.config)
 hp = shapes.HPARAMS[a.config]
 acts, gouts, _ = layer_inputs(layers, seed=0, device="cuda")
-pc = KFACPreconditioner(layers, damping=hp["damping"], decay=hp["decay"])
+pc = KFACPreconditioner(layers, damping=hp["damping"], xi=hp["xi"])
 pc.update_factors([torch.from_numpy(x).cuda() for x in acts], [torch.from_numpy(x).cuda() for x in gouts], True)
 torch.cuda.synchronize()
 dims, layer_of = pc.dims, pc.layer_of

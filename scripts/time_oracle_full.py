@@ -28,7 +28,7 @@ def main(cfg):
     t_gen = time.perf_counter()
     acts, gouts, grads = layer_inputs(layers, seed=0)
     t0 = time.perf_counter()
-    A, G = oracle.update_factors(layers, acts, gouts, decay=hp["decay"], first=True)
+    A, G = oracle.update_factors(layers, acts, gouts, xi=hp["xi"], first=True)
     t1 = time.perf_counter()
     Qs, vs = oracle.symeig_batch(A + G)
     t2 = time.perf_counter()

@@ -54,7 +54,7 @@ def _worker(rank, world, port, exchange, out_dir):
         from paper_2007_00784_b200.preconditioner import KFACPreconditioner
         layers_r, _, shards, _, _, grads = _global_inputs(world)
         hp = shapes.HPARAMS["r32"]
-        pc = KFACPreconditioner(layers_r, device="cuda:0", damping=hp["damping"], decay=hp["decay"],
+        pc = KFACPreconditioner(layers_r, device="cuda:0", damping=hp["damping"], xi=hp["xi"],
                                 kappa=hp["kappa"], lr=hp["lr"], exchange=exchange)
         g = KFACPreconditioner.grad_buffer(layers_r, "cuda:0")
         for t, w in zip(g, grads):

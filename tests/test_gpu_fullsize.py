@@ -42,7 +42,7 @@ def _factors(layers, seed):
     """Running factors of one cold update (first = True) from the seeded inputs, on the GPU."""
     from paper_2007_00784_b200.preconditioner import KFACPreconditioner
     hp = shapes.HPARAMS["r50"]
-    pc = KFACPreconditioner(layers, damping=hp["damping"], decay=hp["decay"], kappa=1e12, lr=hp["lr"])
+    pc = KFACPreconditioner(layers, damping=hp["damping"], xi=hp["xi"], kappa=1e12, lr=hp["lr"])
     acts, gouts, _ = layer_inputs(layers, seed=seed, with_grad=False)
     pc.update_factors([torch.from_numpy(a).cuda() for a in acts], [torch.from_numpy(g).cuda() for g in gouts],
                       first=True)
@@ -107,7 +107,7 @@ def test_full_size_r50_3x3_layer_vs_oracle(L, name):
     lay = {l.name: l for l in shapes.resnet50()}[name]
     hp = shapes.HPARAMS["r50"]
     acts, gouts, grads = layer_inputs([lay], seed=int(g["seed"]))
-    pc = KFACPreconditioner([lay], damping=hp["damping"], decay=hp["decay"], kappa=1e12, lr=hp["lr"])
+    pc = KFACPreconditioner([lay], damping=hp["damping"], xi=hp["xi"], kappa=1e12, lr=hp["lr"])
     gb = KFACPreconditioner.grad_buffer([lay], "cuda")
     gb[0].copy_(torch.from_numpy(grads[0]))
     P = pc.step([torch.from_numpy(acts[0]).cuda()], [torch.from_numpy(gouts[0]).cuda()], gb, first=True)

@@ -48,8 +48,8 @@ def test_kfac_model_step_matches_oracle(orc):
     net = Net().cuda()
     x = torch.randn(6, 3, 8, 8, device="cuda")
     y = torch.randint(0, 10, (6,), device="cuda")
-    hp = dict(damping=3e-3, decay=0.95, kappa=1e-3, lr=0.1)
-    kfac = KFAC(net, lr=hp["lr"], damping=hp["damping"], decay=hp["decay"], kappa=hp["kappa"])
+    hp = dict(damping=3e-3, xi=0.95, kappa=1e-3, lr=0.1)
+    kfac = KFAC(net, lr=hp["lr"], damping=hp["damping"], xi=hp["xi"], kappa=hp["kappa"])
     rec = {}
     mods = [net.c1, net.c2, net.fc]
     hooks = [m.register_forward_pre_hook(lambda m, i: rec.__setitem__((id(m), "a"), i[0].detach().clone()))

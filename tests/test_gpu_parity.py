@@ -169,15 +169,15 @@ def test_update_factors_first_and_running_average(L, orc):
     G = [empty(l.d_g, l.d_g) for l in layers]
     L.kfac_update_factors(layers, [torch.from_numpy(a).cuda() for a in a1],
                           [torch.from_numpy(g).cuda() for g in g1], A, G, 0.95, True, 1.0)
-    rA, rG = orc.update_factors(layers, a1, g1, decay=0.95, first=True)
+    rA, rG = orc.update_factors(layers, a1, g1, xi=0.95, first=True)
     torch.cuda.synchronize()
     for x, r in zip(A + G, rA + rG):
         assert relF(host(x), r) <= 1e-5
         assert np.array_equal(host(x), host(x).T)                  # both triangles, bitwise symmetric
-    # second call: running average with decay 0.95 and out_scale 0.5 (1/W before an allreduce-SUM)
+    # second call: running average with xi 0.95 and out_scale 0.5 (1/W before an allreduce-SUM)
     L.kfac_update_factors(layers, [torch.from_numpy(a).cuda() for a in a2],
                           [torch.from_numpy(g).cuda() for g in g2], A, G, 0.95, False, 0.5)
-    rA, rG = orc.update_factors(layers, a2, g2, A=rA, G=rG, decay=0.95, first=False)
+    rA, rG = orc.update_factors(layers, a2, g2, A=rA, G=rG, xi=0.95, first=False)
     torch.cuda.synchronize()
     for x, r in zip(A + G, rA + rG):
         assert relF(host(x), 0.5 * r) <= 1e-5
@@ -236,7 +236,7 @@ def test_compute_inverse_reports_not_spd(L):
 # ------------------------------------------------------------- full chains --
 def _full_chain(L, layers, acts, gouts, grads, hp, variant="eigen"):
     from paper_2007_00784_b200.preconditioner import KFACPreconditioner
-    pc = KFACPreconditioner(layers, damping=hp["damping"], decay=hp["decay"], kappa=hp["kappa"],
+    pc = KFACPreconditioner(layers, damping=hp["damping"], xi=hp["xi"], kappa=hp["kappa"],
                             lr=hp["lr"], variant=variant)
     g = KFACPreconditioner.grad_buffer(layers, "cuda")
     for t, w in zip(g, grads):

@@ -84,7 +84,7 @@ def test_update_factors_conv_and_linear(orc):
     rng = np.random.default_rng(2)
     acts = [rng.standard_normal(l.act_shape).astype(np.float32) for l in layers]
     gouts = [rng.standard_normal(l.gout_shape).astype(np.float32) for l in layers]
-    A, G = orc.update_factors(layers, acts, gouts, decay=0.95, first=True)
+    A, G = orc.update_factors(layers, acts, gouts, xi=0.95, first=True)
     for l, a, g, Af, Gf in zip(layers, acts, gouts, A, G):
         X = orc.im2col(l, a)
         n = l.rows
@@ -95,16 +95,22 @@ def test_update_factors_conv_and_linear(orc):
 
 
 def test_running_average_rules(orc):
-    """Eqs. 16-17 (P:383-386) read as R5: decay 0 -> batch; first -> batch (S:195);
-    constant batch -> geometric convergence |F_k - B| = decay^k |F_0 - B|."""
+    """Eqs. 16-17: xi weights the new batch estimate.  S:190 examples: xi = 1 -> the
+    batch estimate exactly; the first call seeds F = batch; a constant batch B is approached
+    geometrically, |F_k - B| = (1 - xi)^k |F_0 - B|; and one step is the convex combination
+    with weight xi on the batch (checked against the endpoints, not the formula)."""
     B = random_spd(6, 3)
     F0 = random_spd(6, 4)
-    assert np.array_equal(orc.running_average(F0, B, 0.0, False), B)
+    assert np.array_equal(orc.running_average(F0, B, 1.0, False), B)
     assert np.array_equal(orc.running_average(F0, B, 0.95, True), B)
+    assert np.array_equal(orc.running_average(F0, B, 0.0, False), F0)
     F = F0
     for k in range(1, 8):
         F = orc.running_average(F, B, 0.9, False)
-        assert np.isclose(np.linalg.norm(F - B), 0.9 ** k * np.linalg.norm(F0 - B), rtol=1e-9)
+        assert np.isclose(np.linalg.norm(F - B), 0.1 ** k * np.linalg.norm(F0 - B), rtol=1e-9)
+    F1 = orc.running_average(F0, B, 0.95, False)
+    assert np.isclose(np.linalg.norm(F1 - B), 0.05 * np.linalg.norm(F0 - B), rtol=1e-12)
+    assert np.isclose(np.linalg.norm(F1 - F0), 0.95 * np.linalg.norm(B - F0), rtol=1e-12)
 
 
 def test_factor_average_over_ranks_is_global_batch(orc):

@@ -146,14 +146,14 @@ CONFIGS = {
     "r152": resnet152,
 }
 
-# Hyper-parameters per config: damping gamma, decay (weight
-# on the previous running factor, reading R5), kappa, lr.
+# Hyper-parameters per config: damping gamma, xi (weight
+# on the new batch estimate, reading R5), kappa, lr.
 HPARAMS = {
-    "mlp": dict(damping=3e-3, decay=0.95, kappa=1e-3, lr=0.1),
-    "r32": dict(damping=3e-3, decay=0.95, kappa=1e-3, lr=0.1),      # lr = W*0.1
-    "r50": dict(damping=1e-3, decay=0.95, kappa=1e-3, lr=0.0125),   # gamma P:542/P:610; lr W*0.0125
-    "r101": dict(damping=1e-3, decay=0.95, kappa=1e-3, lr=0.0125),
-    "r152": dict(damping=1e-3, decay=0.95, kappa=1e-3, lr=0.0125),
+    "mlp": dict(damping=3e-3, xi=0.95, kappa=1e-3, lr=0.1),
+    "r32": dict(damping=3e-3, xi=0.95, kappa=1e-3, lr=0.1),      # lr = W*0.1
+    "r50": dict(damping=1e-3, xi=0.95, kappa=1e-3, lr=0.0125),   # gamma P:542/P:610; lr W*0.0125
+    "r101": dict(damping=1e-3, xi=0.95, kappa=1e-3, lr=0.0125),
+    "r152": dict(damping=1e-3, xi=0.95, kappa=1e-3, lr=0.0125),
 }
 
 
