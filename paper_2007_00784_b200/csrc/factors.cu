@@ -181,7 +181,18 @@ __global__ void __launch_bounds__(NT) syrk_partial_kernel(const __grid_constant_
     }
 }
 
-// One CTA (32x8 threads) per 32x32 sub-tile of an upper 128x128 tile.
+// Column of the SYRK's (possibly channel-padded) geometry that holds column c of the real factor.
+__device__ __forceinline__ int padded_col(const FactorJob &J, int c) {
+    if (!J.c_real || !J.is_a) return c;                  // no padding, or padding after the last column
+    const int patch_real = J.c_real * (J.patch_cols / J.c_in);
+    if (c >= patch_real) return J.patch_cols;            // bias column
+    return (c / J.c_real) * J.c_in + c % J.c_real;
+}
+
+// Upper-tile index of tile (ti, tj), ti <= tj, in a t1d x t1d tile grid.
+__device__ __forceinline__ int upper_index(int ti, int tj, int t1d) { return ti * t1d - ti * (ti - 1) / 2 + (tj - ti); }
+
+// One CTA (32x8 threads) per 32x32 sub-tile of an upper 128x128 tile of the real factor.
 __global__ void __launch_bounds__(256) syrk_reduce_kernel(const __grid_constant__ FactorBatch batch) {
     __shared__ float tr[32][33];
     const int blk = blockIdx.x;                  // tile_begin counts sub-tiles (16 per tile)
@@ -189,28 +200,32 @@ __global__ void __launch_bounds__(256) syrk_reduce_kernel(const __grid_constant_
     const int local = blk - J.tile_begin;
     const int tau = local / 16, sub = local % 16;
     int ti, tj;
-    upper_tile(tau, J.t1d, ti, tj);
+    upper_tile(tau, J.t1d_out, ti, tj);
     const int si = sub / 4, sj = sub % 4;
     if (ti == tj && si > sj) return;             // the (sj, si) sub-tile writes both copies
     const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;
     const float inv_n = 1.0f / (float)J.n;
+    const int d = J.d_out;
     const int gj = tj * T + sj * 32 + tx;
     for (int rr = ty; rr < 32; rr += 8) {
         const int li = si * 32 + rr, lj = sj * 32 + tx;
         const int gi = ti * T + li;
         // diagonal tiles: read the upper entry for both (i, j) and (j, i) -> exact symmetry
-        const int pi = (ti == tj && li > lj) ? lj : li, pj = (ti == tj && li > lj) ? li : lj;
-        float s = 0.f;
-        for (int sp = 0; sp < J.splits; ++sp)
-            s += J.partial[((size_t)sp * J.tiles + tau) * (T * T) + pi * T + pj];
-        float v = s * inv_n;
-        if (gi < J.d && gj < J.d) {
+        const bool swap = ti == tj && li > lj;
+        const int ui = swap ? gj : gi, uj = swap ? gi : gj;       // ui <= uj (real columns)
+        float v = 0.f;
+        if (gi < d && gj < d) {
+            const int mi = padded_col(J, ui), mj = padded_col(J, uj);   // monotone: mi <= mj
+            const size_t off = (size_t)upper_index(mi / T, mj / T, J.t1d) * (T * T) + (mi % T) * T + (mj % T);
+            float s = 0.f;
+            for (int sp = 0; sp < J.splits; ++sp) s += J.partial[(size_t)sp * J.tiles * (T * T) + off];
+            v = s * inv_n;
             float *dst = J.F + (size_t)gi * J.ldF + gj;
             if (!batch.first) v = batch.xi * v + (1.f - batch.xi) * (*dst);
             v *= batch.out_scale;
             *dst = v;
             if (J.packed && gi <= gj)            // each upper entry once: row gi starts at gi d - gi (gi - 1) / 2
-                J.packed[(long long)gi * J.d - (long long)gi * (gi - 1) / 2 + (gj - gi)] = v;
+                J.packed[(long long)gi * d - (long long)gi * (gi - 1) / 2 + (gj - gi)] = v;
         }
         tr[rr][tx] = v;
     }
@@ -219,7 +234,7 @@ __global__ void __launch_bounds__(256) syrk_reduce_kernel(const __grid_constant_
     const int gcol = ti * T + si * 32 + tx;      // mirrored write: F[gj][gi]
     for (int rr = ty; rr < 32; rr += 8) {
         const int grow = tj * T + sj * 32 + rr;
-        if (grow < J.d && gcol < J.d) J.F[(size_t)grow * J.ldF + gcol] = tr[tx][rr];
+        if (grow < d && gcol < d) J.F[(size_t)grow * J.ldF + gcol] = tr[tx][rr];
     }
 }
 
@@ -257,6 +272,23 @@ Plan make_plan(const kfac_layer_t *layers, int nl, float *const *A, const int32_
             j.bias_col = L.bias_col;
             j.chunk = kChunkRows;
             j.splits = (int)((j.n + kChunkRows - 1) / kChunkRows);
+            j.d_out = j.d;
+            j.t1d_out = cdiv(j.d, T);
+            j.tiles_out = j.t1d_out * (j.t1d_out + 1) / 2;
+            if (j.d >= 64 && j.n >= 32 && j.c_in % 4 != 0) {
+                // tensor-core SYRK on zero-padded channels (the fold gathers the real columns);
+                // kept only if the padded job is one the tensor-core engine takes
+                FactorJob pj = j;
+                pj.c_real = j.c_in;
+                pj.c_in = (int)round_up((size_t)j.c_in, 4);
+                if (pj.is_a) {
+                    pj.patch_cols = pj.c_in * L.k_h * L.k_w;
+                    pj.d = pj.patch_cols + L.bias_col;
+                } else {
+                    pj.d = pj.c_in;
+                }
+                if (syrk_tc_supported(pj)) j = pj;
+            }
             j.t1d = cdiv(j.d, T);
             j.tiles = j.t1d * (j.t1d + 1) / 2;
             j.partial = reinterpret_cast<float *>(p.partial_floats);   // offset, rebased later
@@ -292,9 +324,9 @@ kfac_status_t factors_run(const kfac_layer_t *layers, int nl, const float *const
         std::vector<SplitJob> sj;
         for (auto &j : tc) {
             const size_t e = round_up((size_t)input_elems(j), 64);
-            const int cols = j.c_in;
-            const int rows = (int)(input_elems(j) / cols);
-            sj.push_back({j.src, pl, pl + e, rows, cols, cols, cols});
+            const int cols = j.c_real ? j.c_real : j.c_in;     // padded jobs: zero channels appended
+            const int rows = (int)(input_elems(j) / j.c_in);
+            sj.push_back({j.src, pl, pl + e, rows, cols, cols, j.c_in});
             j.src = pl;
             j.src_lo = pl + e;
             pl += 2 * e;
@@ -330,7 +362,7 @@ kfac_status_t factors_run(const kfac_layer_t *layers, int nl, const float *const
         for (size_t i = b0; i < p.jobs.size() && fb.count < kMaxJobs; ++i) {
             FactorJob j = p.jobs[i];
             j.tile_begin = subtiles;
-            subtiles += j.tiles * 16;
+            subtiles += j.tiles_out * 16;
             fb.j[fb.count++] = j;
         }
         syrk_reduce_kernel<<<subtiles, 256, 0, s>>>(fb);

@@ -336,8 +336,14 @@ __global__ void __launch_bounds__(256) split_planes_kernel(const __grid_constant
         const int w4 = J.ld_dst / 4;
         const long long r = v / w4;
         const int c = (int)(v - r * w4) * 4;
-        const float4 x4 = __ldg(reinterpret_cast<const float4 *>(J.src + r * J.ld_src + c));
-        float x[4] = {x4.x, x4.y, x4.z, x4.w}, h[4], l[4];
+        float x[4], h[4], l[4];
+        if (J.ld_src >= J.ld_dst) {
+            const float4 x4 = __ldg(reinterpret_cast<const float4 *>(J.src + r * J.ld_src + c));
+            x[0] = x4.x; x[1] = x4.y; x[2] = x4.z; x[3] = x4.w;
+        } else {                                   // rows padded with zero columns (ld_dst > cols)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) x[e] = c + e < J.cols ? __ldg(J.src + r * J.ld_src + c + e) : 0.f;
+        }
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
             const float xe = c + e < J.cols ? x[e] : 0.f;
@@ -705,8 +711,11 @@ kfac_status_t split_planes(const SplitJob *jobs, int count, cudaStream_t s) {
         long long units = 0;
         for (int i = base; i < count && b.count < 64; ++i) {
             const SplitJob &J = jobs[i];
-            KFAC_CHECK_ARG(J.ld_dst % 4 == 0 && J.ld_src % 4 == 0 && J.ld_dst <= J.ld_src && J.cols <= J.ld_dst &&
-                               aligned16(J.src) && aligned16(J.hi) && aligned16(J.lo),
+            // destination rows 16-byte aligned; source rows too unless they are padded (ld_src < ld_dst:
+            // zero columns appended, scalar loads)
+            const bool padded = J.ld_src < J.ld_dst;
+            KFAC_CHECK_ARG(J.ld_dst % 4 == 0 && J.cols <= J.ld_dst && J.cols <= J.ld_src && aligned16(J.hi) &&
+                               aligned16(J.lo) && (padded || (J.ld_src % 4 == 0 && aligned16(J.src))),
                            KFAC_ERR_ALIGNMENT, "split_planes: rows must be 16-byte aligned");
             b.j[b.count] = J;
             b.unit_begin[b.count] = units;

@@ -112,6 +112,11 @@ struct FactorJob {
     int splits, chunk, t1d, tiles, item_begin, tile_begin;
     int c_in, h_in, w_in, h_out, w_out, k_w, stride_h, stride_w, pad_h, pad_w;  // G: c_in = row length
     int patch_cols, bias_col;
+    // Row length not a multiple of 4 (e.g. ResNet conv1, C_in = 3): the tensor-core SYRK runs on a
+    // copy padded with zero channels to c_in (multiple of 4) -- d, t1d, tiles, c_in and patch_cols
+    // above describe that padded geometry -- and the fold maps the real factor's columns into it.
+    int c_real;             // real row length / channel count (0: no padding)
+    int d_out, t1d_out, tiles_out;   // geometry of the real factor F (== d, t1d, tiles unpadded)
 };
 
 // Tensor-core (tcgen05 3xTF32) partial SYRK for the jobs it supports (row length % 4 == 0).

@@ -158,6 +158,8 @@ FACTOR_LAYERS = [
     shapes.linear("fc2", 5000, 20, 10),                  # 2 row chunks
     shapes.conv("c3big", 2, 64, 128, 3, 2, 30),          # tcgen05 path, im2col stride 2 + padding, d_A 577
     shapes.conv("c1big", 4, 256, 64, 1, 1, 36),          # tcgen05 path, 5184 rows = 2 row chunks
+    shapes.conv("c7s2c3", 2, 3, 64, 7, 2, 40),           # C_in = 3 (ResNet conv1 shape): channel-padded
+    shapes.conv("c5c5", 3, 5, 70, 5, 1, 14),             # C_in = 5, d_A 126, d_G 70: both padded
 ]
 
 
