@@ -194,6 +194,7 @@ kfac_status_t kfac_update_factors(const kfac_layer_t *layers, int32_t num_layers
                                   const int32_t *ld_G, float *const *packed_A, float *const *packed_G,
                                   float xi, int32_t first, float out_scale,
                                   void *ws, size_t ws_bytes, kfac_stream_t stream) {
+    kfac::NvtxRange nvtx_range("kfac_update_factors");
     KFAC_CHECK_ARG(layers && act && gout && A && ld_A && G && ld_G, KFAC_ERR_INVALID_VALUE,
                    "kfac_update_factors: NULL argument");
     KFAC_CHECK_ARG(num_layers > 0, KFAC_ERR_INVALID_VALUE, "kfac_update_factors: num_layers <= 0");
@@ -219,6 +220,7 @@ kfac_status_t kfac_update_factors(const kfac_layer_t *layers, int32_t num_layers
 
 kfac_status_t kfac_unpack_factors(const float *const *packed, const int32_t *dims, float *const *F,
                                   const int32_t *ld_F, int32_t count, kfac_stream_t stream) {
+    kfac::NvtxRange nvtx_range("kfac_unpack_factors");
     KFAC_CHECK_ARG(packed && dims && F && ld_F, KFAC_ERR_INVALID_VALUE, "kfac_unpack_factors: NULL argument");
     KFAC_CHECK_ARG(count > 0, KFAC_ERR_INVALID_VALUE, "kfac_unpack_factors: count <= 0");
     for (int i = 0; i < count; ++i) {
@@ -241,6 +243,7 @@ kfac_status_t kfac_compute_eigen(const float *const *F, const int32_t *dims, con
                                  int32_t count, float *const *Q, const int32_t *ld_Q,
                                  float *const *evals, int32_t *info, uint32_t flags, void *ws,
                                  size_t ws_bytes, kfac_stream_t stream) {
+    kfac::NvtxRange nvtx_range("kfac_compute_eigen");
     KFAC_CHECK_ARG(F && dims && ld_F && Q && ld_Q && evals, KFAC_ERR_INVALID_VALUE,
                    "kfac_compute_eigen: NULL argument");
     KFAC_CHECK_ARG(count > 0, KFAC_ERR_INVALID_VALUE, "kfac_compute_eigen: count <= 0");
@@ -272,6 +275,7 @@ kfac_status_t kfac_compute_inverse(const float *const *F, const int32_t *dims, c
                                    int32_t count, float damping, float *const *Finv,
                                    const int32_t *ld_Finv, int32_t *info, void *ws, size_t ws_bytes,
                                    kfac_stream_t stream) {
+    kfac::NvtxRange nvtx_range("kfac_compute_inverse");
     KFAC_CHECK_ARG(F && dims && ld_F && Finv && ld_Finv, KFAC_ERR_INVALID_VALUE,
                    "kfac_compute_inverse: NULL argument");
     KFAC_CHECK_ARG(count > 0, KFAC_ERR_INVALID_VALUE, "kfac_compute_inverse: count <= 0");
@@ -299,6 +303,7 @@ kfac_status_t kfac_precondition(const int32_t *d_g, const int32_t *d_a, int32_t 
                                 const int32_t *ld_QA, const float *const *v_A, float damping,
                                 int32_t mode, float *const *out, void *ws, size_t ws_bytes,
                                 kfac_stream_t stream) {
+    kfac::NvtxRange nvtx_range("kfac_precondition");
     KFAC_CHECK_ARG(d_g && d_a && grad && ld_W && Q_G && ld_QG && Q_A && ld_QA && out,
                    KFAC_ERR_INVALID_VALUE, "kfac_precondition: NULL argument");
     KFAC_CHECK_ARG(num_layers > 0, KFAC_ERR_INVALID_VALUE, "kfac_precondition: num_layers <= 0");
@@ -331,6 +336,7 @@ kfac_status_t kfac_kl_clip(float *const *precond, const float *const *grad, cons
                            const int32_t *cols, const int32_t *ld, int32_t num_layers, float lr,
                            float kappa, float *nu_out, double *s_out, void *ws, size_t ws_bytes,
                            kfac_stream_t stream) {
+    kfac::NvtxRange nvtx_range("kfac_kl_clip");
     KFAC_CHECK_ARG(precond && grad && rows && cols && ld, KFAC_ERR_INVALID_VALUE, "kfac_kl_clip: NULL argument");
     KFAC_CHECK_ARG(num_layers > 0, KFAC_ERR_INVALID_VALUE, "kfac_kl_clip: num_layers <= 0");
     KFAC_CHECK_ARG(lr > 0.f && kappa > 0.f, KFAC_ERR_INVALID_VALUE, "kfac_kl_clip: lr and kappa must be > 0");

@@ -8,6 +8,8 @@
 #include <atomic>
 #include <string>
 
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: no-ops unless a tool (ncu --nvtx) attaches
+
 #include "kfac.h"
 
 namespace kfac {
@@ -70,6 +72,15 @@ struct WsArena {
 };
 
 int num_sms();   // multiprocessor count of the current device (cached per device)
+
+// Host-side NVTX range over the launches of one stage (ncu --nvtx --nvtx-include "kfac_compute_eigen/"
+// selects a stage's kernels; names follow the C-ABI calls and the eigensolver phases).
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange &) = delete;
+    NvtxRange &operator=(const NvtxRange &) = delete;
+};
 
 // cudaFuncSetAttribute(kernel, MaxDynamicSharedMemorySize, bytes) on the current device, done once
 // per (kernel, device, bytes); thread-safe.

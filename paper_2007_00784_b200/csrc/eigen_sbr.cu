@@ -584,6 +584,7 @@ __device__ __forceinline__ double chase_interior(double *rowa, int k, int lane, 
     double wr[B];
 #pragma unroll
     for (int i = 0; i < B; ++i) wr[i] = __shfl_sync(0xffffffffu, w, i);
+    __syncwarp();                    // lanes 16..31 read these rows (d3) before lanes 0..15 write them
     if (lane < B) {
         double *Rr = rowa + L * (kBandLd + 1);
 #pragma unroll
@@ -664,6 +665,7 @@ __device__ __forceinline__ double chase_step(double *rowa, double *nxt, int lh, 
     double wr[B];
 #pragma unroll
     for (int i = 0; i < B; ++i) wr[i] = __shfl_sync(0xffffffffu, w, i);
+    __syncwarp();
     if (lane < B && ok(L)) {
 #pragma unroll
         for (int m = 0; m < B; ++m)

@@ -25,6 +25,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <optional>
 #include <vector>
 
 #define RET_OK(expr)                         \
@@ -1621,6 +1622,7 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
     KFAC_LAUNCHED();
     std::vector<Gemm64Desc> gd;
     if (mode != TRD_DEBUG_STEDC) {
+    NvtxRange nvtx_red("eigen: tridiagonal reduction");
     trd_init<<<dim3(std::min(2048, cdiv((long long)ldw_for(max_n), 32) * cdiv((long long)ldw_for(max_n), 32)), count), 256,
                0, s>>>(djobs);
     KFAC_LAUNCHED();
@@ -1737,6 +1739,8 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
         KFAC_CUDA_TRY(cudaMemcpyAsync(P.jobs[0].e, dbg_e, sizeof(double) * P.jobs[0].n, cudaMemcpyDeviceToDevice, s));
     }
     // ---- (2) divide and conquer on T ----
+    std::optional<NvtxRange> nvtx_dc;
+    nvtx_dc.emplace("eigen: divide and conquer");
     dc_tear<<<dim3(cdiv(max_n, 256), count), 256, 0, s>>>(djobs);
     KFAC_LAUNCHED();
     if (!P.leaves.empty()) {
@@ -1805,6 +1809,8 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
     }
 
     // ---- (3) back-transformation X = H Z, last block of reflectors first ----
+    nvtx_dc.reset();
+    NvtxRange nvtx_bt("eigen: back-transformation");
     if (mode != TRD_DEBUG_STEDC) {
         std::vector<int> sbr_ids;
         for (int i = 0; i < count; ++i)
