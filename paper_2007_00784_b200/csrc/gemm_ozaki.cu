@@ -199,6 +199,11 @@ __global__ void __launch_bounds__(256) ozk_slice(const __grid_constant__ OzOpBat
     const int rr = tid / 8, kseg = (tid % 8) * 16, r = r0 + rr;
     if (r >= o.R || kt0 + kseg >= o.Kp) return;
     const int e = ex[rr];
+    // 2^(7 - e) as a double built from its exponent bits (exact scaling): one multiply per element
+    // instead of ldexp; rows whose maximum is denormal (7 - e outside the normal range) keep ldexp
+    const int be = 1023 + 7 - e;
+    const bool fast = be >= 1 && be <= 2046;
+    const double scale = fast ? __longlong_as_double((long long)be << 52) : 0.0;
     uint32_t w[kOzS][4];
 #pragma unroll
     for (int s = 0; s < kOzS; ++s)
@@ -206,7 +211,7 @@ __global__ void __launch_bounds__(256) ozk_slice(const __grid_constant__ OzOpBat
         for (int q = 0; q < 4; ++q) w[s][q] = 0u;
 #pragma unroll
     for (int u = 0; u < 16; ++u) {
-        double v = ldexp(tile[rr][kseg + u], -e) * 128.0;      // exact scalings
+        double v = fast ? tile[rr][kseg + u] * scale : ldexp(tile[rr][kseg + u], 7 - e);
 #pragma unroll
         for (int s = 0; s < kOzS; ++s) {
             const double d = rint(v);
