@@ -116,7 +116,20 @@ __device__ __forceinline__ int find_op(const OzOpBatch &b, int blk) {
     return lo;
 }
 
-// max |op(X)[r][k]| over the valid range, per row; 32 rows x 256 k per CTA of 32 x 8 threads.
+// 16-byte load of op(X) elements (i, i+1) (fp64: one double2; fp32: one float2 widened).
+__device__ __forceinline__ double2 ld_pair(const OzOperand &o, size_t i) {
+    if (o.dt == DT_F64) return __ldg(reinterpret_cast<const double2 *>(static_cast<const double *>(o.X) + i));
+    const float2 f = __ldg(reinterpret_cast<const float2 *>(static_cast<const float *>(o.X) + i));
+    return make_double2((double)f.x, (double)f.y);
+}
+// pairs along the contiguous index are aligned: even leading dimension and 16-byte (fp64) / 8-byte
+// (fp32) aligned base
+__device__ __forceinline__ bool pair_ok(const OzOperand &o) {
+    return (o.ld & 1) == 0 && (reinterpret_cast<uintptr_t>(o.X) & (o.dt == DT_F64 ? 15 : 7)) == 0;
+}
+
+// max |op(X)[r][k]| over the valid range, per row; 32 rows x 256 k per CTA of 32 x 8 threads.  All of
+// a thread's loads are issued before any is used (pairs along the contiguous index when aligned).
 __global__ void __launch_bounds__(256) ozk_rowmax(const __grid_constant__ OzOpBatch b) {
     __shared__ double red[8][33];
     const OzOperand &o = b.op[find_op(b, blockIdx.x)];
@@ -125,17 +138,38 @@ __global__ void __launch_bounds__(256) ozk_rowmax(const __grid_constant__ OzOpBa
     int k0, k1, r1;
     op_range(o, k0, k1, r1);
     const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;
+    const bool vec = pair_ok(o);
     double m = 0.0;
     if (!o.trans) {
         // X[r][k]: lanes along k (coalesced); warp ty covers rows ty, ty + 8, ...; reduce per row
+#pragma unroll
         for (int j = 0; j < 4; ++j) {
             const int r = r0 + ty + 8 * j;
             double mr = 0.0;
-            if (r < r1)
-                for (int i = 0; i < 8; ++i) {
-                    const int k = kt0 + tx + 32 * i;
-                    if (k >= k0 && k < k1) mr = fmax(mr, fabs(ld_op(o, r, k)));
+            if (r < r1) {
+                double x[8];
+                if (vec) {                                   // lane: k pairs kt0 + 2 tx + 64 i
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const int k = kt0 + 2 * tx + 64 * i;
+                        const double2 p = (k + 1 < k1 && k >= k0) ? ld_pair(o, (size_t)r * o.ld + k) : make_double2(0.0, 0.0);
+                        x[2 * i] = p.x;
+                        x[2 * i + 1] = p.y;
+                        if (!(k + 1 < k1 && k >= k0)) {      // ragged edge: element loads
+                            x[2 * i] = (k >= k0 && k < k1) ? ld_op(o, r, k) : 0.0;
+                            x[2 * i + 1] = (k + 1 >= k0 && k + 1 < k1) ? ld_op(o, r, k + 1) : 0.0;
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const int k = kt0 + tx + 32 * i;
+                        x[i] = (k >= k0 && k < k1) ? ld_op(o, r, k) : 0.0;
+                    }
                 }
+#pragma unroll
+                for (int i = 0; i < 8; ++i) mr = fmax(mr, fabs(x[i]));
+            }
 #pragma unroll
             for (int s = 16; s > 0; s >>= 1) mr = fmax(mr, __shfl_xor_sync(0xffffffffu, mr, s));
             if (tx == 0 && r < r1 && mr > 0.0)
@@ -145,11 +179,19 @@ __global__ void __launch_bounds__(256) ozk_rowmax(const __grid_constant__ OzOpBa
     }
     // X[k][r]: lanes along r (coalesced); thread (ty, tx) covers k = ty, ty + 8, ... of row r0 + tx
     const int r = r0 + tx;
-    if (r < r1)
-        for (int i = 0; i < 32; ++i) {
-            const int k = kt0 + ty + 8 * i;
-            if (k >= k0 && k < k1) m = fmax(m, fabs(ld_op(o, r, k)));
+    if (r < r1) {
+#pragma unroll
+        for (int i0 = 0; i0 < 32; i0 += 8) {
+            double x[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int k = kt0 + ty + 8 * (i0 + i);
+                x[i] = (k >= k0 && k < k1) ? ld_op(o, r, k) : 0.0;
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) m = fmax(m, fabs(x[i]));
         }
+    }
     red[ty][tx] = m;
     __syncthreads();
     if (ty == 0) {
@@ -183,15 +225,41 @@ __global__ void __launch_bounds__(256) ozk_slice(const __grid_constant__ OzOpBat
         }
         ex[tid] = e;
     }
-    if (!o.trans) {
-        for (int i = tid; i < 32 * 128; i += 256) {
-            const int rr = i / 128, kk = i % 128, r = r0 + rr, k = kt0 + kk;
-            tile[rr][kk] = (r < r1 && k >= k0 && k < k1) ? ld_op(o, r, k) : 0.0;
+    // stage the 32 x 128 tile: every thread issues its 8 pair loads (16 bytes each, along the
+    // contiguous index) before storing any; element loads at ragged edges / unaligned operands
+    {
+        const bool vec = pair_ok(o);
+        double2 x[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int i2 = tid + 256 * u;                // pair index in the tile
+            int rr, kk;
+            if (!o.trans) { rr = i2 / 64; kk = 2 * (i2 % 64); }
+            else          { kk = i2 / 16; rr = 2 * (i2 % 16); }
+            const int r = r0 + rr, k = kt0 + kk;
+            const bool full = !o.trans ? (r < r1 && k >= k0 && k + 1 < k1) : (r + 1 < r1 && k >= k0 && k < k1);
+            if (vec && full) {
+                x[u] = ld_pair(o, !o.trans ? (size_t)r * o.ld + k : (size_t)k * o.ld + r);
+            } else if (!o.trans) {
+                x[u].x = (r < r1 && k >= k0 && k < k1) ? ld_op(o, r, k) : 0.0;
+                x[u].y = (r < r1 && k + 1 >= k0 && k + 1 < k1) ? ld_op(o, r, k + 1) : 0.0;
+            } else {
+                x[u].x = (r < r1 && k >= k0 && k < k1) ? ld_op(o, r, k) : 0.0;
+                x[u].y = (r + 1 < r1 && k >= k0 && k < k1) ? ld_op(o, r + 1, k) : 0.0;
+            }
         }
-    } else {
-        for (int i = tid; i < 32 * 128; i += 256) {
-            const int kk = i / 32, rr = i % 32, r = r0 + rr, k = kt0 + kk;
-            tile[rr][kk] = (r < r1 && k >= k0 && k < k1) ? ld_op(o, r, k) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int i2 = tid + 256 * u;
+            if (!o.trans) {
+                const int rr = i2 / 64, kk = 2 * (i2 % 64);
+                tile[rr][kk] = x[u].x;
+                tile[rr][kk + 1] = x[u].y;
+            } else {
+                const int kk = i2 / 16, rr = 2 * (i2 % 16);
+                tile[rr][kk] = x[u].x;
+                tile[rr + 1][kk] = x[u].y;
+            }
         }
     }
     __syncthreads();
