@@ -151,8 +151,7 @@ __global__ void trd_init(const TrdJob *jobs) {
             }
             float a = 0.f;
             if (c < n) a = 0.5f * (J.F[(size_t)r * J.ldF + c] + tr[tx][y]);
-            J.A[(size_t)r * ldw + c] = a;
-            J.Vb[(size_t)r * ldw + c] = 0.f;
+            J.A[(size_t)r * ldw + c] = a;             // (Vb above the reflectors is masked when read)
         }
     }
 }
@@ -1384,27 +1383,49 @@ __global__ void bt_larft(const TrdJob *jobs, const BtStep *steps) {
 }
 
 
+// Q = (float) Z and the clamped eigenvalues: one CTA per 8 rows (blockIdx.x strides over row
+// blocks), threads along the columns with 16-byte fp64 reads.
 __global__ void trd_output(const TrdJob *jobs) {
     const TrdJob &J = jobs[blockIdx.y];
     const double *Z = final_z(J);
-    const long long total = (long long)J.n * J.n;
-    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
-         e += (long long)gridDim.x * blockDim.x) {
-        const int r = (int)(e / J.n), c = (int)(e % J.n);
-        J.Q[(size_t)r * J.ldQ + c] = (float)Z[(size_t)r * J.ldw + c];
-        if (r == 0) J.evals[c] = (float)fmax(J.D[c], 0.0);
+    const int n = J.n;
+    const bool pairs = (J.ldQ & 1) == 0 && (reinterpret_cast<uintptr_t>(J.Q) & 7) == 0;
+    for (int r0 = blockIdx.x * 8; r0 < n; r0 += gridDim.x * 8) {
+        const int rr = r0 + threadIdx.x / 32;
+        if (rr >= n) continue;
+        const double *zr = Z + (size_t)rr * J.ldw;
+        float *qr = J.Q + (size_t)rr * J.ldQ;
+        for (int c = 2 * (threadIdx.x % 32); c < n; c += 64) {
+            if (c + 1 < n) {
+                const double2 z = __ldcs(reinterpret_cast<const double2 *>(zr + c));   // ldw even
+                if (pairs) *reinterpret_cast<float2 *>(qr + c) = make_float2((float)z.x, (float)z.y);
+                else { qr[c] = (float)z.x; qr[c + 1] = (float)z.y; }
+            } else {
+                qr[c] = (float)zr[c];
+            }
+        }
     }
+    if (blockIdx.x == 0)
+        for (int c = threadIdx.x; c < n; c += blockDim.x) J.evals[c] = (float)fmax(J.D[c], 0.0);
 }
 
 // Vd = (double) Vb (exact), so every back-transformation GEMM has fp64 operands (one-stage factors;
 // the two-stage reduction writes Vd itself).
 __global__ void trd_vb_to_f64(const TrdJob *jobs) {
+    // Vd = (double) Vb on and below the reflectors (column k holds v_k in rows >= k + 1), zero above:
+    // Vb is never initialised above the reflectors.  float4 reads, two 16-byte writes per thread.
     const TrdJob &J = jobs[blockIdx.y];
     if (J.off != 1) return;
-    const long long total = (long long)J.n * J.ldw;
+    const int n = J.n, ldw = J.ldw, q4 = ldw / 4;
+    const long long total = (long long)n * q4;
     for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
-         e += (long long)gridDim.x * blockDim.x)
-        J.Vd[e] = (double)J.Vb[e];
+         e += (long long)gridDim.x * blockDim.x) {
+        const int r = (int)(e / q4), c = (int)(e - (long long)r * q4) * 4;
+        const float4 v = __ldcs(reinterpret_cast<const float4 *>(J.Vb + (size_t)r * ldw + c));
+        double2 *dst = reinterpret_cast<double2 *>(J.Vd + (size_t)r * ldw + c);
+        dst[0] = make_double2(c + 0 < r ? (double)v.x : 0.0, c + 1 < r ? (double)v.y : 0.0);
+        dst[1] = make_double2(c + 2 < r ? (double)v.z : 0.0, c + 3 < r ? (double)v.w : 0.0);
+    }
 }
 
 __global__ void trd_zero_info(const TrdJob *jobs) {
@@ -1863,7 +1884,7 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
         for (int i = 0; i < count; ++i)
             if (P.jobs[i].off != 1) sbr_ids.push_back(i);
         if (!sbr_ids.empty()) RET_OK(sbr::apply_q2(djobs, P.jobs, sbr_ids, s));
-        trd_vb_to_f64<<<dim3(std::min(1024, cdiv((long long)max_n * ldw_for(max_n), 256)), count), 256, 0, s>>>(djobs);
+        trd_vb_to_f64<<<dim3(std::min(1024, cdiv((long long)max_n * ldw_for(max_n) / 4, 256)), count), 256, 0, s>>>(djobs);
         KFAC_LAUNCHED();
     }
     size_t boff = 0;
@@ -1987,7 +2008,7 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
         RET_OK(gemm64_grouped(g3.data(), (int)g3.size(), s));
         boff += ns;
     }
-    trd_output<<<dim3(std::min(1024, cdiv((long long)max_n * max_n, 256)), count), 256, 0, s>>>(djobs);
+    trd_output<<<dim3(std::min(1024, cdiv(max_n, 8)), count), 256, 0, s>>>(djobs);
     KFAC_LAUNCHED();
     if (mode == TRD_DEBUG_STEDC)
         KFAC_CUDA_TRY(cudaMemcpyAsync(dbg_d, P.jobs[0].D, sizeof(double) * P.jobs[0].n, cudaMemcpyDeviceToDevice, s));
