@@ -1099,6 +1099,17 @@ __global__ void dc_rotate(const TrdJob *jobs, const MergeDesc *merges) {
 // origin at the nearer pole so that d_i - lambda_j = (d_i - d_org) - tau keeps full relative
 // accuracy.  Iteration: two-pole rational model of psi (poles <= j) and phi (poles > j) fitted to
 // value and slope at tau (fixed-weight / "middle way" family), safeguarded by the bracket.
+// 1/x to ~1 ulp: rcp.approx (about 20 bits) refined by two Newton steps (the secular sums need no
+// correctly rounded division; the same instruction sequence everywhere keeps them deterministic)
+__device__ __forceinline__ double rcp_nr(double x) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    double e = fma(-x, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-x, r, 1.0);
+    return fma(r, e, r);
+}
+
 __global__ void dc_secular(const TrdJob *jobs, const MergeDesc *merges) {
     const MergeDesc M = merges[blockIdx.y];
     const TrdJob &J = jobs[M.job];
@@ -1146,7 +1157,7 @@ __global__ void dc_secular(const TrdJob *jobs, const MergeDesc *merges) {
         double psi = 0.0, dpsi = 0.0, phi = 0.0, dphi = 0.0;
         for (int i = lane; i < k; i += 32) {
             const double del = (dv[i] - dorg) - tau;
-            const double tq = zv[i] / del;
+            const double tq = zv[i] * rcp_nr(del);
             const double term = zv[i] * tq, dterm = tq * tq;
             if (i <= L) { psi += term; dpsi += dterm; }
             else { phi += term; dphi += dterm; }
