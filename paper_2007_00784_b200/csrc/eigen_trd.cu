@@ -64,7 +64,9 @@ constexpr int kMaxRb = 16384 / kPairR;   // super blocks for n <= 16384
 #define KFAC_SYMV_FP32 1                  // fp32 products with 4/8-term fp32 partial sums, fp64 beyond (R23)
 #endif
 constexpr int kBt = 512;                // reflectors per back-transformation block
-constexpr int kTs = 128;                // dlarft sub-block (T built recursively from 128-blocks)
+constexpr int kTs = 64;                 // dlarft sub-block (T built recursively from 64-blocks: 33 KB of
+                                        // shared memory, several CTAs per SM; 128-blocks ran the first
+                                        // back-transformation step in 3 waves of one CTA per SM)
 constexpr double kEps = 1.1102230246251565e-16;   // 2^-53, LAPACK dlamch('E')
 
 
@@ -1357,7 +1359,7 @@ __global__ void dc_assemble(const TrdJob *jobs, const MergeDesc *merges, int pin
 // ------------------------------------------------- back-transformation --
 // T (upper triangular) of H_b0 ... H_{b0+nr-1} = I - V T V^T from G = V^T V (LAPACK dlarft,
 // forward / columnwise): T_jj = tau_j, T[0:j, j] = -tau_j T[0:j, 0:j] G[0:j, j].  This kernel builds
-// one 128x128 diagonal block per CTA (blockIdx.x = 4 step-entry + sub-block) and zeroes the rest of
+// one kTs x kTs diagonal block per CTA (blockIdx.x = (kBt / kTs) step-entry + sub-block) and zeroes the rest of
 // its block row; the off-diagonal blocks follow from T12 = -T1 (V1^T V2) T2 (two GEMMs per level).
 struct BtStep {
     int job, b0, nr;
@@ -1987,9 +1989,8 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
         RET_OK(gemm64_grouped(g1.data(), (int)g1.size(), s));
         bt_larft<<<ns * (kBt / kTs), kTs, kLarftSmem, s>>>(djobs, dbt + boff);
         KFAC_LAUNCHED();
-        // recursive off-diagonal blocks of T: level 1 pairs of 128-blocks, level 2 pair of 256-blocks
-        for (int lvl = 1; lvl <= 2; ++lvl) {
-            const int h = kTs << (lvl - 1);              // size of the halves being joined
+        // recursive off-diagonal blocks of T: pairs of 64-blocks, then of 128-blocks, then of 256-blocks
+        for (int h = kTs; h < kBt; h *= 2) {          // h: size of the halves being joined
             std::vector<Gemm64Desc> ga, gb;
             for (auto &b : stp) {
                 const TrdJob &J = P.jobs[b.job];
