@@ -194,6 +194,39 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def parity_record(args, layers, hp):
+    """relF(P) of the CUDA path against the FP64 oracle on the cpu_baseline sample
+    layers (one cold step through the C-ABI, KL-clip off so P is the preconditioned gradient itself),
+    next to each layer's noise floor -- the oracle run on its own factors rounded to fp32 against the
+    all-fp64 oracle.  Outside the timed region."""
+    import oracle
+    from workloads.gen import layer_inputs
+    from paper_2007_00784_b200.preconditioner import KFACPreconditioner
+    sub = [layers[i] for i in SAMPLE[args.config]]
+    acts, gouts, grads = layer_inputs(sub, seed=args.seed + 1000)
+    ref = oracle.full_step(sub, acts, gouts, grads, hp["damping"], hp["lr"], 1e12, xi=hp["xi"])
+    pc = KFACPreconditioner(sub, damping=hp["damping"], xi=hp["xi"], kappa=1e12, lr=hp["lr"])
+    g = KFACPreconditioner.grad_buffer(sub, "cuda")
+    for t, w in zip(g, grads):
+        t.copy_(torch.from_numpy(w))
+    P = pc.step([torch.from_numpy(a).cuda() for a in acts], [torch.from_numpy(x).cuda() for x in gouts], g,
+                first=True)
+    torch.cuda.synchronize()
+
+    def relF(x, r):
+        return float(np.linalg.norm(np.asarray(x, np.float64) - r) / max(np.linalg.norm(r), 1e-300))
+
+    got = [relF(p.detach().cpu().numpy(), r) for p, r in zip(P, ref["P"])]
+    r32 = [np.asarray(F, np.float32).astype(np.float64) for F in ref["A"] + ref["G"]]
+    Qs, vs = oracle.symeig_batch(r32)
+    n = len(sub)
+    Pf = oracle.precondition_batch(grads, Qs[n:], vs[n:], Qs[:n], vs[:n], hp["damping"])
+    floor = [relF(a, r) for a, r in zip(Pf, ref["P"])]
+    return {"layers": [l.name for l in sub], "relF_P": got, "noise_floor_fp32_factors": floor, "bar": 1e-3,
+            "definition": "relF = ||P_cuda - P_oracle||_F / ||P_oracle||_F per layer (cold step, no KL-clip); "
+                          "floor = same for the oracle on its fp32-rounded factors"}
+
+
 def oracle_full_record(cfg):
     """The oracle timed once on the whole workload (scripts/time_oracle_full.py): the measured
     cross-check of the sample extrapolation (its host and core count are in the record)."""
@@ -485,6 +518,7 @@ def run_ours(args):
                                     "sample": f"oracle on layers {det['names']}, per-stage times scaled by "
                                               f"algorithmic work to all {len(layers)} layers; measured "
                                               f"{det['factors_s']:.1f}/{det['eigen_s']:.1f}/{det['precond_s']:.1f} s"}
+            line["parity"] = parity_record(args, layers, hp)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

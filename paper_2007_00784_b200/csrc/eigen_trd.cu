@@ -781,13 +781,23 @@ struct LeafDesc {
 
 // Implicit QL with Wilkinson-type shifts (EISPACK tql2) on one leaf; every lane runs the scalar
 // recurrence redundantly (identical arithmetic) and owns one row of the eigenvector matrix.
-__global__ void dc_leaf(const TrdJob *jobs, const LeafDesc *leaves, int nleaves) {
+// The QL sweeps index d, e and the eigenvector row z with run-time bounds; in registers they would
+// live in local (stack) memory, so every lane keeps its own copies in shared memory as [i][lane]
+// (conflict-free; lanes share nothing: each runs the same recurrence on its own d, e).
+constexpr int kLeafWarps = 2;                 // 3 x 8 KB per warp of static shared memory (48 KB cap)
+struct LeafCol {                                      // x[i] -> buf[i][lane]
+    double (*p)[32];
+    int lane;
+    __device__ double &operator[](int i) const { return p[i][lane]; }
+};
+__global__ void __launch_bounds__(kLeafWarps * 32) dc_leaf(const TrdJob *jobs, const LeafDesc *leaves, int nleaves) {
+    __shared__ double sd[kLeafWarps][kLeaf][32], se[kLeafWarps][kLeaf][32], sz[kLeafWarps][kLeaf][32];
     const int li = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     if (li >= nleaves) return;
     const LeafDesc Ld = leaves[li];
     const TrdJob &J = jobs[Ld.job];
-    const int lane = threadIdx.x % 32, ns = Ld.size, a = Ld.a;
-    double d[kLeaf], e[kLeaf], z[kLeaf];
+    const int lane = threadIdx.x % 32, ns = Ld.size, a = Ld.a, w = threadIdx.x / 32;
+    const LeafCol d{sd[w], lane}, e{se[w], lane}, z{sz[w], lane};
     for (int i = 0; i < kLeaf; ++i) {
         d[i] = i < ns ? J.D[a + i] : 0.0;
         e[i] = (i + 1 < ns) ? J.e[a + i] : 0.0;       // e[i] = T[i+1][i]
@@ -1101,17 +1111,6 @@ __global__ void dc_rotate(const TrdJob *jobs, const MergeDesc *merges) {
 // origin at the nearer pole so that d_i - lambda_j = (d_i - d_org) - tau keeps full relative
 // accuracy.  Iteration: two-pole rational model of psi (poles <= j) and phi (poles > j) fitted to
 // value and slope at tau (fixed-weight / "middle way" family), safeguarded by the bracket.
-// 1/x to ~1 ulp: rcp.approx (about 20 bits) refined by two Newton steps (the secular sums need no
-// correctly rounded division; the same instruction sequence everywhere keeps them deterministic)
-__device__ __forceinline__ double rcp_nr(double x) {
-    double r;
-    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-    double e = fma(-x, r, 1.0);
-    r = fma(r, e, r);
-    e = fma(-x, r, 1.0);
-    return fma(r, e, r);
-}
-
 __global__ void dc_secular(const TrdJob *jobs, const MergeDesc *merges) {
     const MergeDesc M = merges[blockIdx.y];
     const TrdJob &J = jobs[M.job];
@@ -1159,7 +1158,7 @@ __global__ void dc_secular(const TrdJob *jobs, const MergeDesc *merges) {
         double psi = 0.0, dpsi = 0.0, phi = 0.0, dphi = 0.0;
         for (int i = lane; i < k; i += 32) {
             const double del = (dv[i] - dorg) - tau;
-            const double tq = zv[i] * rcp_nr(del);
+            const double tq = zv[i] / del;
             const double term = zv[i] * tq, dterm = tq * tq;
             if (i <= L) { psi += term; dpsi += dterm; }
             else { phi += term; dphi += dterm; }
@@ -1817,7 +1816,7 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
     dc_tear<<<dim3(cdiv(max_n, 256), count), 256, 0, s>>>(djobs);
     KFAC_LAUNCHED();
     if (!P.leaves.empty()) {
-        dc_leaf<<<cdiv((long long)P.leaves.size(), 4), 128, 0, s>>>(djobs, dleaves, (int)P.leaves.size());
+        dc_leaf<<<cdiv((long long)P.leaves.size(), kLeafWarps), kLeafWarps * 32, 0, s>>>(djobs, dleaves, (int)P.leaves.size());
         KFAC_LAUNCHED();
     }
     int ping = 0;                  // level l reads Z0 (l odd) / Z1 (l even) for every factor
