@@ -37,10 +37,13 @@ def parse():
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
-    p.add_argument("--config", default="r50", choices=["mlp", "r32", "r50", "r101"])
+    p.add_argument("--config", default="r50", choices=["mlp", "r32", "r50", "r101", "r152"])
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--variant", default="eigen", choices=["eigen", "factored", "inverse"])
     p.add_argument("--exchange", default="bcast-eig", choices=["bcast-eig", "allgather-grad"])
+    p.add_argument("--factor-comm", default="allreduce", choices=["allreduce", "reduce-owner"],
+                   help="W > 1: packed-factor allreduce every update, or reduce to the eigen owners "
+                        "(local running averages, SURVEY 8(e) reduce-to-owner)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-graph", action="store_true")
@@ -163,7 +166,7 @@ def oracle_sample(layers, hp, seed, sample_idx):
                      names=[l.name for l in sub])
 
 
-SAMPLE = {"r50": [0, 1, 5, 12], "r101": [0, 1, 5, 12], "r32": [0, 1, 12, 31], "mlp": [0, 1]}
+SAMPLE = {"r50": [0, 1, 5, 12], "r101": [0, 1, 5, 12], "r152": [0, 1, 5, 12], "r32": [0, 1, 12, 31], "mlp": [0, 1]}
 
 
 def run_reference(args):
@@ -239,16 +242,17 @@ def oracle_full_record(cfg):
 
 
 def metric_name(cfg):
-    name = {"r50": "ResNet-50", "r101": "ResNet-101", "r32": "ResNet-32", "mlp": "MLP-784-64-10"}[cfg]
+    name = {"r50": "ResNet-50", "r101": "ResNet-101", "r152": "ResNet-152", "r32": "ResNet-32",
+            "mlp": "MLP-784-64-10"}[cfg]
     return f"{name} K-FAC update ms/iter"
 
 
 def config_block(args, layers):
     return {"workload": f"{args.config} full K-FAC update (factors+allreduce+eigen+exchange+precondition+KL-clip)",
             "layers": len(layers), "batch_per_gpu": layers[0].batch, "variant": args.variant,
-            "exchange": args.exchange, "assignment": "lpt-d3" if args.exchange == "bcast-eig" else "layerwise-lpt",
+            "exchange": args.exchange, "factor_comm": args.factor_comm, "assignment": "lpt-d3" if args.exchange == "bcast-eig" else "layerwise-lpt",
             "l2": "inputs larger than L2 (activations+gradients stream >2.7 GB per step)"
-            if args.config in ("r50", "r101") else "no flush (small config)"}
+            if args.config in ("r50", "r101", "r152") else "no flush (small config)"}
 
 
 # ----------------------------------------------------------------- our arm ----
@@ -277,7 +281,7 @@ def run_ours(args):
         host_sets.append((acts_h, gouts_h, grads_h))
         dev_sets.append(([torch.from_numpy(a).cuda() for a in acts_h], [torch.from_numpy(g).cuda() for g in gouts_h]))
     pc = KFACPreconditioner(layers, damping=hp["damping"], xi=hp["xi"], kappa=hp["kappa"], lr=lr,
-                            variant=args.variant, exchange=args.exchange)
+                            variant=args.variant, exchange=args.exchange, factor_comm=args.factor_comm)
     grad_bufs = []
     for b in range(2):
         grads, grad_flat = KFACPreconditioner.grad_buffer(layers, "cuda", return_flat=True)

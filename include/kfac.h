@@ -125,9 +125,11 @@ kfac_status_t kfac_update_factors(const kfac_layer_t *layers, int32_t num_layers
                                   void *ws, size_t ws_bytes, kfac_stream_t stream);
 
 /* Packed upper triangles (layout of kfac_update_factors' packed outputs) -> both triangles of F[i]
- * (device dims[i] x ld_F[i]).  No workspace. */
+ * (device dims[i] x ld_F[i]), each element multiplied by `scale` (1: a bitwise copy; 1/W after a
+ * reduce-SUM of W ranks' local running averages, whose mean is the running average of the
+ * averaged batches because Eqs. 16-17 are linear).  No workspace. */
 kfac_status_t kfac_unpack_factors(const float *const *packed, const int32_t *dims, float *const *F,
-                                  const int32_t *ld_F, int32_t count, kfac_stream_t stream);
+                                  const int32_t *ld_F, int32_t count, float scale, kfac_stream_t stream);
 
 /* ---- Stage 2: symmetric eigendecomposition of each factor (Alg. 1).
  * F[i]: device dims[i] x ld_F[i] (read only; (F + F^T)/2 is decomposed).

@@ -45,7 +45,7 @@ def _load():
     L.kfac_update_factors_workspace_size.restype = SZ
     L.kfac_update_factors.argtypes = [C.POINTER(kfac_layer_t), C.c_int32, PP, PP, PP, I32P, PP, I32P, PP, PP,
                                       C.c_float, C.c_int32, C.c_float, P, SZ, P]
-    L.kfac_unpack_factors.argtypes = [PP, I32P, PP, I32P, C.c_int32, P]
+    L.kfac_unpack_factors.argtypes = [PP, I32P, PP, I32P, C.c_int32, C.c_float, P]
     L.kfac_compute_eigen_workspace_size.argtypes = [I32P, C.c_int32]
     L.kfac_compute_eigen_workspace_size.restype = SZ
     L.kfac_compute_eigen.argtypes = [PP, I32P, I32P, C.c_int32, PP, I32P, PP, P, C.c_uint32, P, SZ, P]
@@ -162,10 +162,11 @@ def kfac_update_factors(layers, acts: List[torch.Tensor], gouts: List[torch.Tens
                                    _stream(stream)), "kfac_update_factors")
 
 
-def kfac_unpack_factors(packed: List[torch.Tensor], F: List[torch.Tensor], stream=None):
+def kfac_unpack_factors(packed: List[torch.Tensor], F: List[torch.Tensor], scale: float = 1.0, stream=None):
     n = len(F)
     _check(lib.kfac_unpack_factors(_ptrs(packed), _i32([f.shape[0] for f in F]), _ptrs(F),
-                                   _i32([_ld(f) for f in F]), n, _stream(stream)), "kfac_unpack_factors")
+                                   _i32([_ld(f) for f in F]), n, float(scale), _stream(stream)),
+           "kfac_unpack_factors")
 
 
 def kfac_compute_eigen(F: List[torch.Tensor], Q: List[torch.Tensor], evals: List[torch.Tensor],

@@ -18,7 +18,7 @@ kfac_status_t factors_run(const kfac_layer_t *layers, int nl, const float *const
                           float *const *G, const int32_t *ldG, float *const *pA, float *const *pG,
                           float xi, int first, float out_scale, void *ws, cudaStream_t s);
 kfac_status_t unpack_run(const float *const *packed, const int32_t *dims, float *const *F, const int32_t *ldF,
-                         int count, cudaStream_t s);
+                         int count, float scale, cudaStream_t s);
 size_t eigen_workspace_bytes(const int32_t *dims, int count);
 kfac_status_t eigen_run(const float *const *F, const int32_t *dims, const int32_t *ldF, int count,
                         float *const *Q, const int32_t *ldQ, float *const *evals, int32_t *info,
@@ -219,7 +219,7 @@ kfac_status_t kfac_update_factors(const kfac_layer_t *layers, int32_t num_layers
 }
 
 kfac_status_t kfac_unpack_factors(const float *const *packed, const int32_t *dims, float *const *F,
-                                  const int32_t *ld_F, int32_t count, kfac_stream_t stream) {
+                                  const int32_t *ld_F, int32_t count, float scale, kfac_stream_t stream) {
     kfac::NvtxRange nvtx_range("kfac_unpack_factors");
     KFAC_CHECK_ARG(packed && dims && F && ld_F, KFAC_ERR_INVALID_VALUE, "kfac_unpack_factors: NULL argument");
     KFAC_CHECK_ARG(count > 0, KFAC_ERR_INVALID_VALUE, "kfac_unpack_factors: count <= 0");
@@ -229,7 +229,8 @@ kfac_status_t kfac_unpack_factors(const float *const *packed, const int32_t *dim
         RET_IF(check_matrix(F[i], dims[i], dims[i], ld_F[i], "F", i));
     }
     RET_IF(check_device());
-    return unpack_run(packed, dims, F, ld_F, count, reinterpret_cast<cudaStream_t>(stream));
+    KFAC_CHECK_ARG(scale == scale, KFAC_ERR_INVALID_VALUE, "kfac_unpack_factors: scale is NaN");
+    return unpack_run(packed, dims, F, ld_F, count, scale, reinterpret_cast<cudaStream_t>(stream));
 }
 
 size_t kfac_compute_eigen_workspace_size(const int32_t *dims, int32_t count) {

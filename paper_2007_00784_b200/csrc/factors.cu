@@ -381,6 +381,7 @@ struct UnpackJob {
 };
 struct UnpackBatch {
     int count;
+    float scale;
     UnpackJob j[64];
 };
 
@@ -401,7 +402,7 @@ __global__ void __launch_bounds__(256) unpack_kernel(const __grid_constant__ Unp
         float v = 0.f;
         if (gi < J.d && gj < J.d) {
             const int a = min(gi, gj), c = max(gi, gj);
-            v = J.packed[(long long)a * J.d - (long long)a * (a - 1) / 2 + (c - a)];
+            v = b.scale * J.packed[(long long)a * J.d - (long long)a * (a - 1) / 2 + (c - a)];
             J.F[(size_t)gi * J.ldF + gj] = v;
         }
         tr[rr][tx] = v;
@@ -415,10 +416,11 @@ __global__ void __launch_bounds__(256) unpack_kernel(const __grid_constant__ Unp
 }
 
 kfac_status_t unpack_run(const float *const *packed, const int32_t *dims, float *const *F, const int32_t *ldF,
-                         int count, cudaStream_t s) {
+                         int count, float scale, cudaStream_t s) {
     for (int b0 = 0; b0 < count; b0 += 64) {
         UnpackBatch b;
         b.count = 0;
+        b.scale = scale;
         int tiles = 0;
         for (int i = b0; i < count && b.count < 64; ++i) {
             UnpackJob &j = b.j[b.count++];

@@ -8,7 +8,14 @@ calls to make, and issues the collectives through torch.distributed:
           factors' packed upper triangles (half the bytes of the full matrices) all-reduced with
           SUM in buckets of layers on a communication stream, each bucket's allreduce overlapping
           the next bucket's factor kernels, then kfac_unpack_factors -- Alg. 1 P:343-345, P:387,
-          P:426-428 (asynchronous, batched communication)
+          P:426-428 (asynchronous, batched communication).
+          factor_comm="reduce-owner" (K-FAC-opt, SURVEY 8(e) "reduce-to-owner"): each rank keeps
+          its LOCAL running average (Eqs. 16-17 are linear, so the mean of the W local running
+          averages is the running average of the averaged batches); only when an eigen refresh
+          follows are the packed triangles reduced (SUM) to each factor's owner -- one reduce per
+          owner over its contiguous owner-major slice, (W-1)/W of the buffer per rank instead of the
+          allreduce's 2(W-1)/W, and no factor traffic at all on iterations without a refresh
+           -- and the owner unpacks them with scale 1/W into its own averaged copy.
   step 2  kfac_assign (host, identical on all ranks) -> kfac_compute_eigen on the
           owned factors -> exchange:
             K-FAC-opt ("bcast-eig"): every owner broadcasts its contiguous, owner-major slice
@@ -59,13 +66,14 @@ class KFACPreconditioner:
     def __init__(self, layers, device=None, damping: float = 1e-3, xi: float = 0.95,
                  kappa: float = 1e-3, lr: float = 0.1, variant: str = "eigen",
                  exchange: str = "bcast-eig", assign_policy: int = _lib.LPT_D3,
-                 process_group=None):
+                 process_group=None, factor_comm: str = "allreduce"):
         self.layers = list(layers)
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.damping, self.xi, self.kappa, self.lr = damping, xi, kappa, lr
         assert variant in ("eigen", "factored", "inverse")
         assert exchange in ("bcast-eig", "allgather-grad")
-        self.variant, self.exchange = variant, exchange
+        assert factor_comm in ("allreduce", "reduce-owner")
+        self.variant, self.exchange, self.factor_comm = variant, exchange, factor_comm
         self.pg = process_group
         self.world = dist.get_world_size(process_group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(process_group) if dist.is_initialized() else 0
@@ -89,18 +97,26 @@ class KFACPreconditioner:
         self.F = _views(self.factor_flat, self.fseg)
         self.A = self.F[0::2]
         self.G = self.F[1::2]
-        # packed upper triangles of the factors (the allreduce buffer, W > 1), same factor order
-        self.packed_seg, off = [], 0
-        for d in self.dims:
-            self.packed_seg.append((off, d * (d + 1) // 2))
+        per_rank = [[f for f in range(len(self.dims)) if self.owner[f] == r] for r in range(self.world)]
+        self.reduce_owner = self.world > 1 and factor_comm == "reduce-owner"
+        # packed upper triangles of the factors (the collective's buffer, W > 1): factor order for the
+        # allreduce (layer buckets), owner-major for the reduce to owners (one contiguous slice each)
+        order = [f for fs in per_rank for f in fs] if self.reduce_owner else range(len(self.dims))
+        self.packed_seg, off = [None] * len(self.dims), 0
+        self.pk_off, self.pk_size = [0] * self.world, [0] * self.world
+        for f in order:
+            d = self.dims[f]
+            self.packed_seg[f] = (off, d * (d + 1) // 2)
+            if self.reduce_owner:
+                self.pk_size[self.owner[f]] += _aligned(d * (d + 1) // 2)
             off += _aligned(d * (d + 1) // 2)
+        self.pk_off = [sum(self.pk_size[:r]) for r in range(self.world)]
         self.packed_flat = torch.zeros(off if self.world > 1 else 64, **f32)
         self.packed = [self.packed_flat[o:o + n] for o, n in self.packed_seg] if self.world > 1 else None
         self.bucket_bytes = 64 << 20
         self.comm_stream = torch.cuda.Stream(self.device) if (self.world > 1 and self.device.type == "cuda") else None
         # eigenbases / inverses: owner-major, each rank's factors contiguous; slices have their real
         # sizes (the exchange broadcasts exactly each owner's bytes)
-        per_rank = [[f for f in range(len(self.dims)) if self.owner[f] == r] for r in range(self.world)]
         self.q_size = [sum(_aligned(self.dims[f] * _ld(self.dims[f])) for f in fs) for fs in per_rank]
         self.v_size = [sum(_aligned(self.dims[f]) for f in fs) for fs in per_rank]
         self.q_off = [sum(self.q_size[:r]) for r in range(self.world)]
@@ -119,6 +135,19 @@ class KFACPreconditioner:
         self.Q = _views(self.q_flat, self.qseg)
         self.v = [self.v_flat[s.offset:s.offset + s.cols] for s in self.vseg]
         self.owned = per_rank[self.rank]
+        # reduce-owner: the averaged copies of the owned factors (the local running averages in F
+        # stay untouched, so the linearity argument above holds at every refresh)
+        self.F_src = self.F
+        if self.reduce_owner:
+            segs, o = {}, 0
+            for f in self.owned:
+                segs[f] = Segment(o, self.dims[f], self.dims[f], _ld(self.dims[f]))
+                o += segs[f].numel
+            self.fown_flat = torch.zeros(max(64, o), **f32)
+            self.F_src = [None] * len(self.dims)
+            for f, v in zip(self.owned, _views(self.fown_flat, [segs[f] for f in self.owned])):
+                self.F_src[f] = v
+        self.reduced = False
         self.info = torch.zeros(max(1, len(self.owned)), dtype=torch.int32, device=self.device)
         # preconditioned gradients: owner-major by layer (K-FAC-lw all-gathers them in place)
         per_rank_l = [[i for i in range(L) if self.layer_owner[i] == r] for r in range(self.world)]
@@ -163,8 +192,11 @@ class KFACPreconditioner:
                 start, acc = i + 1, 0
         return out
 
-    def update_factors(self, acts, gouts, first: bool):
+    def update_factors(self, acts, gouts, first: bool, refresh: bool = True):
         """Alg. 1 step 1: local factors + running average, then the factor allreduce.
+
+        factor_comm="reduce-owner": the local running averages only; when `refresh` (an eigen
+        decomposition follows) their packed triangles are reduced to the owners (reduce_to_owners).
 
         W > 1: the factors' packed upper triangles are all-reduced (SUM of the out_scale = 1/W
         factors = their average) bucket by bucket; with NCCL each bucket's allreduce runs on the
@@ -173,6 +205,24 @@ class KFACPreconditioner:
         if self.world == 1:
             _lib.kfac_update_factors(self.layers, acts, gouts, self.A, self.G, self.xi, first,
                                      1.0, ws=self.ws["factors"])
+            return
+        if self.reduce_owner:
+            pk = dict(packed_A=self.packed[0::2], packed_G=self.packed[1::2]) if refresh else {}
+            _lib.kfac_update_factors(self.layers, acts, gouts, self.A, self.G, self.xi, first, 1.0,
+                                     ws=self.ws["factors"], **pk)
+            if refresh:
+                compute = torch.cuda.current_stream(self.device) if self.comm_stream is not None else None
+                if compute is not None:
+                    self.comm_stream.wait_stream(compute)
+                    with torch.cuda.stream(self.comm_stream):
+                        reduce_to_owners(self.packed_flat, self.pk_off, self.pk_size, self.pg)
+                    compute.wait_stream(self.comm_stream)
+                else:
+                    reduce_to_owners(self.packed_flat, self.pk_off, self.pk_size, self.pg)
+                if self.owned:
+                    _lib.kfac_unpack_factors([self.packed[f] for f in self.owned],
+                                             [self.F_src[f] for f in self.owned], 1.0 / self.world)
+                self.reduced = True
             return
         compute = torch.cuda.current_stream(self.device) if self.comm_stream is not None else None
         works = []
@@ -203,8 +253,13 @@ class KFACPreconditioner:
         KL-clip silently).  Default: on the first decomposition only (one host sync)."""
         if check is None:
             check = not self.have_eigen
+        if self.reduce_owner:
+            if not self.reduced:
+                raise RuntimeError("factor_comm='reduce-owner': call update_factors(..., refresh=True) "
+                                   "before compute_eigen (the owners' averaged factors are stale)")
+            self.reduced = False
         if self.owned:
-            F = [self.F[f] for f in self.owned]
+            F = [self.F_src[f] for f in self.owned]
             Q = [self.Q[f] for f in self.owned]
             if self.variant == "inverse":
                 _lib.kfac_compute_inverse(F, self.damping, Q, self.info, ws=self.ws["eigen"])
@@ -247,10 +302,22 @@ class KFACPreconditioner:
 
     def step(self, acts, gouts, grads, update_factors=True, update_eigen=True, first=False, warm=False):
         if update_factors:
-            self.update_factors(acts, gouts, first)
+            self.update_factors(acts, gouts, first, refresh=update_eigen or not self.have_eigen)
         if update_eigen or not self.have_eigen:
             self.compute_eigen(warm=warm)
         return self.precondition(grads)
+
+
+def reduce_to_owners(flat: torch.Tensor, offs, sizes, group=None):
+    """Rank r owns flat[offs[r]:offs[r]+sizes[r]]; afterwards rank r's slice holds the SUM of every
+    rank's copy of it (other ranks' copies of slices they do not own are left as the collective
+    leaves them).  One reduce per owner, all issued before any is waited on."""
+    world = dist.get_world_size(group)
+    works = [dist.reduce(flat[offs[r]:offs[r] + sizes[r]], dst=dist.get_global_rank(group, r) if group else r,
+                         op=dist.ReduceOp.SUM, group=group, async_op=True)
+             for r in range(world) if sizes[r] > 0]
+    for w in works:
+        w.wait()
 
 
 def exchange_from_owners(flat: torch.Tensor, offs, sizes, group=None):

@@ -72,6 +72,25 @@ def _worker(rank, world, port, cfg, exchange, q):
         if exchange == "allgather-grad":
             for i in range(len(layers)):
                 assert pc.owner[2 * i] == pc.owner[2 * i + 1]
+        # 5) reduce-to-owner (factor_comm="reduce-owner"): the packed buffer is owner-major, each
+        # owner's factors lie inside its contiguous slice, the slices tile the buffer, and one
+        # reduce per owner leaves the SUM of every rank's copy in the owner's slice
+        from paper_2007_00784_b200.preconditioner import reduce_to_owners
+        pr = KFACPreconditioner(layers, device="cpu", exchange=exchange, factor_comm="reduce-owner")
+        assert pr.owner == pc.owner
+        assert pr.pk_off[0] == 0 and all(pr.pk_off[r] + pr.pk_size[r] == pr.pk_off[r + 1] for r in range(world - 1))
+        for f, (o, n) in enumerate(pr.packed_seg):
+            r = pr.owner[f]
+            assert pr.pk_off[r] <= o and o + n <= pr.pk_off[r] + pr.pk_size[r]
+        assert sum(pr.pk_size) <= pr.packed_flat.numel()
+        pv = torch.arange(pr.packed_flat.numel(), dtype=torch.float32) % 89
+        pr.packed_flat.copy_(pv + 10 * rank)
+        reduce_to_owners(pr.packed_flat, pr.pk_off, pr.pk_size)
+        lo, hi = pr.pk_off[rank], pr.pk_off[rank] + pr.pk_size[rank]
+        assert torch.equal(pr.packed_flat[lo:hi], world * pv[lo:hi] + 10 * sum(range(world)))
+        # the averaged copies are private to the owner (shape = the owned factors only)
+        assert sum(pr.F_src[f].numel() for f in pr.owned) <= pr.fown_flat.numel()
+        assert all(pr.F_src[f] is None for f in range(len(pr.dims)) if pr.owner[f] != rank)
         q.put((rank, "ok", len(pc.owned)))
     except Exception as e:  # pragma: no cover - reported to the parent
         q.put((rank, repr(e), 0))

@@ -128,6 +128,33 @@ def test_factor_average_over_ranks_is_global_batch(orc):
     assert np.abs((G0[0] + G1[0]) / 2 - Gg[0]).max() <= 1e-12
 
 
+def test_mean_of_local_running_averages_is_global_running_average(orc):
+    """Reduce-to-owner pin: Eqs. 16-17 are linear, so the mean of
+    the ranks' LOCAL running averages after k steps equals the running average of the global
+    batches (each step's global factor is the mean of the shard factors, previous test) -- the
+    factors need no exchange on iterations without an eigen refresh."""
+    l_rank = shapes.conv("c", 2, 3, 4, 3, 1, 5)
+    l_glob = shapes.conv("c", 4, 3, 4, 3, 1, 5)
+    rng = np.random.default_rng(5)
+    loc = [[None, None], [None, None]]
+    glob = [None, None]
+    for k in range(4):
+        a = rng.standard_normal(l_glob.act_shape).astype(np.float32)
+        g = rng.standard_normal(l_glob.gout_shape).astype(np.float32)
+        first = k == 0
+        A, G = orc.update_factors([l_glob], [a], [g], A=glob[0], G=glob[1], xi=0.3, first=first)
+        glob = [A, G]
+        for r in range(2):
+            A, G = orc.update_factors([l_rank], [a[2 * r:2 * r + 2]], [g[r * l_rank.rows:(r + 1) * l_rank.rows]],
+                                      A=loc[r][0], G=loc[r][1], xi=0.3, first=first)
+            loc[r] = [A, G]
+        for t in range(2):
+            mean = (loc[0][t][0] + loc[1][t][0]) / 2
+            assert np.abs(mean - glob[t][0]).max() <= 1e-12 * max(1.0, np.abs(glob[t][0]).max())
+    # and the non-trivial part: the local averages themselves differ from the global one
+    assert np.abs(loc[0][0][0] - glob[0][0]).max() > 1e-3
+
+
 # ---------------------------------------------------------------- eigen --
 @pytest.mark.parametrize("method", ["qr", "jacobi"])
 def test_symeig_trivial_cases(orc, method):
