@@ -39,7 +39,10 @@ namespace kfac {
 
 namespace {
 
-constexpr int kOzS = 6;                               // digits per element
+#ifndef KFAC_OZ_DIGITS
+#define KFAC_OZ_DIGITS 6
+#endif
+constexpr int kOzS = KFAC_OZ_DIGITS;                  // digits per element
 constexpr int kOzPairs = kOzS * (kOzS + 1) / 2;       // 21
 constexpr int OBM = 128, OBN = 64, OBK = 64;          // tile M x N, k-block bytes
 constexpr int kOzStages = 3;
@@ -649,6 +652,8 @@ kfac_status_t oz_gemm_grouped(const Gemm64Desc *descs, int count, cudaStream_t s
 // Test hooks: one Ozaki GEMM (fp64 operands; epi 0 store / 3 C -= ...).  kfac_debug_ozaki allocates
 // the scratch and synchronises; kfac_debug_ozaki_ws takes caller scratch (size: kfac_debug_ozaki_bytes)
 // and only enqueues (timing).
+extern "C" int kfac_debug_ozaki_digits(void) { return kfac::kOzS; }
+
 extern "C" size_t kfac_debug_ozaki_bytes(int M, int N, int K) {
     kfac::Gemm64Desc d{};
     d.M = M; d.N = N; d.K = K;

@@ -82,7 +82,7 @@ class KFAC:
                  damping_decay_steps: Sequence[int] = (), damping_decay_rate: float = 0.5,
                  update_freq_decay_steps: Sequence[int] = (), update_freq_decay_rate: float = 1.0,
                  variant: str = "eigen", exchange: str = "bcast-eig", grad_scale: str = "batch",
-                 process_group=None, skip_modules: Sequence[nn.Module] = ()):
+                 process_group=None, skip_modules: Sequence[nn.Module] = (), factor_comm: str = "allreduce"):
         self.model = model
         self.lr, self.damping, self.xi, self.kappa = lr, damping, xi, kappa
         self.kfac_update_freq, self.factor_update_freq = int(kfac_update_freq), int(factor_update_freq)
@@ -92,6 +92,7 @@ class KFAC:
         self.update_freq_decay_rate = update_freq_decay_rate
         self.variant, self.exchange, self.grad_scale = variant, exchange, grad_scale
         self.process_group = process_group
+        self.factor_comm = factor_comm
         skip = set(id(m) for m in skip_modules)
         self.modules: List[nn.Module] = [m for m in model.modules() if supported(m) and id(m) not in skip]
         self.names = {id(m): n for n, m in model.named_modules()}
@@ -159,7 +160,8 @@ class KFAC:
     # -------------------------------------------------------------------- step --
     def _build(self, descs):
         self.pc = KFACPreconditioner(descs, damping=self.damping, xi=self.xi, kappa=self.kappa, lr=self.lr,
-                                     variant=self.variant, exchange=self.exchange, process_group=self.process_group)
+                                     variant=self.variant, exchange=self.exchange, process_group=self.process_group,
+                                     factor_comm=self.factor_comm)
         self._grads, self._grad_flat = KFACPreconditioner.grad_buffer(descs, self.pc.device, return_flat=True)
 
     def _schedules(self):
@@ -195,14 +197,18 @@ class KFAC:
             gbuf[:, :w.shape[1]].copy_(w)
             if m.bias is not None:
                 gbuf[:, w.shape[1]].copy_(m.bias.grad)
+        refresh = self.steps % self.kfac_update_freq == 0 or not pc.have_eigen
+        if refresh and not update_factors and pc.reduce_owner:
+            raise RuntimeError("KFAC.step(): factor_comm='reduce-owner' needs the factors updated on every "
+                               "eigen-refresh step (kfac_update_freq a multiple of factor_update_freq)")
         if update_factors:
             acts = [self._act_nhwc(m, self._acts[id(m)]) for m in self.modules]
             gouts = [self._gout_rows(m, self._gouts[id(m)], self._acts[id(m)].shape[0]) for m in self.modules]
-            pc.update_factors(acts, gouts, first=not self._seeded)
+            pc.update_factors(acts, gouts, first=not self._seeded, refresh=refresh)
             self._seeded = True
             self._acts.clear()
             self._gouts.clear()
-        if self.steps % self.kfac_update_freq == 0 or not pc.have_eigen:
+        if refresh:
             pc.compute_eigen()
         P = pc.precondition(self._grads)
         for m, p in zip(self.modules, P):
