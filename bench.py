@@ -202,6 +202,7 @@ def parity_record(args, layers, hp):
     layers (one cold step through the C-ABI, KL-clip off so P is the preconditioned gradient itself),
     next to each layer's noise floor -- the oracle run on its own factors rounded to fp32 against the
     all-fp64 oracle.  Outside the timed region."""
+    import torch
     import oracle
     from workloads.gen import layer_inputs
     from paper_2007_00784_b200.preconditioner import KFACPreconditioner
