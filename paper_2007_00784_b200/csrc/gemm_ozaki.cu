@@ -45,7 +45,7 @@ namespace {
 constexpr int kOzS = KFAC_OZ_DIGITS;                  // digits per element
 constexpr int kOzPairs = kOzS * (kOzS + 1) / 2;       // 21
 constexpr int OBM = 128, OBN = 64, OBK = 64;          // tile M x N, k-block bytes
-constexpr int kOzStages = 3;
+constexpr int kOzStages = kOzS <= 4 ? 4 : 3;              // stages of the k-block ring (fit 227 KB)
 constexpr int kOzATile = OBM * OBK;                   // 8 KB per digit plane
 constexpr int kOzBTile = OBN * OBK;                   // 4 KB
 constexpr int kOzStageBytes = kOzS * (kOzATile + kOzBTile);   // 72 KB
