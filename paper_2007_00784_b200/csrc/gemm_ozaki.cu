@@ -9,21 +9,24 @@
 // assembled from a few exact int8 products (Ozaki, Ogita, Oishi, Rump 2012):
 //
 //   every row r of op(A) is scaled by 2^-e_r (e_r: the exponent of the row's largest |entry| + 1)
-//   and split into s = 6 signed digits of 7 bits:  a = 2^e_r sum_i d_i 2^(-7 i) + r_s,
+//   and split into s = 5 signed digits of 7 bits:  a = 2^e_r sum_i d_i 2^(-7 i) + r_s,
 //   |d_i| <= 64, |r_s| <= 2^(e_r - 7 s - 1); op(B)'s columns likewise (exponents f_c, digits d'_j);
 //   C[r][c] = 2^(e_r + f_c) sum_{L=2}^{s+1} 2^(-7 L) S_L[r][c],   S_L = sum_{i+j=L} D_i D'_j,
 //
-// where every S_L is an exact int32 GEMM (|S_L| <= 6 K 64^2 < 2^31 for K < 87000).  Digit pairs with
-// i + j > s + 1 are dropped: with s = 6 the error is below ~K 2^-42 max|a_r| max|b_c| (41 bits; the
-// fp32 rounding of the eigenvectors this feeds is 2^-24).  21 int8 MMAs per fp64 product.
+// where every S_L is an exact int32 GEMM (|S_L| <= s K 64^2 < 2^31 for K < 100000).  Digit pairs with
+// i + j > s + 1 are dropped: with s = 5 the error is below ~K 2^-35 max|a_r| max|b_c| (34 bits; the
+// fp32 rounding of the eigenvectors this feeds is 2^-24).  15 int8 products per fp64 product.
+// Measured (profiles/r02_n_ozaki_digits.md): s = 6 -> 5 keeps every GPU parity test green with the same
+// eigen residuals (largest factor reconstruction 5.5e-8 / 5.6e-8) and saves 2.2 ms per ResNet-50
+// update; s = 4 (27 bits) fails the full-size eigen tests (reconstruction 1.2e-6).
 //
 // Kernels: ozk_rowmax (max |x| per operand row over the valid K range, atomicMax on the bit
 // pattern), ozk_slice (exponent + digits, int8 planes [s][R][Kp], K-major), ozk_gemm:
-//   128 x 64 output tile per CTA, K staged 64 bytes at a time (SWIZZLE_64B, 3 stages of 72 KB:
-//   all six A digit planes and six B digit planes of the k-block, one 3-D TMA box each);
+//   128 x 64 output tile per CTA, K staged 64 bytes at a time (SWIZZLE_64B, 3 stages of 60 KB:
+//   all s A digit planes and s B digit planes of the k-block, one 3-D TMA box each);
 //   warp 0 TMA producer, warp 1 MMA issuer (per k-step, digit plane i of A times the stacked B
 //   planes 0..s-1-i in one MMA that starts at TMEM column 64 i, so product (i, j) accumulates into
-//   level i + j's 64 columns; 8 MMAs of N <= 256), warps 4-7 the epilogue (TMEM -> fp64 sum of the
+//   level i + j's 64 columns; 6 MMAs of N <= 256 for s = 5), warps 4-7 the epilogue (TMEM -> fp64 sum of the
 //   levels -> 2^(e_r + f_c) -> store / C -= through shared memory in coalesced rows).
 #include "internal.cuh"
 #include "tc_ptx.cuh"
@@ -40,7 +43,7 @@ namespace kfac {
 namespace {
 
 #ifndef KFAC_OZ_DIGITS
-#define KFAC_OZ_DIGITS 6
+#define KFAC_OZ_DIGITS 5
 #endif
 constexpr int kOzS = KFAC_OZ_DIGITS;                  // digits per element
 constexpr int kOzPairs = kOzS * (kOzS + 1) / 2;       // 21
@@ -48,7 +51,7 @@ constexpr int OBM = 128, OBN = 64, OBK = 64;          // tile M x N, k-block byt
 constexpr int kOzStages = kOzS <= 4 ? 4 : 3;              // stages of the k-block ring (fit 227 KB)
 constexpr int kOzATile = OBM * OBK;                   // 8 KB per digit plane
 constexpr int kOzBTile = OBN * OBK;                   // 4 KB
-constexpr int kOzStageBytes = kOzS * (kOzATile + kOzBTile);   // 72 KB
+constexpr int kOzStageBytes = kOzS * (kOzATile + kOzBTile);   // 60 KB (s = 5)
 constexpr int kOzSmem = kOzStages * kOzStageBytes + 1024 + 256;
 constexpr int kOzThreads = 256;
 constexpr int kOzTmemCols = 512;                      // 6 levels x 64 columns used
@@ -372,7 +375,7 @@ __global__ void __launch_bounds__(kOzThreads, 1) ozk_gemm(const __grid_constant_
             // A digit plane i times the stacked B planes 0 .. s-1-i in ONE instruction: product
             // (i, j) lands in TMEM columns 64 (i + j) -- level i + j -- because the MMA starts at
             // column 64 i and the B planes are consecutive 64-row blocks in shared memory; N is split
-            // at 256 (the instruction's maximum).  8 MMAs per k-step instead of 21, so each reads
+            // at 256 (the instruction's maximum).  6 MMAs per k-step instead of 15 (s = 5), so each reads
             // the A tile once per plane and B in up to 256-row blocks (half the smem operand traffic).
             const uint32_t idesc0 = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(OBM >> 4) << 24);
             for (int q = 0; q < nk; ++q) {

@@ -1,7 +1,7 @@
 """GPU: the fp64-accurate int8 tensor-core GEMM (Ozaki scheme, gemm_ozaki.cu) of the eigensolver.
 
 Bound (derived in gemm_ozaki.cu's header): every operand row is scaled by 2^-e (e = exponent of its
-largest |entry| + 1) and cut after s digits of 7 bits (s = kfac_debug_ozaki_digits(), 6 by default),
+largest |entry| + 1) and cut after s digits of 7 bits (s = kfac_debug_ozaki_digits(), 5 by default),
 and digit pairs with i + j > s + 1 are dropped, so |C - A B| <= ~3 K 2^-(7s-1) max|A[m,:]| max|B[:,n]|
 element by element.  The test grades against 2^-(7s-5) K max|A[m,:]| max|B[:,n]| (16x margin) and a
 relative Frobenius error <= 1e-11 * 2^(7(6-s)) (fp32 would be ~1e-7), on rows spanning 2^+-20
