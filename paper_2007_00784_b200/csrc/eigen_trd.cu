@@ -128,6 +128,178 @@ __device__ __forceinline__ void part_range(int r0, int n, int c, int nc, int &lo
     hi = r0 + (int)(len * (c + 1) / nc);
 }
 
+// ------------------------------------------- small factors: cluster-resident dsytd2 --
+// For a call whose factors are all small (d <= ~880: the MLP and ResNet-32 configurations) the
+// panel kernel's grid-wide barriers dominate: a d = 785 factor pays ~20 us per column for ~1 us of
+// mat-vec bytes.  Here one thread-block cluster of CL <= 16 CTAs holds the factor's lower triangle
+// in fp64 in distributed shared memory (row r on CTA r % CL) and runs unblocked Householder
+// tridiagonalisation (LAPACK dsytd2, lower; Golub & Van Loan Alg. 8.3.1) with three cluster barriers
+// per column and every matrix access local:
+//   1  x = A[k+1:n, k] all-gathered (each CTA stores its rows' entries into every CTA's copy);
+//   -  every CTA forms the same reflector from the full x (fixed-order sums: bit-identical);
+//   2  y = A22 v: row sums of the CTA's rows + column sums over its rows (the mirrored upper triangle),
+//      exchanged through shared memory and summed in rank order for each owned row; v^T A v from
+//      the CTA's own rows (= sum_r v_r (2 rowsum_r - A_rr v_r));
+//   3  w = tau y - (tau^2/2)(v^T A v) v all-gathered;  A22 -= v w^T + w v^T on the own rows.
+// Outputs as the panel kernel's: d, e, tau (fp64) and the reflectors in Vb (v_k[k+1] = 1).
+constexpr int kSmThreads = 512;
+constexpr int kSmMaxCl = 16;
+constexpr int kSmMaxJobs = 64;
+constexpr size_t kSmSmemCap = 225 * 1024;
+
+struct SmallSet {
+    const TrdJob *jobs;
+    int count;
+    int job[kSmMaxJobs];
+};
+
+// local lower-triangle storage of CTA `rank` (rows r = rank + CL i): offset of local row i
+__host__ __device__ inline long long sm_row_off(int i, int cl, int rank) {
+    return (long long)cl * i * (i - 1) / 2 + (long long)i * (rank + 1);
+}
+__host__ __device__ inline int sm_rows(int n, int cl, int rank) { return rank < n ? (n - rank + cl - 1) / cl : 0; }
+// dynamic shared memory of one CTA: triangle | x/v (2 buffers) | w | column sums | row sums | slots
+__host__ __device__ inline size_t sm_smem_bytes(int n, int cl) {
+    const int nl = sm_rows(n, cl, 0);
+    return sizeof(double) * ((size_t)sm_row_off(nl, cl, 0) + 4 * (size_t)n + (size_t)nl + 64);
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t cluster_nctas() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+    return r;
+}
+// shared-memory address of the same variable in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t map_rank(const void *p, uint32_t rank) {
+    uint32_t a = (uint32_t)__cvta_generic_to_shared(p), r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_cluster(uint32_t addr, double v) {
+    asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
+}
+__device__ __forceinline__ double ld_cluster(uint32_t addr) {
+    double v;
+    asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(addr) : "memory");
+    return v;
+}
+
+__global__ void __launch_bounds__(kSmThreads, 1) trd_small(const __grid_constant__ SmallSet S) {
+    extern __shared__ __align__(16) double smd[];
+    __shared__ double sh[kSmThreads / 32];
+    const int cl = (int)cluster_nctas(), rank = (int)cluster_rank();
+    const TrdJob &J = S.jobs[S.job[blockIdx.x / cl]];
+    const int n = J.n, ldw = J.ldw;
+    const int t = threadIdx.x, lane = t % 32, warp = t / 32, nwarp = kSmThreads / 32;
+    const int nl = sm_rows(n, cl, rank);
+    double *Al = smd;                                            // local lower triangle
+    double *xv = Al + sm_row_off(sm_rows(n, cl, 0), cl, 0);      // [2][n]: x, then v (by column parity)
+    double *wv = xv + 2 * n;                                     // [n]: w
+    double *cs = wv + n;                                         // [n]: column sums over own rows
+    double *rs = cs + n;                                         // [nl]: row sums of own rows
+    double *slot = rs + nl;                                      // [0]: partial v^T A v
+    // A = (F + F^T)/2 in fp64, own rows
+    for (int i = warp; i < nl; i += nwarp) {
+        const int r = rank + cl * i;
+        double *row = Al + sm_row_off(i, cl, rank);
+        for (int c = lane; c <= r; c += 32)
+            row[c] = 0.5 * ((double)J.F[(size_t)r * J.ldF + c] + (double)J.F[(size_t)c * J.ldF + r]);
+    }
+    cluster_sync_all();
+    for (int k = 0; k < n - 1; ++k) {
+        double *x = xv + (k & 1) * n;
+        // ---- 1: all-gather x = A[k+1:n, k]; d_k from row k's owner ----
+        const int i0 = (k + 1 - rank + cl - 1) / cl;             // first own row >= k+1
+        for (int i = i0 + t; i < nl; i += kSmThreads) {
+            const int r = rank + cl * i;
+            const double a = Al[sm_row_off(i, cl, rank) + k];
+            for (int q = 0; q < cl; ++q) st_cluster(map_rank(x + r, q), a);
+        }
+        if (t == 0 && k % cl == rank) J.d[k] = Al[sm_row_off(k / cl, cl, rank) + k];
+        cluster_sync_all();
+        // ---- reflector (dlarfg), the same in every CTA ----
+        double q2 = 0.0;
+        for (int r = k + 2 + t; r < n; r += kSmThreads) q2 += x[r] * x[r];
+        const double nrm2 = block_sum(q2, sh);
+        const double alpha = x[k + 1];
+        double tau = 0.0, beta = alpha, scale = 0.0;
+        if (nrm2 > 0.0) {
+            beta = -copysign(sqrt(alpha * alpha + nrm2), alpha);
+            tau = (beta - alpha) / beta;
+            scale = 1.0 / (alpha - beta);
+        }
+        if (rank == 0 && t == 0) {
+            J.e[k] = beta;
+            J.tau[k] = tau;
+        }
+        __syncthreads();                                         // every thread has read x[k+1]
+        for (int r = k + 1 + t; r < n; r += kSmThreads) x[r] = r == k + 1 ? 1.0 : x[r] * scale;
+        __syncthreads();
+        for (int i = i0 + t; i < nl; i += kSmThreads) {
+            const int r = rank + cl * i;
+            J.Vb[(size_t)r * ldw + k] = (float)x[r];
+        }
+        if (tau == 0.0) continue;                                // H_k = I (the same in every CTA)
+        const double *v = x;
+        // ---- 2: y = A22 v.  Row sums (warp per own row) ----
+        for (int i = i0 + warp; i < nl; i += nwarp) {
+            const int r = rank + cl * i;
+            const double *row = Al + sm_row_off(i, cl, rank);
+            double a = 0.0;
+            for (int c = k + 1 + lane; c <= r; c += 32) a += row[c] * v[c];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+            if (lane == 0) rs[i] = a;
+        }
+        // column sums over own rows below the diagonal (thread per column)
+        for (int c = k + 1 + t; c < n; c += kSmThreads) {
+            double a = 0.0;
+            for (int i = max(i0, (c + 1 - rank + cl - 1) / cl); i < nl; ++i)
+                a += Al[sm_row_off(i, cl, rank) + c] * v[rank + cl * i];
+            cs[c] = a;
+        }
+        __syncthreads();
+        double pv = 0.0;                                         // v^T A v over own rows
+        for (int i = i0 + t; i < nl; i += kSmThreads) {
+            const int r = rank + cl * i;
+            pv += v[r] * (2.0 * rs[i] - Al[sm_row_off(i, cl, rank) + r] * v[r]);
+        }
+        pv = block_sum(pv, sh);
+        if (t == 0) slot[0] = pv;
+        cluster_sync_all();
+        // ---- 3: w = tau y - (tau^2 / 2)(v^T A v) v on own rows, all-gathered ----
+        double vav = 0.0;
+        for (int q = 0; q < cl; ++q) vav += ld_cluster(map_rank(slot, q));
+        const double alpha2 = -0.5 * tau * tau * vav;
+        for (int i = i0 + t; i < nl; i += kSmThreads) {
+            const int r = rank + cl * i;
+            double y = rs[i];
+            for (int q = 0; q < cl; ++q) y += ld_cluster(map_rank(cs + r, q));
+            const double w = tau * y + alpha2 * v[r];
+            for (int q = 0; q < cl; ++q) st_cluster(map_rank(wv + r, q), w);
+        }
+        cluster_sync_all();
+        // A22 -= v w^T + w v^T, own rows
+        for (int i = i0 + warp; i < nl; i += nwarp) {
+            const int r = rank + cl * i;
+            double *row = Al + sm_row_off(i, cl, rank);
+            const double vr = v[r], wr = wv[r];
+            for (int c = k + 1 + lane; c <= r; c += 32) row[c] -= vr * wv[c] + wr * v[c];
+        }
+        __syncthreads();
+    }
+    if (t == 0 && (n - 1) % cl == rank) J.d[n - 1] = Al[sm_row_off((n - 1) / cl, cl, rank) + n - 1];
+    cluster_sync_all();                                          // no CTA exits while others read it
+}
+
 // ------------------------------------------------------------ init --
 // A = (F + F^T)/2 in fp32 (pads zero), Vb = 0.
 __global__ void trd_init(const TrdJob *jobs) {
@@ -1661,6 +1833,50 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
 
 }  // namespace
 
+// Cluster size of the small-factor reduction for order n (0: does not fit kSmMaxCl CTAs).
+int sm_cluster_size(int n) {
+    for (int cl = 1; cl <= kSmMaxCl; ++cl)
+        if (sm_smem_bytes(n, cl) <= kSmSmemCap) return cl;
+    return 0;
+}
+
+kfac_status_t small_reduce(const TrdJob *djobs, const std::vector<TrdJob> &jobs, cudaStream_t s) {
+    KFAC_CUDA_TRY(cudaFuncSetAttribute((const void *)trd_small, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    const int count = (int)jobs.size();
+    for (int cl = 1; cl <= kSmMaxCl; ++cl) {
+        std::vector<int> grp;
+        for (int i = 0; i < count; ++i)
+            if (sm_cluster_size(jobs[i].n) == cl) grp.push_back(i);
+        for (size_t c0 = 0; c0 < grp.size(); c0 += kSmMaxJobs) {
+            thread_local SmallSet SS;
+            const int na = (int)std::min(grp.size() - c0, (size_t)kSmMaxJobs);
+            SS.jobs = djobs;
+            SS.count = na;
+            size_t smem = 0;
+            for (int u = 0; u < na; ++u) {
+                SS.job[u] = grp[c0 + u];
+                smem = std::max(smem, sm_smem_bytes(jobs[grp[c0 + u]].n, cl));
+            }
+            KFAC_CUDA_TRY(set_smem_attr((const void *)trd_small, (int)smem));
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3(na * cl);
+            cfg.blockDim = dim3(kSmThreads);
+            cfg.dynamicSmemBytes = smem;
+            cfg.stream = s;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = cl;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            KFAC_CUDA_TRY(cudaLaunchKernelEx(&cfg, trd_small, SS));
+            KFAC_LAUNCHED();
+        }
+    }
+    return KFAC_OK;
+}
+
 size_t trd_workspace_bytes(const int32_t *dims, int count) { return plan(dims, count).bytes; }
 
 kfac_status_t trd_run(const float *const *F, const int32_t *dims, const int32_t *ldF, int count,
@@ -1728,12 +1944,19 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
     std::vector<Gemm64Desc> gd;
     if (mode != TRD_DEBUG_STEDC) {
     NvtxRange nvtx_red("eigen: tridiagonal reduction");
-    trd_init<<<dim3(std::min(2048, cdiv((long long)ldw_for(max_n), 32) * cdiv((long long)ldw_for(max_n), 32)), count), 256,
-               0, s>>>(djobs);
-    KFAC_LAUNCHED();
-
-    // ---- (1) tridiagonalisation: one persistent launch + one trailing GEMM per panel ----
+    // a call whose factors all fit one cluster's shared memory runs the cluster-resident dsytd2
+    bool small_path = true;
+    for (int i = 0; i < count; ++i)
+        if (P.jobs[i].off != 1 || sm_cluster_size(P.jobs[i].n) == 0) small_path = false;
+    if (!small_path) {
+        trd_init<<<dim3(std::min(2048, cdiv((long long)ldw_for(max_n), 32) * cdiv((long long)ldw_for(max_n), 32)), count),
+                   256, 0, s>>>(djobs);
+        KFAC_LAUNCHED();
+    }
     KFAC_CUDA_TRY(set_smem_attr((const void *)bt_larft, (int)kLarftSmem));
+    if (small_path) RET_OK(small_reduce(djobs, P.jobs, s));
+    if (!small_path) {
+    // ---- (1) tridiagonalisation: one persistent launch + one trailing GEMM per panel ----
     const int ring_off = (int)round_up(round_up(max_n, kSymvC) + kSymvC + 8, 64);
     // v (floats) | symv ring | x of the merged column (doubles, phase B; only if it fits)
     const size_t smem_base = (size_t)ring_off * sizeof(float) + (size_t)kTrdWarps * 2 * 8 * 32 * sizeof(float4);
@@ -1841,6 +2064,7 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
     }
 
     if (!sbr_ids.empty()) RET_OK(sbr::reduce(djobs, P.jobs, sbr_ids, s));
+    }   // !small_path
     }   // mode != TRD_DEBUG_STEDC
     if (mode == TRD_DEBUG_TRIDIAG) {
         KFAC_CUDA_TRY(cudaMemcpyAsync(dbg_d, P.jobs[0].d, sizeof(double) * P.jobs[0].n, cudaMemcpyDeviceToDevice, s));

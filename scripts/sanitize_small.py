@@ -53,6 +53,15 @@ for flags in ((16,) if one_stage else (0, 4 | 8)):        # default routing, the
     assert int(info.abs().max()) == 0
     print("eigen ok flags", flags, flush=True)
 
+# every factor <= ~880: the cluster-resident small-factor reduction (d = 300 on a 2-CTA cluster)
+Q = [torch.zeros_like(F) for F in Fs[1:3]]
+v = [torch.zeros(n, device=dev) for n in dims[1:3]]
+info = torch.zeros(2, dtype=torch.int32, device=dev)
+_lib.kfac_compute_eigen(Fs[1:3], Q, v, info, 0)
+torch.cuda.synchronize()
+assert int(info.abs().max()) == 0
+print("eigen ok (small-factor cluster path)", flush=True)
+
 Finv = [torch.zeros_like(F) for F in Fs[:3]]
 info = torch.zeros(3, dtype=torch.int32, device=dev)
 _lib.kfac_compute_inverse(Fs[:3], 1e-3, Finv, info)
