@@ -44,11 +44,6 @@ kfac_status_t trd_run(const float *const *F, const int32_t *dims, const int32_t 
 namespace {
 
 constexpr int kNb = 32;                 // panel width (reflectors per syr2k)
-#ifndef KFAC_TRD_L2PF_MB
-#define KFAC_TRD_L2PF_MB 96
-#endif
-// symv L2 prefetch threshold: lower-triangle fp32 bytes of a launch's active trailing matrices
-constexpr double kTrdL2pfBytes = KFAC_TRD_L2PF_MB * 1048576.0;
 #ifndef KFAC_TRD_THREADS
 #define KFAC_TRD_THREADS 512
 #endif
@@ -362,8 +357,6 @@ struct PanelLaunch {
     int cta_begin[kMaxGroupCtas + 1];
     int ring_off;                          // float offset of the symv prefetch ring in dynamic smem
     int use_xs;                            // x of the merged column kept in shared memory
-    int l2pf;                              // prefetch each warp's next symv unit into L2 (the active
-                                           // trailing matrices exceed L2: the mat-vec streams from HBM)
 };
 
 // One panel of 32 columns (LAPACK dlatrd, lower) for every active factor.  Column k (i = k - p0):
@@ -605,32 +598,9 @@ __global__ void __launch_bounds__(kTrdThreads, kTrdCtasPerSm) trd_panel(const __
                 }
                 asm volatile("cp.async.commit_group;" ::: "memory");
             };
-            // L2 prefetch of the unit after the current one (the ring holds one octet ahead; when
-            // the trailing matrices stream from HBM that is too few bytes in flight per SM, so each
-            // warp also asks L2 for its next 32-row x 128-column half unit, 16 KB, one unit ahead)
-            auto prefetch_next = [&]() {
-                const int it2 = it + W;
-                if (!L.l2pf || it2 >= total) return;
-                int lo2 = bq, hi2 = nrb - 1;
-                while (lo2 < hi2) {
-                    const int mid = (lo2 + hi2 + 1) >> 1;
-                    if (tpre[mid] <= it2) lo2 = mid; else hi2 = mid - 1;
-                }
-                const int j2 = it2 - tpre[lo2];
-                const int rs = r00 + kPairR * lo2 + kSymvR * half;
-                const int rend = min(n, rs + kSymvR);
-                const int cl = c0 + kSymvC * j2 + 32 * (lane & 3);     // this lane's 128-byte line
-#pragma unroll
-                for (int u = 0; u < kSymvR / 8; ++u) {
-                    const int rr = rs + (lane >> 2) + 8 * u;
-                    if (rr < rend && cl <= rr)
-                        asm volatile("prefetch.global.L2 [%0];" ::"l"(A + (size_t)rr * ldw + cl));
-                }
-            };
             if (it < total) {
                 locate();
                 issue(0);
-                prefetch_next();
             }
             // panel dot partials over the owned rows (lane q -> panel column q), loads in flight
             // together with the first symv octet
@@ -659,10 +629,7 @@ __global__ void __launch_bounds__(kTrdThreads, kTrdCtasPerSm) trd_panel(const __
                 const bool unit_end = rq >= r1;
                 if (unit_end) {
                     it += W;
-                    if (it < total) {
-                        locate();
-                        prefetch_next();
-                    }
+                    if (it < total) locate();
                 }
                 const bool more = it < total;
                 if (more) {
@@ -2020,14 +1987,6 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
         PL.count = na;
         PL.ring_off = ring_off;
         PL.use_xs = use_xs;
-        {   // L2 prefetch only when the launch's lower-triangle working set exceeds most of L2
-            double ws_bytes = 0.0;
-            for (int q = 0; q < na; ++q) {
-                const double m = P.jobs[act[q]].n - pst[q];
-                ws_bytes += 2.0 * m * m;
-            }
-            PL.l2pf = ws_bytes > kTrdL2pfBytes ? 1 : 0;
-        }
         int tot = 0;
         for (int q = 0; q < na; ++q) {
             PL.job[q] = act[q];
