@@ -153,10 +153,18 @@ __host__ __device__ inline long long sm_row_off(int i, int cl, int rank) {
     return (long long)cl * i * (i - 1) / 2 + (long long)i * (rank + 1);
 }
 __host__ __device__ inline int sm_rows(int n, int cl, int rank) { return rank < n ? (n - rank + cl - 1) / cl : 0; }
+// largest local triangle over the cluster's CTAs (doubles): every CTA uses the same layout
+__host__ __device__ inline long long sm_tri_max(int n, int cl) {
+    long long m = 0;
+    for (int r = 0; r < cl; ++r) {
+        const long long t = sm_row_off(sm_rows(n, cl, r), cl, r);
+        m = t > m ? t : m;
+    }
+    return m;
+}
 // dynamic shared memory of one CTA: triangle | x/v (2 buffers) | w | column sums | row sums | slots
 __host__ __device__ inline size_t sm_smem_bytes(int n, int cl) {
-    const int nl = sm_rows(n, cl, 0);
-    return sizeof(double) * ((size_t)sm_row_off(nl, cl, 0) + 4 * (size_t)n + (size_t)nl + 64);
+    return sizeof(double) * ((size_t)sm_tri_max(n, cl) + 4 * (size_t)n + (size_t)sm_rows(n, cl, 0) + 64);
 }
 
 __device__ __forceinline__ void cluster_sync_all() {
@@ -196,7 +204,7 @@ __global__ void __launch_bounds__(kSmThreads, 1) trd_small(const __grid_constant
     const int t = threadIdx.x, lane = t % 32, warp = t / 32, nwarp = kSmThreads / 32;
     const int nl = sm_rows(n, cl, rank);
     double *Al = smd;                                            // local lower triangle
-    double *xv = Al + sm_row_off(sm_rows(n, cl, 0), cl, 0);      // [2][n]: x, then v (by column parity)
+    double *xv = Al + sm_tri_max(n, cl);                         // [2][n]: x, then v (by column parity)
     double *wv = xv + 2 * n;                                     // [n]: w
     double *cs = wv + n;                                         // [n]: column sums over own rows
     double *rs = cs + n;                                         // [nl]: row sums of own rows
@@ -257,8 +265,14 @@ __global__ void __launch_bounds__(kSmThreads, 1) trd_small(const __grid_constant
         // column sums over own rows below the diagonal (thread per column)
         for (int c = k + 1 + t; c < n; c += kSmThreads) {
             double a = 0.0;
-            for (int i = max(i0, (c + 1 - rank + cl - 1) / cl); i < nl; ++i)
-                a += Al[sm_row_off(i, cl, rank) + c] * v[rank + cl * i];
+            int i = max(i0, (c + 1 - rank + cl - 1) / cl);
+            long long o = sm_row_off(i, cl, rank) + c;
+#pragma unroll 4
+            for (; i < nl; ++i) {                                // row i + 1 starts r + 1 doubles later
+                const int r = rank + cl * i;
+                a += Al[o] * v[r];
+                o += r + 1;
+            }
             cs[c] = a;
         }
         __syncthreads();
@@ -271,13 +285,21 @@ __global__ void __launch_bounds__(kSmThreads, 1) trd_small(const __grid_constant
         if (t == 0) slot[0] = pv;
         cluster_sync_all();
         // ---- 3: w = tau y - (tau^2 / 2)(v^T A v) v on own rows, all-gathered ----
+        // remote loads issued together, then summed in rank order (bit-identical in every CTA)
+        double rp[kSmMaxCl];
+#pragma unroll
+        for (int q = 0; q < kSmMaxCl; ++q) rp[q] = q < cl ? ld_cluster(map_rank(slot, q)) : 0.0;
         double vav = 0.0;
-        for (int q = 0; q < cl; ++q) vav += ld_cluster(map_rank(slot, q));
+#pragma unroll
+        for (int q = 0; q < kSmMaxCl; ++q) vav += rp[q];
         const double alpha2 = -0.5 * tau * tau * vav;
         for (int i = i0 + t; i < nl; i += kSmThreads) {
             const int r = rank + cl * i;
+#pragma unroll
+            for (int q = 0; q < kSmMaxCl; ++q) rp[q] = q < cl ? ld_cluster(map_rank(cs + r, q)) : 0.0;
             double y = rs[i];
-            for (int q = 0; q < cl; ++q) y += ld_cluster(map_rank(cs + r, q));
+#pragma unroll
+            for (int q = 0; q < kSmMaxCl; ++q) y += rp[q];
             const double w = tau * y + alpha2 * v[r];
             for (int q = 0; q < cl; ++q) st_cluster(map_rank(wv + r, q), w);
         }
