@@ -208,7 +208,8 @@ __global__ void __launch_bounds__(kSmThreads, 1) trd_small(const __grid_constant
     double *wv = xv + 2 * n;                                     // [n]: w
     double *cs = wv + n;                                         // [n]: column sums over own rows
     double *rs = cs + n;                                         // [nl]: row sums of own rows
-    double *slot = rs + nl;                                      // [0]: partial v^T A v
+    double *slot = rs + sm_rows(n, cl, 0);                       // [0]: partial v^T A v (same offset in
+                                                                 // every CTA: read through the cluster)
     // A = (F + F^T)/2 in fp64, own rows
     for (int i = warp; i < nl; i += nwarp) {
         const int r = rank + cl * i;
