@@ -162,13 +162,22 @@ __host__ __device__ inline long long sm_tri_max(int n, int cl) {
     }
     return m;
 }
-// dynamic shared memory of one CTA: triangle | x/v (2 buffers) | w | column sums | row sums | slots
+constexpr int kSmBlk = 32;              // columns of outputs buffered in shared memory per flush
+// dynamic shared memory of one CTA: triangle | x/v (2 buffers) | w | column sums | row sums | slots |
+// output buffers (the own rows' reflector entries and d, e, tau of kSmBlk columns)
 __host__ __device__ inline size_t sm_smem_bytes(int n, int cl) {
-    return sizeof(double) * ((size_t)sm_tri_max(n, cl) + 4 * (size_t)n + (size_t)sm_rows(n, cl, 0) + 64);
+    const size_t nl0 = (size_t)sm_rows(n, cl, 0);
+    return sizeof(double) * ((size_t)sm_tri_max(n, cl) + 4 * (size_t)n + nl0 + 64 + (kSmBlk * nl0 + 1) / 2 +
+                             3 * kSmBlk);
 }
 
 __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// the small reduction's barrier: a CTA barrier when the cluster is one CTA (cl is uniform)
+__device__ __forceinline__ void sm_sync(int cl) {
+    if (cl == 1) __syncthreads();
+    else cluster_sync_all();
 }
 __device__ __forceinline__ uint32_t cluster_rank() {
     uint32_t r;
@@ -208,8 +217,28 @@ __global__ void __launch_bounds__(kSmThreads, 1) trd_small(const __grid_constant
     double *wv = xv + 2 * n;                                     // [n]: w
     double *cs = wv + n;                                         // [n]: column sums over own rows
     double *rs = cs + n;                                         // [nl]: row sums of own rows
-    double *slot = rs + sm_rows(n, cl, 0);                       // [0]: partial v^T A v (same offset in
+    const int nl0 = sm_rows(n, cl, 0);
+    double *slot = rs + nl0;                                     // [0]: partial v^T A v (same offset in
                                                                  // every CTA: read through the cluster)
+    // outputs are buffered for kSmBlk columns and written together: a global store outstanding at a
+    // cluster barrier's release would make that barrier wait for it
+    float *vbuf = reinterpret_cast<float *>(slot + 64);          // [kSmBlk][nl0] own rows' v entries
+    double *dbuf = slot + 64 + (kSmBlk * nl0 + 1) / 2;           // [3][kSmBlk]: d, e, tau
+    auto flush = [&](int k0, int nb) {                           // columns k0 .. k0 + nb - 1
+        __syncthreads();
+        const int ib = (k0 + 1 - rank + cl - 1) / cl;
+        for (int e = t; e < (nl - ib) * nb; e += kSmThreads) {
+            const int i = ib + e / nb, j = e % nb;
+            J.Vb[(size_t)(rank + cl * i) * ldw + k0 + j] = vbuf[j * nl0 + i];   // rows <= k0 + j: masked
+        }
+        for (int j = t; j < nb; j += kSmThreads) {
+            if ((k0 + j) % cl == rank) J.d[k0 + j] = dbuf[j];
+            if (rank == 0) {
+                J.e[k0 + j] = dbuf[kSmBlk + j];
+                J.tau[k0 + j] = dbuf[2 * kSmBlk + j];
+            }
+        }
+    };
     // A = (F + F^T)/2 in fp64, own rows
     for (int i = warp; i < nl; i += nwarp) {
         const int r = rank + cl * i;
@@ -217,9 +246,10 @@ __global__ void __launch_bounds__(kSmThreads, 1) trd_small(const __grid_constant
         for (int c = lane; c <= r; c += 32)
             row[c] = 0.5 * ((double)J.F[(size_t)r * J.ldF + c] + (double)J.F[(size_t)c * J.ldF + r]);
     }
-    cluster_sync_all();
+    sm_sync(cl);
     for (int k = 0; k < n - 1; ++k) {
         double *x = xv + (k & 1) * n;
+        const int jb = k % kSmBlk;
         // ---- 1: all-gather x = A[k+1:n, k]; d_k from row k's owner ----
         const int i0 = (k + 1 - rank + cl - 1) / cl;             // first own row >= k+1
         for (int i = i0 + t; i < nl; i += kSmThreads) {
@@ -227,8 +257,8 @@ __global__ void __launch_bounds__(kSmThreads, 1) trd_small(const __grid_constant
             const double a = Al[sm_row_off(i, cl, rank) + k];
             for (int q = 0; q < cl; ++q) st_cluster(map_rank(x + r, q), a);
         }
-        if (t == 0 && k % cl == rank) J.d[k] = Al[sm_row_off(k / cl, cl, rank) + k];
-        cluster_sync_all();
+        if (t == 0 && k % cl == rank) dbuf[jb] = Al[sm_row_off(k / cl, cl, rank) + k];
+        sm_sync(cl);
         // ---- reflector (dlarfg), the same in every CTA ----
         double q2 = 0.0;
         for (int r = k + 2 + t; r < n; r += kSmThreads) q2 += x[r] * x[r];
@@ -241,16 +271,14 @@ __global__ void __launch_bounds__(kSmThreads, 1) trd_small(const __grid_constant
             scale = 1.0 / (alpha - beta);
         }
         if (rank == 0 && t == 0) {
-            J.e[k] = beta;
-            J.tau[k] = tau;
+            dbuf[kSmBlk + jb] = beta;
+            dbuf[2 * kSmBlk + jb] = tau;
         }
         __syncthreads();                                         // every thread has read x[k+1]
         for (int r = k + 1 + t; r < n; r += kSmThreads) x[r] = r == k + 1 ? 1.0 : x[r] * scale;
         __syncthreads();
-        for (int i = i0 + t; i < nl; i += kSmThreads) {
-            const int r = rank + cl * i;
-            J.Vb[(size_t)r * ldw + k] = (float)x[r];
-        }
+        for (int i = i0 + t; i < nl; i += kSmThreads) vbuf[jb * nl0 + i] = (float)x[rank + cl * i];
+        if (jb == kSmBlk - 1 || k == n - 2) flush(k - jb, jb + 1);
         if (tau == 0.0) continue;                                // H_k = I (the same in every CTA)
         const double *v = x;
         // ---- 2: y = A22 v.  Row sums (warp per own row) ----
@@ -284,7 +312,7 @@ __global__ void __launch_bounds__(kSmThreads, 1) trd_small(const __grid_constant
         }
         pv = block_sum(pv, sh);
         if (t == 0) slot[0] = pv;
-        cluster_sync_all();
+        sm_sync(cl);
         // ---- 3: w = tau y - (tau^2 / 2)(v^T A v) v on own rows, all-gathered ----
         // remote loads issued together, then summed in rank order (bit-identical in every CTA)
         double rp[kSmMaxCl];
@@ -304,7 +332,7 @@ __global__ void __launch_bounds__(kSmThreads, 1) trd_small(const __grid_constant
             const double w = tau * y + alpha2 * v[r];
             for (int q = 0; q < cl; ++q) st_cluster(map_rank(wv + r, q), w);
         }
-        cluster_sync_all();
+        sm_sync(cl);
         // A22 -= v w^T + w v^T, own rows
         for (int i = i0 + warp; i < nl; i += nwarp) {
             const int r = rank + cl * i;
@@ -315,7 +343,7 @@ __global__ void __launch_bounds__(kSmThreads, 1) trd_small(const __grid_constant
         __syncthreads();
     }
     if (t == 0 && (n - 1) % cl == rank) J.d[n - 1] = Al[sm_row_off((n - 1) / cl, cl, rank) + n - 1];
-    cluster_sync_all();                                          // no CTA exits while others read it
+    sm_sync(cl);                                                 // no CTA exits while others read it
 }
 
 // ------------------------------------------------------------ init --
