@@ -57,9 +57,14 @@ constexpr int kLeaf = 32;               // D&C leaf size
 #define KFAC_SYMV_ROWS 32
 #endif
 constexpr int kSymvR = KFAC_SYMV_ROWS;  // symv tile rows (lower triangle only), multiple of 8
+// Rows per warp half of the symv unit in the launches with a single active factor (a lone factor:
+// one rank's share at W >= 4): finer units balance the unit count over the warp pairs (measured:
+// lone d = 4609 116 -> 107 ms with 24 rows, the batched ResNet-50 launches slower, session r2q).
+constexpr int kSymvRLone = 24;
+constexpr int kSymvRMin = kSymvRLone < kSymvR ? kSymvRLone : kSymvR;   // sizes the TP partials
 constexpr int kSymvC = 128;             // symv tile columns (one float4 per lane)
 constexpr int kPairR = 2 * kSymvR;       // rows per column partial (a warp pair's two half tiles)
-constexpr int kMaxRb = 16384 / kPairR;   // super blocks for n <= 16384
+constexpr int kMaxRb = (16384 / kPairR + 31) / 32 * 32;   // super blocks for n <= 16384
 #ifndef KFAC_SYMV_FP32
 #define KFAC_SYMV_FP32 1                  // fp32 products with 4/8-term fp32 partial sums, fp64 beyond (R23)
 #endif
@@ -417,7 +422,12 @@ struct PanelLaunch {
 //   C: y -= W (V^T v) + V (W^T v);  w = tau y;  partial w^T v
 //   D: W[:, i] = w - (tau/2)(w^T v) v
 // so that after the panel A_p[q:n, q:n] - V W^T - W V^T is the reduced trailing matrix (q = p0+32).
+template <int SYMV_ROWS>
 __global__ void __launch_bounds__(kTrdThreads, kTrdCtasPerSm) trd_panel(const __grid_constant__ PanelLaunch L) {
+    // the symv unit geometry of this instantiation (shadows the namespace defaults)
+    constexpr int kSymvR = SYMV_ROWS;
+    constexpr int kPairR = 2 * kSymvR;
+    constexpr int kMaxRb = (16384 / kPairR + 31) / 32 * 32;
     extern __shared__ __align__(16) float vsm[];     // v, 4-aligned, zero padded
     __shared__ double sh[kTrdWarps];
     __shared__ double red[kTrdWarps][2 * kNb];
@@ -1778,7 +1788,7 @@ Plan plan(const int32_t *dims, int count) {
         TAKE(part, double, (size_t)kMaxGroupCtas * kPart);
         J.ldp = cdiv(n + 3, kSymvC) + 1;
         TAKE(DP, double, (size_t)n * J.ldp);
-        J.ldtp = cdiv(n, kPairR) + 1;
+        J.ldtp = cdiv(n, 2 * kSymvRMin) + 1;
         TAKE(TP, double, (size_t)n * J.ldtp);
 #undef TAKE
         // leaves and merges
@@ -1835,8 +1845,12 @@ T *rebase(T *p, char *base) {           // offsets from plan(); fields a factor 
 
 int panel_capacity(size_t smem) {
     int per_sm = 0;
-    set_smem_attr((const void *)trd_panel, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, trd_panel, kTrdThreads, smem);
+    set_smem_attr((const void *)trd_panel<kSymvR>, (int)smem);
+    set_smem_attr((const void *)trd_panel<kSymvRLone>, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, trd_panel<kSymvR>, kTrdThreads, smem);
+    int per_sm_lone = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_lone, trd_panel<kSymvRLone>, kTrdThreads, smem);
+    per_sm = std::min(per_sm, per_sm_lone);
     return std::min(std::max(1, per_sm) * num_sms(), kMaxGroupCtas);
 }
 
@@ -2049,7 +2063,8 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
         KFAC_CUDA_TRY(cudaMemsetAsync(base + P.bar_off, 0, (size_t)count * 64, s));   // every counter, one call
         void *args[] = {&PL};
         const int prof = prof_begin(KFAC_PROF_TRD_PANEL, s);
-        KFAC_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)trd_panel, dim3(tot), dim3(kTrdThreads), args, smem, s));
+        const void *kern = na == 1 ? (const void *)trd_panel<kSymvRLone> : (const void *)trd_panel<kSymvR>;
+        KFAC_CUDA_TRY(cudaLaunchCooperativeKernel(kern, dim3(tot), dim3(kTrdThreads), args, smem, s));
         KFAC_LAUNCHED();
         if (prof >= 0) {
             // algorithmic work: per column k, the lower triangle of the m x m trailing matrix
