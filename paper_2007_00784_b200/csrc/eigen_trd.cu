@@ -2040,7 +2040,8 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
         int spare = cap - na;
         for (int q = 0; q < na; ++q) {
             const double m = P.jobs[act[q]].n - pst[q];
-            const int tiles = cdiv((long long)m, kSymvR) * (cdiv((long long)m, kSymvC) + 1) / 2;
+            const int srows = na == 1 ? kSymvRLone : kSymvR;   // the instantiation this launch uses
+            const int tiles = cdiv((long long)m, srows) * (cdiv((long long)m, kSymvC) + 1) / 2;
             int want = (int)std::floor((cap - na) * std::pow(m, wexp) / wsum);
             want = std::min(want, std::max(0, (int)(m / 16) - 1));
             want = std::min(want, std::max(0, cdiv(tiles, kTrdWarps) - 1));
