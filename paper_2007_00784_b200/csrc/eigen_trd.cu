@@ -57,9 +57,9 @@ constexpr int kLeaf = 32;               // D&C leaf size
 #define KFAC_SYMV_ROWS 32
 #endif
 constexpr int kSymvR = KFAC_SYMV_ROWS;  // symv tile rows (lower triangle only), multiple of 8
-// Rows per warp half of the symv unit in the launches with a single active factor (a lone factor:
-// one rank's share at W >= 4): finer units balance the unit count over the warp pairs (measured:
-// lone d = 4609 116 -> 107 ms with 24 rows, the batched ResNet-50 launches slower, session r2q).
+// Rows per warp half of the finer symv unit geometry, the alternative each launch may take (the
+// host picks per launch the geometry whose busiest warp pair streams the fewest rows; measured:
+// lone d = 4609 116 -> 107 ms with 24 rows throughout, session r2q).
 constexpr int kSymvRLone = 24;
 constexpr int kSymvRMin = kSymvRLone < kSymvR ? kSymvRLone : kSymvR;   // sizes the TP partials
 constexpr int kSymvC = 128;             // symv tile columns (one float4 per lane)
@@ -2034,21 +2034,35 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
             wsum += std::pow(m, wexp);
         }
         const int na = (int)act.size();
-        // CTAs per factor ~ remaining work, >= 1, total <= cap, and no more than one 64 x 128 symv
-        // tile per warp (more CTAs would only add barrier participants and partials)
-        std::vector<int> nc(na, 1);
-        int spare = cap - na;
-        for (int q = 0; q < na; ++q) {
-            const double m = P.jobs[act[q]].n - pst[q];
-            const int srows = na == 1 ? kSymvRLone : kSymvR;   // the instantiation this launch uses
-            const int tiles = cdiv((long long)m, srows) * (cdiv((long long)m, kSymvC) + 1) / 2;
-            int want = (int)std::floor((cap - na) * std::pow(m, wexp) / wsum);
-            want = std::min(want, std::max(0, (int)(m / 16) - 1));
-            want = std::min(want, std::max(0, cdiv(tiles, kTrdWarps) - 1));
-            want = std::min(want, spare);
-            nc[q] += want;
-            spare -= want;
-        }
+        // CTAs per factor ~ remaining work, >= 1, total <= cap, and no more than one symv unit per warp
+        // (more CTAs would only add barrier participants and partials).  Two unit geometries are
+        // instantiated (32- and 24-row warp halves); the launch takes the one whose busiest warp pair
+        // streams the fewest rows: units are indivisible, so the pair count rarely divides the unit
+        // count and the finer units often cut the critical pair's share (measured on a lone d = 4609
+        // factor: 116 -> 107 ms)
+        auto plan_groups = [&](int srows, std::vector<int> &nc) {
+            nc.assign(na, 1);
+            int spare = cap - na;
+            double worst = 0.0;
+            for (int q = 0; q < na; ++q) {
+                const double m = P.jobs[act[q]].n - pst[q];
+                const int tiles = cdiv((long long)m, srows) * (cdiv((long long)m, kSymvC) + 1) / 2;
+                int want = (int)std::floor((cap - na) * std::pow(m, wexp) / wsum);
+                want = std::min(want, std::max(0, (int)(m / 16) - 1));
+                want = std::min(want, std::max(0, cdiv(tiles, kTrdWarps) - 1));
+                want = std::min(want, spare);
+                nc[q] += want;
+                spare -= want;
+                const long long units = cdiv((long long)m, 2 * srows) * (cdiv((long long)m, kSymvC) + 1) / 2;
+                const double per_pair = (double)cdiv(units, (long long)nc[q] * (kTrdWarps / 2));
+                worst = std::max(worst, per_pair * (2 * srows + 8));      // rows streamed + per-unit cost
+            }
+            return worst;
+        };
+        std::vector<int> nc, nc_lone;
+        const double cost = plan_groups(kSymvR, nc), cost_lone = plan_groups(kSymvRLone, nc_lone);
+        const bool fine = cost_lone < cost;
+        if (fine) nc.swap(nc_lone);
         PL.jobs = djobs;
         PL.count = na;
         PL.ring_off = ring_off;
@@ -2064,7 +2078,7 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
         KFAC_CUDA_TRY(cudaMemsetAsync(base + P.bar_off, 0, (size_t)count * 64, s));   // every counter, one call
         void *args[] = {&PL};
         const int prof = prof_begin(KFAC_PROF_TRD_PANEL, s);
-        const void *kern = na == 1 ? (const void *)trd_panel<kSymvRLone> : (const void *)trd_panel<kSymvR>;
+        const void *kern = fine ? (const void *)trd_panel<kSymvRLone> : (const void *)trd_panel<kSymvR>;
         KFAC_CUDA_TRY(cudaLaunchCooperativeKernel(kern, dim3(tot), dim3(kTrdThreads), args, smem, s));
         KFAC_LAUNCHED();
         if (prof >= 0) {
