@@ -157,6 +157,8 @@ struct SmallSet {
 __host__ __device__ inline long long sm_row_off(int i, int cl, int rank) {
     return (long long)cl * i * (i - 1) / 2 + (long long)i * (rank + 1);
 }
+// the same in 32-bit arithmetic (device: a CTA's triangle holds < 2^15 doubles)
+__device__ __forceinline__ int sm_off(int i, int cl, int rank) { return (cl * i * (i - 1) >> 1) + i * (rank + 1); }
 __host__ __device__ inline int sm_rows(int n, int cl, int rank) { return rank < n ? (n - rank + cl - 1) / cl : 0; }
 // largest local triangle over the cluster's CTAs (doubles): every CTA uses the same layout
 __host__ __device__ inline long long sm_tri_max(int n, int cl) {
@@ -247,7 +249,7 @@ __global__ void __launch_bounds__(kSmThreads, 1) trd_small(const __grid_constant
     // A = (F + F^T)/2 in fp64, own rows
     for (int i = warp; i < nl; i += nwarp) {
         const int r = rank + cl * i;
-        double *row = Al + sm_row_off(i, cl, rank);
+        double *row = Al + sm_off(i, cl, rank);
         for (int c = lane; c <= r; c += 32)
             row[c] = 0.5 * ((double)J.F[(size_t)r * J.ldF + c] + (double)J.F[(size_t)c * J.ldF + r]);
     }
@@ -259,10 +261,10 @@ __global__ void __launch_bounds__(kSmThreads, 1) trd_small(const __grid_constant
         const int i0 = (k + 1 - rank + cl - 1) / cl;             // first own row >= k+1
         for (int i = i0 + t; i < nl; i += kSmThreads) {
             const int r = rank + cl * i;
-            const double a = Al[sm_row_off(i, cl, rank) + k];
+            const double a = Al[sm_off(i, cl, rank) + k];
             for (int q = 0; q < cl; ++q) st_cluster(map_rank(x + r, q), a);
         }
-        if (t == 0 && k % cl == rank) dbuf[jb] = Al[sm_row_off(k / cl, cl, rank) + k];
+        if (t == 0 && k % cl == rank) dbuf[jb] = Al[sm_off(k / cl, cl, rank) + k];
         sm_sync(cl);
         // ---- reflector (dlarfg), the same in every CTA ----
         double q2 = 0.0;
@@ -289,9 +291,15 @@ __global__ void __launch_bounds__(kSmThreads, 1) trd_small(const __grid_constant
         // ---- 2: y = A22 v.  Row sums (warp per own row) ----
         for (int i = i0 + warp; i < nl; i += nwarp) {
             const int r = rank + cl * i;
-            const double *row = Al + sm_row_off(i, cl, rank);
-            double a = 0.0;
-            for (int c = k + 1 + lane; c <= r; c += 32) a += row[c] * v[c];
+            const double *row = Al + sm_off(i, cl, rank);
+            double a = 0.0, a2 = 0.0;
+            int c = k + 1 + lane;
+            for (; c + 32 <= r; c += 64) {
+                a += row[c] * v[c];
+                a2 += row[c + 32] * v[c + 32];
+            }
+            if (c <= r) a += row[c] * v[c];
+            a += a2;
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
             if (lane == 0) rs[i] = a;
@@ -300,20 +308,24 @@ __global__ void __launch_bounds__(kSmThreads, 1) trd_small(const __grid_constant
         for (int c = k + 1 + t; c < n; c += kSmThreads) {
             double a = 0.0;
             int i = max(i0, (c + 1 - rank + cl - 1) / cl);
-            long long o = sm_row_off(i, cl, rank) + c;
-#pragma unroll 4
-            for (; i < nl; ++i) {                                // row i + 1 starts r + 1 doubles later
-                const int r = rank + cl * i;
+            int o = sm_off(i, cl, rank) + c, r = rank + cl * i;
+            double a2 = 0.0;                                     // two chains (fixed order: even/odd rows)
+            for (; i + 1 < nl; i += 2) {                         // row i + 1 starts r + 1 doubles later
                 a += Al[o] * v[r];
                 o += r + 1;
+                a2 += Al[o] * v[r + cl];
+                o += r + cl + 1;
+                r += 2 * cl;
             }
+            if (i < nl) a += Al[o] * v[r];
+            a += a2;
             cs[c] = a;
         }
         __syncthreads();
         double pv = 0.0;                                         // v^T A v over own rows
         for (int i = i0 + t; i < nl; i += kSmThreads) {
             const int r = rank + cl * i;
-            pv += v[r] * (2.0 * rs[i] - Al[sm_row_off(i, cl, rank) + r] * v[r]);
+            pv += v[r] * (2.0 * rs[i] - Al[sm_off(i, cl, rank) + r] * v[r]);
         }
         pv = block_sum(pv, sh);
         if (t == 0) slot[0] = pv;
@@ -341,13 +353,14 @@ __global__ void __launch_bounds__(kSmThreads, 1) trd_small(const __grid_constant
         // A22 -= v w^T + w v^T, own rows
         for (int i = i0 + warp; i < nl; i += nwarp) {
             const int r = rank + cl * i;
-            double *row = Al + sm_row_off(i, cl, rank);
+            double *row = Al + sm_off(i, cl, rank);
             const double vr = v[r], wr = wv[r];
+#pragma unroll 2
             for (int c = k + 1 + lane; c <= r; c += 32) row[c] -= vr * wv[c] + wr * v[c];
         }
         __syncthreads();
     }
-    if (t == 0 && (n - 1) % cl == rank) J.d[n - 1] = Al[sm_row_off((n - 1) / cl, cl, rank) + n - 1];
+    if (t == 0 && (n - 1) % cl == rank) J.d[n - 1] = Al[sm_off((n - 1) / cl, cl, rank) + n - 1];
     sm_sync(cl);                                                 // no CTA exits while others read it
 }
 
