@@ -181,6 +181,91 @@ __global__ void __launch_bounds__(NT) syrk_partial_kernel(const __grid_constant_
     }
 }
 
+// Small factors (d <= 64, the ones the tensor-core engine does not take: ResNet-32's gradient
+// factors d_G = 16 / 32 and its conv1 d_A = 28, the MLP's d_G = 10): the 128 x 128 SIMT tile would
+// spend (128/d)^2 of its FMAs on padding.  Here one CTA per row chunk stages 128 rows x d columns
+// of X = [im2col | 1] (or of the gradient rows) in shared memory and each thread accumulates one
+// upper-triangle entry (or a 1/P share of its rows, combined in a fixed order), fp32 like the SIMT
+// tile; the partial lands where the SIMT tile would put it, so the fold is unchanged.
+constexpr int kSmallD = 64;
+constexpr int kSmallRows = 128;
+
+__global__ void __launch_bounds__(256) syrk_small_kernel(const __grid_constant__ FactorBatch batch) {
+    __shared__ float X[kSmallRows][kSmallD + 1];
+    __shared__ ColInfo cinf[kSmallD];
+    __shared__ int rorg[kSmallRows][3];          // per staged row: element offset of the receptive
+                                                 // field origin, ih0, iw0 (A); -1 offset: past the end
+    __shared__ float red[256];
+    const int item = blockIdx.x;
+    const FactorJob &J = batch.j[find_job(batch, item, false)];
+    const int split = item - J.item_begin;       // one tile (d <= 64 < T): item = split
+    const int t = threadIdx.x, d = J.d;
+    const int E = d * (d + 1) / 2, P = max(1, 256 / E);
+    const bool active = t < E * P;
+    const int e = active ? t % E : 0, p = active ? t / E : 0;
+    int ei = 0, ej = 0;                          // entry e of the row-major upper triangle
+    {
+        int rem = e;
+        while (rem >= d - ei) { rem -= d - ei; ++ei; }
+        ej = ei + rem;
+    }
+    if (t < d) cinf[t] = col_info(J, t);
+    const long long r_begin = (long long)split * J.chunk;
+    const long long r_end = min(J.n, r_begin + J.chunk);
+    const int hw = J.h_out * J.w_out;
+    float acc = 0.f, acc2 = 0.f;
+    for (long long r0 = r_begin; r0 < r_end; r0 += kSmallRows) {
+        const int nr = (int)min((long long)kSmallRows, r_end - r0);
+        __syncthreads();                         // previous step's reads done (and cinf ready)
+        if (J.is_a && t < kSmallRows) {
+            const long long r = r0 + t;
+            if (t < nr) {
+                const int img = (int)(r / hw);
+                const int pp = (int)(r - (long long)img * hw);
+                const int oh = pp / J.w_out, ow = pp - oh * J.w_out;
+                const int ih0 = oh * J.stride_h - J.pad_h, iw0 = ow * J.stride_w - J.pad_w;
+                rorg[t][0] = ((img * J.h_in + ih0) * J.w_in + iw0) * J.c_in;
+                rorg[t][1] = ih0;
+                rorg[t][2] = iw0;
+            }
+        }
+        if (J.is_a) __syncthreads();
+        for (int q = t; q < kSmallRows * d; q += 256) {
+            const int rr = q / d, c = q - rr * d;
+            float v = 0.f;
+            if (rr < nr) {
+                const ColInfo ci = cinf[c];
+                if (!J.is_a) {
+                    v = __ldg(J.src + (r0 + rr) * J.c_in + ci.off);
+                } else if (ci.kind == 1) {
+                    v = 1.f;
+                } else if (ci.kind == 0) {
+                    const int ih = rorg[rr][1] + ci.kh, iw = rorg[rr][2] + ci.kw;
+                    if (ih >= 0 && ih < J.h_in && iw >= 0 && iw < J.w_in) v = __ldg(J.src + rorg[rr][0] + ci.off);
+                }
+            }
+            X[rr][c] = v;
+        }
+        __syncthreads();
+        if (active) {
+            int rr = p;
+            for (; rr + P < nr; rr += 2 * P) {
+                acc = fmaf(X[rr][ei], X[rr][ej], acc);
+                acc2 = fmaf(X[rr + P][ei], X[rr + P][ej], acc2);
+            }
+            if (rr < nr) acc = fmaf(X[rr][ei], X[rr][ej], acc);
+        }
+    }
+    acc += acc2;
+    red[t] = acc;
+    __syncthreads();
+    if (active && p == 0) {
+        float sum = 0.f;
+        for (int q = 0; q < P; ++q) sum += red[q * E + e];     // fixed order over the row phases
+        J.partial[(size_t)split * J.tiles * (T * T) + ei * T + ej] = sum;
+    }
+}
+
 // Column of the SYRK's (possibly channel-padded) geometry that holds column c of the real factor.
 __device__ __forceinline__ int padded_col(const FactorJob &J, int c) {
     if (!J.c_real || !J.is_a) return c;                  // no padding, or padding after the last column
@@ -338,12 +423,27 @@ kfac_status_t factors_run(const kfac_layer_t *layers, int nl, const float *const
         kfac_status_t st = syrk_tc_partial(tc.data(), (int)tc.size(), s);
         if (st != KFAC_OK) return st;
     }
-    for (size_t b0 = 0; b0 < simt.size(); b0 += kMaxJobs) {
+    std::vector<FactorJob> small, tile;
+    for (auto &j : simt) (j.d <= kSmallD && input_elems(j) < (1ll << 31) ? small : tile).push_back(j);
+    for (size_t b0 = 0; b0 < small.size(); b0 += kMaxJobs) {
         FactorBatch fb;
         fb.count = 0;
         int items = 0;
-        for (size_t i = b0; i < simt.size() && fb.count < kMaxJobs; ++i) {
-            FactorJob j = simt[i];
+        for (size_t i = b0; i < small.size() && fb.count < kMaxJobs; ++i) {
+            FactorJob j = small[i];
+            j.item_begin = items;
+            items += j.splits;                       // one tile
+            fb.j[fb.count++] = j;
+        }
+        syrk_small_kernel<<<items, 256, 0, s>>>(fb);
+        KFAC_LAUNCHED();
+    }
+    for (size_t b0 = 0; b0 < tile.size(); b0 += kMaxJobs) {
+        FactorBatch fb;
+        fb.count = 0;
+        int items = 0;
+        for (size_t i = b0; i < tile.size() && fb.count < kMaxJobs; ++i) {
+            FactorJob j = tile[i];
             j.item_begin = items;
             items += j.tiles * j.splits;
             fb.j[fb.count++] = j;
