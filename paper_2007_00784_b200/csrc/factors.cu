@@ -189,8 +189,9 @@ __global__ void __launch_bounds__(NT) syrk_partial_kernel(const __grid_constant_
 // tile; the partial lands where the SIMT tile would put it, so the fold is unchanged.
 constexpr int kSmallD = 64;
 constexpr int kSmallRows = 128;
+constexpr int kSmallEpt = (kSmallD * (kSmallD + 1) / 2 + 255) / 256;   // upper entries per thread (9)
 
-__global__ void __launch_bounds__(256) syrk_small_kernel(const __grid_constant__ FactorBatch batch) {
+__global__ void __launch_bounds__(256, 2) syrk_small_kernel(const __grid_constant__ FactorBatch batch) {
     __shared__ float X[kSmallRows][kSmallD + 1];
     __shared__ ColInfo cinf[kSmallD];
     __shared__ int rorg[kSmallRows][3];          // per staged row: element offset of the receptive
@@ -200,20 +201,27 @@ __global__ void __launch_bounds__(256) syrk_small_kernel(const __grid_constant__
     const FactorJob &J = batch.j[find_job(batch, item, false)];
     const int split = item - J.item_begin;       // one tile (d <= 64 < T): item = split
     const int t = threadIdx.x, d = J.d;
+    // E upper entries: E <= 256 -> P row phases of one entry per thread; else kSmallEpt entries per
+    // thread (t, t + 256, ...) over all rows
     const int E = d * (d + 1) / 2, P = max(1, 256 / E);
     const bool active = t < E * P;
-    const int e = active ? t % E : 0, p = active ? t / E : 0;
-    int ei = 0, ej = 0;                          // entry e of the row-major upper triangle
-    {
-        int rem = e;
-        while (rem >= d - ei) { rem -= d - ei; ++ei; }
-        ej = ei + rem;
+    const int p = active && E <= 256 ? t / E : 0;
+    int ei[kSmallEpt], ej[kSmallEpt];
+#pragma unroll
+    for (int q = 0; q < kSmallEpt; ++q) {
+        const int e = E <= 256 ? (q == 0 && active ? t % E : -1) : (t + 256 * q < E ? t + 256 * q : -1);
+        int a = 0, rem = e < 0 ? 0 : e;          // entry e of the row-major upper triangle
+        while (rem >= d - a) { rem -= d - a; ++a; }
+        ei[q] = e < 0 ? -1 : a;
+        ej[q] = e < 0 ? 0 : a + rem;
     }
     if (t < d) cinf[t] = col_info(J, t);
     const long long r_begin = (long long)split * J.chunk;
     const long long r_end = min(J.n, r_begin + J.chunk);
     const int hw = J.h_out * J.w_out;
-    float acc = 0.f, acc2 = 0.f;
+    float acc[kSmallEpt], acc2 = 0.f;
+#pragma unroll
+    for (int q = 0; q < kSmallEpt; ++q) acc[q] = 0.f;
     for (long long r0 = r_begin; r0 < r_end; r0 += kSmallRows) {
         const int nr = (int)min((long long)kSmallRows, r_end - r0);
         __syncthreads();                         // previous step's reads done (and cinf ready)
@@ -247,22 +255,38 @@ __global__ void __launch_bounds__(256) syrk_small_kernel(const __grid_constant__
             X[rr][c] = v;
         }
         __syncthreads();
-        if (active) {
-            int rr = p;
-            for (; rr + P < nr; rr += 2 * P) {
-                acc = fmaf(X[rr][ei], X[rr][ej], acc);
-                acc2 = fmaf(X[rr + P][ei], X[rr + P][ej], acc2);
+        if (E <= 256) {
+            if (active) {
+                const int a = ei[0], b = ej[0];
+                int rr = p;
+                for (; rr + P < nr; rr += 2 * P) {
+                    acc[0] = fmaf(X[rr][a], X[rr][b], acc[0]);
+                    acc2 = fmaf(X[rr + P][a], X[rr + P][b], acc2);
+                }
+                if (rr < nr) acc[0] = fmaf(X[rr][a], X[rr][b], acc[0]);
             }
-            if (rr < nr) acc = fmaf(X[rr][ei], X[rr][ej], acc);
+        } else {
+            for (int rr = 0; rr < nr; ++rr) {
+#pragma unroll
+                for (int q = 0; q < kSmallEpt; ++q)
+                    if (ei[q] >= 0) acc[q] = fmaf(X[rr][ei[q]], X[rr][ej[q]], acc[q]);
+            }
         }
     }
-    acc += acc2;
-    red[t] = acc;
-    __syncthreads();
-    if (active && p == 0) {
-        float sum = 0.f;
-        for (int q = 0; q < P; ++q) sum += red[q * E + e];     // fixed order over the row phases
-        J.partial[(size_t)split * J.tiles * (T * T) + ei * T + ej] = sum;
+    float *out = J.partial + (size_t)split * J.tiles * (T * T);
+    if (E <= 256) {
+        red[t] = acc[0] + acc2;
+        __syncthreads();
+        if (active && p == 0) {
+            const int e = t % E;
+            float sum = 0.f;
+            for (int q = 0; q < P; ++q) sum += red[q * E + e];     // fixed order over the row phases
+            out[ei[0] * T + ej[0]] = sum;
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < kSmallEpt; ++q)
+            if (ei[q] >= 0) out[ei[q] * T + ej[q]] = acc[q];
     }
 }
 
