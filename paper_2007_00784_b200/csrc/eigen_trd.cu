@@ -289,7 +289,10 @@ __global__ void __launch_bounds__(kSmThreads, 1) trd_small(const __grid_constant
         if (tau == 0.0) continue;                                // H_k = I (the same in every CTA)
         const double *v = x;
         // ---- 2: y = A22 v.  Row sums: a warp per two own rows (independent chains) ----
-        for (int i = i0 + warp; i < nl; i += 2 * nwarp) {
+#ifndef KFAC_SM_NOWORK                                           // diagnostic: skip the matrix passes
+#define KFAC_SM_NOWORK 0
+#endif
+        for (int i = i0 + warp; i < (KFAC_SM_NOWORK ? 0 : nl); i += 2 * nwarp) {
             const int ib = i + nwarp;
             const int r = rank + cl * i, rb = ib < nl ? rank + cl * ib : -1;
             const double *row = Al + sm_off(i, cl, rank), *rowb = Al + sm_off(ib < nl ? ib : i, cl, rank);
@@ -315,7 +318,7 @@ __global__ void __launch_bounds__(kSmThreads, 1) trd_small(const __grid_constant
             const int m = n - k - 1;
             const int Q = m <= 128 ? 4 : (m <= 256 ? 2 : 1);
             double *csq = rs + nl0 + 64 + (kSmBlk * nl0 + 1) / 2 + 3 * kSmBlk;   // [4][256] (Q > 1)
-            for (int u = t; u < m * Q; u += kSmThreads) {
+            for (int u = t; u < (KFAC_SM_NOWORK ? 0 : m * Q); u += kSmThreads) {
                 const int cidx = u / Q, qq = u - cidx * Q, c = k + 1 + cidx;
                 double a = 0.0;
                 for (int i = max(i0, (c + 1 - rank + cl - 1) / cl) + qq; i < nl; i += Q)
@@ -362,7 +365,7 @@ __global__ void __launch_bounds__(kSmThreads, 1) trd_small(const __grid_constant
         }
         sm_sync(cl);
         // A22 -= v w^T + w v^T, own rows
-        for (int i = i0 + warp; i < nl; i += nwarp) {
+        for (int i = i0 + warp; i < (KFAC_SM_NOWORK ? 0 : nl); i += nwarp) {
             const int r = rank + cl * i;
             double *row = Al + sm_off(i, cl, rank);
             const double vr = v[r], wr = wv[r];
