@@ -175,7 +175,7 @@ constexpr int kSmBlk = 32;              // columns of outputs buffered in shared
 __host__ __device__ inline size_t sm_smem_bytes(int n, int cl) {
     const size_t nl0 = (size_t)sm_rows(n, cl, 0);
     return sizeof(double) * ((size_t)sm_tri_max(n, cl) + 4 * (size_t)n + nl0 + 64 + (kSmBlk * nl0 + 1) / 2 +
-                             3 * kSmBlk + 4 * 256);
+                             3 * kSmBlk);
 }
 
 __device__ __forceinline__ void cluster_sync_all() {
@@ -209,6 +209,23 @@ __device__ __forceinline__ double ld_cluster(uint32_t addr) {
     double v;
     asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(addr) : "memory");
     return v;
+}
+
+// Block sum with the warp partials combined by shuffles in every warp (a fixed tree: every thread,
+// and every CTA of the cluster, gets the same bits) instead of a serial pass over shared memory.
+__device__ __forceinline__ double sm_block_sum(double v, double *sh) {
+    constexpr int kW = kSmThreads / 32;
+    static_assert(kW <= 32 && (kW & (kW - 1)) == 0, "warps per CTA");
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
+    __syncthreads();
+    if (lane == 0) sh[w] = v;
+    __syncthreads();
+    double s = lane < kW ? sh[lane] : 0.0;
+#pragma unroll
+    for (int o = kW / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    return s;
 }
 
 __global__ void __launch_bounds__(kSmThreads, 1) trd_small(const __grid_constant__ SmallSet S) {
@@ -269,7 +286,7 @@ __global__ void __launch_bounds__(kSmThreads, 1) trd_small(const __grid_constant
         // ---- reflector (dlarfg), the same in every CTA ----
         double q2 = 0.0;
         for (int r = k + 2 + t; r < n; r += kSmThreads) q2 += x[r] * x[r];
-        const double nrm2 = block_sum(q2, sh);
+        const double nrm2 = sm_block_sum(q2, sh);
         const double alpha = x[k + 1];
         double tau = 0.0, beta = alpha, scale = 0.0;
         if (nrm2 > 0.0) {
@@ -288,52 +305,41 @@ __global__ void __launch_bounds__(kSmThreads, 1) trd_small(const __grid_constant
         if (jb == kSmBlk - 1 || k == n - 2) flush(k - jb, jb + 1);
         if (tau == 0.0) continue;                                // H_k = I (the same in every CTA)
         const double *v = x;
-        // ---- 2: y = A22 v.  Row sums: a warp per two own rows (independent chains) ----
+        // ---- 2: y = A22 v.  Row sums (warp per own row) ----
 #ifndef KFAC_SM_NOWORK                                           // diagnostic: skip the matrix passes
 #define KFAC_SM_NOWORK 0
 #endif
-        for (int i = i0 + warp; i < (KFAC_SM_NOWORK ? 0 : nl); i += 2 * nwarp) {
-            const int ib = i + nwarp;
-            const int r = rank + cl * i, rb = ib < nl ? rank + cl * ib : -1;
-            const double *row = Al + sm_off(i, cl, rank), *rowb = Al + sm_off(ib < nl ? ib : i, cl, rank);
-            double a = 0.0, b = 0.0;
-            for (int c = k + 1 + lane; c <= max(r, rb); c += 32) {
-                const double vc = v[c];
-                if (c <= r) a += row[c] * vc;
-                if (c <= rb) b += rowb[c] * vc;
+        for (int i = i0 + warp; i < (KFAC_SM_NOWORK ? 0 : nl); i += nwarp) {
+            const int r = rank + cl * i;
+            const double *row = Al + sm_off(i, cl, rank);
+            double a = 0.0, a2 = 0.0;
+            int c = k + 1 + lane;
+            for (; c + 32 <= r; c += 64) {
+                a += row[c] * v[c];
+                a2 += row[c + 32] * v[c + 32];
             }
+            if (c <= r) a += row[c] * v[c];
+            a += a2;
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                a += __shfl_xor_sync(0xffffffffu, a, o);
-                b += __shfl_xor_sync(0xffffffffu, b, o);
-            }
-            if (lane == 0) {
-                rs[i] = a;
-                if (ib < nl) rs[ib] = b;
-            }
+            for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+            if (lane == 0) rs[i] = a;
         }
-        // column sums over own rows below the diagonal: a thread per column, or Q threads per column
-        // (each a fixed residue class of the rows, combined in order) when there are few columns
-        {
-            const int m = n - k - 1;
-            const int Q = m <= 128 ? 4 : (m <= 256 ? 2 : 1);
-            double *csq = rs + nl0 + 64 + (kSmBlk * nl0 + 1) / 2 + 3 * kSmBlk;   // [4][256] (Q > 1)
-            for (int u = t; u < (KFAC_SM_NOWORK ? 0 : m * Q); u += kSmThreads) {
-                const int cidx = u / Q, qq = u - cidx * Q, c = k + 1 + cidx;
-                double a = 0.0;
-                for (int i = max(i0, (c + 1 - rank + cl - 1) / cl) + qq; i < nl; i += Q)
-                    a += Al[sm_off(i, cl, rank) + c] * v[rank + cl * i];
-                if (Q == 1) cs[c] = a;
-                else csq[qq * 256 + cidx] = a;
+        // column sums over own rows below the diagonal (thread per column)
+        for (int c = k + 1 + t; c < (KFAC_SM_NOWORK ? 0 : n); c += kSmThreads) {
+            double a = 0.0;
+            int i = max(i0, (c + 1 - rank + cl - 1) / cl);
+            int o = sm_off(i, cl, rank) + c, r = rank + cl * i;
+            double a2 = 0.0;                                     // two chains (fixed order: even/odd rows)
+            for (; i + 1 < nl; i += 2) {                         // row i + 1 starts r + 1 doubles later
+                a += Al[o] * v[r];
+                o += r + 1;
+                a2 += Al[o] * v[r + cl];
+                o += r + cl + 1;
+                r += 2 * cl;
             }
-            if (Q > 1) {
-                __syncthreads();
-                for (int cidx = t; cidx < m; cidx += kSmThreads) {
-                    double a = 0.0;
-                    for (int qq = 0; qq < Q; ++qq) a += csq[qq * 256 + cidx];
-                    cs[k + 1 + cidx] = a;
-                }
-            }
+            if (i < nl) a += Al[o] * v[r];
+            a += a2;
+            cs[c] = a;
         }
         __syncthreads();
         double pv = 0.0;                                         // v^T A v over own rows
@@ -341,7 +347,7 @@ __global__ void __launch_bounds__(kSmThreads, 1) trd_small(const __grid_constant
             const int r = rank + cl * i;
             pv += v[r] * (2.0 * rs[i] - Al[sm_off(i, cl, rank) + r] * v[r]);
         }
-        pv = block_sum(pv, sh);
+        pv = sm_block_sum(pv, sh);
         if (t == 0) slot[0] = pv;
         sm_sync(cl);
         // ---- 3: w = tau y - (tau^2 / 2)(v^T A v) v on own rows, all-gathered ----
