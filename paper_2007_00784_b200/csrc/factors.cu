@@ -266,10 +266,16 @@ __global__ void __launch_bounds__(256, 2) syrk_small_kernel(const __grid_constan
                 if (rr < nr) acc[0] = fmaf(X[rr][a], X[rr][b], acc[0]);
             }
         } else {
+            // ne entries for this thread (warp-uniform except in one warp): the unrolled body stops
+            // at ne, so threads with 2 entries do not issue the other 7 slots
+            const int ne = (E - t + 255) / 256;
             for (int rr = 0; rr < nr; ++rr) {
+                const float *xr = X[rr];
 #pragma unroll
-                for (int q = 0; q < kSmallEpt; ++q)
-                    if (ei[q] >= 0) acc[q] = fmaf(X[rr][ei[q]], X[rr][ej[q]], acc[q]);
+                for (int q = 0; q < kSmallEpt; ++q) {
+                    if (q >= ne) break;
+                    acc[q] = fmaf(xr[ei[q]], xr[ej[q]], acc[q]);
+                }
             }
         }
     }
