@@ -223,8 +223,10 @@ __device__ __forceinline__ double sm_block_sum(double v, double *sh) {
     if (lane == 0) sh[w] = v;
     __syncthreads();
     double s = lane < kW ? sh[lane] : 0.0;
+    // butterfly over all 32 lanes (a pairwise sum is commutative, so partners hold the same bits and
+    // every lane ends with the same total; a 16-lane butterfly left lanes 16..31 with 0)
 #pragma unroll
-    for (int o = kW / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     return s;
 }
 
