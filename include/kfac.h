@@ -143,8 +143,10 @@ kfac_status_t kfac_unpack_factors(const float *const *packed, const int32_t *dim
  * DESIGN.md §8) for 1024 <= dims <= 5632; by default the two-stage reduction takes a factor that
  * carries most of the call's d^3 (a latency-bound lone factor, e.g. one rank's share at W >= 4) and
  * is measured faster at its size; KFAC_EIG_TWO_STAGE / KFAC_EIG_ONE_STAGE force either reduction.
+ * When every dims >= 64 factor of the call fits one thread-block cluster's shared memory in fp64
+ * (dims <= ~870), the one-stage reduction runs cluster-resident (DESIGN.md §8b'); same outputs.
  * KFAC_EIG_WARM_START: Q[i] holds the previous orthonormal eigenbasis on entry and the Jacobi
- * factors start from it.  Eigenvector sign/order within equal eigenvalues is free (R11).
+ * factors start from it (the dims >= 64 path stays cold: DESIGN.md §8c).  Eigenvector sign/order within equal eigenvalues is free (R11).
  * 1 <= dims[i] <= 16384. */
 size_t kfac_compute_eigen_workspace_size(const int32_t *dims, int32_t count);
 kfac_status_t kfac_compute_eigen(const float *const *F, const int32_t *dims, const int32_t *ld_F,
