@@ -238,10 +238,16 @@ __global__ void __launch_bounds__(256, 2) syrk_small_kernel(const __grid_constan
             }
         }
         if (J.is_a) __syncthreads();
-        for (int q = t; q < kSmallRows * d; q += 256) {
+        // every load of the step issued before any is stored (a load-store loop waits out the
+        // memory latency once per element)
+        constexpr int kPer = kSmallRows * kSmallD / 256;
+        float vals[kPer];
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+            const int q = t + 256 * u;
             const int rr = q / d, c = q - rr * d;
             float v = 0.f;
-            if (rr < nr) {
+            if (q < kSmallRows * d && rr < nr) {
                 const ColInfo ci = cinf[c];
                 if (!J.is_a) {
                     v = __ldg(J.src + (r0 + rr) * J.c_in + ci.off);
@@ -252,7 +258,15 @@ __global__ void __launch_bounds__(256, 2) syrk_small_kernel(const __grid_constan
                     if (ih >= 0 && ih < J.h_in && iw >= 0 && iw < J.w_in) v = __ldg(J.src + rorg[rr][0] + ci.off);
                 }
             }
-            X[rr][c] = v;
+            vals[u] = v;
+        }
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+            const int q = t + 256 * u;
+            if (q < kSmallRows * d) {
+                const int rr = q / d;
+                X[rr][q - rr * d] = vals[u];
+            }
         }
         __syncthreads();
         if (E <= 256) {
