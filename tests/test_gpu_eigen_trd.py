@@ -243,3 +243,34 @@ def test_compute_eigen_tridiag_batched(lib):
         F64 = F.astype(np.float64)
         assert np.abs(Qn.T @ Qn - np.eye(n)).max() <= 2e-5, n
         assert np.linalg.norm((Qn * wn) @ Qn.T - F64) / np.linalg.norm(F64) <= 1e-5, n
+
+
+@pytest.mark.parametrize("n", [65, 289, 785])
+def test_small_cluster_path_matches_panel_path(lib, n):
+    """The cluster-resident small-factor reduction (a call whose factors all fit one cluster,
+    DESIGN.md 8b') and the grid-synchronised panel path (the same factor in a call with a large
+    one) are two implementations of the same Householder reduction: both decompositions meet the
+    fp32-storage bars against LAPACK, and their eigenvalues agree to the same bar (eigenvectors
+    through the reconstruction: sign and order within clusters are free, R11)."""
+    rng = np.random.default_rng(700 + n)
+    F = _wishart(rng, n, max(16, n // 2)).astype(np.float32)
+    big = _wishart(rng, 1000, 400).astype(np.float32)          # 1000 > ~870: forces the panel path
+    res = []
+    for fs in ([F], [F, big]):
+        fd = [_dev(x) for x in fs]
+        Q = [torch.zeros_like(f) for f in fd]
+        v = [torch.zeros(x.shape[0], device="cuda") for x in fs]
+        info = torch.full((len(fs),), -7, dtype=torch.int32, device="cuda")
+        lib.kfac_compute_eigen(fd, Q, v, info=info, flags=4)
+        torch.cuda.synchronize()
+        assert (info.cpu().numpy() == 0).all()
+        res.append((Q[0][:, :n].double().cpu().numpy(), v[0].double().cpu().numpy()))
+    F64 = F.astype(np.float64)
+    w_ref = np.clip(np.linalg.eigvalsh(F64), 0, None)
+    scale = w_ref.max()
+    for Qn, vn in res:
+        assert np.abs(vn - w_ref).max() <= 2e-6 * scale
+        assert np.abs(Qn.T @ Qn - np.eye(n)).max() <= 2e-5
+        rec = (Qn * vn) @ Qn.T
+        assert np.linalg.norm(rec - F64) / np.linalg.norm(F64) <= 1e-5
+    assert np.abs(res[0][1] - res[1][1]).max() <= 2e-6 * scale
