@@ -25,6 +25,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <map>
+#include <mutex>
 #include <optional>
 #include <vector>
 
@@ -1901,8 +1903,48 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
 }  // namespace
 
 // Cluster size of the small-factor reduction for order n (0: does not fit kSmMaxCl CTAs).
+// Largest cluster of trd_small CTAs (full shared-memory budget each) the device can co-schedule
+// (non-portable sizes above 8 depend on the GPC layout), cached per device.
+int sm_max_cluster() {
+    static std::mutex mu;
+    static std::map<int, int> cache;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 8;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(dev);
+    if (it != cache.end()) return it->second;
+    int best = 8;                                                // portable
+    if (cudaFuncSetAttribute((const void *)trd_small, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+            cudaSuccess &&
+        set_smem_attr((const void *)trd_small, (int)kSmSmemCap) == cudaSuccess) {
+        for (int cl = kSmMaxCl; cl > 8; --cl) {
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3(cl);
+            cfg.blockDim = dim3(kSmThreads);
+            cfg.dynamicSmemBytes = kSmSmemCap;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = cl;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            int nclusters = 0;
+            if (cudaOccupancyMaxActiveClusters(&nclusters, (const void *)trd_small, &cfg) == cudaSuccess &&
+                nclusters > 0) {
+                best = cl;
+                break;
+            }
+        }
+    }
+    cudaGetLastError();                                          // a refused query is not an error
+    cache[dev] = best;
+    return best;
+}
+
 int sm_cluster_size(int n) {
-    for (int cl = 1; cl <= kSmMaxCl; ++cl)
+    const int max_cl = sm_max_cluster();
+    for (int cl = 1; cl <= max_cl; ++cl)
         if (sm_smem_bytes(n, cl) <= kSmSmemCap) return cl;
     return 0;
 }
