@@ -184,58 +184,60 @@ __global__ void __launch_bounds__(NT) syrk_partial_kernel(const __grid_constant_
 // Small factors (d <= 64, the ones the tensor-core engine does not take: ResNet-32's gradient
 // factors d_G = 16 / 32 and its conv1 d_A = 28, the MLP's d_G = 10): the 128 x 128 SIMT tile would
 // spend (128/d)^2 of its FMAs on padding.  Here one CTA per row chunk stages 128 rows x d columns
-// of X = [im2col | 1] (or of the gradient rows) in shared memory and each thread accumulates one
-// upper-triangle entry (or a 1/P share of its rows, combined in a fixed order), fp32 like the SIMT
-// tile; the partial lands where the SIMT tile would put it, so the fold is unchanged.
+// of X = [im2col | 1] (or of the gradient rows) in shared memory; each thread accumulates 2 x 2
+// register blocks of the upper triangle (4 FMAs per two 8-byte loads), over all rows or, when
+// there are fewer blocks than threads, over one of P row phases combined in a fixed order; fp32
+// like the SIMT tile, and the partial lands where the SIMT tile would put it, so the fold is
+// unchanged.
 constexpr int kSmallD = 64;
 constexpr int kSmallRows = 128;
-constexpr int kSmallEpt = (kSmallD * (kSmallD + 1) / 2 + 255) / 256;   // upper entries per thread (9)
+constexpr int kSmallLd = kSmallD + 2;                        // even row stride: 8-byte column pairs
+constexpr int kSmallBpt = ((kSmallD / 2) * (kSmallD / 2 + 1) / 2 + 255) / 256;   // blocks per thread (3)
 
 __global__ void __launch_bounds__(256, 2) syrk_small_kernel(const __grid_constant__ FactorBatch batch) {
-    __shared__ float X[kSmallRows][kSmallD + 1];
+    __shared__ __align__(16) float X[kSmallRows][kSmallLd];
     __shared__ ColInfo cinf[kSmallD];
     __shared__ int rorg[kSmallRows][3];          // per staged row: element offset of the receptive
-                                                 // field origin, ih0, iw0 (A); -1 offset: past the end
-    __shared__ float red[256];
+                                                 // field origin, ih0, iw0 (A)
+    __shared__ float red[256 * 4];
     const int item = blockIdx.x;
     const FactorJob &J = batch.j[find_job(batch, item, false)];
     const int split = item - J.item_begin;       // one tile (d <= 64 < T): item = split
     const int t = threadIdx.x, d = J.d;
-    // E upper entries: E <= 256 -> P row phases of one entry per thread; else kSmallEpt entries per
-    // thread (t, t + 256, ...) over all rows
-    const int E = d * (d + 1) / 2, P = max(1, 256 / E);
-    const bool active = t < E * P;
-    const int p = active && E <= 256 ? t / E : 0;
-    int ei[kSmallEpt], ej[kSmallEpt];
+    const int nb = (d + 1) / 2, dp = 2 * nb;     // column pairs; column d (odd d) is staged as 0
+    const int B = nb * (nb + 1) / 2;             // upper 2 x 2 blocks
+    const int P = max(1, 256 / B);
+    const bool active = t < B * P;
+    const int p = B <= 256 ? t / B : 0;
+    int bi[kSmallBpt], bj[kSmallBpt];
 #pragma unroll
-    for (int q = 0; q < kSmallEpt; ++q) {
-        const int e = E <= 256 ? (q == 0 && active ? t % E : -1) : (t + 256 * q < E ? t + 256 * q : -1);
-        int a = 0, rem = e < 0 ? 0 : e;          // entry e of the row-major upper triangle
-        while (rem >= d - a) { rem -= d - a; ++a; }
-        ei[q] = e < 0 ? -1 : a;
-        ej[q] = e < 0 ? 0 : a + rem;
+    for (int q = 0; q < kSmallBpt; ++q) {
+        const int b = B <= 256 ? (q == 0 && active ? t % B : -1) : (t + 256 * q < B ? t + 256 * q : -1);
+        int a = 0, rem = b < 0 ? 0 : b;          // block b of the row-major upper triangle of nb x nb
+        while (rem >= nb - a) { rem -= nb - a; ++a; }
+        bi[q] = b < 0 ? -1 : a;
+        bj[q] = b < 0 ? 0 : a + rem;
     }
+    const int nblk = B <= 256 ? (active ? 1 : 0) : (B - t + 255) / 256;
     if (t < d) cinf[t] = col_info(J, t);
     const long long r_begin = (long long)split * J.chunk;
     const long long r_end = min(J.n, r_begin + J.chunk);
     const int hw = J.h_out * J.w_out;
-    float acc[kSmallEpt], acc2 = 0.f;
+    float acc[kSmallBpt][4];
 #pragma unroll
-    for (int q = 0; q < kSmallEpt; ++q) acc[q] = 0.f;
+    for (int q = 0; q < kSmallBpt; ++q) acc[q][0] = acc[q][1] = acc[q][2] = acc[q][3] = 0.f;
     for (long long r0 = r_begin; r0 < r_end; r0 += kSmallRows) {
         const int nr = (int)min((long long)kSmallRows, r_end - r0);
         __syncthreads();                         // previous step's reads done (and cinf ready)
-        if (J.is_a && t < kSmallRows) {
+        if (J.is_a && t < kSmallRows && t < nr) {
             const long long r = r0 + t;
-            if (t < nr) {
-                const int img = (int)(r / hw);
-                const int pp = (int)(r - (long long)img * hw);
-                const int oh = pp / J.w_out, ow = pp - oh * J.w_out;
-                const int ih0 = oh * J.stride_h - J.pad_h, iw0 = ow * J.stride_w - J.pad_w;
-                rorg[t][0] = ((img * J.h_in + ih0) * J.w_in + iw0) * J.c_in;
-                rorg[t][1] = ih0;
-                rorg[t][2] = iw0;
-            }
+            const int img = (int)(r / hw);
+            const int pp = (int)(r - (long long)img * hw);
+            const int oh = pp / J.w_out, ow = pp - oh * J.w_out;
+            const int ih0 = oh * J.stride_h - J.pad_h, iw0 = ow * J.stride_w - J.pad_w;
+            rorg[t][0] = ((img * J.h_in + ih0) * J.w_in + iw0) * J.c_in;
+            rorg[t][1] = ih0;
+            rorg[t][2] = iw0;
         }
         if (J.is_a) __syncthreads();
         // every load of the step issued before any is stored (a load-store loop waits out the
@@ -245,9 +247,9 @@ __global__ void __launch_bounds__(256, 2) syrk_small_kernel(const __grid_constan
 #pragma unroll
         for (int u = 0; u < kPer; ++u) {
             const int q = t + 256 * u;
-            const int rr = q / d, c = q - rr * d;
+            const int rr = q / dp, c = q - rr * dp;
             float v = 0.f;
-            if (q < kSmallRows * d && rr < nr) {
+            if (q < kSmallRows * dp && rr < nr && c < d) {
                 const ColInfo ci = cinf[c];
                 if (!J.is_a) {
                     v = __ldg(J.src + (r0 + rr) * J.c_in + ci.off);
@@ -263,50 +265,51 @@ __global__ void __launch_bounds__(256, 2) syrk_small_kernel(const __grid_constan
 #pragma unroll
         for (int u = 0; u < kPer; ++u) {
             const int q = t + 256 * u;
-            if (q < kSmallRows * d) {
-                const int rr = q / d;
-                X[rr][q - rr * d] = vals[u];
+            if (q < kSmallRows * dp) {
+                const int rr = q / dp;
+                X[rr][q - rr * dp] = vals[u];
             }
         }
         __syncthreads();
-        if (E <= 256) {
-            if (active) {
-                const int a = ei[0], b = ej[0];
-                int rr = p;
-                for (; rr + P < nr; rr += 2 * P) {
-                    acc[0] = fmaf(X[rr][a], X[rr][b], acc[0]);
-                    acc2 = fmaf(X[rr + P][a], X[rr + P][b], acc2);
-                }
-                if (rr < nr) acc[0] = fmaf(X[rr][a], X[rr][b], acc[0]);
-            }
-        } else {
-            // ne entries for this thread (warp-uniform except in one warp): the unrolled body stops
-            // at ne, so threads with 2 entries do not issue the other 7 slots
-            const int ne = (E - t + 255) / 256;
-            for (int rr = 0; rr < nr; ++rr) {
-                const float *xr = X[rr];
+        for (int rr = p; rr < nr; rr += P) {
+            const float *xr = X[rr];
 #pragma unroll
-                for (int q = 0; q < kSmallEpt; ++q) {
-                    if (q >= ne) break;
-                    acc[q] = fmaf(xr[ei[q]], xr[ej[q]], acc[q]);
-                }
+            for (int q = 0; q < kSmallBpt; ++q) {
+                if (q >= nblk) break;
+                const float2 a = *reinterpret_cast<const float2 *>(xr + 2 * bi[q]);
+                const float2 b = *reinterpret_cast<const float2 *>(xr + 2 * bj[q]);
+                acc[q][0] = fmaf(a.x, b.x, acc[q][0]);
+                acc[q][1] = fmaf(a.x, b.y, acc[q][1]);
+                acc[q][2] = fmaf(a.y, b.x, acc[q][2]);
+                acc[q][3] = fmaf(a.y, b.y, acc[q][3]);
             }
         }
     }
     float *out = J.partial + (size_t)split * J.tiles * (T * T);
-    if (E <= 256) {
-        red[t] = acc[0] + acc2;
+    if (B <= 256) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) red[u * 256 + t] = acc[0][u];
         __syncthreads();
         if (active && p == 0) {
-            const int e = t % E;
-            float sum = 0.f;
-            for (int q = 0; q < P; ++q) sum += red[q * E + e];     // fixed order over the row phases
-            out[ei[0] * T + ej[0]] = sum;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int i = 2 * bi[0] + (u >> 1), j = 2 * bj[0] + (u & 1);
+                if (i >= d || j >= d || i > j) continue;
+                float sum = 0.f;
+                for (int q = 0; q < P; ++q) sum += red[u * 256 + q * B + t];   // fixed order over the phases
+                out[i * T + j] = sum;
+            }
         }
     } else {
 #pragma unroll
-        for (int q = 0; q < kSmallEpt; ++q)
-            if (ei[q] >= 0) out[ei[q] * T + ej[q]] = acc[q];
+        for (int q = 0; q < kSmallBpt; ++q) {
+            if (q >= nblk) break;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int i = 2 * bi[q] + (u >> 1), j = 2 * bj[q] + (u & 1);
+                if (i < d && j < d && i <= j) out[i * T + j] = acc[q][u];
+            }
+        }
     }
 }
 
