@@ -290,8 +290,8 @@ __global__ void __launch_bounds__(kSmThreads, 1) trd_small(const __grid_constant
         // ---- reflector (dlarfg), the same in every CTA ----
         double q2 = 0.0;
         for (int r = k + 2 + t; r < n; r += kSmThreads) q2 += x[r] * x[r];
-        const double nrm2 = sm_block_sum(q2, sh);
-        const double alpha = x[k + 1];
+        const double alpha = x[k + 1];                           // read before the block sum's barriers,
+        const double nrm2 = sm_block_sum(q2, sh);                // which order it before x[k+1] = 1
         double tau = 0.0, beta = alpha, scale = 0.0;
         if (nrm2 > 0.0) {
             beta = -copysign(sqrt(alpha * alpha + nrm2), alpha);
@@ -302,7 +302,6 @@ __global__ void __launch_bounds__(kSmThreads, 1) trd_small(const __grid_constant
             dbuf[kSmBlk + jb] = beta;
             dbuf[2 * kSmBlk + jb] = tau;
         }
-        __syncthreads();                                         // every thread has read x[k+1]
         for (int r = k + 1 + t; r < n; r += kSmThreads) x[r] = r == k + 1 ? 1.0 : x[r] * scale;
         __syncthreads();
         for (int i = i0 + t; i < nl; i += kSmThreads) vbuf[jb * nl0 + i] = (float)x[rank + cl * i];
