@@ -247,9 +247,10 @@ __global__ void __launch_bounds__(256, 2) syrk_small_kernel(const __grid_constan
 #pragma unroll
         for (int u = 0; u < kPer; ++u) {
             const int q = t + 256 * u;
+            if (256 * u >= kSmallRows * dp) break;   // uniform: 128 dp is a multiple of 256
             const int rr = q / dp, c = q - rr * dp;
             float v = 0.f;
-            if (q < kSmallRows * dp && rr < nr && c < d) {
+            if (rr < nr && c < d) {
                 const ColInfo ci = cinf[c];
                 if (!J.is_a) {
                     v = __ldg(J.src + (r0 + rr) * J.c_in + ci.off);
@@ -265,10 +266,9 @@ __global__ void __launch_bounds__(256, 2) syrk_small_kernel(const __grid_constan
 #pragma unroll
         for (int u = 0; u < kPer; ++u) {
             const int q = t + 256 * u;
-            if (q < kSmallRows * dp) {
-                const int rr = q / dp;
-                X[rr][q - rr * dp] = vals[u];
-            }
+            if (256 * u >= kSmallRows * dp) break;
+            const int rr = q / dp;
+            X[rr][q - rr * dp] = vals[u];
         }
         __syncthreads();
         for (int rr = p; rr < nr; rr += P) {
