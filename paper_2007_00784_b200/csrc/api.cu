@@ -80,6 +80,54 @@ cudaError_t set_smem_attr(const void *kernel, int bytes) {
 }
 
 namespace {
+struct SidePool {                          // per thread: streams and events of the current device
+    int dev = -1;
+    std::vector<cudaStream_t> st;
+    std::vector<cudaEvent_t> ev;           // ev[0]: fork; ev[1 + g]: join of stream g
+};
+}  // namespace
+
+cudaError_t SideFork::fork(cudaStream_t s, int n) {
+    thread_local SidePool P;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (n > kMaxSide) return cudaErrorInvalidValue;
+    if (P.dev != dev) {                    // a thread that switched devices starts a new pool
+        P = SidePool{};
+        P.dev = dev;
+        P.st.reserve(kMaxSide);            // never reallocated: handed-out pointers stay valid
+        P.ev.reserve(kMaxSide + 1);
+    }
+    while ((int)P.st.size() < n) {
+        cudaStream_t x;
+        if ((e = cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking)) != cudaSuccess) return e;
+        P.st.push_back(x);
+    }
+    while ((int)P.ev.size() < n + 1) {
+        cudaEvent_t x;
+        if ((e = cudaEventCreateWithFlags(&x, cudaEventDisableTiming)) != cudaSuccess) return e;
+        P.ev.push_back(x);
+    }
+    st_ = P.st.data();
+    ev_ = P.ev.data();
+    n_ = n;
+    if ((e = cudaEventRecord(ev_[0], s)) != cudaSuccess) return e;
+    for (int g = 0; g < n; ++g)
+        if ((e = cudaStreamWaitEvent(st_[g], ev_[0], 0)) != cudaSuccess) return e;
+    return cudaSuccess;
+}
+
+cudaError_t SideFork::join(cudaStream_t s) {
+    cudaError_t e;
+    for (int g = 0; g < n_; ++g) {
+        if ((e = cudaEventRecord(ev_[1 + g], st_[g])) != cudaSuccess) return e;
+        if ((e = cudaStreamWaitEvent(s, ev_[1 + g], 0)) != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+namespace {
 
 kfac_status_t check_device() {
     int dev = -1;

@@ -86,6 +86,22 @@ struct NvtxRange {
 // per (kernel, device, bytes); thread-safe.
 cudaError_t set_smem_attr(const void *kernel, int bytes);
 
+// Fork/join of independent launches onto side streams of the calling thread (current device):
+// fork(s, n) records an event on s and makes n side streams wait for it; side(g) is stream g;
+// join(s) makes s wait for every side stream used since the fork.  Stream-ordered for the caller
+// and capturable in a CUDA graph.
+class SideFork {
+public:
+    static constexpr int kMaxSide = 64;     // side streams per thread and device
+    cudaError_t fork(cudaStream_t s, int n);
+    cudaStream_t side(int g) const { return st_[g]; }
+    cudaError_t join(cudaStream_t s);
+private:
+    cudaStream_t *st_ = nullptr;
+    cudaEvent_t *ev_ = nullptr;
+    int n_ = 0;
+};
+
 // Per-launch instrumentation (kfac_profile_start/stop).  prof_begin returns a slot (< 0 when the
 // class is not armed); prof_end records the closing event and the launch's algorithmic work.
 int prof_begin(int kernel_class, cudaStream_t s);

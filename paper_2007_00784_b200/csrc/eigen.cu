@@ -577,12 +577,18 @@ kfac_status_t eigen_run(const float *const *F, const int32_t *dims, const int32_
     char *base = static_cast<char *>(ws);
     const size_t joff = round_up(jacobi_bytes(dims, count), 256);
     int32_t *local = reinterpret_cast<int32_t *>(base + joff + round_up(trd_workspace_bytes(dims, count), 256));
+    // the Jacobi factors (d < 64) and the tridiagonal path share nothing (disjoint workspace and
+    // info slots): the Jacobi sweeps run on a side stream next to the reduction
+    SideFork fk;
+    const bool par = !jd.empty() && !td.empty();
+    if (par) KFAC_CUDA_TRY(fk.fork(s, 1));
     if (!jd.empty()) {
+        const cudaStream_t js = par ? fk.side(0) : s;
         kfac_status_t st = jacobi_run(jF.data(), jd.data(), jl.data(), (int)jd.size(), jQ.data(), jlq.data(),
-                                      je.data(), local, flags & KFAC_EIG_WARM_START, base, s);
+                                      je.data(), local, flags & KFAC_EIG_WARM_START, base, js);
         if (st != KFAC_OK) return st;
         if (info) {
-            st = scatter_info(local, jidx, info, s);
+            st = scatter_info(local, jidx, info, js);
             if (st != KFAC_OK) return st;
         }
     }
@@ -595,6 +601,7 @@ kfac_status_t eigen_run(const float *const *F, const int32_t *dims, const int32_
             if (st != KFAC_OK) return st;
         }
     }
+    if (par) KFAC_CUDA_TRY(fk.join(s));
     return KFAC_OK;
 }
 

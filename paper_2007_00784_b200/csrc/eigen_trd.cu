@@ -1948,38 +1948,9 @@ int sm_cluster_size(int n) {
     return 0;
 }
 
-// Side streams (and fork/join events) of the calling thread on the current device: the small
-// reduction's launches of different cluster sizes are independent, so they run side by side (a
-// ResNet-32 call has d = 145 / 289 / 577 factors on 1-, 2- and 7-CTA clusters) and the caller's
-// stream waits for all of them -- stream-ordered as seen by the caller, and capturable in a graph.
-struct SideStreams {
-    int dev = -1;
-    std::vector<cudaStream_t> st;
-    std::vector<cudaEvent_t> ev;            // ev[0]: fork; ev[1 + g]: join of side stream g
-};
-
-static kfac_status_t side_streams(int need, SideStreams *&out) {
-    thread_local SideStreams S;
-    int dev = 0;
-    KFAC_CUDA_TRY(cudaGetDevice(&dev));
-    if (S.dev != dev) {                     // per device (a thread may switch devices): start over
-        S = SideStreams{};
-        S.dev = dev;
-    }
-    while ((int)S.st.size() < need) {
-        cudaStream_t x;
-        KFAC_CUDA_TRY(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
-        S.st.push_back(x);
-    }
-    while ((int)S.ev.size() < need + 1) {
-        cudaEvent_t e;
-        KFAC_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-        S.ev.push_back(e);
-    }
-    out = &S;
-    return KFAC_OK;
-}
-
+// The small reduction's launches of different cluster sizes are independent, so they run side by
+// side on side streams (SideFork: forked from and joined back into the caller's stream) -- a
+// ResNet-32 call has d = 145 / 289 / 577 factors on 1-, 2- and 7-CTA clusters.
 kfac_status_t small_reduce(const TrdJob *djobs, const std::vector<TrdJob> &jobs, cudaStream_t s) {
     KFAC_CUDA_TRY(cudaFuncSetAttribute((const void *)trd_small, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     const int count = (int)jobs.size();
@@ -1997,18 +1968,12 @@ kfac_status_t small_reduce(const TrdJob *djobs, const std::vector<TrdJob> &jobs,
                                                      grp.begin() + std::min(grp.size(), c0 + (size_t)kSmMaxJobs))});
     }
     const int nl = (int)launches.size();
-    SideStreams *S = nullptr;
-    if (nl > 1) {
-        RET_OK(side_streams(nl, S));
-        KFAC_CUDA_TRY(cudaEventRecord(S->ev[0], s));
-    }
+    SideFork fk;
+    const bool par = nl > 1 && nl <= SideFork::kMaxSide;
+    if (par) KFAC_CUDA_TRY(fk.fork(s, nl));
     for (int g = 0; g < nl; ++g) {
         const Launch &L = launches[g];
-        cudaStream_t ls = s;
-        if (nl > 1) {
-            ls = S->st[g];
-            KFAC_CUDA_TRY(cudaStreamWaitEvent(ls, S->ev[0], 0));
-        }
+        const cudaStream_t ls = par ? fk.side(g) : s;
         thread_local SmallSet SS;
         const int na = (int)L.ids.size();
         SS.jobs = djobs;
@@ -2033,11 +1998,8 @@ kfac_status_t small_reduce(const TrdJob *djobs, const std::vector<TrdJob> &jobs,
         cfg.numAttrs = 1;
         KFAC_CUDA_TRY(cudaLaunchKernelEx(&cfg, trd_small, SS));
         KFAC_LAUNCHED();
-        if (nl > 1) {
-            KFAC_CUDA_TRY(cudaEventRecord(S->ev[1 + g], ls));
-            KFAC_CUDA_TRY(cudaStreamWaitEvent(s, S->ev[1 + g], 0));
-        }
     }
+    if (par) KFAC_CUDA_TRY(fk.join(s));
     return KFAC_OK;
 }
 

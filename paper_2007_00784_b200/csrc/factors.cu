@@ -451,6 +451,12 @@ kfac_status_t factors_run(const kfac_layer_t *layers, int nl, const float *const
     // so the SYRK kernel gathers both planes and never splits in shared memory.
     std::vector<FactorJob> tc, simt;
     for (auto &j : p.jobs) (syrk_tc_supported(j) ? tc : simt).push_back(j);
+    // the SIMT / small-d partial SYRKs are independent of the tensor-core ones: they run on a side
+    // stream forked from s and joined back before the fold
+    SideFork fk;
+    const bool par = !tc.empty() && !simt.empty();
+    if (par) KFAC_CUDA_TRY(fk.fork(s, 1));
+    const cudaStream_t ss = par ? fk.side(0) : s;
     if (!tc.empty()) {
         float *pl = base + round_up(p.partial_floats, 64);
         std::vector<SplitJob> sj;
@@ -482,7 +488,7 @@ kfac_status_t factors_run(const kfac_layer_t *layers, int nl, const float *const
             items += j.splits;                       // one tile
             fb.j[fb.count++] = j;
         }
-        syrk_small_kernel<<<items, 256, 0, s>>>(fb);
+        syrk_small_kernel<<<items, 256, 0, ss>>>(fb);
         KFAC_LAUNCHED();
     }
     for (size_t b0 = 0; b0 < tile.size(); b0 += kMaxJobs) {
@@ -495,9 +501,10 @@ kfac_status_t factors_run(const kfac_layer_t *layers, int nl, const float *const
             items += j.tiles * j.splits;
             fb.j[fb.count++] = j;
         }
-        syrk_partial_kernel<<<items, NT, 0, s>>>(fb);
+        syrk_partial_kernel<<<items, NT, 0, ss>>>(fb);
         KFAC_LAUNCHED();
     }
+    if (par) KFAC_CUDA_TRY(fk.join(s));
     // Fixed-order reduction + running average for every factor.
     for (size_t b0 = 0; b0 < p.jobs.size(); b0 += kMaxJobs) {
         FactorBatch fb;
