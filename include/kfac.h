@@ -15,8 +15,11 @@
  *    (global) memory; "host" pointers are ordinary host memory.  Arrays of
  *    pointers (e.g. `const float* const* act`) are HOST arrays holding DEVICE
  *    pointers.  The library allocates no device memory, keeps no pointer after
- *    return, never synchronises the device and launches only on `stream`
- *    (cudaStream_t; 0 = legacy default stream).
+ *    return, never synchronises the device and launches on `stream`
+ *    (cudaStream_t; 0 = legacy default stream) -- independent launches of one call
+ *    may run on per-thread side streams forked from `stream` by an event and joined
+ *    back into it before the call returns, so the call stays stream-ordered (and
+ *    capturable in a CUDA graph) as seen by the caller.
  *  - Matrices are fp32, row-major, with a leading dimension `ld` (elements)
  *    that is >= the column count and a multiple of 4 (16-byte rows, TMA rule);
  *    every matrix base address must be 16-byte aligned.
