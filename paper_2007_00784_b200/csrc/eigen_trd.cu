@@ -54,7 +54,10 @@ constexpr int kTrdCtasPerSm = 512 / kTrdThreads;
 constexpr int kTrdWarps = kTrdThreads / 32;
 constexpr int kPart = 2 * kNb + 2;      // per-CTA partials: V^T v, W^T v, ||x||^2, w^T v
 constexpr int kMaxGroupCtas = 512;
-constexpr int kLeaf = 32;               // D&C leaf size
+#ifndef KFAC_LEAF
+#define KFAC_LEAF 32
+#endif
+constexpr int kLeaf = KFAC_LEAF;               // D&C leaf size
 #ifndef KFAC_SYMV_ROWS
 #define KFAC_SYMV_ROWS 32
 #endif
