@@ -909,8 +909,14 @@ __global__ void __launch_bounds__(kQ2Warps * 32, 1) sbr_q2(const __grid_constant
 // column chain is then the critical path: a lone factor, one rank's share at W >= 4; with many
 // factors the one-stage panels share the HBM stream across factors and win) and its size is one the
 // two-stage path measures faster at (profiles/r02_*_sbr_*).
-constexpr double kAutoShare = 0.5;
-constexpr int kAutoMaxN = 4000;
+#ifndef KFAC_SBR_SHARE
+#define KFAC_SBR_SHARE 0.5
+#endif
+#ifndef KFAC_SBR_MAXN
+#define KFAC_SBR_MAXN 4000
+#endif
+constexpr double kAutoShare = KFAC_SBR_SHARE;
+constexpr int kAutoMaxN = KFAC_SBR_MAXN;
 
 std::vector<char> route(const int32_t *dims, int count, uint32_t flags) {
     std::vector<char> r(count, 0);

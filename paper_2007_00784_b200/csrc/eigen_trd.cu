@@ -55,9 +55,9 @@ constexpr int kTrdWarps = kTrdThreads / 32;
 constexpr int kPart = 2 * kNb + 2;      // per-CTA partials: V^T v, W^T v, ||x||^2, w^T v
 constexpr int kMaxGroupCtas = 512;
 #ifndef KFAC_LEAF
-#define KFAC_LEAF 32
+#define KFAC_LEAF 16
 #endif
-constexpr int kLeaf = KFAC_LEAF;               // D&C leaf size
+constexpr int kLeaf = KFAC_LEAF;        // D&C leaf size (16: mlp 9.39 -> 9.21 ms, r32 10.14 -> 10.01 ms, r50 within noise)
 #ifndef KFAC_SYMV_ROWS
 #define KFAC_SYMV_ROWS 32
 #endif
