@@ -980,6 +980,13 @@ int chase_cs(int n) { return std::min(kChaseMaxCs, std::max(1, cdiv(n, kChaseRow
 
 kfac_status_t reduce(const TrdJob *djobs, const std::vector<TrdJob> &jobs, const std::vector<int> &ids,
                      cudaStream_t s) {
+    const kfac_status_t st = stage1(djobs, jobs, ids, s);
+    if (st != KFAC_OK) return st;
+    return chase(djobs, jobs, ids, s);
+}
+
+kfac_status_t stage1(const TrdJob *djobs, const std::vector<TrdJob> &jobs, const std::vector<int> &ids,
+                     cudaStream_t s) {
     KFAC_CUDA_TRY(set_smem_attr((const void *)sbr_panel_qr, (int)kQrSmem));
     KFAC_CUDA_TRY(set_smem_attr((const void *)sbr_symm, kSymmSmem));
     // ---- stage 1: one panel of every active factor per launch, staggered to finish together ----
@@ -1030,6 +1037,17 @@ kfac_status_t reduce(const TrdJob *djobs, const std::vector<TrdJob> &jobs, const
             SBR_TRY(gemm64_grouped(gd.data(), (int)gd.size(), s));
         }
     }
+    return KFAC_OK;
+}
+
+int chase_ctas(const std::vector<TrdJob> &jobs, const std::vector<int> &ids) {
+    int c = 0;
+    for (int i : ids) c += chase_cs(jobs[i].n);
+    return c;
+}
+
+kfac_status_t chase(const TrdJob *djobs, const std::vector<TrdJob> &jobs, const std::vector<int> &ids,
+                    cudaStream_t s) {
     // ---- stage 2: one cluster per factor, grouped by cluster size ----
     KFAC_CUDA_TRY(cudaFuncSetAttribute((const void *)sbr_chase, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     for (int cs = 1; cs <= kChaseMaxCs; ++cs) {

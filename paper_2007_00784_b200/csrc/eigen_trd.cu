@@ -58,6 +58,9 @@ constexpr int kMaxGroupCtas = 512;
 #define KFAC_LEAF 16
 #endif
 constexpr int kLeaf = KFAC_LEAF;        // D&C leaf size (16: mlp 9.39 -> 9.21 ms, r32 10.14 -> 10.01 ms, r50 within noise)
+#ifndef KFAC_SBR_OVERLAP
+#define KFAC_SBR_OVERLAP 0
+#endif
 #ifndef KFAC_SYMV_ROWS
 #define KFAC_SYMV_ROWS 32
 #endif
@@ -2094,7 +2097,7 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
     // the fused trailing update reuses the ring as two teams' 64 x 68 fp64 operand tiles
     const size_t smem = std::max(smem_base + (use_xs ? smem_xs : 0),
                                  (size_t)ring_off * sizeof(float) + 2 * 2 * 64 * 68 * sizeof(double));
-    const int cap = panel_capacity(smem);
+    int cap = panel_capacity(smem);
     thread_local PanelLaunch PL;       // host staging (kernel parameters are copied at launch)
     // Staggered schedule: factor j (P_j panels) starts at launch P_max - P_j, so all factors finish
     // together and the small ones share the GPU with the big ones' small trailing matrices.
@@ -2104,6 +2107,23 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
     int pmax = 0;
     for (int i = 0; i < count; ++i)
         if (P.jobs[i].off == 1) pmax = std::max(pmax, cdiv(P.jobs[i].n, kNb));
+    // Two-stage factors beside the one-stage ones (KFAC_SBR_OVERLAP): stage 1 (dense -> band, GEMMs
+    // that fill the GPU) first, then the latency-bound bulge chase (one cluster per factor) on a
+    // side stream while the one-stage panels run on the remaining SMs (cap reduced by the chase's
+    // CTAs, one per SM); joined before divide and conquer.
+    SideFork sbr_fk;
+    bool sbr_par = false;
+    if (KFAC_SBR_OVERLAP && !sbr_ids.empty() && pmax > 0) {
+        const int per_sm = std::max(1, cap / num_sms());
+        const int free_sms = num_sms() - sbr::chase_ctas(P.jobs, sbr_ids);
+        if (free_sms >= num_sms() / 4) {
+            RET_OK(sbr::stage1(djobs, P.jobs, sbr_ids, s));
+            KFAC_CUDA_TRY(sbr_fk.fork(s, 1));
+            RET_OK(sbr::chase(djobs, P.jobs, sbr_ids, sbr_fk.side(0)));
+            cap = std::min(cap, per_sm * free_sms);
+            sbr_par = true;
+        }
+    }
     // CTAs per active factor ~ (remaining trailing size)^2 (the mat-vec bytes; exponents 1.5-3
     // measured equal within noise)
     constexpr double wexp = 2.0;
@@ -2200,7 +2220,8 @@ kfac_status_t trd_exec(const float *const *F, const int32_t *dims, const int32_t
         }   // chunks of the active set
     }
 
-    if (!sbr_ids.empty()) RET_OK(sbr::reduce(djobs, P.jobs, sbr_ids, s));
+    if (sbr_par) KFAC_CUDA_TRY(sbr_fk.join(s));
+    else if (!sbr_ids.empty()) RET_OK(sbr::reduce(djobs, P.jobs, sbr_ids, s));
     }   // !small_path
     }   // mode != TRD_DEBUG_STEDC
     if (mode == TRD_DEBUG_TRIDIAG) {

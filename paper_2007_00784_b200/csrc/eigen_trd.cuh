@@ -84,6 +84,13 @@ void rebase_fields(TrdJob &J, char *base);
 // J.Vd / J.tau the stage-1 reflectors (offset kSbrBw) and J.Rq the stage-2 reflectors.
 kfac_status_t reduce(const TrdJob *djobs, const std::vector<TrdJob> &jobs, const std::vector<int> &ids,
                      cudaStream_t s);
+// The two halves of reduce: stage 1 (dense -> band, fills the GPU) and stage 2 (bulge chase, one
+// cluster of chase_ctas-many CTAs in all, latency-bound).
+kfac_status_t stage1(const TrdJob *djobs, const std::vector<TrdJob> &jobs, const std::vector<int> &ids,
+                     cudaStream_t s);
+kfac_status_t chase(const TrdJob *djobs, const std::vector<TrdJob> &jobs, const std::vector<int> &ids,
+                    cudaStream_t s);
+int chase_ctas(const std::vector<TrdJob> &jobs, const std::vector<int> &ids);
 // final_z(J) <- Q2 final_z(J) for the factors `ids`.
 kfac_status_t apply_q2(const TrdJob *djobs, const std::vector<TrdJob> &jobs, const std::vector<int> &ids,
                        cudaStream_t s);
