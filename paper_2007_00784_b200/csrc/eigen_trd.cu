@@ -59,7 +59,7 @@ constexpr int kMaxGroupCtas = 512;
 #endif
 constexpr int kLeaf = KFAC_LEAF;        // D&C leaf size (16: mlp 9.39 -> 9.21 ms, r32 10.14 -> 10.01 ms, r50 within noise)
 #ifndef KFAC_SBR_OVERLAP
-#define KFAC_SBR_OVERLAP 0
+#define KFAC_SBR_OVERLAP 1
 #endif
 #ifndef KFAC_SYMV_ROWS
 #define KFAC_SYMV_ROWS 32
