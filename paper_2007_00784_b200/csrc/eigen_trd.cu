@@ -10,14 +10,14 @@
 //       (d, e, tau) in fp64.  Factors the router sends to the two-stage reduction (eigen_sbr.cu:
 //       dense -> band 16 -> tridiagonal) skip these panels.
 //   (2) Cuppen's divide and conquer on T (fp64 arithmetic and fp64 eigenvector storage):
-//       leaves of <= 32 rows by implicit QL (one warp each); each merge solves
+//       leaves of <= kLeaf (16) rows by implicit QL (one warp each); each merge solves
 //       D + rho z z^T with LAPACK-style deflation (small z_i, and close d_i by a Givens rotation),
 //       a bracketed rational-Newton secular solver (one warp per root), the Gu-Eisenstat
 //       recomputed z-hat (orthogonal eigenvectors without extra precision), and the
 //       eigenvector update Q_nd S as grouped fp64 GEMMs (DMMA, or the Ozaki int8 engine for the
 //       large ones) whose N and K are the device-side count of non-deflated roots.
 //   (3) back-transformation X = H Z in blocks of 512 reflectors with the compact WY form
-//       H_b...H_{b+511} = I - V T V^T (LAPACK dlarft by 128-blocks joined recursively), three
+//       H_b...H_{b+511} = I - V T V^T (LAPACK dlarft by kTs = 64-blocks joined recursively), three
 //       grouped fp64 GEMMs per block (for two-stage factors after Q2, with reflector offset 16).
 //
 // One-sided block Jacobi (eigen.cu) remains the solver for factors below 64 and warm starts.
