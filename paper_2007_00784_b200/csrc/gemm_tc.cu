@@ -408,6 +408,9 @@ struct SyrkGeom {
 // w fills k-rows w + 8j, j < 4) and 8 drain warps (two per TMEM lane quadrant, 64 columns each,
 // so an accumulator row needs 64 registers), 18 warps in all.
 constexpr int NT2 = 576;
+#ifndef KFAC_SYRK_SPLIT_MAJOR
+#define KFAC_SYRK_SPLIT_MAJOR 1
+#endif
 constexpr int W2_DRAIN0 = 8, W2_ALLOC = 16, W2_MMA = 17;
 
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
@@ -503,7 +506,13 @@ __global__ void __launch_bounds__(NT2, 1) syrk_tc_planes8_kernel(const __grid_co
     const int item = blockIdx.x;
     const FactorJob &J = batch.j[find_job(batch, item)];
     const int local = item - J.item_begin;
+#if KFAC_SYRK_SPLIT_MAJOR
+    // row-chunk-major: the CTAs resident together share row chunks, so the column blocks every
+    // tile of a chunk re-reads (and the im2col halo) come from L2, not HBM
+    const int tau = local % J.tiles, split = local / J.tiles;
+#else
     const int tau = local / J.splits, split = local % J.splits;
+#endif
     int ti, tj;
     upper_tile(tau, J.t1d, ti, tj);
     const bool diag = ti == tj;
