@@ -21,7 +21,10 @@ namespace kfac {
 namespace {
 
 constexpr int T = 128, BK = 16, NT = 256;
-constexpr int kChunkRows = 4096;
+#ifndef KFAC_SYRK_CHUNK
+#define KFAC_SYRK_CHUNK 4096
+#endif
+constexpr int kChunkRows = KFAC_SYRK_CHUNK;   // rows per partial (split-K chunk of the SYRKs)
 constexpr int kMaxJobs = 64;
 
 struct FactorBatch {
