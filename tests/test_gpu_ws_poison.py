@@ -1,0 +1,70 @@
+"""The eigensolver's result must not depend on the workspace contents (kfac.h: the workspace is
+caller-owned scratch, no state is carried between calls).  Every call here runs on a workspace
+filled with NaN bytes, so a read of a workspace word the call did not write first poisons the
+output: Q and the eigenvalues must come out finite and meet the LAPACK bars of test_gpu_sbr."""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+TRIDIAG, TWO_STAGE, ONE_STAGE = 4, 8, 16
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2007_00784_b200.build import build
+    build()
+    from paper_2007_00784_b200 import _lib
+    return _lib
+
+
+def _dev(x):
+    n, m = x.shape
+    t = torch.zeros(n, (m + 3) // 4 * 4, dtype=torch.float32, device="cuda")
+    t[:, :m] = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32))
+    return t
+
+
+def _wishart(rng, n, rows):
+    X = rng.standard_normal((rows, n))
+    X[:, -1] = 1.0
+    return (X.T @ X / rows).astype(np.float32)
+
+
+def _run(lib, dims, rows, flags, seed):
+    rng = np.random.default_rng(seed)
+    Fs = [_wishart(rng, n, r) for n, r in zip(dims, rows)]
+    fd = [_dev(F) for F in Fs]
+    Q = [torch.zeros_like(f) for f in fd]
+    v = [torch.zeros(n, device="cuda") for n in dims]
+    info = torch.full((len(dims),), -7, dtype=torch.int32, device="cuda")
+    ws = lib.Workspace()
+    need = lib.lib.kfac_compute_eigen_workspace_size(lib._i32(dims), len(dims))
+    ws.get(need).fill_(0xFF)                                      # every byte NaN-patterned
+    lib.kfac_compute_eigen(fd, Q, v, info=info, flags=flags, ws=ws)
+    torch.cuda.synchronize()
+    assert (info.cpu().numpy() == 0).all()
+    for n, F, q, w in zip(dims, Fs, Q, v):
+        Qn = q[:, :n].double().cpu().numpy()
+        vn = w.double().cpu().numpy()
+        assert np.isfinite(Qn).all() and np.isfinite(vn).all(), f"non-finite output for d = {n}"
+        F64 = F.astype(np.float64)
+        w_ref = np.clip(np.linalg.eigvalsh(F64), 0, None)
+        assert np.abs(vn - w_ref).max() <= 2e-6 * w_ref.max()
+        assert np.abs(Qn.T @ Qn - np.eye(n)).max() <= 2e-5
+        R = (Qn * vn) @ Qn.T
+        assert np.linalg.norm(R - F64) / np.linalg.norm(F64) <= 1e-5
+
+
+@pytest.mark.parametrize("n,rows,flags", [(1041, 300, TRIDIAG | TWO_STAGE), (1024, 3000, TRIDIAG | TWO_STAGE),
+                                          (1041, 300, TRIDIAG | ONE_STAGE), (785, 200, TRIDIAG),
+                                          (65, 40, 0), (300, 100, TRIDIAG), (2305, 800, TRIDIAG | TWO_STAGE)])
+def test_eigen_on_poisoned_workspace(lib, n, rows, flags):
+    _run(lib, [n], [rows], flags, seed=n + rows)
+
+
+def test_mixed_batch_on_poisoned_workspace(lib):
+    dims = [65, 1041, 513, 2305, 1153, 300, 1600, 17]
+    rows = [40, 300, 200, 900, 500, 100, 700, 10]
+    _run(lib, dims, rows, TRIDIAG | TWO_STAGE, seed=11)
