@@ -22,7 +22,7 @@ namespace {
 
 constexpr int T = 128, BK = 16, NT = 256;
 #ifndef KFAC_SYRK_CHUNK
-#define KFAC_SYRK_CHUNK 4096
+#define KFAC_SYRK_CHUNK 8192
 #endif
 constexpr int kChunkRows = KFAC_SYRK_CHUNK;   // rows per partial (split-K chunk of the SYRKs)
 constexpr int kMaxJobs = 64;
