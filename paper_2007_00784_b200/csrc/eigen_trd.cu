@@ -402,6 +402,11 @@ __global__ void trd_init(const TrdJob *jobs) {
     const TrdJob &J = jobs[blockIdx.y];
     const int n = J.n, ldw = J.ldw;
     const int tn = (ldw + 31) / 32, tiles = tn * tn;
+    // two-stage factors: stage 1 writes tau only for the columns of its panels (0 .. 16 num_panels
+    // - 1); the back-transformation walks reflectors 0 .. n - 2, so the rest are identities (tau = 0)
+    // -- never workspace left over from an earlier call (tests/test_gpu_ws_poison.py)
+    if (J.off != 1 && blockIdx.x == 0)
+        for (int c = threadIdx.x; c < n; c += blockDim.x) J.tau[c] = 0.0;
     const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;      // 32 x 8 threads
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
         const int r0 = (tile / tn) * 32, c0 = (tile % tn) * 32;
