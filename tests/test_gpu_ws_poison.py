@@ -68,3 +68,25 @@ def test_mixed_batch_on_poisoned_workspace(lib):
     dims = [65, 1041, 513, 2305, 1153, 300, 1600, 17]
     rows = [40, 300, 200, 900, 500, 100, 700, 10]
     _run(lib, dims, rows, TRIDIAG | TWO_STAGE, seed=11)
+
+
+def test_inverse_on_poisoned_workspace(lib):
+    """Explicit damped inverse (Eq. 8 variant) on a NaN-filled workspace: finite and equal to the
+    fp64 inverse of F + gamma I (numpy, not the CUDA path) to the fp32 output rounding."""
+    dims = [5, 65, 300, 1041]
+    rng = np.random.default_rng(4)
+    Fs = [_wishart(rng, n, max(8, n // 2)).astype(np.float64) for n in dims]
+    damping = 1e-3
+    Finv = [torch.zeros(n, (n + 3) // 4 * 4, dtype=torch.float32, device="cuda") for n in dims]
+    info = torch.full((len(dims),), -1, dtype=torch.int32, device="cuda")
+    ws = lib.Workspace()
+    need = lib.lib.kfac_compute_inverse_workspace_size(lib._i32(dims), len(dims))
+    ws.get(need).fill_(0xFF)
+    lib.kfac_compute_inverse([_dev(F) for F in Fs], damping, Finv, info=info, ws=ws)
+    torch.cuda.synchronize()
+    assert (info.cpu().numpy() == 0).all()
+    for n, F, X in zip(dims, Fs, Finv):
+        Xn = X[:, :n].double().cpu().numpy()
+        assert np.isfinite(Xn).all()
+        ref = np.linalg.inv(F.astype(np.float32).astype(np.float64) + damping * np.eye(n))
+        assert np.linalg.norm(Xn - ref) / np.linalg.norm(ref) <= 1e-5
