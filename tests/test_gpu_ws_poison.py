@@ -90,3 +90,41 @@ def test_inverse_on_poisoned_workspace(lib):
         assert np.isfinite(Xn).all()
         ref = np.linalg.inv(F.astype(np.float32).astype(np.float64) + damping * np.eye(n))
         assert np.linalg.norm(Xn - ref) / np.linalg.norm(ref) <= 1e-5
+
+
+@pytest.mark.parametrize("cfg,variant", [("mlp", "eigen"), ("r32", "eigen"), ("r32", "factored"),
+                                         ("r32", "inverse")])
+def test_full_step_independent_of_workspace_contents(lib, monkeypatch, cfg, variant):
+    """One full K-FAC update (factors, decomposition, preconditioning, KL-clip) through the
+    preconditioner, with every workspace handed to the library refilled before each call -- once
+    with zero bytes, once with 0xFF (NaN) bytes: the outputs must be bitwise identical, so no stage
+    reads scratch it did not write first in the same call."""
+    from paper_2007_00784_b200.preconditioner import KFACPreconditioner
+    from workloads import shapes
+    from workloads.gen import layer_inputs
+
+    layers = shapes.mlp() if cfg == "mlp" else shapes.resnet32(batch=4)
+    hp = shapes.HPARAMS[cfg]
+    acts, gouts, grads = layer_inputs(layers, seed=3)
+    orig_get = lib.Workspace.get
+    out = {}
+    for fill in (0x00, 0xFF):
+        def get(self, nbytes, _fill=fill):
+            buf = orig_get(self, nbytes)
+            buf.fill_(_fill)
+            return buf
+        monkeypatch.setattr(lib.Workspace, "get", get)
+        pc = KFACPreconditioner(layers, damping=hp["damping"], xi=hp["xi"], kappa=hp["kappa"],
+                                lr=hp["lr"], variant=variant)
+        g = KFACPreconditioner.grad_buffer(layers, "cuda")
+        for t, w in zip(g, grads):
+            t.copy_(torch.from_numpy(w))
+        P = pc.step([torch.from_numpy(a).cuda() for a in acts], [torch.from_numpy(x).cuda() for x in gouts], g,
+                    first=True)
+        torch.cuda.synchronize()
+        out[fill] = ([p.cpu().numpy().copy() for p in P], float(pc.nu.item()))
+    monkeypatch.setattr(lib.Workspace, "get", orig_get)
+    for a, b in zip(out[0x00][0], out[0xFF][0]):
+        assert np.isfinite(b).all()
+        assert np.array_equal(a, b)
+    assert out[0x00][1] == out[0xFF][1]
