@@ -92,8 +92,12 @@ def test_inverse_on_poisoned_workspace(lib):
         assert np.linalg.norm(Xn - ref) / np.linalg.norm(ref) <= 1e-5
 
 
+R50_SUB = ("conv1", "layer1.0.conv2", "layer2.0.conv2", "layer3.0.conv2", "layer4.0.conv2",
+           "layer4.0.downsample", "fc")
+
+
 @pytest.mark.parametrize("cfg,variant", [("mlp", "eigen"), ("r32", "eigen"), ("r32", "factored"),
-                                         ("r32", "inverse")])
+                                         ("r32", "inverse"), ("r50sub", "eigen")])
 def test_full_step_independent_of_workspace_contents(lib, monkeypatch, cfg, variant):
     """One full K-FAC update (factors, decomposition, preconditioning, KL-clip) through the
     preconditioner, with every workspace handed to the library refilled before each call -- once
@@ -103,8 +107,12 @@ def test_full_step_independent_of_workspace_contents(lib, monkeypatch, cfg, vari
     from workloads import shapes
     from workloads.gen import layer_inputs
 
-    layers = shapes.mlp() if cfg == "mlp" else shapes.resnet32(batch=4)
-    hp = shapes.HPARAMS[cfg]
+    if cfg == "r50sub":        # full-size ResNet-50 layers: tensor-core SYRK, one-stage panels, Ozaki
+        layers = [l for l in shapes.layers_for("r50") if l.name in R50_SUB]
+        hp = shapes.HPARAMS["r50"]
+    else:
+        layers = shapes.mlp() if cfg == "mlp" else shapes.resnet32(batch=4)
+        hp = shapes.HPARAMS[cfg]
     acts, gouts, grads = layer_inputs(layers, seed=3)
     orig_get = lib.Workspace.get
     out = {}
