@@ -148,41 +148,34 @@ __global__ void __launch_bounds__(256) ozk_rowmax(const __grid_constant__ OzOpBa
     double m = 0.0;
     if (!o.trans) {
         // X[r][k]: lanes along k (coalesced); warp ty covers rows ty, ty + 8, ...; reduce per row
-        // all four rows' loads are issued before any reduction (32 values in flight per thread)
-        double x[4][8];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const int r = r0 + ty + 8 * j;
-#pragma unroll
-            for (int i = 0; i < 8; ++i) x[j][i] = 0.0;
+            double mr = 0.0;
             if (r < r1) {
+                double x[8];
                 if (vec) {                                   // lane: k pairs kt0 + 2 tx + 64 i
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
                         const int k = kt0 + 2 * tx + 64 * i;
                         const double2 p = (k + 1 < k1 && k >= k0) ? ld_pair(o, (size_t)r * o.ld + k) : make_double2(0.0, 0.0);
-                        x[j][2 * i] = p.x;
-                        x[j][2 * i + 1] = p.y;
+                        x[2 * i] = p.x;
+                        x[2 * i + 1] = p.y;
                         if (!(k + 1 < k1 && k >= k0)) {      // ragged edge: element loads
-                            x[j][2 * i] = (k >= k0 && k < k1) ? ld_op(o, r, k) : 0.0;
-                            x[j][2 * i + 1] = (k + 1 >= k0 && k + 1 < k1) ? ld_op(o, r, k + 1) : 0.0;
+                            x[2 * i] = (k >= k0 && k < k1) ? ld_op(o, r, k) : 0.0;
+                            x[2 * i + 1] = (k + 1 >= k0 && k + 1 < k1) ? ld_op(o, r, k + 1) : 0.0;
                         }
                     }
                 } else {
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
                         const int k = kt0 + tx + 32 * i;
-                        x[j][i] = (k >= k0 && k < k1) ? ld_op(o, r, k) : 0.0;
+                        x[i] = (k >= k0 && k < k1) ? ld_op(o, r, k) : 0.0;
                     }
                 }
+#pragma unroll
+                for (int i = 0; i < 8; ++i) mr = fmax(mr, fabs(x[i]));
             }
-        }
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int r = r0 + ty + 8 * j;
-            double mr = 0.0;
-#pragma unroll
-            for (int i = 0; i < 8; ++i) mr = fmax(mr, fabs(x[j][i]));
 #pragma unroll
             for (int s = 16; s > 0; s >>= 1) mr = fmax(mr, __shfl_xor_sync(0xffffffffu, mr, s));
             if (tx == 0 && r < r1 && mr > 0.0)
@@ -193,14 +186,17 @@ __global__ void __launch_bounds__(256) ozk_rowmax(const __grid_constant__ OzOpBa
     // X[k][r]: lanes along r (coalesced); thread (ty, tx) covers k = ty, ty + 8, ... of row r0 + tx
     const int r = r0 + tx;
     if (r < r1) {
-        double x[32];                                    // every load issued before the reduction
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-            const int k = kt0 + ty + 8 * i;
-            x[i] = (k >= k0 && k < k1) ? ld_op(o, r, k) : 0.0;
+        for (int i0 = 0; i0 < 32; i0 += 8) {
+            double x[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int k = kt0 + ty + 8 * (i0 + i);
+                x[i] = (k >= k0 && k < k1) ? ld_op(o, r, k) : 0.0;
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) m = fmax(m, fabs(x[i]));
         }
-#pragma unroll
-        for (int i = 0; i < 32; ++i) m = fmax(m, fabs(x[i]));
     }
     red[ty][tx] = m;
     __syncthreads();
